@@ -1,0 +1,1091 @@
+// vie_oracle.cpp -- CPU restatement of the reference hot path.
+//
+// TEST INFRASTRUCTURE ONLY (see vie_oracle.h).  Never linked by the product.
+//
+// Reference: /root/reference/proj/include/vie/{tensor,grid,components,fft,
+// operator,decomp,solver}.hpp.  Eigen3/FFTW3 are absent here, so the GEMMs,
+// the DFT (own Stockham mixed-radix FFT) and the SVD (Householder QR + one-sided
+// Jacobi) are restated from their published algorithms.  Parity with the
+// reference is pinned at the definition level by the reference's own tests
+// (see tests/test_oracle_*.py): dense BTTB expansion vs FFT path, factor
+// transform vs dense embedding, adjointness, linearity, GMRES known answers.
+#include "vie_oracle.h"
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+namespace {
+
+using cd = std::complex<double>;
+using I64 = int64_t;
+
+thread_local std::string g_err;
+int g_threads = 1;
+
+struct invalid : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+template <class F>
+void parallel_for(I64 n, F&& fn) {
+  const int nt = static_cast<int>(std::min<I64>(std::max(1, g_threads), std::max<I64>(n, 1)));
+  if (nt <= 1) {
+    for (I64 i = 0; i < n; ++i) fn(i, 0);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      const I64 lo = n * t / nt, hi = n * (t + 1) / nt;
+      for (I64 i = lo; i < hi; ++i) fn(i, t);
+    });
+  for (auto& x : th) x.join();
+}
+
+// ---------------------------------------------------------------------------
+// DFT service restatement (fft.hpp:22-96): forward e^{-i}, unnormalised;
+// inverse e^{+i} divided by N.  Own Stockham autosort mixed-radix FFT.
+// ---------------------------------------------------------------------------
+struct FftPlan {
+  I64 n = 0;
+  std::vector<int> radices;
+  std::vector<cd> w;  // w[t] = exp(-2 pi i t / n)
+};
+
+std::mutex g_plan_mu;
+std::map<I64, FftPlan*> g_plans;
+
+const FftPlan& get_plan(I64 n) {
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  auto it = g_plans.find(n);
+  if (it != g_plans.end()) return *it->second;
+  auto* p = new FftPlan;
+  p->n = n;
+  I64 m = n;
+  while (m % 4 == 0) { p->radices.push_back(4); m /= 4; }
+  while (m % 2 == 0) { p->radices.push_back(2); m /= 2; }
+  for (I64 f = 3; f * f <= m; f += 2)
+    while (m % f == 0) { p->radices.push_back(static_cast<int>(f)); m /= f; }
+  if (m > 1) p->radices.push_back(static_cast<int>(m));
+  p->w.resize(static_cast<size_t>(n));
+  const double two_pi = 6.283185307179586476925286766559;
+  for (I64 t = 0; t < n; ++t) {
+    const double a = -two_pi * static_cast<double>(t) / static_cast<double>(n);
+    p->w[static_cast<size_t>(t)] = cd(std::cos(a), std::sin(a));
+  }
+  g_plans[n] = p;
+  return *p;
+}
+
+// In-place 1D transform of a contiguous line; `work` holds n + radix scratch.
+void fft_line(cd* data, I64 n, bool inverse, std::vector<cd>& work) {
+  if (n <= 1) return;
+  const FftPlan& P = get_plan(n);
+  if (static_cast<I64>(work.size()) < 2 * n + 64) work.resize(static_cast<size_t>(2 * n + 64));
+  cd* x = data;
+  cd* y = work.data();
+  cd* v = work.data() + n;  // radix scratch (max radix <= n)
+  std::vector<cd> vbig;
+  auto tw = [&](I64 e) {
+    const cd c = P.w[static_cast<size_t>(e % n)];
+    return inverse ? std::conj(c) : c;
+  };
+  I64 ns = 1;
+  for (int p : P.radices) {
+    cd* vv = v;
+    if (p > 63) {
+      vbig.resize(static_cast<size_t>(2 * p));
+      vv = vbig.data();
+    }
+    const I64 np = n / p;
+    const I64 tstep = n / (ns * p);
+    for (I64 j = 0; j < np; ++j) {
+      const I64 k = j % ns;
+      for (int r = 0; r < p; ++r) vv[r] = x[j + r * np];
+      if (ns > 1)
+        for (int r = 1; r < p; ++r) vv[r] *= tw(static_cast<I64>(r) * k * tstep);
+      // radix-p DFT
+      if (p == 2) {
+        const cd a = vv[0], b = vv[1];
+        vv[0] = a + b;
+        vv[1] = a - b;
+      } else if (p == 4) {
+        const cd a0 = vv[0], a1 = vv[1], a2 = vv[2], a3 = vv[3];
+        const cd s02 = a0 + a2, d02 = a0 - a2, s13 = a1 + a3, d13 = a1 - a3;
+        // -i*d13 for forward, +i*d13 for inverse
+        const cd rot = inverse ? cd(-d13.imag(), d13.real()) : cd(d13.imag(), -d13.real());
+        vv[0] = s02 + s13;
+        vv[1] = d02 + rot;
+        vv[2] = s02 - s13;
+        vv[3] = d02 - rot;
+      } else {
+        cd* o = vv + p;
+        const I64 wstep = n / p;
+        for (int q = 0; q < p; ++q) {
+          cd acc = vv[0];
+          for (int r = 1; r < p; ++r) acc += vv[r] * tw(static_cast<I64>((r * q) % p) * wstep);
+          o[q] = acc;
+        }
+        for (int q = 0; q < p; ++q) vv[q] = o[q];
+      }
+      const I64 base = (j / ns) * ns * p + k;
+      for (int r = 0; r < p; ++r) y[base + r * ns] = vv[r];
+    }
+    std::swap(x, y);
+    ns *= p;
+  }
+  if (x != data) std::memcpy(data, x, sizeof(cd) * static_cast<size_t>(n));
+}
+
+// 3D transform of a Tensor3 (axis-1 fastest).  fft.hpp:51-71 passes FFTW the
+// dims reversed; the transform itself is the plain separable 3D DFT.
+void fft3(cd* t, I64 n1, I64 n2, I64 n3, bool inverse) {
+  const I64 dims[3] = {n1, n2, n3};
+  const I64 strides[3] = {1, n1, n1 * n2};
+  for (int ax = 0; ax < 3; ++ax) {
+    const I64 n = dims[ax], st = strides[ax];
+    if (n <= 1) continue;
+    const I64 nlines = n1 * n2 * n3 / n;
+    const int nt = std::max(1, std::min<int>(g_threads, static_cast<int>(nlines)));
+    std::vector<std::vector<cd>> lines(static_cast<size_t>(nt)), works(static_cast<size_t>(nt));
+    parallel_for(nlines, [&](I64 li, int tid) {
+      // line index -> base offset
+      I64 base;
+      if (ax == 0) base = li * n1;
+      else if (ax == 1) base = (li % n1) + (li / n1) * n1 * n2;
+      else base = li;
+      auto& line = lines[static_cast<size_t>(tid)];
+      line.resize(static_cast<size_t>(n));
+      for (I64 e = 0; e < n; ++e) line[static_cast<size_t>(e)] = t[base + e * st];
+      fft_line(line.data(), n, inverse, works[static_cast<size_t>(tid)]);
+      for (I64 e = 0; e < n; ++e) t[base + e * st] = line[static_cast<size_t>(e)];
+    });
+  }
+  if (inverse) {  // fft.hpp:36: t.flat() /= t.size()
+    const double nn = static_cast<double>(n1 * n2 * n3);
+    const I64 tot = n1 * n2 * n3;
+    for (I64 i = 0; i < tot; ++i) t[i] /= nn;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Component tables: components.hpp:46-92 and operator.hpp:205-219 for PWC;
+// the PWL generalisation (not in the reference, BASELINE north star) follows
+// the same reciprocity/parity rules.
+// ---------------------------------------------------------------------------
+struct Comp {
+  int q, qp, l, lp;
+  int par[3];
+};
+struct Block {
+  int t, s, c, dsign;
+};
+
+void build_table(int kind, int basis, std::vector<Comp>& comps, std::vector<Block>& blocks) {
+  if (kind != 0 && kind != 1) throw invalid("component table: kind must be 0 (N) or 1 (K)");
+  if (basis != 0 && basis != 1) throw invalid("component table: basis must be 0 (PWC) or 1 (PWL)");
+  const int L = basis == 0 ? 1 : 4;
+  comps.clear();
+  blocks.clear();
+  for (int q = 0; q < 3; ++q)
+    for (int qp = (kind == 0 ? q : q + 1); qp < 3; ++qp)
+      for (int l = 0; l < L; ++l)
+        for (int lp = l; lp < L; ++lp) {
+          Comp c{q, qp, l, lp, {1, 1, 1}};
+          for (int a = 0; a < 3; ++a) {
+            int odd = (l == a + 1) + (lp == a + 1);
+            if (kind == 0) odd += (q == a) + (qp == a);
+            else odd += (a == 3 - q - qp);
+            c.par[a] = (odd % 2) ? -1 : 1;
+          }
+          comps.push_back(c);
+        }
+  for (int ci = 0; ci < static_cast<int>(comps.size()); ++ci) {
+    const Comp& c = comps[static_cast<size_t>(ci)];
+    const int kappa = kind == 0 ? 1 : -1;
+    const int sigma = c.par[0] * c.par[1] * c.par[2];
+    auto idx = [&](int q, int l) { return q * L + l; };
+    const Block cand[4] = {{idx(c.q, c.l), idx(c.qp, c.lp), ci, 1},
+                           {idx(c.qp, c.l), idx(c.q, c.lp), ci, kappa},
+                           {idx(c.q, c.lp), idx(c.qp, c.l), ci, kappa * sigma},
+                           {idx(c.qp, c.lp), idx(c.q, c.l), ci, sigma}};
+    std::vector<Block> mine;
+    for (const Block& b : cand) {
+      bool dup = false;
+      for (const Block& m : mine) dup |= (m.t == b.t && m.s == b.s);
+      if (!dup) mine.push_back(b);
+    }
+    blocks.insert(blocks.end(), mine.begin(), mine.end());
+  }
+}
+
+int ncur(int basis) { return basis == 0 ? 3 : 12; }
+
+// ---------------------------------------------------------------------------
+// operator.hpp restatements
+// ---------------------------------------------------------------------------
+// circulant_embed (operator.hpp:39-59)
+void circulant_embed(const cd* t, const I64 d[3], const int sg[3], cd* e) {
+  const I64 n1 = d[0], n2 = d[1], n3 = d[2];
+  const I64 m1 = 2 * n1, m2 = 2 * n2, m3 = 2 * n3;
+  std::fill(e, e + m1 * m2 * m3, cd(0.0));
+  for (I64 k = 0; k < m3; ++k) {
+    if (k == n3) continue;
+    const I64 ok = k < n3 ? k : m3 - k;
+    const double sk = k < n3 ? 1.0 : sg[2];
+    for (I64 j = 0; j < m2; ++j) {
+      if (j == n2) continue;
+      const I64 oj = j < n2 ? j : m2 - j;
+      const double sj = j < n2 ? 1.0 : sg[1];
+      for (I64 i = 0; i < m1; ++i) {
+        if (i == n1) continue;
+        const I64 oi = i < n1 ? i : m1 - i;
+        const double si = i < n1 ? 1.0 : sg[0];
+        e[i + m1 * (j + m2 * k)] = si * sj * sk * t[oi + n1 * (oj + n2 * ok)];
+      }
+    }
+  }
+}
+
+// embed_column + forward1 per column (operator.hpp:64-90)
+void transform_factor(const cd* u, I64 n, I64 r, int sign, cd* out) {
+  std::vector<cd> work;
+  for (I64 c = 0; c < r; ++c) {
+    cd* e = out + 2 * n * c;
+    std::fill(e, e + 2 * n, cd(0.0));
+    for (I64 m = 0; m < n; ++m) e[m] = u[m + n * c];
+    for (I64 m = n + 1; m < 2 * n; ++m) e[m] = static_cast<double>(sign) * u[2 * n - m + n * c];
+    fft_line(e, 2 * n, false, work);
+  }
+}
+
+// decompress_tucker (operator.hpp:224-244): three GEMM stages.
+void decompress_tucker(const I64 ed[3], const I64 rk[3], const cd* core, const cd* u1,
+                       const cd* u2, const cd* u3, cd* dst) {
+  const I64 m1 = ed[0], m2 = ed[1], m3 = ed[2];
+  const I64 r1 = rk[0], r2 = rk[1], r3 = rk[2];
+  if (r1 == 0 || r2 == 0 || r3 == 0) {
+    std::fill(dst, dst + m1 * m2 * m3, cd(0.0));
+    return;
+  }
+  // c1 = U1 * G(r1 x r2r3)
+  std::vector<cd> c1(static_cast<size_t>(m1 * r2 * r3));
+  parallel_for(r2 * r3, [&](I64 col, int) {
+    for (I64 i = 0; i < m1; ++i) {
+      cd acc = 0.0;
+      for (I64 a = 0; a < r1; ++a) acc += u1[i + m1 * a] * core[a + r1 * col];
+      c1[static_cast<size_t>(i + m1 * col)] = acc;
+    }
+  });
+  // c2 slab g = c1_g (m1 x r2) * U2^T
+  std::vector<cd> c2(static_cast<size_t>(m1 * m2 * r3));
+  parallel_for(r3, [&](I64 g, int) {
+    for (I64 j = 0; j < m2; ++j)
+      for (I64 i = 0; i < m1; ++i) {
+        cd acc = 0.0;
+        for (I64 b = 0; b < r2; ++b) acc += c1[static_cast<size_t>(i + m1 * (b + r2 * g))] * u2[j + m2 * b];
+        c2[static_cast<size_t>(i + m1 * j + m1 * m2 * g)] = acc;
+      }
+  });
+  // dst (m1m2 x m3) = c2 * U3^T
+  const I64 m12 = m1 * m2;
+  parallel_for(m3, [&](I64 k, int) {
+    cd* col = dst + m12 * k;
+    for (I64 p = 0; p < m12; ++p) col[p] = 0.0;
+    for (I64 g = 0; g < r3; ++g) {
+      const cd w = u3[k + m3 * g];
+      const cd* src = c2.data() + m12 * g;
+      for (I64 p = 0; p < m12; ++p) col[p] += src[p] * w;
+    }
+  });
+}
+
+// mac_elementwise (operator.hpp:263-265): y += coeff * s * x
+void mac_elementwise(cd* y, const cd* s, const cd* x, double coeff, I64 n) {
+  parallel_for(std::max<I64>(1, std::min<I64>(n / 65536, 64)), [&](I64 part, int) {
+    const I64 parts = std::max<I64>(1, std::min<I64>(n / 65536, 64));
+    const I64 lo = n * part / parts, hi = n * (part + 1) / parts;
+    for (I64 i = lo; i < hi; ++i) y[i] += coeff * s[i] * x[i];
+  });
+}
+
+// apply_operator (operator.hpp:273-382) for strategies HosvdDecompress and Dense.
+struct TuckerIn {
+  const I64* ranks;
+  const double* const* cores;
+  const double* const* u1s;
+  const double* const* u2s;
+  const double* const* u3s;
+};
+
+void apply_operator(int kind, int basis, const I64 grid[3], const TuckerIn* tk,
+                    const double* const* spectra, const cd* x, cd* y) {
+  std::vector<Comp> comps;
+  std::vector<Block> blocks;
+  build_table(kind, basis, comps, blocks);
+  for (int a = 0; a < 3; ++a)
+    if (grid[a] < 1) throw invalid("apply_operator: dim mismatch");
+  const int S = ncur(basis);
+  const I64 n1 = grid[0], n2 = grid[1], n3 = grid[2];
+  const I64 ed[3] = {2 * n1, 2 * n2, 2 * n3};
+  const I64 nv = n1 * n2 * n3, ne = ed[0] * ed[1] * ed[2];
+  std::vector<std::vector<cd>> xhat(static_cast<size_t>(S), std::vector<cd>(static_cast<size_t>(ne)));
+  for (int q = 0; q < S; ++q) {
+    cd* p = xhat[static_cast<size_t>(q)].data();
+    for (I64 k = 0; k < n3; ++k)
+      for (I64 j = 0; j < n2; ++j)
+        for (I64 i = 0; i < n1; ++i)
+          p[i + ed[0] * (j + ed[1] * k)] = x[q * nv + i + n1 * (j + n2 * k)];
+    fft3(p, ed[0], ed[1], ed[2], false);
+  }
+  std::vector<std::vector<cd>> yhat(static_cast<size_t>(S), std::vector<cd>(static_cast<size_t>(ne), cd(0.0)));
+  std::vector<cd> buffer(tk ? static_cast<size_t>(ne) : 0);
+  for (int ci = 0; ci < static_cast<int>(comps.size()); ++ci) {
+    const Comp& c = comps[static_cast<size_t>(ci)];
+    const double sigma = c.par[0] * c.par[1] * c.par[2];
+    const cd* s;
+    if (tk) {
+      const I64* rk = tk->ranks + 3 * ci;
+      decompress_tucker(ed, rk, reinterpret_cast<const cd*>(tk->cores[ci]),
+                        reinterpret_cast<const cd*>(tk->u1s[ci]),
+                        reinterpret_cast<const cd*>(tk->u2s[ci]),
+                        reinterpret_cast<const cd*>(tk->u3s[ci]), buffer.data());
+      s = buffer.data();
+    } else {
+      if (!spectra[ci]) throw invalid("apply_operator: dense spectrum absent");
+      s = reinterpret_cast<const cd*>(spectra[ci]);
+    }
+    for (const Block& b : blocks)
+      if (b.c == ci)
+        mac_elementwise(yhat[static_cast<size_t>(b.t)].data(), s,
+                        xhat[static_cast<size_t>(b.s)].data(), b.dsign * sigma, ne);
+  }
+  for (int q = 0; q < S; ++q) {
+    cd* p = yhat[static_cast<size_t>(q)].data();
+    fft3(p, ed[0], ed[1], ed[2], true);
+    for (I64 k = 0; k < n3; ++k)
+      for (I64 j = 0; j < n2; ++j)
+        for (I64 i = 0; i < n1; ++i)
+          y[q * nv + i + n1 * (j + n2 * k)] = p[i + ed[0] * (j + ed[1] * k)];
+  }
+}
+
+// apply_system (solver.hpp:183-200), with the PWL Gram weights g_l.
+void apply_system(int basis, const I64 grid[3], const TuckerIn& tk, const cd* eps, double inv_v,
+                  const cd* x, cd* y) {
+  const int S = ncur(basis);
+  const I64 nv = grid[0] * grid[1] * grid[2];
+  std::vector<cd> nx(static_cast<size_t>(S * nv));
+  apply_operator(0, basis, grid, &tk, nullptr, x, nx.data());
+  for (int q = 0; q < S; ++q) {
+    const int l = basis == 0 ? 0 : q % 4;
+    const double g = l == 0 ? 1.0 : 1.0 / 12.0;
+    for (I64 m = 0; m < nv; ++m) {
+      const cd e = eps[m];
+      const cd chi = e - 1.0;
+      const cd eg = basis == 0 ? e : e * g;
+      y[q * nv + m] = eg * x[q * nv + m] - chi * inv_v * nx[static_cast<size_t>(q * nv + m)];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GMRES restatement (solver.hpp:34-142)
+// ---------------------------------------------------------------------------
+using VecFn = std::function<void(const cd*, cd*)>;
+
+double vnorm(const cd* v, I64 n) {
+  double s = 0.0;
+  for (I64 i = 0; i < n; ++i) s += std::norm(v[i]);
+  return std::sqrt(s);
+}
+cd vdot(const cd* a, const cd* b, I64 n) {  // Eigen a.dot(b) = sum conj(a) b
+  cd s = 0.0;
+  for (I64 i = 0; i < n; ++i) s += std::conj(a[i]) * b[i];
+  return s;
+}
+
+struct GmresOut {
+  int iterations = 0;
+  bool converged = false;
+  double final_rel = 0.0;
+  std::vector<double> history;
+};
+
+GmresOut gmres(const VecFn& apply, const VecFn* precond, I64 n, const cd* rhs, const cd* x0,
+               double tol, int inner, int outer, cd* sol) {
+  for (I64 i = 0; i < n; ++i)
+    if (!std::isfinite(rhs[i].real()) || !std::isfinite(rhs[i].imag()))
+      throw invalid("gmres: non-finite right-hand side");
+  if (tol < 0 || inner < 1 || outer < 1) throw invalid("gmres: invalid configuration");
+  GmresOut res;
+  const double bnorm = vnorm(rhs, n);
+  for (I64 i = 0; i < n; ++i) sol[i] = x0 ? x0[i] : cd(0.0);
+  if (bnorm == 0.0) {
+    for (I64 i = 0; i < n; ++i) sol[i] = 0.0;
+    res.converged = true;
+    res.history.push_back(0.0);
+    return res;
+  }
+  const int m = inner;
+  std::vector<cd> basis(static_cast<size_t>(n * (m + 1)));
+  std::vector<cd> hess(static_cast<size_t>((m + 1) * m), cd(0.0));
+  auto H = [&](int i, int j) -> cd& { return hess[static_cast<size_t>(i + (m + 1) * j)]; };
+  std::vector<cd> g(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m));
+  std::vector<cd> r(static_cast<size_t>(n)), w(static_cast<size_t>(n)), tmp(static_cast<size_t>(n));
+  auto col = [&](int j) { return basis.data() + n * j; };
+
+  for (int restart = 0; restart < outer && !res.converged; ++restart) {
+    apply(sol, tmp.data());
+    for (I64 i = 0; i < n; ++i) r[static_cast<size_t>(i)] = rhs[i] - tmp[static_cast<size_t>(i)];
+    const double beta = vnorm(r.data(), n);
+    if (beta / bnorm <= tol) {
+      res.converged = true;
+      break;
+    }
+    for (I64 i = 0; i < n; ++i) col(0)[i] = r[static_cast<size_t>(i)] / beta;
+    std::fill(g.begin(), g.end(), cd(0.0));
+    g[0] = beta;
+    int j = 0;
+    bool breakdown = false;
+    for (; j < m; ++j) {
+      if (precond) {
+        (*precond)(col(j), tmp.data());
+        apply(tmp.data(), w.data());
+      } else {
+        apply(col(j), w.data());
+      }
+      for (int i = 0; i <= j; ++i) {
+        H(i, j) = vdot(col(i), w.data(), n);
+        const cd h = H(i, j);
+        const cd* v = col(i);
+        for (I64 e = 0; e < n; ++e) w[static_cast<size_t>(e)] -= h * v[e];
+      }
+      const double wnorm = vnorm(w.data(), n);
+      H(j + 1, j) = wnorm;
+      for (int i = 0; i < j; ++i) {
+        const cd t = cs[static_cast<size_t>(i)] * H(i, j) + sn[static_cast<size_t>(i)] * H(i + 1, j);
+        H(i + 1, j) = -std::conj(sn[static_cast<size_t>(i)]) * H(i, j) + std::conj(cs[static_cast<size_t>(i)]) * H(i + 1, j);
+        H(i, j) = t;
+      }
+      {
+        const cd a = H(j, j), b = H(j + 1, j);
+        const double denom = std::sqrt(std::norm(a) + std::norm(b));
+        if (denom == 0.0) {
+          cs[static_cast<size_t>(j)] = 1.0;
+          sn[static_cast<size_t>(j)] = 0.0;
+        } else {
+          cs[static_cast<size_t>(j)] = std::conj(a) / denom;
+          sn[static_cast<size_t>(j)] = std::conj(b) / denom;
+        }
+        H(j, j) = cs[static_cast<size_t>(j)] * a + sn[static_cast<size_t>(j)] * b;
+        H(j + 1, j) = 0.0;
+        const cd t = cs[static_cast<size_t>(j)] * g[static_cast<size_t>(j)];
+        g[static_cast<size_t>(j + 1)] = -std::conj(sn[static_cast<size_t>(j)]) * g[static_cast<size_t>(j)];
+        g[static_cast<size_t>(j)] = t;
+      }
+      ++res.iterations;
+      const double rel = std::abs(g[static_cast<size_t>(j + 1)]) / bnorm;
+      res.history.push_back(rel);
+      if (rel <= tol) {
+        ++j;
+        res.converged = true;
+        break;
+      }
+      if (wnorm < 1e-14 * beta) {
+        ++j;
+        breakdown = true;
+        break;
+      }
+      for (I64 e = 0; e < n; ++e) col(j + 1)[e] = w[static_cast<size_t>(e)] / wnorm;
+    }
+    std::vector<cd> y(static_cast<size_t>(j), cd(0.0));
+    for (int i = j - 1; i >= 0; --i) {
+      cd s = g[static_cast<size_t>(i)];
+      for (int l = i + 1; l < j; ++l) s -= H(i, l) * y[static_cast<size_t>(l)];
+      y[static_cast<size_t>(i)] = s / H(i, i);
+    }
+    std::vector<cd> update(static_cast<size_t>(n), cd(0.0));
+    for (int l = 0; l < j; ++l)
+      for (I64 e = 0; e < n; ++e) update[static_cast<size_t>(e)] += col(l)[e] * y[static_cast<size_t>(l)];
+    if (precond) {
+      (*precond)(update.data(), tmp.data());
+      for (I64 e = 0; e < n; ++e) sol[e] += tmp[static_cast<size_t>(e)];
+    } else {
+      for (I64 e = 0; e < n; ++e) sol[e] += update[static_cast<size_t>(e)];
+    }
+    if (breakdown && !res.converged) {
+      apply(sol, tmp.data());
+      for (I64 e = 0; e < n; ++e) r[static_cast<size_t>(e)] = rhs[e] - tmp[static_cast<size_t>(e)];
+      const double rel = vnorm(r.data(), n) / bnorm;
+      res.converged = rel <= tol;
+      if (res.converged) break;
+    }
+  }
+  apply(sol, tmp.data());
+  for (I64 e = 0; e < n; ++e) r[static_cast<size_t>(e)] = rhs[e] - tmp[static_cast<size_t>(e)];
+  res.final_rel = vnorm(r.data(), n) / bnorm;
+  return res;
+}
+
+// ---------------------------------------------------------------------------
+// decomp.hpp restatement: thin_svd (QR + Jacobi), truncation_rank, hosvd.
+// ---------------------------------------------------------------------------
+struct Mat {  // column-major complex
+  I64 rows = 0, cols = 0;
+  std::vector<cd> a;
+  Mat() = default;
+  Mat(I64 r, I64 c) : rows(r), cols(c), a(static_cast<size_t>(r * c), cd(0.0)) {}
+  cd& operator()(I64 i, I64 j) { return a[static_cast<size_t>(i + rows * j)]; }
+  cd operator()(I64 i, I64 j) const { return a[static_cast<size_t>(i + rows * j)]; }
+};
+
+Mat adjoint(const Mat& m) {
+  Mat o(m.cols, m.rows);
+  for (I64 j = 0; j < m.cols; ++j)
+    for (I64 i = 0; i < m.rows; ++i) o(j, i) = std::conj(m(i, j));
+  return o;
+}
+Mat matmul(const Mat& a, const Mat& b) {
+  Mat o(a.rows, b.cols);
+  for (I64 j = 0; j < b.cols; ++j)
+    for (I64 k = 0; k < a.cols; ++k) {
+      const cd bk = b(k, j);
+      if (bk == cd(0.0)) continue;
+      for (I64 i = 0; i < a.rows; ++i) o(i, j) += a(i, k) * bk;
+    }
+  return o;
+}
+
+// Householder QR (Eigen::HouseholderQR restated): returns thin Q (rows x n) and R (n x n)
+void householder_qr(const Mat& m, Mat& q, Mat& r) {
+  const I64 rows = m.rows, n = m.cols;
+  Mat a = m;
+  std::vector<std::vector<cd>> vs;
+  std::vector<cd> taus;
+  for (I64 k = 0; k < n && k < rows; ++k) {
+    double xnorm = 0.0;
+    for (I64 i = k; i < rows; ++i) xnorm += std::norm(a(i, k));
+    xnorm = std::sqrt(xnorm);
+    std::vector<cd> v(static_cast<size_t>(rows - k), cd(0.0));
+    cd tau = 0.0;
+    if (xnorm > 0.0) {
+      const cd x0 = a(k, k);
+      const cd alpha = x0 == cd(0.0) ? cd(-xnorm) : -(x0 / std::abs(x0)) * xnorm;
+      for (I64 i = k; i < rows; ++i) v[static_cast<size_t>(i - k)] = a(i, k);
+      v[0] -= alpha;
+      double vn = 0.0;
+      for (auto& e : v) vn += std::norm(e);
+      if (vn > 0.0) {
+        tau = 2.0 / vn;
+        for (I64 j = k; j < n; ++j) {
+          cd s = 0.0;
+          for (I64 i = k; i < rows; ++i) s += std::conj(v[static_cast<size_t>(i - k)]) * a(i, j);
+          s *= tau;
+          for (I64 i = k; i < rows; ++i) a(i, j) -= s * v[static_cast<size_t>(i - k)];
+        }
+      }
+    }
+    vs.push_back(v);
+    taus.push_back(tau);
+  }
+  const I64 kk = std::min(rows, n);
+  r = Mat(kk, n);
+  for (I64 j = 0; j < n; ++j)
+    for (I64 i = 0; i <= std::min(j, kk - 1); ++i) r(i, j) = a(i, j);
+  q = Mat(rows, kk);
+  for (I64 i = 0; i < kk; ++i) q(i, i) = 1.0;
+  for (I64 k = static_cast<I64>(vs.size()) - 1; k >= 0; --k) {
+    const auto& v = vs[static_cast<size_t>(k)];
+    const cd tau = taus[static_cast<size_t>(k)];
+    if (tau == cd(0.0)) continue;
+    for (I64 j = 0; j < kk; ++j) {
+      cd s = 0.0;
+      for (I64 i = k; i < rows; ++i) s += std::conj(v[static_cast<size_t>(i - k)]) * q(i, j);
+      s *= tau;
+      for (I64 i = k; i < rows; ++i) q(i, j) -= s * v[static_cast<size_t>(i - k)];
+    }
+  }
+}
+
+// One-sided (Hestenes) Jacobi SVD of a rows >= cols matrix: A = U S V^H.
+void jacobi_svd_tall(const Mat& m, Mat& u, std::vector<double>& s, Mat& v) {
+  const I64 rows = m.rows, n = m.cols;
+  Mat a = m;
+  v = Mat(n, n);
+  for (I64 i = 0; i < n; ++i) v(i, i) = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rotated = false;
+    for (I64 p = 0; p < n - 1; ++p)
+      for (I64 qq = p + 1; qq < n; ++qq) {
+        double alpha = 0.0, beta = 0.0;
+        cd gamma = 0.0;
+        for (I64 i = 0; i < rows; ++i) {
+          alpha += std::norm(a(i, p));
+          beta += std::norm(a(i, qq));
+          gamma += std::conj(a(i, p)) * a(i, qq);
+        }
+        const double ag = std::abs(gamma);
+        if (ag == 0.0 || ag <= 1e-15 * std::sqrt(alpha * beta)) continue;
+        rotated = true;
+        const cd ph = gamma / ag;  // a_q * conj(ph) makes the coupling real
+        const double zeta = (beta - alpha) / (2.0 * ag);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::abs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (I64 i = 0; i < rows; ++i) {
+          const cd ap = a(i, p), aq = a(i, qq) * std::conj(ph);
+          a(i, p) = c * ap - sn * aq;
+          a(i, qq) = sn * ap + c * aq;
+        }
+        for (I64 i = 0; i < n; ++i) {
+          const cd vp = v(i, p), vq = v(i, qq) * std::conj(ph);
+          v(i, p) = c * vp - sn * vq;
+          v(i, qq) = sn * vp + c * vq;
+        }
+      }
+    if (!rotated) break;
+  }
+  std::vector<double> nrm(static_cast<size_t>(n));
+  for (I64 j = 0; j < n; ++j) {
+    double s2 = 0.0;
+    for (I64 i = 0; i < rows; ++i) s2 += std::norm(a(i, j));
+    nrm[static_cast<size_t>(j)] = std::sqrt(s2);
+  }
+  std::vector<I64> order(static_cast<size_t>(n));
+  for (I64 j = 0; j < n; ++j) order[static_cast<size_t>(j)] = j;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](I64 x, I64 y) { return nrm[static_cast<size_t>(x)] > nrm[static_cast<size_t>(y)]; });
+  u = Mat(rows, n);
+  Mat v2(n, n);
+  s.assign(static_cast<size_t>(n), 0.0);
+  for (I64 jj = 0; jj < n; ++jj) {
+    const I64 j = order[static_cast<size_t>(jj)];
+    const double sj = nrm[static_cast<size_t>(j)];
+    s[static_cast<size_t>(jj)] = sj;
+    for (I64 i = 0; i < rows; ++i) u(i, jj) = sj > 0 ? a(i, j) / sj : cd(0.0);
+    for (I64 i = 0; i < n; ++i) v2(i, jj) = v(i, j);
+  }
+  v = v2;
+  // Columns of numerically zero singular values carry no direction after the
+  // one-sided sweep; complete U to an orthonormal set (Eigen's JacobiSVD
+  // returns orthonormal thin U for rank-deficient input as well).
+  const double smax = s.empty() ? 0.0 : s[0];
+  for (I64 jj = 0; jj < n; ++jj) {
+    if (s[static_cast<size_t>(jj)] > 1e-13 * smax && smax > 0.0) continue;
+    for (I64 e = 0; e < rows; ++e) {
+      std::vector<cd> w(static_cast<size_t>(rows), cd(0.0));
+      w[static_cast<size_t>(e)] = 1.0;
+      for (int pass = 0; pass < 2; ++pass)
+        for (I64 o = 0; o < n; ++o) {
+          if (o == jj) continue;
+          if (o > jj && !(s[static_cast<size_t>(o)] > 1e-13 * smax && smax > 0.0)) continue;
+          cd d = 0.0;
+          for (I64 i = 0; i < rows; ++i) d += std::conj(u(i, o)) * w[static_cast<size_t>(i)];
+          for (I64 i = 0; i < rows; ++i) w[static_cast<size_t>(i)] -= d * u(i, o);
+        }
+      double wn = 0.0;
+      for (auto& x : w) wn += std::norm(x);
+      wn = std::sqrt(wn);
+      if (wn > 0.5) {
+        for (I64 i = 0; i < rows; ++i) u(i, jj) = w[static_cast<size_t>(i)] / wn;
+        break;
+      }
+    }
+  }
+}
+
+void jacobi_svd(const Mat& m, Mat& u, std::vector<double>& s, Mat& v) {
+  if (m.rows >= m.cols) {
+    jacobi_svd_tall(m, u, s, v);
+  } else {
+    jacobi_svd_tall(adjoint(m), v, s, u);
+  }
+}
+
+// thin_svd (decomp.hpp:40-70)
+void thin_svd(const Mat& m, Mat& u, std::vector<double>& s, Mat& v) {
+  const I64 rows = m.rows, cols = m.cols;
+  if (rows == 0 || cols == 0) throw invalid("truncated_svd: empty matrix");
+  if (cols > 2 * rows) {
+    Mat q, r;
+    householder_qr(adjoint(m), q, r);  // m^H = Q R, R rows x rows
+    Mat su, sv;
+    jacobi_svd(adjoint(r), su, s, sv);
+    u = su;
+    v = matmul(q, sv);
+  } else if (rows > 2 * cols) {
+    Mat q, r;
+    householder_qr(m, q, r);
+    Mat su, sv;
+    jacobi_svd(r, su, s, sv);
+    u = matmul(q, su);
+    v = sv;
+  } else {
+    jacobi_svd(m, u, s, v);
+  }
+}
+
+// truncation_rank (decomp.hpp:72-103)
+I64 truncation_rank(const std::vector<double>& s, double tol, int rule) {
+  const I64 n = static_cast<I64>(s.size());
+  if (n == 0) return 0;
+  const double smax = s[0];
+  if (smax <= 0.0) return 0;
+  if (rule == 0) {
+    const double threshold = (tol / std::sqrt(3.0)) * smax;
+    I64 r = 0;
+    for (I64 j = 0; j < n; ++j)
+      if (s[static_cast<size_t>(j)] > 0.0 && s[static_cast<size_t>(j)] >= threshold - 1e-14 * smax) r = j + 1;
+    return r;
+  }
+  double total = 0.0;
+  for (double x : s) total += x * x;
+  const double budget = (tol / std::sqrt(3.0)) * std::sqrt(total);
+  const double budget2 = budget * budget;
+  double tail = 0.0;
+  I64 r = n;
+  while (r > 0) {
+    const double cand = tail + s[static_cast<size_t>(r - 1)] * s[static_cast<size_t>(r - 1)];
+    if (cand <= budget2 || s[static_cast<size_t>(r - 1)] == 0.0) {
+      tail = cand;
+      --r;
+    } else {
+      break;
+    }
+  }
+  return r;
+}
+
+// unfold (tensor.hpp:81-98)
+Mat unfold(const cd* t, const I64 d[3], int mode) {
+  const I64 n1 = d[0], n2 = d[1], n3 = d[2];
+  Mat m;
+  if (mode == 1) {
+    m = Mat(n1, n2 * n3);
+    std::copy(t, t + n1 * n2 * n3, m.a.begin());
+  } else if (mode == 2) {
+    m = Mat(n2, n1 * n3);
+    for (I64 k = 0; k < n3; ++k)
+      for (I64 j = 0; j < n2; ++j)
+        for (I64 i = 0; i < n1; ++i) m(j, i + n1 * k) = t[i + n1 * (j + n2 * k)];
+  } else {
+    m = Mat(n3, n1 * n2);
+    for (I64 k = 0; k < n3; ++k)
+      for (I64 p = 0; p < n1 * n2; ++p) m(k, p) = t[p + n1 * n2 * k];
+  }
+  return m;
+}
+
+// n_mode_product (tensor.hpp:128-135)
+std::vector<cd> n_mode(const std::vector<cd>& t, I64 d[3], const Mat& u, int mode) {
+  Mat un = unfold(t.data(), d, mode);
+  Mat prod = matmul(u, un);
+  I64 od[3] = {d[0], d[1], d[2]};
+  od[mode - 1] = u.rows;
+  std::vector<cd> out(static_cast<size_t>(od[0] * od[1] * od[2]));
+  const I64 n1 = od[0], n2 = od[1], n3 = od[2];
+  for (I64 k = 0; k < n3; ++k)
+    for (I64 j = 0; j < n2; ++j)
+      for (I64 i = 0; i < n1; ++i) {
+        cd v;
+        if (mode == 1) v = prod(i, j + n2 * k);
+        else if (mode == 2) v = prod(j, i + n1 * k);
+        else v = prod(k, i + n1 * j);
+        out[static_cast<size_t>(i + n1 * (j + n2 * k))] = v;
+      }
+  d[0] = od[0];
+  d[1] = od[1];
+  d[2] = od[2];
+  return out;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* orc_last_error(void) { return g_err.c_str(); }
+void orc_set_threads(int nthreads) { g_threads = std::max(1, nthreads); }
+
+int orc_random_tensor(int64_t n1, int64_t n2, int64_t n3, uint64_t seed, double* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    cd* o = reinterpret_cast<cd*>(out);
+    for (I64 n = 0; n < n1 * n2 * n3; ++n) o[n] = cd(gauss(rng), gauss(rng));
+  });
+}
+
+int orc_random_matrix(int64_t rows, int64_t cols, uint64_t seed, double* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    cd* o = reinterpret_cast<cd*>(out);
+    for (I64 j = 0; j < cols; ++j)
+      for (I64 i = 0; i < rows; ++i) o[i + rows * j] = cd(gauss(rng), gauss(rng));
+  });
+}
+
+int orc_gauss_stream(uint64_t seed, int64_t count, double* out) {
+  return guard([&] {
+    std::mt19937_64 rng(seed);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    cd* o = reinterpret_cast<cd*>(out);
+    for (I64 n = 0; n < count; ++n) o[n] = cd(gauss(rng), gauss(rng));
+  });
+}
+
+int orc_fft1(double* v, int64_t n, int inverse) {
+  return guard([&] {
+    std::vector<cd> work;
+    cd* p = reinterpret_cast<cd*>(v);
+    fft_line(p, n, inverse != 0, work);
+    if (inverse)
+      for (I64 i = 0; i < n; ++i) p[i] /= static_cast<double>(n);
+  });
+}
+
+int orc_fft3(double* t, int64_t n1, int64_t n2, int64_t n3, int inverse) {
+  return guard([&] { fft3(reinterpret_cast<cd*>(t), n1, n2, n3, inverse != 0); });
+}
+
+int orc_circulant_embed(const double* t, const int64_t dims[3], const int sign[3], double* out) {
+  return guard([&] {
+    circulant_embed(reinterpret_cast<const cd*>(t), dims, sign, reinterpret_cast<cd*>(out));
+  });
+}
+
+int orc_transform_factor(const double* u, int64_t n, int64_t r, int sign, double* out) {
+  return guard([&] {
+    transform_factor(reinterpret_cast<const cd*>(u), n, r, sign, reinterpret_cast<cd*>(out));
+  });
+}
+
+int orc_component_table(int kind, int basis, int* ncomp, int* comps, int* parity, int* nblock,
+                        int* blocks) {
+  return guard([&] {
+    std::vector<Comp> cs;
+    std::vector<Block> bs;
+    build_table(kind, basis, cs, bs);
+    *ncomp = static_cast<int>(cs.size());
+    *nblock = static_cast<int>(bs.size());
+    for (size_t i = 0; i < cs.size(); ++i) {
+      if (comps) {
+        comps[4 * i] = cs[i].q;
+        comps[4 * i + 1] = cs[i].qp;
+        comps[4 * i + 2] = cs[i].l;
+        comps[4 * i + 3] = cs[i].lp;
+      }
+      if (parity)
+        for (int a = 0; a < 3; ++a) parity[3 * i + static_cast<size_t>(a)] = cs[i].par[a];
+    }
+    if (blocks)
+      for (size_t i = 0; i < bs.size(); ++i) {
+        blocks[4 * i] = bs[i].t;
+        blocks[4 * i + 1] = bs[i].s;
+        blocks[4 * i + 2] = bs[i].c;
+        blocks[4 * i + 3] = bs[i].dsign;
+      }
+  });
+}
+
+int orc_decompress_tucker(const int64_t edims[3], const int64_t ranks[3], const double* core,
+                          const double* u1, const double* u2, const double* u3, double* dst) {
+  return guard([&] {
+    decompress_tucker(edims, ranks, reinterpret_cast<const cd*>(core),
+                      reinterpret_cast<const cd*>(u1), reinterpret_cast<const cd*>(u2),
+                      reinterpret_cast<const cd*>(u3), reinterpret_cast<cd*>(dst));
+  });
+}
+
+int orc_apply_operator_tucker(int kind, int basis, const int64_t grid[3], const int64_t* ranks,
+                              const double* const* cores, const double* const* u1s,
+                              const double* const* u2s, const double* const* u3s,
+                              const double* x, double* y) {
+  return guard([&] {
+    TuckerIn tk{ranks, cores, u1s, u2s, u3s};
+    apply_operator(kind, basis, grid, &tk, nullptr, reinterpret_cast<const cd*>(x),
+                   reinterpret_cast<cd*>(y));
+  });
+}
+
+int orc_apply_operator_dense(int kind, int basis, const int64_t grid[3],
+                             const double* const* spectra, const double* x, double* y) {
+  return guard([&] {
+    apply_operator(kind, basis, grid, nullptr, spectra, reinterpret_cast<const cd*>(x),
+                   reinterpret_cast<cd*>(y));
+  });
+}
+
+int orc_dense_spectrum(const double* t, const int64_t dims[3], const int sign[3], double* out) {
+  return guard([&] {
+    cd* o = reinterpret_cast<cd*>(out);
+    circulant_embed(reinterpret_cast<const cd*>(t), dims, sign, o);
+    fft3(o, 2 * dims[0], 2 * dims[1], 2 * dims[2], false);
+  });
+}
+
+int orc_dense_bttb(int kind, int basis, const int64_t dims[3], const double* const* tensors,
+                   double* out) {
+  return guard([&] {
+    std::vector<Comp> comps;
+    std::vector<Block> blocks;
+    build_table(kind, basis, comps, blocks);
+    const int S = ncur(basis);
+    const I64 n1 = dims[0], n2 = dims[1], n3 = dims[2], nv = n1 * n2 * n3;
+    const I64 ld = S * nv;
+    cd* a = reinterpret_cast<cd*>(out);
+    std::fill(a, a + ld * ld, cd(0.0));
+    for (const Block& b : blocks) {
+      const Comp& c = comps[static_cast<size_t>(b.c)];
+      const cd* t = reinterpret_cast<const cd*>(tensors[b.c]);
+      for (I64 k = 0; k < n3; ++k)
+        for (I64 j = 0; j < n2; ++j)
+          for (I64 i = 0; i < n1; ++i) {
+            const I64 row = i + n1 * (j + n2 * k);
+            for (I64 kp = 0; kp < n3; ++kp)
+              for (I64 jp = 0; jp < n2; ++jp)
+                for (I64 ip = 0; ip < n1; ++ip) {
+                  const I64 coln = ip + n1 * (jp + n2 * kp);
+                  I64 oi = ip - i, oj = jp - j, ok = kp - k;
+                  double sign = 1.0;
+                  if (oi < 0) { oi = -oi; sign *= c.par[0]; }
+                  if (oj < 0) { oj = -oj; sign *= c.par[1]; }
+                  if (ok < 0) { ok = -ok; sign *= c.par[2]; }
+                  a[(b.t * nv + row) + ld * (b.s * nv + coln)] +=
+                      static_cast<double>(b.dsign) * sign * t[oi + n1 * (oj + n2 * ok)];
+                }
+          }
+    }
+  });
+}
+
+int orc_apply_system_tucker(int basis, const int64_t grid[3], const int64_t* ranks,
+                            const double* const* cores, const double* const* u1s,
+                            const double* const* u2s, const double* const* u3s,
+                            const double* eps_r, double inv_v, const double* x, double* y) {
+  return guard([&] {
+    TuckerIn tk{ranks, cores, u1s, u2s, u3s};
+    apply_system(basis, grid, tk, reinterpret_cast<const cd*>(eps_r), inv_v,
+                 reinterpret_cast<const cd*>(x), reinterpret_cast<cd*>(y));
+  });
+}
+
+static void fill_gmres_out(const GmresOut& g, int* iterations, int* converged,
+                           double* final_rel_res, double* history, int history_cap,
+                           int* history_len) {
+  if (iterations) *iterations = g.iterations;
+  if (converged) *converged = g.converged ? 1 : 0;
+  if (final_rel_res) *final_rel_res = g.final_rel;
+  if (history_len) *history_len = static_cast<int>(g.history.size());
+  if (history)
+    for (int i = 0; i < history_cap && i < static_cast<int>(g.history.size()); ++i)
+      history[i] = g.history[static_cast<size_t>(i)];
+}
+
+int orc_gmres(orc_linmap apply, void* apply_ctx, orc_linmap precond, void* precond_ctx,
+              int64_t n, const double* rhs, const double* x0, double tol, int inner, int outer,
+              double* x, int* iterations, int* converged, double* final_rel_res,
+              double* history, int history_cap, int* history_len) {
+  return guard([&] {
+    VecFn ap = [&](const cd* a, cd* b) {
+      apply(reinterpret_cast<const double*>(a), reinterpret_cast<double*>(b), apply_ctx);
+    };
+    VecFn pc = [&](const cd* a, cd* b) {
+      precond(reinterpret_cast<const double*>(a), reinterpret_cast<double*>(b), precond_ctx);
+    };
+    GmresOut g = gmres(ap, precond ? &pc : nullptr, n, reinterpret_cast<const cd*>(rhs),
+                       reinterpret_cast<const cd*>(x0), tol, inner, outer, reinterpret_cast<cd*>(x));
+    fill_gmres_out(g, iterations, converged, final_rel_res, history, history_cap, history_len);
+  });
+}
+
+int orc_gmres_system_tucker(int basis, const int64_t grid[3], const int64_t* ranks,
+                            const double* const* cores, const double* const* u1s,
+                            const double* const* u2s, const double* const* u3s,
+                            const double* eps_r, double inv_v, const double* rhs,
+                            const double* x0, double tol, int inner, int outer, double* x,
+                            int* iterations, int* converged, double* final_rel_res,
+                            double* history, int history_cap, int* history_len) {
+  return guard([&] {
+    TuckerIn tk{ranks, cores, u1s, u2s, u3s};
+    const I64 n = static_cast<I64>(ncur(basis)) * grid[0] * grid[1] * grid[2];
+    VecFn ap = [&](const cd* a, cd* b) {
+      apply_system(basis, grid, tk, reinterpret_cast<const cd*>(eps_r), inv_v, a, b);
+    };
+    GmresOut g = gmres(ap, nullptr, n, reinterpret_cast<const cd*>(rhs),
+                       reinterpret_cast<const cd*>(x0), tol, inner, outer, reinterpret_cast<cd*>(x));
+    fill_gmres_out(g, iterations, converged, final_rel_res, history, history_cap, history_len);
+  });
+}
+
+int orc_truncated_svd_values(const double* m, int64_t rows, int64_t cols, double tol, int rule,
+                             int64_t* rank, double* sigma) {
+  return guard([&] {
+    if (tol < 0.0) throw invalid("truncated_svd: tol must be >= 0");
+    Mat a(rows, cols);
+    std::copy(reinterpret_cast<const cd*>(m), reinterpret_cast<const cd*>(m) + rows * cols,
+              a.a.begin());
+    Mat u, v;
+    std::vector<double> s;
+    thin_svd(a, u, s, v);
+    *rank = truncation_rank(s, tol, rule);
+    if (sigma)
+      for (size_t i = 0; i < s.size(); ++i) sigma[i] = s[i];
+  });
+}
+
+int orc_hosvd(const double* t, const int64_t dims[3], double tol, int rule, int64_t ranks[3],
+              double* core, double* u1, double* u2, double* u3) {
+  return guard([&] {
+    if (dims[0] <= 0 || dims[1] <= 0 || dims[2] <= 0)
+      throw invalid("hosvd: degenerate tensor dimensions");
+    if (tol < 0.0) throw invalid("truncated_svd: tol must be >= 0");
+    const cd* tc = reinterpret_cast<const cd*>(t);
+    Mat factors[3];
+    for (int q = 0; q < 3; ++q) {
+      Mat m = unfold(tc, dims, q + 1);
+      Mat u, v;
+      std::vector<double> s;
+      thin_svd(m, u, s, v);
+      const I64 r = truncation_rank(s, tol, rule);
+      factors[q] = Mat(u.rows, r);
+      for (I64 j = 0; j < r; ++j)
+        for (I64 i = 0; i < u.rows; ++i) factors[q](i, j) = u(i, j);
+      ranks[q] = r;
+    }
+    if (!core) return;
+    std::vector<cd> c(tc, tc + dims[0] * dims[1] * dims[2]);
+    I64 d[3] = {dims[0], dims[1], dims[2]};
+    for (int q = 0; q < 3; ++q) c = n_mode(c, d, adjoint(factors[q]), q + 1);
+    std::copy(c.begin(), c.end(), reinterpret_cast<cd*>(core));
+    double* us[3] = {u1, u2, u3};
+    for (int q = 0; q < 3; ++q)
+      if (us[q]) std::copy(factors[q].a.begin(), factors[q].a.end(), reinterpret_cast<cd*>(us[q]));
+  });
+}
+
+}  // extern "C"
