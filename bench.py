@@ -1,0 +1,347 @@
+#!/usr/bin/env python3
+"""Benchmark: Tucker-compressed VIE matvecs/s at the 1 mm head grid (BASELINE.json).
+
+One step = one apply_operator (vie_matvec) of the PWL N operator (60 unique
+Tucker components, rank 25, 12 current components) on the 200 x 240 x 200 grid
+(embedded 400 x 480 x 400) with synthetic spatial-domain Tucker forms
+ and a synthetic current; inputs (1.84 GB) exceed the 126 MB L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Under torchrun (N > 1) the components are sharded over ranks and the partial
+output currents are summed with an NCCL all-reduce (north star); the time is
+the max over ranks.  --impl reference times the CPU oracle (restatement of the
+reference, which cannot be compiled here) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (grid, basis, rank)
+    "head_1mm": ((200, 240, 200), 1, 25),     # BASELINE configs[3] (headline)
+    "head_2mm": ((100, 120, 100), 1, 25),     # configs[2]
+    "cube_64": ((64, 64, 64), 1, 25),         # configs[1]
+    "cube_32": ((32, 32, 32), 1, 25),         # configs[0]
+    "head_1mm_pwc": ((200, 240, 200), 0, 25),
+}
+METRIC = "compressed-VIE matvecs/s at 1mm head grid; achieved HBM GB/s vs B200 peak"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="head_1mm", choices=sorted(CONFIGS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def bytes_model(grid, basis, nc):
+    """Algorithmic HBM bytes; B = 16 bytes per complex."""
+    n1, n2, n3 = grid
+    nv = n1 * n2 * n3
+    ne = 8 * nv
+    S = 3 if basis == 0 else 12
+    noct = (n1 + 1) * (n2 + 1) * (n3 + 1)
+    return {
+        "matvec_staged": 16 * (2 * S) * (nv + 2 * ne),  # SURVEY bytes_mv
+        # per kernel of this implementation (read + write of its operands)
+        "row_fwd": 16 * S * (nv + 2 * nv),
+        "col_fwd": 16 * S * (2 * nv + 4 * nv),
+        "decomp": 16 * nc * noct,  # octant spectra written (Z and forms negligible)
+        "pencil": 16 * (2 * S) * 4 * nv + 16 * nc * noct,  # x^/y^ slabs + octant spectra read once
+        "col_inv": 16 * S * (4 * nv + 2 * nv),
+        "row_inv": 16 * S * (2 * nv + nv),
+    }
+
+
+STAGES = ["row_fwd", "col_fwd", "decomp", "pencil", "col_inv", "row_inv"]
+
+
+def flops_model(grid, basis, nc, rank):
+    n1, n2, n3 = grid
+    noct = (n1 + 1) * (n2 + 1) * (n3 + 1)
+    nb = 9 if basis == 0 else 144
+    ne = 8 * n1 * n2 * n3
+    return {"decomp": 8.0 * nc * rank * noct, "hadamard": 8.0 * nb * ne}
+
+
+# ----------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self, gpu_index=0):
+        self.samples = []
+        self.proc = None
+        self.gpu_index = gpu_index
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu_index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [s for s in self.samples if len(s) >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def measured_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ CPU sample
+def cpu_sample(grid, basis, rank, threads, seed=1234):
+    """Bounded sample of the oracle matvec: one full forward 3D FFT of the
+    embedded grid and one component's decompress + multiply-accumulate, scaled
+    to one matvec (2S FFTs + NC components).  Returns (matvecs/s, info)."""
+    from oracle import oracle as orc
+    from tests.helpers import spatial_tucker_forms, fourier_forms
+
+    orc.set_threads(threads)
+    n1, n2, n3 = grid
+    ed = (2 * n1, 2 * n2, 2 * n3)
+    S = 3 if basis == 0 else 12
+    comps, par, blocks = orc.component_table(0, basis)
+    nc = len(comps)
+    rng = np.random.default_rng(seed)
+    ne = int(np.prod(ed))
+    v = (rng.standard_normal(ne) + 1j * rng.standard_normal(ne)).astype(np.complex128)
+    t0 = time.perf_counter()
+    orc.fft3(v, ed)
+    t_fft = time.perf_counter() - t0
+    spatial, par = spatial_tucker_forms(0, basis, grid, rank, seed)
+    f = fourier_forms(spatial[:1], par[:1])[0]
+    t0 = time.perf_counter()
+    buf = orc.decompress_tucker(ed, f)
+    nblk = int(np.sum(blocks[:, 2] == 0))
+    acc = np.zeros(ne, np.complex128)
+    for _ in range(nblk):  # mac_elementwise per block of the component
+        acc += buf * v
+    t_comp = time.perf_counter() - t0
+    per_mv = 2 * S * t_fft + nc * t_comp
+    info = {"t_fft3_s": round(t_fft, 3), "t_component_s": round(t_comp, 3), "extrapolated_matvec_s": round(per_mv, 2),
+            "sample": f"1 forward 3D FFT of the {ed[0]}x{ed[1]}x{ed[2]} embedded grid + 1 of {nc} components' "
+                      f"decompress+MAC, scaled to {2 * S} FFTs + {nc} components"}
+    return 1.0 / per_mv, info
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    grid, basis, r = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    vals = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        v, info = cpu_sample(grid, basis, r, threads, seed=1234 + i)
+        if i >= args.warmup:
+            vals.append(v)
+    val = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "matvecs/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / val, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
+        "config": {"workload": f"{args.config}: PWL N operator apply, grid {grid}, rank {r}", "grid": grid,
+                   "basis": "PWL" if basis else "PWC", "rank": r},
+        "cpu_baseline": {"value": val, "unit": "matvecs/s", "cores": threads, "kind": "port",
+                         "sample": info["sample"]},
+        "e2e": {"value": val, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "detail": info,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ B200 arm
+def run_b200(args):
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_1811_00484_b200 as vie
+    from tests.helpers import spatial_tucker_forms
+
+    grid, basis, r = CONFIGS[args.config]
+    S = vie.ncur(basis)
+    nv = int(np.prod(grid))
+    n = S * nv
+    comps, _, _ = vie.component_table(0, basis)
+    nc = len(comps)
+    mine = [c for c in range(nc) if c % world == rank]
+    dft = vie.DftService(local)
+    spatial, par = spatial_tucker_forms(0, basis, grid, r, 1234)
+    forms = [vie.TuckerForm(dft, grid, spatial[c][0], spatial[c][1], par[c]) for c in mine]
+    op = vie.build_operator_spectra(0, basis, grid, [comps[c] for c in mine], forms, dft)
+    g = torch.Generator(device="cuda").manual_seed(2024)
+    x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        vie.apply_operator(op, x, out=y, stream=stream.cuda_stream)
+        if dist is not None:
+            dist.all_reduce(y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = 1000.0 / ms  # matvecs/s (one matvec per step for the whole job)
+
+    # per-kernel device times over a profiled pass (CUDA events on the op stream)
+    op.set_profiling(True)
+    stage_ms = np.zeros(6)
+    nprof = max(3, min(args.steps, 10))
+    for _ in range(nprof):
+        vie.apply_operator(op, x, out=y, stream=stream.cuda_stream)
+        launches, st = op.last_stats()
+        stage_ms += np.array(st[:6])
+    stage_ms /= nprof
+    op.set_profiling(False)
+    bm = bytes_model(grid, basis, len(mine))
+    peak, peak_kind = measured_peak()
+    dom = STAGES[int(np.argmax(stage_ms))]
+    achieved = bm[dom] / (stage_ms[STAGES.index(dom)] * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(args.config, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    # end-to-end through the reference-facing C-ABI call with pinned host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        xh = torch.empty(n, dtype=torch.complex128).pin_memory()
+        yh = torch.empty(n, dtype=torch.complex128).pin_memory()
+        xh.copy_(x.cpu())
+        L = vie.lib()
+        for _ in range(2):
+            assert L.vie_matvec_host(op.handle, xh.data_ptr(), yh.data_ptr()) == 0
+        ne2e = max(2, min(args.steps, 5))
+        t0 = time.perf_counter()
+        for _ in range(ne2e):
+            assert L.vie_matvec_host(op.handle, xh.data_ptr(), yh.data_ptr()) == 0
+        t_e2e = (time.perf_counter() - t0) / ne2e
+        e2e = {"value": 1.0 / t_e2e, "unit": "matvecs/s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        v, info = cpu_sample(grid, basis, r, threads)
+        cpu = {"value": v, "unit": "matvecs/s", "cores": threads, "kind": "port", "sample": info["sample"],
+               "detail": info}
+
+    fl = flops_model(grid, basis, nc, r)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (spatial-domain Tucker forms, CN(0,1), parity rows zeroed; CN(0,1) currents)",
+            "config": {"workload": f"{args.config}: PWL N-operator apply_operator (vie_matvec), grid {grid}, "
+                                   f"embedded {tuple(2 * d for d in grid)}, {nc} Tucker components rank {r}, "
+                                   f"{S} currents", "grid": list(grid), "basis": "PWL" if basis else "PWC",
+                       "rank": r, "components": nc, "parallelism": f"components sharded x{world}" if world > 1 else "1 GPU",
+                       "l2": "inputs 1.8 GB > 126 MB L2 (no flush needed)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "algorithmic_bytes_per_launch": bm[dom]},
+            "staged_model": {"bytes_per_matvec": bm["matvec_staged"],
+                             "achieved_gbs": bm["matvec_staged"] / (ms * 1e-3) / 1e9,
+                             "frac": bm["matvec_staged"] / (ms * 1e-3) / 1e9 / peak},
+            "stage_ms": {k: round(float(v), 4) for k, v in zip(STAGES, stage_ms)},
+            "fp64_gflop": {k: v / 1e9 for k, v in fl.items()},
+            "gpu_launches": 7 * args.steps,
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

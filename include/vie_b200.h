@@ -1,0 +1,119 @@
+/*
+ * vie_b200.h -- C ABI of the B200-native Tucker-compressed VIE matvec.
+ *
+ * Drop-in boundary for the reference's operator API (header-only C++ library
+ * /root/reference/proj/include/vie).  Each entry point names the reference
+ * interface it replaces.  All complex data is interleaved double (re, im),
+ * i.e. std::complex<double> / double2, in the reference layouts:
+ *   Tensor3:        flat = i + n1*(j + n2*k)                 tensor.hpp:17-21
+ *   factor matrix:  column-major, rows x cols                tensor.hpp:15-17
+ *   current field:  component-major blocks of N_v            grid.hpp:122-127
+ *                   PWC: 3 blocks (q); PWL: 12 blocks (s = 4q + l)
+ * Pointers are DEVICE pointers unless the name ends in _host.  `stream` is a
+ * cudaStream_t passed as void* (NULL = the context's stream).
+ *
+ * Every function returns VIE_OK (0) or an error code, and sets a thread-local
+ * message readable with vie_last_error().  VIE_EINVAL corresponds to the
+ * reference's std::invalid_argument (operator.hpp:277-284, solver.hpp:37-39).
+ * GMRES non-convergence is a flag, not an error (solver.hpp:28-33).
+ */
+#ifndef VIE_B200_H
+#define VIE_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VIE_OK 0
+#define VIE_EINVAL 1
+#define VIE_ENOMEM 2
+#define VIE_ECUDA 3
+#define VIE_ENCCL 4
+
+#define VIE_KIND_N 0 /* OperatorKind::N  (components.hpp:14) */
+#define VIE_KIND_K 1 /* OperatorKind::K                      */
+#define VIE_BASIS_PWC 0 /* BasisOrder::PWC (grid.hpp:103)    */
+#define VIE_BASIS_PWL 1 /* BasisOrder::PWL (generalised) */
+#define VIE_RULE_SIGMA_MAX 0 /* TruncationRule (decomp.hpp:23) */
+#define VIE_RULE_ENERGY 1
+
+typedef struct vie_ctx_s* vie_ctx;       /* device, stream, FFT plan cache   (fft.hpp DftService) */
+typedef struct vie_tucker_s* vie_tucker; /* device-resident Fourier Tucker form (decomp.hpp:123 + operator.hpp:76) */
+typedef struct vie_op_s* vie_op;         /* immutable device operator        (operator.hpp:120 EmbeddedSpectrum) */
+
+const char* vie_last_error(void);
+const char* vie_version(void);
+
+/* DftService construction (fft.hpp:13-21): binds a CUDA device. */
+int vie_ctx_create(vie_ctx* out, int device);
+int vie_ctx_destroy(vie_ctx ctx);
+int vie_ctx_sync(vie_ctx ctx);
+
+/* tucker_compress = hosvd + transform_factors (decomp.hpp:160-176,
+ * operator.hpp:76-90): HOSVD of a spatial Toeplitz-defining tensor (host
+ * buffer, n1*n2*n3 complex), then embedding + 1D DFT of every factor column
+ * on the device.  sign[3] = component parity (components.hpp:51-65).
+ * rule: VIE_RULE_*.  ranks_out receives (r1, r2, r3).                        */
+int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3],
+                        double tol, int rule, vie_tucker* out, int64_t ranks_out[3]);
+
+/* Tucker form from given factors (the synthetic-input path, no SVD).
+ * domain 0: spatial factors U_q (n_q x r_q, host) -> transform_factors on device
+ * domain 1: Fourier factors (2n_q x r_q, host) as returned by transform_factors
+ * core_host: r1*r2*r3.  Rows that the parity forces to zero (row 0 of an odd
+ * axis) must be zero to 1e-12 relative; VIE_EINVAL otherwise.               */
+int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ranks[3],
+                            const double* core_host, const double* u1_host, const double* u2_host,
+                            const double* u3_host, const int sign[3], int domain, vie_tucker* out);
+int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]);
+int vie_tucker_destroy(vie_tucker t);
+
+/* Canonical component table of (kind, basis): components.hpp:71-92 for PWC,
+ * its PWL generalisation otherwise.  comps: ncomp x 4 ints (q, q', l, l');
+ * parity: ncomp x 3; blocks: nblock x 4 (target, source, comp, dense_sign).
+ * Any output pointer may be NULL (counts only).                             */
+int vie_component_table(int kind, int basis, int* ncomp, int* comps, int* parity, int* nblock,
+                        int* blocks);
+
+/* build_operator_spectra (operator.hpp:144-177) from compressed forms.
+ * comp: ncomp x 4 ints (q, q', l, l') naming which canonical component each
+ * form holds (any order, each at most once; absent components are zero, which
+ * is how components are sharded over GPUs).  Forms are copied.               */
+int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int ncomp,
+                  const int* comp, const vie_tucker* forms, vie_op* out);
+int vie_op_destroy(vie_op op);
+/* sizes: n_cur (= current components S), n_vox (= N_v), bytes of workspace   */
+int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_bytes);
+
+/* apply_operator (operator.hpp:273-382), strategy HosvdDecompress semantics:
+ * y = A x for device vectors of n_cur * n_vox complex values.                */
+int vie_matvec(vie_op op, const double* x, double* y, void* stream);
+/* Same call with HOST buffers (H2D, matvec, D2H) -- the reference-facing call. */
+int vie_matvec_host(vie_op op, const double* x_host, double* y_host);
+
+/* apply_system (solver.hpp:183-200): y = eps_r*g*x - (eps_r - 1)*inv_v*(N x)
+ * with g = 1 (PWC; PWL constant) or 1/12 (PWL linear), eps_r: n_vox complex.
+ * diag_term = 0 omits eps_r*g*x (component-sharded ranks other than 0).      */
+int vie_system_matvec(vie_op op, const double* eps_r, double inv_v, const double* x, double* y,
+                      int diag_term, void* stream);
+
+/* gmres (solver.hpp:34-142) on apply_system, device resident: restarted
+ * GMRES(inner), modified Gram-Schmidt, complex Givens rotations.  x0 may be
+ * NULL (zero start).  history_host receives |g_{j+1}|/||b|| per iteration
+ * (up to history_cap values; *history_len = total count).                   */
+int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* rhs,
+                    const double* x0, double tol, int inner, int outer, double* x, int* iterations,
+                    double* final_rel_res, double* history_host, int history_cap, int* history_len,
+                    int* converged);
+
+/* Timing helpers for the bench: number of kernels the last vie_matvec
+ * launched, and per-stage device times (ms) of the last vie_matvec when
+ * profiling was enabled with vie_op_set_profiling(op, 1).                   */
+int vie_op_set_profiling(vie_op op, int enable);
+int vie_op_last_stats(vie_op op, int* launches, double* stage_ms /* [8] */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

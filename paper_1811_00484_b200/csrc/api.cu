@@ -1,0 +1,780 @@
+// api.cu -- C ABI (include/vie_b200.h): context + FFT plan cache, device
+// Tucker forms, the operator and its matvec pipeline, device-resident GMRES.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/vie_b200.h"
+#include "kernels.cuh"
+
+using vie::CompDev;
+using vie::FftPlan;
+using vie::Geom;
+using cd = std::complex<double>;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Invalid : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return VIE_OK;
+  } catch (const Invalid& e) {
+    g_err = e.what();
+    return VIE_EINVAL;
+  } catch (const vie::CudaError& e) {
+    g_err = e.what();
+    return e.code == cudaErrorMemoryAllocation ? VIE_ENOMEM : VIE_ECUDA;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return VIE_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VIE_EINVAL;
+  }
+}
+
+template <class T>
+T* dev_alloc(size_t count) {
+  void* p = nullptr;
+  if (count == 0) return nullptr;
+  VIE_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+  return static_cast<T*>(p);
+}
+void dev_free(void* p) {
+  if (p) cudaFree(p);
+}
+
+struct PlanHolder {
+  FftPlan plan{};
+  double2* tw = nullptr;
+  int* slot = nullptr;
+  vie::StageDesc* st = nullptr;
+  ~PlanHolder() {
+    dev_free(tw);
+    dev_free(slot);
+    dev_free(st);
+  }
+};
+
+}  // namespace
+
+struct vie_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  std::map<int, std::unique_ptr<PlanHolder>> plans;
+};
+
+struct vie_tucker_s {
+  vie_ctx ctx = nullptr;
+  int64_t dims[3] = {0, 0, 0};
+  int64_t ranks[3] = {0, 0, 0};
+  int sign[3] = {1, 1, 1};
+  double2* core = nullptr;   // r1*r2*r3
+  double2* uo[3] = {nullptr, nullptr, nullptr};  // (n_q + 1) x r_q octant rows
+  ~vie_tucker_s() {
+    dev_free(core);
+    for (auto* u : uo) dev_free(u);
+  }
+};
+
+struct vie_op_s {
+  vie_ctx ctx = nullptr;
+  int kind = 0, basis = 0;
+  Geom g{};
+  int rmax = 0;
+  uint64_t active = 0;
+  std::vector<CompDev> comps_host;
+  CompDev* comps_dev = nullptr;
+  double2* forms = nullptr;
+  double2* Z = nullptr;
+  double2* Shat = nullptr;
+  double2* A = nullptr;
+  double2* B = nullptr;
+  int64_t ws_bytes = 0;
+  FftPlan P1{}, P2{}, P3{};
+  // host-buffer staging (vie_matvec_host)
+  double2* hx = nullptr;
+  double2* hy = nullptr;
+  // GMRES state
+  int g_inner = 0;
+  double2* V = nullptr;
+  double2* tmp = nullptr;
+  double2* scal = nullptr;  // device scalars
+  double2* red_partials = nullptr;
+  unsigned int* red_counter = nullptr;
+  // stats
+  int profiling = 0;
+  int last_launches = 0;
+  double stage_ms[8] = {0};
+  cudaEvent_t ev[8] = {};
+  ~vie_op_s() {
+    for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
+                    static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B),
+                    static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(V),
+                    static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
+                    static_cast<void*>(red_counter)})
+      dev_free(p);
+    for (auto& e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- FFT plans
+const FftPlan& get_plan(vie_ctx ctx, int n) {
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  auto it = ctx->plans.find(n);
+  if (it != ctx->plans.end()) return it->second->plan;
+  if (n < 2 || (n & 1)) throw Invalid("FFT plan: embedded length must be even and >= 2");
+  std::vector<int> rad;
+  int rest = n;
+  rad.push_back(rest % 4 == 0 ? 4 : 2);  // even first radix: pad/crop pruning
+  rest /= rad.back();
+  while (rest % 8 == 0) { rad.push_back(8); rest /= 8; }
+  while (rest % 4 == 0) { rad.push_back(4); rest /= 4; }
+  while (rest % 2 == 0) { rad.push_back(2); rest /= 2; }
+  for (int p : {3, 5, 7})
+    while (rest % p == 0) { rad.push_back(p); rest /= p; }
+  if (rest != 1)
+    throw Invalid("FFT plan: embedded length " + std::to_string(n) + " has a prime factor > 7");
+  if (static_cast<int>(rad.size()) > vie::kMaxStages) throw Invalid("FFT plan: too many stages");
+  auto h = std::make_unique<PlanHolder>();
+  FftPlan& P = h->plan;
+  P.n = n;
+  P.nst = static_cast<int>(rad.size());
+  std::vector<vie::StageDesc> sd(rad.size());
+  int L = n;
+  for (int s = 0; s < P.nst; ++s) {
+    sd[s].radix = rad[s];
+    sd[s].L = L;
+    sd[s].M = L / rad[s];
+    sd[s].tws = n / L;
+    sd[s].div_nbf.init(static_cast<uint32_t>(n / rad[s]));
+    sd[s].div_M.init(static_cast<uint32_t>(sd[s].M));
+    L = sd[s].M;
+  }
+  std::vector<double2> tw(static_cast<size_t>(n));
+  for (int e = 0; e < n; ++e) {
+    const long double a = -2.0L * 3.14159265358979323846264338327950288L * e / n;
+    tw[static_cast<size_t>(e)] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(sinl(a)));
+  }
+  std::vector<int> slot(static_cast<size_t>(n));
+  for (int f = 0; f < n; ++f) {
+    int rem = f, sl = 0;
+    for (int s = 0; s < P.nst; ++s) {
+      sl += (rem % sd[s].radix) * sd[s].M;
+      rem /= sd[s].radix;
+    }
+    slot[static_cast<size_t>(f)] = sl;
+  }
+  h->tw = dev_alloc<double2>(static_cast<size_t>(n));
+  h->slot = dev_alloc<int>(static_cast<size_t>(n));
+  h->st = dev_alloc<vie::StageDesc>(sd.size());
+  VIE_CUDA_CHECK(cudaMemcpy(h->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
+  VIE_CUDA_CHECK(cudaMemcpy(h->slot, slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+  VIE_CUDA_CHECK(cudaMemcpy(h->st, sd.data(), sizeof(vie::StageDesc) * sd.size(), cudaMemcpyHostToDevice));
+  P.tw = h->tw;
+  P.slot = h->slot;
+  P.st = h->st;
+  const FftPlan& ref = h->plan;
+  ctx->plans[n] = std::move(h);
+  return ref;
+}
+
+// ---------------------------------------------------------------- tables (host)
+struct HComp {
+  int q, qp, l, lp;
+  int par[3];
+};
+struct HBlock {
+  int t, s, c, dsign;
+};
+
+template <int KIND, int BASIS>
+void copy_table(std::vector<HComp>& cs, std::vector<HBlock>& bs) {
+  constexpr auto tb = vie::make_table<KIND, BASIS>();
+  for (const auto& c : tb.comps) cs.push_back({c.q, c.qp, c.l, c.lp, {c.p0, c.p1, c.p2}});
+  for (const auto& b : tb.blocks) {
+    const auto& c = tb.comps[static_cast<size_t>(b.c)];
+    bs.push_back({b.t, b.s, b.c, b.coef * c.p0 * c.p1 * c.p2});  // back to the dense sign
+  }
+}
+
+void host_table(int kind, int basis, std::vector<HComp>& cs, std::vector<HBlock>& bs) {
+  cs.clear();
+  bs.clear();
+  if (kind == 0 && basis == 0) copy_table<0, 0>(cs, bs);
+  else if (kind == 1 && basis == 0) copy_table<1, 0>(cs, bs);
+  else if (kind == 0 && basis == 1) copy_table<0, 1>(cs, bs);
+  else if (kind == 1 && basis == 1) copy_table<1, 1>(cs, bs);
+  else throw Invalid("component table: kind must be N/K and basis PWC/PWL");
+}
+
+// ---------------------------------------------------------------- matvec
+void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const double2* eps, double inv_v,
+                int diag) {
+  const Geom& g = op->g;
+  const double ne = 8.0 * g.n1 * static_cast<double>(g.n2) * g.n3;
+  if (op->profiling) {
+    for (auto& e : op->ev)
+      if (!e) VIE_CUDA_CHECK(cudaEventCreate(&e));
+    VIE_CUDA_CHECK(cudaEventRecord(op->ev[0], st));
+  }
+  int k = 1;
+  auto mark = [&] {
+    if (op->profiling) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
+  };
+  vie::launch_row_fwd(x, op->A, g, op->P1, st);
+  mark();
+  vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
+  mark();
+  vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
+  mark();
+  vie::launch_pencil(op->kind, op->basis, op->B, op->Shat, g, op->P3, op->active, st);
+  mark();
+  vie::launch_col_inv(op->B, op->A, g, op->P2, st);
+  mark();
+  // reference inverse3 divides by N_e (fft.hpp:34-37)
+  vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+  mark();
+  op->last_launches = 7;
+  if (op->profiling) {
+    VIE_CUDA_CHECK(cudaEventSynchronize(op->ev[k - 1]));
+    for (int i = 1; i < k; ++i) {
+      float ms = 0.f;
+      VIE_CUDA_CHECK(cudaEventElapsedTime(&ms, op->ev[i - 1], op->ev[i]));
+      op->stage_ms[i - 1] = ms;
+    }
+  }
+}
+
+cudaStream_t pick_stream(vie_op op, void* stream) {
+  return stream ? static_cast<cudaStream_t>(stream) : op->ctx->stream;
+}
+
+void check_cplx_finite_host(const double* p, size_t n, const char* what) {
+  for (size_t i = 0; i < 2 * n; ++i)
+    if (!std::isfinite(p[i])) throw Invalid(std::string(what) + ": non-finite value");
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+const char* vie_last_error(void) { return g_err.c_str(); }
+const char* vie_version(void) { return "vie-b200 0.1.0 (sm_100a)"; }
+
+int vie_ctx_create(vie_ctx* out, int device) {
+  return guard([&] {
+    if (!out) throw Invalid("vie_ctx_create: null output");
+    int ndev = 0;
+    VIE_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw Invalid("vie_ctx_create: no such CUDA device");
+    VIE_CUDA_CHECK(cudaSetDevice(device));
+    auto* c = new vie_ctx_s;
+    c->device = device;
+    VIE_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int vie_ctx_destroy(vie_ctx ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->plans.clear();
+    cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int vie_ctx_sync(vie_ctx ctx) {
+  return guard([&] {
+    if (!ctx) throw Invalid("vie_ctx_sync: null context");
+    VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int vie_component_table(int kind, int basis, int* ncomp, int* comps, int* parity, int* nblock, int* blocks) {
+  return guard([&] {
+    std::vector<HComp> cs;
+    std::vector<HBlock> bs;
+    host_table(kind, basis, cs, bs);
+    if (ncomp) *ncomp = static_cast<int>(cs.size());
+    if (nblock) *nblock = static_cast<int>(bs.size());
+    for (size_t i = 0; i < cs.size(); ++i) {
+      if (comps) {
+        comps[4 * i] = cs[i].q;
+        comps[4 * i + 1] = cs[i].qp;
+        comps[4 * i + 2] = cs[i].l;
+        comps[4 * i + 3] = cs[i].lp;
+      }
+      if (parity)
+        for (int a = 0; a < 3; ++a) parity[3 * i + static_cast<size_t>(a)] = cs[i].par[a];
+    }
+    if (blocks)
+      for (size_t i = 0; i < bs.size(); ++i) {
+        blocks[4 * i] = bs[i].t;
+        blocks[4 * i + 1] = bs[i].s;
+        blocks[4 * i + 2] = bs[i].c;
+        blocks[4 * i + 3] = bs[i].dsign;
+      }
+  });
+}
+
+int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ranks[3], const double* core_host,
+                            const double* u1_host, const double* u2_host, const double* u3_host, const int sign[3],
+                            int domain, vie_tucker* out) {
+  return guard([&] {
+    if (!ctx || !dims || !ranks || !core_host || !u1_host || !u2_host || !u3_host || !sign || !out)
+      throw Invalid("vie_tucker_from_factors: null argument");
+    if (domain != 0 && domain != 1) throw Invalid("vie_tucker_from_factors: domain must be 0 or 1");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    for (int q = 0; q < 3; ++q) {
+      if (dims[q] < 1) throw Invalid("vie_tucker_from_factors: dims must be >= 1");
+      if (ranks[q] < 1) throw Invalid("vie_tucker_from_factors: ranks must be >= 1");
+      if (sign[q] != 1 && sign[q] != -1) throw Invalid("vie_tucker_from_factors: sign must be +-1");
+    }
+    std::unique_ptr<vie_tucker_s> t(new vie_tucker_s);
+    t->ctx = ctx;
+    for (int q = 0; q < 3; ++q) {
+      t->dims[q] = dims[q];
+      t->ranks[q] = ranks[q];
+      t->sign[q] = sign[q];
+    }
+    const size_t ncore = static_cast<size_t>(ranks[0] * ranks[1] * ranks[2]);
+    check_cplx_finite_host(core_host, ncore, "vie_tucker_from_factors: core");
+    t->core = dev_alloc<double2>(ncore);
+    VIE_CUDA_CHECK(cudaMemcpy(t->core, core_host, ncore * sizeof(double2), cudaMemcpyHostToDevice));
+    const double* uh[3] = {u1_host, u2_host, u3_host};
+    for (int q = 0; q < 3; ++q) {
+      const int64_t n = dims[q], r = ranks[q];
+      t->uo[q] = dev_alloc<double2>(static_cast<size_t>((n + 1) * r));
+      const cd* u = reinterpret_cast<const cd*>(uh[q]);
+      if (domain == 0) {
+        check_cplx_finite_host(uh[q], static_cast<size_t>(n * r), "vie_tucker_from_factors: factor");
+        if (sign[q] < 0) {  // odd axis: the tensor (hence the factor) vanishes at offset 0
+          double nrm = 0.0, row0 = 0.0;
+          for (int64_t c = 0; c < r; ++c) {
+            for (int64_t i = 0; i < n; ++i) nrm += std::norm(u[i + n * c]);
+            row0 += std::norm(u[n * c]);
+          }
+          if (row0 > 1e-24 * nrm)
+            throw Invalid("vie_tucker_from_factors: odd-parity factor has a nonzero row 0");
+        }
+        double2* du = dev_alloc<double2>(static_cast<size_t>(n * r));
+        try {
+          VIE_CUDA_CHECK(cudaMemcpy(du, uh[q], sizeof(double2) * n * r, cudaMemcpyHostToDevice));
+          const FftPlan& P = get_plan(ctx, static_cast<int>(2 * n));
+          vie::launch_factor_transform(du, static_cast<int>(n), static_cast<int>(r), sign[q], P.tw, t->uo[q],
+                                       ctx->stream);
+          VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+        } catch (...) {
+          dev_free(du);
+          throw;
+        }
+        dev_free(du);
+      } else {
+        const int64_t m = 2 * n;
+        check_cplx_finite_host(uh[q], static_cast<size_t>(m * r), "vie_tucker_from_factors: factor");
+        double amax = 0.0, dev = 0.0;
+        for (int64_t c = 0; c < r; ++c)
+          for (int64_t p = 0; p < m; ++p) {
+            amax = std::max(amax, std::abs(u[p + m * c]));
+            const cd mir = u[(m - p) % m + m * c];
+            dev = std::max(dev, std::abs(u[p + m * c] - static_cast<double>(sign[q]) * mir));
+            if (p == 0 && sign[q] < 0) dev = std::max(dev, std::abs(u[p + m * c]));
+          }
+        if (dev > 1e-10 * std::max(amax, 1e-300))
+          throw Invalid("vie_tucker_from_factors: Fourier factor lacks the parity symmetry U(m-p) = sign U(p)");
+        std::vector<cd> oct(static_cast<size_t>((n + 1) * r));
+        for (int64_t c = 0; c < r; ++c)
+          for (int64_t p = 0; p <= n; ++p) oct[static_cast<size_t>(p + (n + 1) * c)] = u[p + m * c];
+        VIE_CUDA_CHECK(cudaMemcpy(t->uo[q], oct.data(), sizeof(double2) * oct.size(), cudaMemcpyHostToDevice));
+      }
+    }
+    *out = t.release();
+  });
+}
+
+int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]) {
+  return guard([&] {
+    if (!t || !ranks_out) throw Invalid("vie_tucker_ranks: null argument");
+    for (int q = 0; q < 3; ++q) ranks_out[q] = t->ranks[q];
+  });
+}
+
+int vie_tucker_destroy(vie_tucker t) {
+  return guard([&] {
+    if (t) {
+      cudaSetDevice(t->ctx->device);
+      delete t;
+    }
+  });
+}
+
+int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int ncomp, const int* comp,
+                  const vie_tucker* forms, vie_op* out) {
+  return guard([&] {
+    if (!ctx || !grid || !out) throw Invalid("vie_op_create: null argument");
+    if (ncomp < 1 || !comp || !forms) throw Invalid("build_operator_spectra: no components");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    std::vector<HComp> cs;
+    std::vector<HBlock> bs;
+    host_table(kind, basis, cs, bs);
+    for (int q = 0; q < 3; ++q)
+      if (grid[q] < 1) throw Invalid("vie_op_create: grid dims must be >= 1");
+    if (grid[0] * grid[1] * grid[2] > (int64_t(1) << 31) / 8)
+      throw Invalid("vie_op_create: grid too large for 32-bit spectral indexing");
+    std::unique_ptr<vie_op_s> op(new vie_op_s);
+    op->ctx = ctx;
+    op->kind = kind;
+    op->basis = basis;
+    Geom& g = op->g;
+    g.n1 = static_cast<int>(grid[0]);
+    g.n2 = static_cast<int>(grid[1]);
+    g.n3 = static_cast<int>(grid[2]);
+    g.m1 = 2 * g.n1;
+    g.m2 = 2 * g.n2;
+    g.m3 = 2 * g.n3;
+    g.S = basis == 0 ? 3 : 12;
+    g.NC = static_cast<int>(cs.size());
+    op->comps_host.assign(cs.size(), CompDev{1, 1, 1, 0, 0, 0, 0, 0, 0});
+    std::vector<const vie_tucker_s*> byc(cs.size(), nullptr);
+    for (int i = 0; i < ncomp; ++i) {
+      const int* e = comp + 4 * i;
+      int found = -1;
+      for (size_t c = 0; c < cs.size(); ++c)
+        if (cs[c].q == e[0] && cs[c].qp == e[1] && cs[c].l == e[2] && cs[c].lp == e[3]) found = static_cast<int>(c);
+      if (found < 0) throw Invalid("vie_op_create: component is not in the canonical table of (kind, basis)");
+      if (byc[static_cast<size_t>(found)]) throw Invalid("vie_op_create: duplicate component");
+      const vie_tucker_s* t = forms[i];
+      if (!t) throw Invalid("vie_op_create: null form");
+      if (t->ctx != ctx) throw Invalid("vie_op_create: form belongs to another context");
+      for (int q = 0; q < 3; ++q) {
+        if (t->dims[q] != grid[q]) throw Invalid("build_operator_spectra: inconsistent component dims");
+        if (t->sign[q] != cs[static_cast<size_t>(found)].par[q])
+          throw Invalid("vie_op_create: form parity differs from the component parity");
+      }
+      byc[static_cast<size_t>(found)] = t;
+    }
+    // pack forms: core, U1o, U2o, U3o per active component; Z offsets
+    int64_t off = 0, zoff = 0;
+    for (size_t c = 0; c < cs.size(); ++c) {
+      const vie_tucker_s* t = byc[c];
+      CompDev& d = op->comps_host[c];
+      if (!t) continue;
+      d.r1 = static_cast<int>(t->ranks[0]);
+      d.r2 = static_cast<int>(t->ranks[1]);
+      d.r3 = static_cast<int>(t->ranks[2]);
+      d.active = 1;
+      op->active |= (1ull << c);
+      op->rmax = std::max({op->rmax, d.r1, d.r2, d.r3});
+      d.off_core = off;
+      off += static_cast<int64_t>(d.r1) * d.r2 * d.r3;
+      d.off_u1 = off;
+      off += static_cast<int64_t>(g.n1 + 1) * d.r1;
+      d.off_u2 = off;
+      off += static_cast<int64_t>(g.n2 + 1) * d.r2;
+      d.off_u3 = off;
+      off += static_cast<int64_t>(g.n3 + 1) * d.r3;
+      d.off_z = zoff;
+      zoff += static_cast<int64_t>(g.n2 + 1) * d.r1 * d.r3;
+    }
+    if (vie::decomp_smem(g.n3, op->rmax) > 220 * 1024)
+      throw Invalid("vie_op_create: Tucker rank too large for the decompression tile (rank * (n3 + 1) too big)");
+    if (vie::pencil_smem(g.m3, g.S) > 220 * 1024) throw Invalid("vie_op_create: grid edge n3 too large");
+    op->forms = dev_alloc<double2>(static_cast<size_t>(off));
+    for (size_t c = 0; c < cs.size(); ++c) {
+      const vie_tucker_s* t = byc[c];
+      if (!t) continue;
+      const CompDev& d = op->comps_host[c];
+      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_core, t->core, sizeof(double2) * d.r1 * d.r2 * d.r3,
+                                cudaMemcpyDeviceToDevice));
+      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u1, t->uo[0], sizeof(double2) * (g.n1 + 1) * d.r1,
+                                cudaMemcpyDeviceToDevice));
+      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u2, t->uo[1], sizeof(double2) * (g.n2 + 1) * d.r2,
+                                cudaMemcpyDeviceToDevice));
+      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u3, t->uo[2], sizeof(double2) * (g.n3 + 1) * d.r3,
+                                cudaMemcpyDeviceToDevice));
+    }
+    op->comps_dev = dev_alloc<CompDev>(cs.size());
+    VIE_CUDA_CHECK(cudaMemcpy(op->comps_dev, op->comps_host.data(), sizeof(CompDev) * cs.size(),
+                              cudaMemcpyHostToDevice));
+    const int64_t nv = static_cast<int64_t>(g.n1) * g.n2 * g.n3;
+    const int64_t noct = static_cast<int64_t>(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
+    op->Z = dev_alloc<double2>(static_cast<size_t>(std::max<int64_t>(zoff, 1)));
+    op->Shat = dev_alloc<double2>(static_cast<size_t>(noct * g.NC));
+    op->A = dev_alloc<double2>(static_cast<size_t>(g.S * 2 * nv));
+    op->B = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
+    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 6 * nv);
+    op->P1 = get_plan(ctx, g.m1);
+    op->P2 = get_plan(ctx, g.m2);
+    op->P3 = get_plan(ctx, g.m3);
+    *out = op.release();
+  });
+}
+
+int vie_op_destroy(vie_op op) {
+  return guard([&] {
+    if (!op) return;
+    cudaSetDevice(op->ctx->device);
+    cudaStreamSynchronize(op->ctx->stream);
+    delete op;
+  });
+}
+
+int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_bytes) {
+  return guard([&] {
+    if (!op) throw Invalid("vie_op_info: null operator");
+    if (n_cur) *n_cur = op->g.S;
+    if (n_vox) *n_vox = static_cast<int64_t>(op->g.n1) * op->g.n2 * op->g.n3;
+    if (workspace_bytes) *workspace_bytes = op->ws_bytes;
+  });
+}
+
+int vie_matvec(vie_op op, const double* x, double* y, void* stream) {
+  return guard([&] {
+    if (!op || !x || !y) throw Invalid("apply_operator: null argument");
+    if (x == y) throw Invalid("apply_operator: x and y must not alias");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    run_matvec(op, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), pick_stream(op, stream),
+               nullptr, 0.0, 0);
+  });
+}
+
+int vie_matvec_host(vie_op op, const double* x_host, double* y_host) {
+  return guard([&] {
+    if (!op || !x_host || !y_host) throw Invalid("apply_operator: null argument");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    const int64_t n = static_cast<int64_t>(op->g.S) * op->g.n1 * op->g.n2 * op->g.n3;
+    if (!op->hx) op->hx = dev_alloc<double2>(static_cast<size_t>(n));
+    if (!op->hy) op->hy = dev_alloc<double2>(static_cast<size_t>(n));
+    cudaStream_t st = op->ctx->stream;
+    VIE_CUDA_CHECK(cudaMemcpyAsync(op->hx, x_host, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
+    run_matvec(op, op->hx, op->hy, st, nullptr, 0.0, 0);
+    VIE_CUDA_CHECK(cudaMemcpyAsync(y_host, op->hy, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int vie_system_matvec(vie_op op, const double* eps_r, double inv_v, const double* x, double* y, int diag_term,
+                      void* stream) {
+  return guard([&] {
+    if (!op || !eps_r || !x || !y) throw Invalid("apply_system: null argument");
+    if (x == y) throw Invalid("apply_system: x and y must not alias");
+    if (op->kind != VIE_KIND_N) throw Invalid("apply_system: needs the N operator");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    run_matvec(op, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), pick_stream(op, stream),
+               reinterpret_cast<const double2*>(eps_r), inv_v, diag_term ? 1 : 0);
+  });
+}
+
+int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* rhs_d, const double* x0_d,
+                    double tol, int inner, int outer, double* x_d, int* iterations, double* final_rel_res,
+                    double* history_host, int history_cap, int* history_len, int* converged) {
+  return guard([&] {
+    if (!op || !eps_r || !rhs_d || !x_d) throw Invalid("gmres: null argument");
+    if (tol < 0 || inner < 1 || outer < 1) throw Invalid("gmres: invalid configuration");
+    if (op->kind != VIE_KIND_N) throw Invalid("gmres: needs the N operator");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    cudaStream_t st = op->ctx->stream;
+    const Geom& g = op->g;
+    const int64_t n = static_cast<int64_t>(g.S) * g.n1 * g.n2 * g.n3;
+    const double2* eps = reinterpret_cast<const double2*>(eps_r);
+    const double2* rhs = reinterpret_cast<const double2*>(rhs_d);
+    double2* x = reinterpret_cast<double2*>(x_d);
+    if (op->g_inner < inner) {
+      dev_free(op->V);
+      op->V = nullptr;
+      op->V = dev_alloc<double2>(static_cast<size_t>(n) * (inner + 1));
+      op->g_inner = inner;
+    }
+    if (!op->tmp) op->tmp = dev_alloc<double2>(static_cast<size_t>(n));
+    if (!op->scal) op->scal = dev_alloc<double2>(256);
+    if (!op->red_partials) {
+      op->red_partials = dev_alloc<double2>(vie::kRedBlocks);
+      op->red_counter = dev_alloc<unsigned int>(1);
+      VIE_CUDA_CHECK(cudaMemset(op->red_counter, 0, sizeof(unsigned int)));
+    }
+    if (inner + 2 > 256) throw Invalid("gmres: inner > 254 not supported");
+    vie::RedBuf rb{op->red_partials, op->red_counter};
+    double2* V = op->V;
+    double2* tmp = op->tmp;
+    double2* hd = op->scal;  // hd[0..j+1]
+    auto fetch = [&](int count, std::vector<double2>& h) {
+      h.resize(static_cast<size_t>(count));
+      VIE_CUDA_CHECK(cudaMemcpyAsync(h.data(), hd, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
+      VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    };
+    auto sysmv = [&](const double2* in, double2* outv) { run_matvec(op, in, outv, st, eps, inv_v, 1); };
+    std::vector<double2> hbuf;
+    std::vector<double> history;
+    int iters = 0;
+    bool conv = false;
+    // ||b|| (solver.hpp:43) and the non-finite check (:37)
+    vie::launch_nrm2sq(rhs, n, hd, rb, st);
+    fetch(1, hbuf);
+    if (!std::isfinite(hbuf[0].x)) throw Invalid("gmres: non-finite right-hand side");
+    const double bnorm = std::sqrt(hbuf[0].x);
+    if (x0_d) {
+      if (x0_d != x_d) VIE_CUDA_CHECK(cudaMemcpyAsync(x, x0_d, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+    } else {
+      VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+    }
+    double final_rel = 0.0;
+    if (bnorm == 0.0) {
+      VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+      conv = true;
+      history.push_back(0.0);
+    } else {
+      const int m = inner;
+      std::vector<cd> hess(static_cast<size_t>((m + 1) * m), cd(0.0));
+      auto H = [&](int i, int j) -> cd& { return hess[static_cast<size_t>(i + (m + 1) * j)]; };
+      std::vector<cd> gv(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m));
+      for (int restart = 0; restart < outer && !conv; ++restart) {
+        sysmv(x, tmp);
+        vie::launch_residual(rhs, tmp, V, n, hd, rb, st);  // V_0 = r
+        fetch(1, hbuf);
+        const double beta = std::sqrt(hbuf[0].x);
+        if (beta / bnorm <= tol) {
+          conv = true;
+          break;
+        }
+        vie::launch_scale_inv(V, V, nullptr, beta, n, st);  // basis.col(0) = r / beta
+        std::fill(gv.begin(), gv.end(), cd(0.0));
+        gv[0] = beta;
+        int j = 0;
+        bool breakdown = false;
+        for (; j < m; ++j) {
+          double2* vj = V + static_cast<int64_t>(j) * n;
+          double2* w = V + static_cast<int64_t>(j + 1) * n;
+          sysmv(vj, w);
+          vie::launch_dot(V, w, n, hd, rb, st);  // h_0j
+          for (int i = 0; i <= j; ++i) {
+            const double2* vi = V + static_cast<int64_t>(i) * n;
+            const double2* vn = i < j ? V + static_cast<int64_t>(i + 1) * n : nullptr;
+            vie::launch_mgs_step(w, vi, hd + i, vn, n, hd + i + 1, rb, st);
+          }
+          fetch(j + 2, hbuf);
+          for (int i = 0; i <= j; ++i) H(i, j) = cd(hbuf[static_cast<size_t>(i)].x, hbuf[static_cast<size_t>(i)].y);
+          const double wnorm = std::sqrt(hbuf[static_cast<size_t>(j + 1)].x);
+          H(j + 1, j) = wnorm;
+          for (int i = 0; i < j; ++i) {
+            const cd t = cs[static_cast<size_t>(i)] * H(i, j) + sn[static_cast<size_t>(i)] * H(i + 1, j);
+            H(i + 1, j) = -std::conj(sn[static_cast<size_t>(i)]) * H(i, j) + std::conj(cs[static_cast<size_t>(i)]) * H(i + 1, j);
+            H(i, j) = t;
+          }
+          {
+            const cd a = H(j, j), b = H(j + 1, j);
+            const double denom = std::sqrt(std::norm(a) + std::norm(b));
+            if (denom == 0.0) {
+              cs[static_cast<size_t>(j)] = 1.0;
+              sn[static_cast<size_t>(j)] = 0.0;
+            } else {
+              cs[static_cast<size_t>(j)] = std::conj(a) / denom;
+              sn[static_cast<size_t>(j)] = std::conj(b) / denom;
+            }
+            H(j, j) = cs[static_cast<size_t>(j)] * a + sn[static_cast<size_t>(j)] * b;
+            H(j + 1, j) = 0.0;
+            const cd t = cs[static_cast<size_t>(j)] * gv[static_cast<size_t>(j)];
+            gv[static_cast<size_t>(j + 1)] = -std::conj(sn[static_cast<size_t>(j)]) * gv[static_cast<size_t>(j)];
+            gv[static_cast<size_t>(j)] = t;
+          }
+          ++iters;
+          const double rel = std::abs(gv[static_cast<size_t>(j + 1)]) / bnorm;
+          history.push_back(rel);
+          if (rel <= tol) {
+            ++j;
+            conv = true;
+            break;
+          }
+          if (wnorm < 1e-14 * beta) {
+            ++j;
+            breakdown = true;
+            break;
+          }
+          vie::launch_scale_inv(w, w, nullptr, wnorm, n, st);  // basis.col(j+1) = w / wnorm
+        }
+        std::vector<cd> yv(static_cast<size_t>(j), cd(0.0));
+        for (int i = j - 1; i >= 0; --i) {
+          cd s = gv[static_cast<size_t>(i)];
+          for (int l = i + 1; l < j; ++l) s -= H(i, l) * yv[static_cast<size_t>(l)];
+          yv[static_cast<size_t>(i)] = s / H(i, i);
+        }
+        if (j > 0) {
+          std::vector<double2> yd(static_cast<size_t>(j));
+          for (int l = 0; l < j; ++l) yd[static_cast<size_t>(l)] = make_double2(yv[static_cast<size_t>(l)].real(), yv[static_cast<size_t>(l)].imag());
+          VIE_CUDA_CHECK(cudaMemcpyAsync(hd, yd.data(), sizeof(double2) * j, cudaMemcpyHostToDevice, st));
+          vie::launch_basis_update(x, V, n, hd, j, n, st);  // x += V y (solver.hpp:130-131)
+        }
+        if (breakdown && !conv) {
+          sysmv(x, tmp);
+          vie::launch_residual(rhs, tmp, nullptr, n, hd, rb, st);
+          fetch(1, hbuf);
+          const double rel = std::sqrt(hbuf[0].x) / bnorm;
+          conv = rel <= tol;
+          if (conv) break;
+        }
+      }
+      sysmv(x, tmp);
+      vie::launch_residual(rhs, tmp, nullptr, n, hd, rb, st);
+      fetch(1, hbuf);
+      final_rel = std::sqrt(hbuf[0].x) / bnorm;
+    }
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (iterations) *iterations = iters;
+    if (final_rel_res) *final_rel_res = final_rel;
+    if (converged) *converged = conv ? 1 : 0;
+    if (history_len) *history_len = static_cast<int>(history.size());
+    if (history_host)
+      for (int i = 0; i < history_cap && i < static_cast<int>(history.size()); ++i)
+        history_host[i] = history[static_cast<size_t>(i)];
+  });
+}
+
+int vie_op_set_profiling(vie_op op, int enable) {
+  return guard([&] {
+    if (!op) throw Invalid("vie_op_set_profiling: null operator");
+    op->profiling = enable ? 1 : 0;
+  });
+}
+
+int vie_op_last_stats(vie_op op, int* launches, double* stage_ms) {
+  return guard([&] {
+    if (!op) throw Invalid("vie_op_last_stats: null operator");
+    if (launches) *launches = op->last_launches;
+    if (stage_ms)
+      for (int i = 0; i < 8; ++i) stage_ms[i] = op->stage_ms[i];
+  });
+}
+
+int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3], double tol,
+                        int rule, vie_tucker* out, int64_t ranks_out[3]) {
+  (void)ctx; (void)dims; (void)t_host; (void)sign; (void)tol; (void)rule; (void)out; (void)ranks_out;
+  g_err = "vie_tucker_compress: not implemented in this build";
+  return VIE_EINVAL;
+}
+
+}  // extern "C"

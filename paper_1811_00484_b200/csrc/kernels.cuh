@@ -1,0 +1,77 @@
+// kernels.cuh -- host-side launch interface of the matvec kernels.
+#pragma once
+#include "common.cuh"
+
+namespace vie {
+
+// Per-component device descriptor of a Fourier-domain Tucker form, octant rows
+// only: U_q^o has (n_q + 1) rows (the rest follow from U(m - p) = sign U(p)).
+struct CompDev {
+  int r1, r2, r3;
+  int active;
+  int64_t off_core;  // r1*r2*r3, core(a,b,g) at a + r1*(b + r2*g)   (decomp.hpp:124)
+  int64_t off_u1;    // (n1+1) x r1 column-major
+  int64_t off_u2;    // (n2+1) x r2
+  int64_t off_u3;    // (n3+1) x r3
+  int64_t off_z;     // Z[p2o][a][g]  (n2+1) x r1 x r3
+};
+
+struct Geom {
+  int n1, n2, n3;  // grid
+  int m1, m2, m3;  // embedded (2n)
+  int S;           // current components (sources = targets)
+  int NC;          // canonical component count
+};
+
+// Tuning constants.
+constexpr int kRowsPerCta = 8;     // row FFT kernels
+constexpr int kColsPerCta = 8;     // column FFT kernels (128 B segments)
+constexpr int kPencilLines = 24;   // pencil kernel: S * W lines in smem
+constexpr int kThreads = 256;
+
+size_t row_smem(int m);
+size_t col_smem(int m);
+size_t pencil_smem(int m3, int S);
+size_t decomp_smem(int n3, int rmax);
+
+void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& P1, cudaStream_t st);
+void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& P2, cudaStream_t st);
+void launch_pencil(int kind, int basis, double2* B, const double2* Shat, const Geom& g, const FftPlan& P3,
+                   uint64_t active_mask, cudaStream_t st);
+void launch_col_inv(const double2* B, double2* A, const Geom& g, const FftPlan& P2, cudaStream_t st);
+// Epilogue: y = scale * (IDFT) or the system form (eps != nullptr):
+//   y = (diag ? eps*g_l*xin : 0) - (eps - 1) * inv_v * scale * (IDFT)
+void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& P1, double scale,
+                    const double2* eps, const double2* xin, double inv_v, int basis, int diag, cudaStream_t st);
+
+void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
+                   double2* Shat, const Geom& g, int rmax, cudaStream_t st);
+
+// transform_factors on device: spatial factor (n x r, col-major) -> octant rows
+// (n+1) x r of the DFT of the parity embedding (operator.hpp:64-90).
+void launch_factor_transform(const double2* u, int n, int r, int sign, const double2* tw2n, double2* out,
+                             cudaStream_t st);
+
+// ---- BLAS-1 for GMRES (deterministic two-level reductions) ----
+struct RedBuf {
+  double2* partials;       // kRedBlocks entries
+  unsigned int* counter;   // zero-initialised
+};
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+// out[0] = sum conj(a) * b
+void launch_dot(const double2* a, const double2* b, int64_t n, double2* out, RedBuf rb, cudaStream_t st);
+// out[0].x = sum |a|^2
+void launch_nrm2sq(const double2* a, int64_t n, double2* out, RedBuf rb, cudaStream_t st);
+// w -= h[0] * v ; then out[0] = sum conj(vnext) * w   (vnext == nullptr: out = |w|^2)
+void launch_mgs_step(double2* w, const double2* v, const double2* h, const double2* vnext, int64_t n,
+                     double2* out, RedBuf rb, cudaStream_t st);
+// r = rhs - ax ; out = |r|^2
+void launch_residual(const double2* rhs, const double2* ax, double2* r, int64_t n, double2* out, RedBuf rb,
+                     cudaStream_t st);
+// y = x / d with d = s[0].x (device) or `divisor` when s == nullptr
+void launch_scale_inv(const double2* x, double2* y, const double2* s, double divisor, int64_t n, cudaStream_t st);
+// x += sum_l V_l * coef[l]
+void launch_basis_update(double2* x, const double2* V, int64_t ldv, const double2* coef, int j, int64_t n,
+                         cudaStream_t st);
+
+}  // namespace vie

@@ -1,0 +1,158 @@
+// kernels_decomp.cu -- Tucker decompression of the component spectra on their
+// octant (|p_q| <= n_q), and the device-side factor transform.
+//
+// Reference: decompress_tucker (operator.hpp:224-244) materialises the full
+// m1 x m2 x m3 spectrum per component (GEMM chain c1 = U1 G, c2 = c1 U2^T,
+// dst = c2 U3^T).  Here only the octant is formed (1/8 of the entries and of
+// the dominant r3 * N_e flops), for all components at once:
+//   k_decomp_z : Z_c[p2][a][g] = sum_b G_c[a,b,g] U2_c[p2,b]        (r^3 per p2)
+//   k_decomp_s : T = U1_c Z_c[p2]  (n1+1 x r3),  S^_c[p2][p1][f3] = T U3_c^T
+// Output layout Shat[p2o][p1o][c][f3o], f3o fastest, read by the pencil kernel.
+#include "kernels.cuh"
+
+namespace vie {
+
+namespace {
+
+// CTA per (component, g): stage one core slice G[:,:,g] in smem.
+__global__ void __launch_bounds__(kThreads) k_decomp_z(const double2* __restrict__ forms,
+                                                       const CompDev* __restrict__ comps, double2* __restrict__ Z,
+                                                       int n2) {
+  extern __shared__ double2 gs[];
+  const CompDev cd = comps[blockIdx.x];
+  const int g = blockIdx.y;
+  if (!cd.active || g >= cd.r3) return;
+  const int r1 = cd.r1, r2 = cd.r2, r3 = cd.r3;
+  const double2* core = forms + cd.off_core + static_cast<int64_t>(g) * r1 * r2;
+  for (int e = threadIdx.x; e < r1 * r2; e += blockDim.x) gs[e] = core[e];  // gs[a + r1*b]
+  __syncthreads();
+  const double2* u2 = forms + cd.off_u2;  // (n2+1) x r2
+  const int np = n2 + 1;
+  double2* zc = Z + cd.off_z;
+  for (int e = threadIdx.x; e < np * r1; e += blockDim.x) {
+    const int a = e % r1, p2 = e / r1;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int b = 0; b < r2; ++b) cfma(acc, gs[a + r1 * b], __ldg(u2 + p2 + static_cast<int64_t>(np) * b));
+    zc[(static_cast<int64_t>(p2) * r1 + a) * r3 + g] = acc;
+  }
+}
+
+constexpr int kTP1 = 32;  // p1 rows per chunk
+constexpr int kQ = 4;     // micro-tile 4 x 4
+
+// CTA per (component, p2o).
+__global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict__ forms,
+                                                       const CompDev* __restrict__ comps,
+                                                       const double2* __restrict__ Z, double2* __restrict__ Shat,
+                                                       Geom geo, int NC) {
+  extern __shared__ double2 sm[];
+  const int c = blockIdx.x;
+  const CompDev cd = comps[c];
+  if (!cd.active) return;
+  const int p2o = blockIdx.y;
+  const int r1 = cd.r1, r3 = cd.r3;
+  const int n1p = geo.n1 + 1, n3p = geo.n3 + 1;
+  double2* zs = sm;                                   // r1 x r3   zs[a*r3 + g]
+  double2* us = zs + r1 * r3;                         // r3 x n3p  us[g*n3p + f]
+  double2* ts = us + static_cast<int64_t>(r3) * n3p;  // r3 x kTP1 ts[g*kTP1 + i]
+  const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;
+  for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) zs[e] = zsrc[e];
+  const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major: u3[f + n3p*g]
+  for (int e = threadIdx.x; e < r3 * n3p; e += blockDim.x) us[e] = u3[e];
+  const double2* u1 = forms + cd.off_u1;  // n1p x r1
+  const int nfq = (n3p + kQ - 1) / kQ;
+  for (int p10 = 0; p10 < n1p; p10 += kTP1) {
+    const int np1 = min(kTP1, n1p - p10);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTP1 * r3; e += blockDim.x) {
+      const int i = e % kTP1, g = e / kTP1;
+      double2 acc = make_double2(0.0, 0.0);
+      if (i < np1)
+        for (int a = 0; a < r1; ++a) cfma(acc, __ldg(u1 + (p10 + i) + static_cast<int64_t>(n1p) * a), zs[a * r3 + g]);
+      ts[g * kTP1 + i] = acc;
+    }
+    __syncthreads();
+    const int tiles = (kTP1 / kQ) * nfq;
+    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
+      const int fq = t % nfq, rq = t / nfq;
+      double2 acc[kQ][kQ];
+#pragma unroll
+      for (int i = 0; i < kQ; ++i)
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) acc[i][j] = make_double2(0.0, 0.0);
+      const int f0 = fq * kQ;
+      for (int g = 0; g < r3; ++g) {
+        double2 tv[kQ], uv[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) tv[i] = ts[g * kTP1 + rq * kQ + i];
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) uv[j] = (f0 + j < n3p) ? us[g * n3p + f0 + j] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < kQ; ++i)
+#pragma unroll
+          for (int j = 0; j < kQ; ++j) cfma(acc[i][j], tv[i], uv[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < kQ; ++i) {
+        const int p1o = p10 + rq * kQ + i;
+        if (rq * kQ + i >= np1) break;
+        double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + p1o) * NC + c) * n3p + f0;
+#pragma unroll
+        for (int j = 0; j < kQ; ++j)
+          if (f0 + j < n3p) dst[j] = acc[i][j];
+      }
+    }
+  }
+}
+
+// Factor transform: out[p + (n+1) c] = sum_m e_c[m] w_{2n}^{p m}, p <= n,
+// with e_c the parity embedding of column c (embed_column).
+__global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, int sign,
+                                   const double2* __restrict__ tw, double2* __restrict__ out) {
+  const int m = 2 * n;
+  const int total = (n + 1) * r;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int p = e % (n + 1), c = e / (n + 1);
+    const double2* col = u + static_cast<int64_t>(n) * c;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int k = 0; k < m; ++k) {
+      if (k == n) continue;
+      const double2 v = k < n ? col[k] : cscale(col[m - k], static_cast<double>(sign));
+      const int e2 = static_cast<int>((static_cast<int64_t>(p) * k) % m);
+      cfma(acc, v, tw[e2]);
+    }
+    out[p + static_cast<int64_t>(n + 1) * c] = acc;
+  }
+}
+
+}  // namespace
+
+size_t decomp_smem(int n3, int rmax) {
+  return sizeof(double2) * (static_cast<size_t>(rmax) * rmax + static_cast<size_t>(rmax) * (n3 + 1) +
+                            static_cast<size_t>(rmax) * kTP1);
+}
+
+void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
+                   double2* Shat, const Geom& g, int rmax, cudaStream_t st) {
+  (void)comps_host;
+  const size_t smz = sizeof(double2) * static_cast<size_t>(rmax) * rmax;
+  VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_z),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smz)));
+  k_decomp_z<<<dim3(g.NC, rmax), kThreads, smz, st>>>(forms, comps_dev, Z, g.n2);
+  VIE_CUDA_CHECK(cudaGetLastError());
+  const size_t sms = decomp_smem(g.n3, rmax);
+  VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
+  k_decomp_s<<<dim3(g.NC, g.n2 + 1), kThreads, sms, st>>>(forms, comps_dev, Z, Shat, g, g.NC);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_factor_transform(const double2* u, int n, int r, int sign, const double2* tw2n, double2* out,
+                             cudaStream_t st) {
+  const int total = (n + 1) * r;
+  const int blocks = (total + 255) / 256;
+  k_factor_transform<<<blocks, 256, 0, st>>>(u, n, r, sign, tw2n, out);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace vie

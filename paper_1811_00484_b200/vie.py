@@ -1,0 +1,308 @@
+"""Host-side mirror of the reference operator API over the C ABI (include/vie_b200.h).
+
+Names, argument meaning and error behaviour follow
+/root/reference/proj/include/vie/{operator,solver}.hpp:
+  * ``build_operator_spectra``  operator.hpp:144-177 (from Tucker forms)
+  * ``apply_operator``          operator.hpp:273-382 (HosvdDecompress semantics)
+  * ``apply_system``            solver.hpp:183-200
+  * ``gmres``                   solver.hpp:34-142 (device resident)
+``ValueError`` is raised where the reference throws ``std::invalid_argument``.
+
+Device memory and streams come from PyTorch (plumbing only); every number is
+computed by libvie_b200.so.  There is no CPU fallback: importing this module
+without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvie_b200.so")
+
+KIND_N, KIND_K = 0, 1
+PWC, PWL = 0, 1
+RULE_SIGMA_MAX, RULE_ENERGY = 0, 1
+
+VIE_OK, VIE_EINVAL, VIE_ENOMEM, VIE_ECUDA, VIE_ENCCL = 0, 1, 2, 3, 4
+
+_dp = C.POINTER(C.c_double)
+_lib = None
+
+
+class VieError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[vie error {code}] {msg}")
+        self.code = code
+
+
+def lib() -> C.CDLL:
+    """Load libvie_b200.so; fail loudly if it is missing (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libvie_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.vie_last_error.restype = C.c_char_p
+        L.vie_version.restype = C.c_char_p
+        L.vie_system_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_int,
+                                        C.c_void_p]
+        L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_gmres_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_double,
+                                      C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                      _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        _lib = L
+    return _lib
+
+
+def _check(rc: int):
+    if rc != VIE_OK:
+        msg = lib().vie_last_error().decode()
+        if rc == VIE_EINVAL:
+            raise ValueError(msg)
+        raise VieError(rc, msg)
+
+
+def _i64(vals):
+    return (C.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def _cplx(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def component_table(kind: int, basis: int):
+    """Canonical components/parities/blocks of (kind, basis) from the product library."""
+    nc, nb = C.c_int(), C.c_int()
+    comps = (C.c_int * 256)()
+    par = (C.c_int * 192)()
+    blocks = (C.c_int * 1024)()
+    _check(lib().vie_component_table(int(kind), int(basis), C.byref(nc), comps, par, C.byref(nb), blocks))
+    return (np.array(comps[: 4 * nc.value], np.int32).reshape(-1, 4),
+            np.array(par[: 3 * nc.value], np.int32).reshape(-1, 3),
+            np.array(blocks[: 4 * nb.value], np.int32).reshape(-1, 4))
+
+
+def ncur(basis: int) -> int:
+    return 3 if basis == PWC else 12
+
+
+class DftService:
+    """Context: CUDA device + stream + FFT plan cache (fft.hpp DftService)."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        _check(lib().vie_ctx_create(C.byref(self._h), int(device)))
+        self.device = device
+
+    @property
+    def handle(self):
+        return self._h
+
+    def synchronize(self):
+        _check(lib().vie_ctx_sync(self._h))
+
+    def close(self):
+        if self._h:
+            lib().vie_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class TuckerForm:
+    """Device-resident Fourier-domain Tucker form of one component."""
+
+    def __init__(self, dft: DftService, dims, core, factors: Sequence, sign, domain: int = 0):
+        core = _cplx(np.asarray(core).reshape(-1, order="F"))
+        us = [np.asfortranarray(np.asarray(u, np.complex128)) for u in factors]
+        ranks = [u.shape[1] for u in us]
+        if core.size != ranks[0] * ranks[1] * ranks[2]:
+            raise ValueError("TuckerForm: core size does not match the factor ranks")
+        rows = [d if domain == 0 else 2 * d for d in dims]
+        for q in range(3):
+            if us[q].shape[0] != rows[q]:
+                raise ValueError("TuckerForm: factor rows do not match dims")
+        self._h = C.c_void_p()
+        self._dft = dft
+        _check(lib().vie_tucker_from_factors(dft.handle, _i64(dims), _i64(ranks), core.ctypes.data_as(_dp),
+                                             us[0].ctypes.data_as(_dp), us[1].ctypes.data_as(_dp),
+                                             us[2].ctypes.data_as(_dp), (C.c_int * 3)(*[int(s) for s in sign]),
+                                             int(domain), C.byref(self._h)))
+        self.dims = tuple(int(d) for d in dims)
+        self.ranks = tuple(ranks)
+        self.sign = tuple(int(s) for s in sign)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().vie_tucker_destroy(self._h)
+        except Exception:
+            pass
+
+
+@dataclass
+class EmbeddedSpectrum:
+    """Device operator (operator.hpp:120-129) holding Tucker forms only."""
+    kind: int
+    basis: int
+    grid_dims: tuple
+    handle: C.c_void_p
+    dft: DftService
+    comps: list = field(default_factory=list)
+
+    @property
+    def embedded_dims(self):
+        return tuple(2 * d for d in self.grid_dims)
+
+    @property
+    def n_cur(self) -> int:
+        return ncur(self.basis)
+
+    @property
+    def n_vox(self) -> int:
+        return int(np.prod(self.grid_dims))
+
+    def workspace_bytes(self) -> int:
+        ws = C.c_int64()
+        _check(lib().vie_op_info(self.handle, None, None, C.byref(ws)))
+        return ws.value
+
+    def set_profiling(self, on: bool):
+        _check(lib().vie_op_set_profiling(self.handle, int(bool(on))))
+
+    def last_stats(self):
+        n = C.c_int()
+        ms = (C.c_double * 8)()
+        _check(lib().vie_op_last_stats(self.handle, C.byref(n), ms))
+        return n.value, list(ms)
+
+    def close(self):
+        if self.handle:
+            lib().vie_op_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def build_operator_spectra(kind: int, basis: int, grid, comps: Sequence, forms: Sequence[TuckerForm],
+                           dft: DftService) -> EmbeddedSpectrum:
+    """operator.hpp:144-177 from compressed forms; comps[i] = (q, q', l, l')."""
+    comps = [tuple(int(v) for v in c) for c in comps]
+    if len(comps) == 0:
+        raise ValueError("build_operator_spectra: no components")
+    if len(comps) != len(forms):
+        raise ValueError("build_operator_spectra: one form per component required")
+    flat = (C.c_int * (4 * len(comps)))(*[v for c in comps for v in c])
+    hs = (C.c_void_p * len(forms))(*[f.handle.value for f in forms])
+    h = C.c_void_p()
+    _check(lib().vie_op_create(dft.handle, int(kind), int(basis), _i64(grid), len(comps), flat, hs, C.byref(h)))
+    return EmbeddedSpectrum(int(kind), int(basis), tuple(int(g) for g in grid), h, dft, comps)
+
+
+# ----------------------------------------------------------------------------- apply
+def _torch():
+    import torch
+    return torch
+
+
+def _dev_vec(op: EmbeddedSpectrum, x):
+    torch = _torch()
+    n = op.n_cur * op.n_vox
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        raise TypeError("expected a CUDA torch.complex128 tensor")
+    if x.dtype != torch.complex128 or x.numel() != n:
+        raise ValueError("apply_operator: dim mismatch")
+    return x.contiguous()
+
+
+def apply_operator(op: EmbeddedSpectrum, x, strategy: str = "hosvd_decompress", policy: str = "with_buffer",
+                   ws=None, dft=None, out=None, stream=None):
+    """y = A x (operator.hpp:273).  ``x``: CUDA complex128 tensor (S*N_v) or host numpy array.
+
+    The B200 path is the fused octant HOSVD decompress x Hadamard; the
+    reference's scratch-policy contract is kept: decompress strategies with
+    policy 'no_buffer' raise ValueError (operator.hpp:278-281)."""
+    if strategy not in ("hosvd_decompress", "hosvd_loop"):
+        raise ValueError(f"apply_operator: strategy {strategy!r} needs a representation this build does not hold")
+    if strategy == "hosvd_decompress" and policy == "no_buffer":
+        raise ValueError("apply_operator: decompress strategies need ScratchPolicy::WithBuffer")
+    if isinstance(x, np.ndarray):
+        xa = _cplx(x).reshape(-1)
+        if xa.size != op.n_cur * op.n_vox:
+            raise ValueError("apply_operator: dim mismatch")
+        y = np.empty_like(xa)
+        _check(lib().vie_matvec_host(op.handle, xa.ctypes.data, y.ctypes.data))
+        return y
+    torch = _torch()
+    x = _dev_vec(op, x)
+    y = out if out is not None else torch.empty_like(x)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().vie_matvec(op.handle, x.data_ptr(), y.data_ptr(), st))
+    return y
+
+
+def apply_system(eps_r, inv_v: float, op: EmbeddedSpectrum, x, out=None, diag_term: bool = True, stream=None):
+    """y = eps*g*x - (eps-1)*inv_v*(N x) (solver.hpp:183-200); CUDA tensors."""
+    torch = _torch()
+    x = _dev_vec(op, x)
+    if not (isinstance(eps_r, torch.Tensor) and eps_r.is_cuda and eps_r.numel() == op.n_vox):
+        raise ValueError("apply_system: dim mismatch")
+    eps_r = eps_r.to(torch.complex128).contiguous()
+    y = out if out is not None else torch.empty_like(x)
+    st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
+    _check(lib().vie_system_matvec(op.handle, eps_r.data_ptr(), float(inv_v), x.data_ptr(), y.data_ptr(),
+                                   int(bool(diag_term)), st))
+    return y
+
+
+@dataclass
+class GmresConfig:  # solver.hpp:12-16
+    tolerance: float = 1e-5
+    inner: int = 50
+    outer: int = 200
+
+
+@dataclass
+class GmresResult:  # solver.hpp:18-24
+    solution: object
+    residual_history: list
+    final_relative_residual: float
+    iterations: int
+    converged: bool
+
+
+def gmres(op: EmbeddedSpectrum, eps_r, inv_v: float, rhs, cfg: GmresConfig = GmresConfig(), x0=None,
+          history_cap: int = 100000) -> GmresResult:
+    """Restarted GMRES on apply_system, device resident (solver.hpp:34-142)."""
+    torch = _torch()
+    rhs = _dev_vec(op, rhs)
+    eps_r = eps_r.to(torch.complex128).contiguous()
+    x = torch.empty_like(rhs)
+    x0p = _dev_vec(op, x0).data_ptr() if x0 is not None else None
+    it, hl, cv = C.c_int(), C.c_int(), C.c_int()
+    fr = C.c_double()
+    hist = np.empty(history_cap, np.float64)
+    torch.cuda.current_stream(rhs.device).synchronize()
+    _check(lib().vie_gmres_solve(op.handle, eps_r.data_ptr(), float(inv_v), rhs.data_ptr(), x0p,
+                                 float(cfg.tolerance), int(cfg.inner), int(cfg.outer), x.data_ptr(),
+                                 C.byref(it), C.byref(fr), hist.ctypes.data_as(_dp), int(history_cap),
+                                 C.byref(hl), C.byref(cv)))
+    return GmresResult(x, hist[: min(hl.value, history_cap)].tolist(), fr.value, it.value, bool(cv.value))

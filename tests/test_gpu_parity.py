@@ -1,0 +1,248 @@
+"""GPU parity: the B200 path (libvie_b200.so via the C ABI) against the CPU oracle
+on identical seeded inputs.  Bar (BASELINE north star): matvec relative l2 error
+<= 1e-10; GMRES iterations within +-1 and final residual within 1e-8."""
+import numpy as np
+import pytest
+
+from tests.helpers import fourier_forms, random_field, rel, spatial_tucker_forms
+
+pytestmark = pytest.mark.gpu
+
+N, K, PWC, PWL = 0, 1, 0, 1
+MATVEC_TOL = 1e-10  # north star: matvec relative l2 <= 1e-10
+
+
+@pytest.fixture(scope="module")
+def vie():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__
+
+    __graft_entry__.build()
+    import paper_1811_00484_b200 as v
+
+    return v
+
+
+@pytest.fixture(scope="module")
+def dft(vie):
+    return vie.DftService(0)
+
+
+def make_ops(vie, dft, orc, kind, basis, dims, rank, seed, subset=None, scale=1.0):
+    spatial, par = spatial_tucker_forms(kind, basis, dims, rank, seed)
+    if scale != 1.0:
+        spatial = [(core * scale, us) for core, us in spatial]
+    comps, _, _ = vie.component_table(kind, basis)
+    idx = list(range(len(comps))) if subset is None else list(subset)
+    forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in idx]
+    op = vie.build_operator_spectra(kind, basis, dims, [comps[c] for c in idx], forms, dft)
+    return op, fourier_forms(spatial, par), spatial, par
+
+
+def to_dev(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+def run_gpu(vie, op, x):
+    import torch
+
+    y = vie.apply_operator(op, to_dev(x))
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+CASES = [
+    (N, PWC, (3, 5, 4), 3), (K, PWC, (3, 5, 4), 3), (N, PWC, (4, 4, 4), 4), (N, PWC, (6, 5, 7), 5),
+    (N, PWC, (1, 1, 2), 2), (N, PWC, (2, 3, 1), 2), (N, PWC, (8, 6, 10), 6), (K, PWC, (7, 9, 5), 4),
+    (N, PWL, (3, 4, 5), 3), (K, PWL, (3, 4, 5), 3), (N, PWL, (2, 2, 2), 2), (N, PWL, (5, 3, 4), 4),
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", CASES)
+def test_matvec_matches_oracle(vie, dft, orc, kind, basis, dims, rank):
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 7 + sum(dims))
+    for trial in range(2):
+        x = random_field(basis, dims, 2024 + trial)
+        y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+        y = run_gpu(vie, op, x)
+        assert rel(y_ref, y) <= MATVEC_TOL, (kind, basis, dims)
+
+
+def test_matvec_c1_cube_pwl(vie, dft, orc):
+    # BASELINE configs[0]: 32^3 PWL grid, r = 25 (CPU-runnable reference case)
+    dims = (32, 32, 32)
+    op, oforms, _, _ = make_ops(vie, dft, orc, N, PWL, dims, 25, 1234)
+    x = random_field(PWL, dims, 2024)
+    y_ref = orc.apply_operator_tucker(N, PWL, dims, oforms, x)
+    assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL
+
+
+def test_matvec_mixed_ranks_and_host_path(vie, dft, orc):
+    dims = (6, 4, 5)
+    spatial, par = spatial_tucker_forms(N, PWC, dims, 5, 99)
+    rng = np.random.default_rng(0)
+    mixed = []
+    for c, (core, us) in enumerate(spatial):
+        r = [1 + (c + q) % 5 for q in range(3)]
+        g = (rng.standard_normal(r[0] * r[1] * r[2]) + 1j * rng.standard_normal(r[0] * r[1] * r[2]))
+        mixed.append((g, [us[q][:, : r[q]] for q in range(3)]))
+    comps, _, _ = vie.component_table(N, PWC)
+    forms = [vie.TuckerForm(dft, dims, mixed[c][0], mixed[c][1], par[c]) for c in range(6)]
+    op = vie.build_operator_spectra(N, PWC, dims, comps, forms, dft)
+    x = random_field(PWC, dims, 5)
+    y_ref = orc.apply_operator_tucker(N, PWC, dims, fourier_forms(mixed, par), x)
+    assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL
+    assert rel(y_ref, vie.apply_operator(op, x)) <= MATVEC_TOL  # host-buffer C-ABI call
+
+
+@pytest.mark.parametrize("basis", [PWC, PWL])
+def test_component_sharding_sums_to_full(vie, dft, orc, basis):
+    # components sharded over "ranks": partial outputs add up to the full matvec
+    dims = (4, 3, 5)
+    op, oforms, spatial, par = make_ops(vie, dft, orc, N, basis, dims, 3, 31)
+    comps, _, _ = vie.component_table(N, basis)
+    x = random_field(basis, dims, 3)
+    full = run_gpu(vie, op, x)
+    nc = len(comps)
+    parts = []
+    for r in range(3):
+        sub = list(range(r, nc, 3))
+        forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in sub]
+        sop = vie.build_operator_spectra(N, basis, dims, [comps[c] for c in sub], forms, dft)
+        parts.append(run_gpu(vie, sop, x))
+    assert rel(full, sum(parts)) < 1e-13
+
+
+def test_zero_input_gives_zero(vie, dft, orc):
+    op, _, _, _ = make_ops(vie, dft, orc, N, PWC, (3, 3, 4), 2, 20)
+    y = run_gpu(vie, op, np.zeros(3 * 36, complex))
+    assert np.linalg.norm(y) == 0.0
+
+
+@pytest.mark.parametrize("basis", [PWC, PWL])
+def test_system_matvec_matches_oracle(vie, dft, orc, basis):
+    import torch
+
+    dims = (5, 4, 6) if basis == PWC else (3, 4, 3)
+    op, oforms, _, _ = make_ops(vie, dft, orc, N, basis, dims, 3, 17)
+    nv = int(np.prod(dims))
+    rng = np.random.default_rng(4)
+    eps = 1 + rng.uniform(0, 60, nv) - 1j * rng.uniform(0, 5, nv)
+    inv_v = 0.37
+    x = random_field(basis, dims, 20)
+    y_ref = orc.apply_system_tucker(basis, dims, oforms, eps, inv_v, x)
+    y = vie.apply_system(to_dev(eps), inv_v, op, to_dev(x))
+    torch.cuda.synchronize()
+    assert rel(y_ref, y.cpu().numpy()) <= MATVEC_TOL
+
+
+def _scene(vie, dft, orc, basis, dims, seed):
+    # synthetic spectra scaled so the system is a well-posed perturbation of M_eps
+    # (oracle: PWC converges in ~17 iterations, PWL in ~66 with restarts)
+    scale = 1e-4 if basis == PWC else 3e-5
+    op, oforms, _, _ = make_ops(vie, dft, orc, N, basis, dims, 4, seed, scale=scale)
+    nv = int(np.prod(dims))
+    rng = np.random.default_rng(seed)
+    eps = 1 + rng.uniform(1, 5, nv) - 1j * rng.uniform(0, 1, nv)
+    rhs = random_field(basis, dims, seed + 1)
+    return op, oforms, eps, rhs
+
+
+@pytest.mark.parametrize("basis,dims", [(PWC, (6, 5, 4)), (PWL, (4, 3, 4))])
+def test_gmres_matches_oracle(vie, dft, orc, basis, dims):
+    op, oforms, eps, rhs = _scene(vie, dft, orc, basis, dims, 77)
+    inv_v = 1.0
+    ref = orc.gmres_system_tucker(basis, dims, oforms, eps, inv_v, rhs, tol=1e-8, inner=8, outer=20)
+    res = vie.gmres(op, to_dev(eps), inv_v, to_dev(rhs), vie.GmresConfig(1e-8, 8, 20))
+    assert ref.converged and res.converged
+    assert abs(ref.iterations - res.iterations) <= 1
+    assert abs(ref.final_relative_residual - res.final_relative_residual) <= 1e-8
+    x = res.solution.cpu().numpy()
+    ext = np.linalg.norm(orc.apply_system_tucker(basis, dims, oforms, eps, inv_v, x) - rhs) / np.linalg.norm(rhs)
+    assert abs(ext - res.final_relative_residual) <= 1e-10
+    assert rel(ref.solution, x) < 1e-6
+    n = min(len(ref.residual_history), len(res.residual_history))
+    assert np.allclose(ref.residual_history[:n], res.residual_history[:n], rtol=1e-6, atol=1e-12)
+
+
+def test_gmres_zero_rhs_warm_start_and_nonconvergence(vie, dft, orc):
+    dims = (4, 4, 3)
+    op, oforms, eps, rhs = _scene(vie, dft, orc, PWC, dims, 5)
+    z = vie.gmres(op, to_dev(eps), 1.0, to_dev(np.zeros_like(rhs)))
+    assert z.converged and z.iterations == 0 and float(z.solution.abs().max()) == 0.0
+    cold = vie.gmres(op, to_dev(eps), 1.0, to_dev(rhs), vie.GmresConfig(1e-10, 10, 10))
+    assert cold.converged
+    warm = vie.gmres(op, to_dev(eps), 1.0, to_dev(rhs), vie.GmresConfig(1e-10, 10, 10), x0=cold.solution)
+    assert warm.converged and warm.iterations == 0
+    bad = vie.gmres(op, to_dev(eps), 1.0, to_dev(rhs), vie.GmresConfig(1e-14, 1, 1))
+    assert not bad.converged and bad.iterations == 1
+    with pytest.raises(ValueError):
+        vie.gmres(op, to_dev(eps), 1.0, to_dev(rhs), vie.GmresConfig(1e-5, 0, 1))
+    nanr = rhs.copy()
+    nanr[0] = np.nan
+    with pytest.raises(ValueError):
+        vie.gmres(op, to_dev(eps), 1.0, to_dev(nanr))
+
+
+def test_error_behaviour(vie, dft, orc):
+    dims = (3, 3, 3)
+    spatial, par = spatial_tucker_forms(N, PWC, dims, 2, 3)
+    comps, _, _ = vie.component_table(N, PWC)
+    forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in range(6)]
+    with pytest.raises(ValueError):  # no components
+        vie.build_operator_spectra(N, PWC, dims, [], [], dft)
+    with pytest.raises(ValueError):  # duplicate component
+        vie.build_operator_spectra(N, PWC, dims, [comps[0], comps[0]], [forms[0], forms[0]], dft)
+    with pytest.raises(ValueError):  # not in the canonical table (K has no xx)
+        vie.build_operator_spectra(K, PWC, dims, [comps[0]], [forms[0]], dft)
+    with pytest.raises(ValueError):  # parity mismatch (form of xx used as xy)
+        vie.build_operator_spectra(N, PWC, dims, [comps[1]], [forms[0]], dft)
+    with pytest.raises(ValueError):  # inconsistent dims
+        other = vie.TuckerForm(dft, (3, 3, 4), np.ones(1), [np.ones((3, 1)), np.ones((3, 1)), np.ones((4, 1))],
+                               (1, 1, 1))
+        vie.build_operator_spectra(N, PWC, dims, [comps[0]], [other], dft)
+    with pytest.raises(ValueError):  # odd axis with a nonzero offset-0 row
+        vie.TuckerForm(dft, dims, np.ones(1), [np.ones((3, 1)), np.ones((3, 1)), np.ones((3, 1))], (-1, -1, 1))
+    with pytest.raises(ValueError):  # embedded length with a prime factor > 7 (2 * 11)
+        f11 = vie.TuckerForm(dft, (11, 3, 3), np.ones(1), [np.ones((11, 1)), np.ones((3, 1)), np.ones((3, 1))],
+                             (1, 1, 1))
+        vie.build_operator_spectra(N, PWC, (11, 3, 3), [comps[0]], [f11], dft)
+    op = vie.build_operator_spectra(N, PWC, dims, comps, forms, dft)
+    with pytest.raises(ValueError):
+        vie.apply_operator(op, np.zeros(5, complex))
+    with pytest.raises(ValueError):
+        vie.apply_operator(op, np.zeros(81, complex), policy="no_buffer")
+
+
+def test_fourier_domain_forms_accepted(vie, dft, orc):
+    # domain=1: factors already transformed (transform_factors output, 2n rows)
+    dims = (4, 5, 3)
+    spatial, par = spatial_tucker_forms(N, PWC, dims, 3, 12)
+    oforms = fourier_forms(spatial, par)
+    comps, _, _ = vie.component_table(N, PWC)
+    forms = [vie.TuckerForm(dft, dims, oforms[c].core, oforms[c].u, par[c], domain=1) for c in range(6)]
+    op = vie.build_operator_spectra(N, PWC, dims, comps, forms, dft)
+    x = random_field(PWC, dims, 8)
+    assert rel(orc.apply_operator_tucker(N, PWC, dims, oforms, x), run_gpu(vie, op, x)) <= MATVEC_TOL
+
+
+def test_linearity_at_head_2mm_size(vie, dft, orc):
+    # size-independent property at BASELINE configs[2] shape (100x120x100, r=25)
+    import torch
+
+    dims = (100, 120, 100)
+    op, _, _, _ = make_ops(vie, dft, orc, N, PWC, dims, 25, 42)
+    n = 3 * int(np.prod(dims))
+    g = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
+    z = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
+    lam = 0.7 - 1.3j
+    lhs = vie.apply_operator(op, x + lam * z)
+    rhs = vie.apply_operator(op, x) + lam * vie.apply_operator(op, z)
+    torch.cuda.synchronize()
+    assert float((lhs - rhs).norm() / rhs.norm()) < 1e-12
