@@ -232,7 +232,8 @@ def run_b200(args):
     g = torch.Generator(device="cuda").manual_seed(2024)
     x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
     y = torch.empty_like(x)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # dedicated stream: events and kernels on the same queue
+    torch.cuda.set_stream(stream)
 
     def step():
         vie.apply_operator(op, x, out=y, stream=stream.cuda_stream)

@@ -223,6 +223,15 @@ def _torch():
     return torch
 
 
+def _stream_handle(stream, device):
+    """CUDA stream handle for the C ABI.  torch's default stream has handle 0,
+    which the C ABI reads as 'context stream'; map it to cudaStreamLegacy (1)
+    so kernels order with torch work on the default stream."""
+    if stream is None:
+        stream = _torch().cuda.current_stream(device).cuda_stream
+    return stream if stream else 1
+
+
 def _dev_vec(op: EmbeddedSpectrum, x):
     torch = _torch()
     n = op.n_cur * op.n_vox
@@ -254,8 +263,7 @@ def apply_operator(op: EmbeddedSpectrum, x, strategy: str = "hosvd_decompress", 
     torch = _torch()
     x = _dev_vec(op, x)
     y = out if out is not None else torch.empty_like(x)
-    st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
-    _check(lib().vie_matvec(op.handle, x.data_ptr(), y.data_ptr(), st))
+    _check(lib().vie_matvec(op.handle, x.data_ptr(), y.data_ptr(), _stream_handle(stream, x.device)))
     return y
 
 
@@ -267,9 +275,8 @@ def apply_system(eps_r, inv_v: float, op: EmbeddedSpectrum, x, out=None, diag_te
         raise ValueError("apply_system: dim mismatch")
     eps_r = eps_r.to(torch.complex128).contiguous()
     y = out if out is not None else torch.empty_like(x)
-    st = stream if stream is not None else torch.cuda.current_stream(x.device).cuda_stream
     _check(lib().vie_system_matvec(op.handle, eps_r.data_ptr(), float(inv_v), x.data_ptr(), y.data_ptr(),
-                                   int(bool(diag_term)), st))
+                                   int(bool(diag_term)), _stream_handle(stream, x.device)))
     return y
 
 
