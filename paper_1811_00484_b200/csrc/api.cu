@@ -108,8 +108,9 @@ struct vie_op_s {
   double2* Shat = nullptr;
   double2* A = nullptr;
   double2* B = nullptr;
+  double2* Bo = nullptr;  // pencil output slab
   int64_t ws_bytes = 0;
-  FftPlan P1{}, P2{}, P3{};
+  FftPlan P1{}, P2{}, P3{}, PH{};
   // host-buffer staging (vie_matvec_host)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -127,7 +128,7 @@ struct vie_op_s {
   cudaEvent_t ev[8] = {};
   ~vie_op_s() {
     for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
-                    static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B),
+                    static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(V),
                     static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
@@ -140,23 +141,44 @@ struct vie_op_s {
 namespace {
 
 // ---------------------------------------------------------------- FFT plans
-const FftPlan& get_plan(vie_ctx ctx, int n) {
+// Radix set of the register DFTs (fft.cuh VIE_FFT_RADICES).  Radices are capped
+// at kMaxRadix: larger register DFTs raise register pressure and cut the warps
+// per SM below what the shared-memory passes need to hide latency (ncu r1).
+const int kRadices[] = {10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES
+constexpr int kMaxRadix = 10;
+
+// Fewest stages, then smallest largest radix; first radix even when the
+// transform is pad/crop pruned (half_in / half_out).
+bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::vector<int>& best) {
+  if (n == 1) {
+    if (best.empty() || cur.size() < best.size() ||
+        (cur.size() == best.size() && *std::max_element(cur.begin(), cur.end()) <
+                                          *std::max_element(best.begin(), best.end())))
+      best = cur;
+    return true;
+  }
+  if (depth == 0) return false;
+  bool any = false;
+  for (int r : kRadices) {
+    if (r > kMaxRadix || n % r) continue;
+    if (even_first && cur.empty() && (r & 1)) continue;
+    cur.push_back(r);
+    any |= factor_plan(n / r, even_first, depth - 1, cur, best);
+    cur.pop_back();
+  }
+  return any;
+}
+
+const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true) {
+  const int key = pruned ? n : -n;
   std::lock_guard<std::mutex> lk(ctx->mu);
-  auto it = ctx->plans.find(n);
+  auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) return it->second->plan;
-  if (n < 2 || (n & 1)) throw Invalid("FFT plan: embedded length must be even and >= 2");
-  std::vector<int> rad;
-  int rest = n;
-  rad.push_back(rest % 4 == 0 ? 4 : 2);  // even first radix: pad/crop pruning
-  rest /= rad.back();
-  while (rest % 8 == 0) { rad.push_back(8); rest /= 8; }
-  while (rest % 4 == 0) { rad.push_back(4); rest /= 4; }
-  while (rest % 2 == 0) { rad.push_back(2); rest /= 2; }
-  for (int p : {3, 5, 7})
-    while (rest % p == 0) { rad.push_back(p); rest /= p; }
-  if (rest != 1)
-    throw Invalid("FFT plan: embedded length " + std::to_string(n) + " has a prime factor > 7");
-  if (static_cast<int>(rad.size()) > vie::kMaxStages) throw Invalid("FFT plan: too many stages");
+  if (n < 1 || (pruned && (n & 1))) throw Invalid("FFT plan: embedded length must be even");
+  std::vector<int> rad, cur;
+  for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth) factor_plan(n, pruned, depth, cur, rad);
+  if (n > 1 && rad.empty())
+    throw Invalid("FFT plan: length " + std::to_string(n) + " has a prime factor > 7");
   auto h = std::make_unique<PlanHolder>();
   FftPlan& P = h->plan;
   P.n = n;
@@ -196,7 +218,7 @@ const FftPlan& get_plan(vie_ctx ctx, int n) {
   P.slot = h->slot;
   P.st = h->st;
   const FftPlan& ref = h->plan;
-  ctx->plans[n] = std::move(h);
+  ctx->plans[key] = std::move(h);
   return ref;
 }
 
@@ -249,9 +271,9 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   mark();
   vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
   mark();
-  vie::launch_pencil(op->kind, op->basis, op->B, op->Shat, g, op->P3, op->active, st);
+  vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->PH, op->P3.tw, op->active, st);
   mark();
-  vie::launch_col_inv(op->B, op->A, g, op->P2, st);
+  vie::launch_col_inv(op->Bo, op->A, g, op->P2, st);
   mark();
   // reference inverse3 divides by N_e (fft.hpp:34-37)
   vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
@@ -504,7 +526,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     }
     if (vie::decomp_smem(g.n3, op->rmax) > 220 * 1024)
       throw Invalid("vie_op_create: Tucker rank too large for the decompression tile (rank * (n3 + 1) too big)");
-    if (vie::pencil_smem(g.m3, g.S) > 220 * 1024) throw Invalid("vie_op_create: grid edge n3 too large");
+    if (vie::pencil_smem(g.n3, g.S, g.NC) > vie::kMaxSmem) throw Invalid("vie_op_create: grid edge n3 too large");
     op->forms = dev_alloc<double2>(static_cast<size_t>(off));
     for (size_t c = 0; c < cs.size(); ++c) {
       const vie_tucker_s* t = byc[c];
@@ -528,10 +550,12 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->Shat = dev_alloc<double2>(static_cast<size_t>(noct * g.NC));
     op->A = dev_alloc<double2>(static_cast<size_t>(g.S * 2 * nv));
     op->B = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
-    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 6 * nv);
+    op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
+    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 10 * nv);
     op->P1 = get_plan(ctx, g.m1);
     op->P2 = get_plan(ctx, g.m2);
     op->P3 = get_plan(ctx, g.m3);
+    op->PH = get_plan(ctx, g.n3, false);
     *out = op.release();
   });
 }

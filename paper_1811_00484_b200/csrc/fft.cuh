@@ -1,128 +1,184 @@
-// fft.cuh -- in-shared-memory mixed-radix FP64 FFT stages for sm_100a.
+// fft.cuh -- in-shared-memory mixed-radix FP64 FFT passes for sm_100a.
 //
-// Forward: decimation-in-frequency, in place, output in digit-reversed slots:
-//   stage s (block length L, radix r, M = L/r): for each block b and m < M
-//   V[k] = DFT_r(x[bL + m + iM])_k * w_L^{k m}  -> x[bL + m + kM].
-// The frequency f = k1 + r1 k2 + r1 r2 k3 + ... lands in slot sum_s k_s M_s.
-// Inverse: the exact adjoint of the forward stages applied in reverse order,
-// consuming digit-reversed slots and producing natural order (unnormalised).
+// Each stage is one shared-memory pass: a thread loads R elements (stride M),
+// runs a radix-R DFT entirely in registers (compile-time factorised, constant
+// twiddles), applies the stage twiddles and stores in place.  Plans use 2-3
+// stages with radices up to 25, so a length-400 line costs two smem round
+// trips instead of four (the v1 radix-4/5 passes were smem-bandwidth bound).
 //
-// Pruning: `half_in` (forward) means the upper half of every line is zero
-// (the circulant pad, operator.hpp:290-297) and is never read; `half_out`
-// (inverse) means only the lower half is needed (the crop, :367-375).  Both
-// need an even first radix.
+// Forward: decimation in frequency, output in digit-reversed slots:
+//   stage s (block length L, radix R, M = L/R): for block b and m < M
+//   V[k] = DFT_R(x[bL + m + iM])_k * w_L^{k m}  ->  x[bL + m + kM]
+// frequency f = k1 + R1 k2 + R1 R2 k3 + ... lands in slot sum_s k_s M_s.
+// Inverse: the exact adjoint of the forward stages in reverse order
+// (digit-reversed in, natural order out, unnormalised).
+// Pruning: `half_in` (forward, first stage) = upper half of every line is
+// the circulant zero pad (operator.hpp:290-297) and is never read; `half_out`
+// (inverse, last stage) = only the lower half is kept (the crop, :367-375).
 #pragma once
+#include <type_traits>
+#include <utility>
+
 #include "common.cuh"
+#include "twiddles_gen.cuh"
 
 namespace vie {
 
-template <int R, bool INV>
-struct Bfly {
-  // generic prime radix via the twiddle table (w_R^{jk} = w_N^{(jk mod R) N/R})
-  __device__ __forceinline__ static void run(double2* v, const double2* tw, int n_over_r) {
-    double2 o[R];
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      double2 acc = v[0];
-#pragma unroll
-      for (int j = 1; j < R; ++j) {
-        double2 w = tw[((j * k) % R) * n_over_r];
-        if (INV) w.y = -w.y;
-        cfma(acc, v[j], w);
-      }
-      o[k] = acc;
-    }
-#pragma unroll
-    for (int k = 0; k < R; ++k) v[k] = o[k];
+// ----------------------------------------------------------------- register DFTs
+// In-place radix-R DFT on the register view v[OFF + ST*i], i < R, fully
+// unrolled (compile-time indices).  Composite R = A*B: A-point DFTs over the
+// strided subsets, constant twiddles, B-point DFTs; the result X[k] is left
+// at register OFF + ST*out_idx<R>(k) (a compile-time permutation, free).
+constexpr int first_factor(int R) {
+  return (R % 4 == 0 && R > 4) ? 4 : (R % 2 == 0 ? 2 : (R % 3 == 0 ? 3 : (R % 5 == 0 ? 5 : R)));
+}
+constexpr bool is_base(int R) { return R == 1 || R == 2 || R == 3 || R == 4 || R == 5 || R == 7; }
+constexpr int out_idx(int R, int k) {
+  return is_base(R) ? k
+                    : (R / first_factor(R)) * out_idx(first_factor(R), k % first_factor(R)) +
+                          out_idx(R / first_factor(R), k / first_factor(R));
+}
+
+template <int... Is, class F>
+__device__ __forceinline__ void sfor_impl(std::integer_sequence<int, Is...>, F&& f) {
+  (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  sfor_impl(std::make_integer_sequence<int, N>{}, f);
+}
+
+// x * exp(-+2 pi i e / R), e a compile-time constant
+template <int R, bool INV, int E0>
+__device__ __forceinline__ double2 twc(double2 x) {
+  constexpr int e = E0 % R;
+  if constexpr (e == 0) {
+    return x;
+  } else if constexpr (4 * e == R) {
+    return mul_mi<INV>(x);  // -i (fwd) / +i (inv)
+  } else if constexpr (2 * e == R) {
+    return make_double2(-x.x, -x.y);
+  } else if constexpr (4 * e == 3 * R) {
+    return mul_mi<!INV>(x);
+  } else {
+    constexpr double c = tw_re(R, e);
+    constexpr double s = INV ? -tw_im(R, e) : tw_im(R, e);
+    return make_double2(fma(x.x, c, -x.y * s), fma(x.x, s, x.y * c));
+  }
+}
+
+template <int R, bool INV, int ST, int OFF>
+struct DFTs {
+  static constexpr int A = first_factor(R);
+  static constexpr int B = R / A;
+  __device__ __forceinline__ static void run(double2* v) {
+    sfor<B>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      DFTs<A, INV, ST * B, OFF + ST * n2>::run(v);
+      sfor<A>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        constexpr int pos = OFF + ST * (B * out_idx(A, k1) + n2);
+        v[pos] = twc<R, INV, n2 * k1>(v[pos]);
+      });
+    });
+    sfor<A>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      DFTs<B, INV, ST, OFF + ST * B * out_idx(A, k1)>::run(v);
+    });
   }
 };
 
-template <bool INV>
-struct Bfly<2, INV> {
-  __device__ __forceinline__ static void run(double2* v, const double2*, int) {
-    const double2 a = v[0], b = v[1];
-    v[0] = cadd(a, b);
-    v[1] = csub(a, b);
+template <bool INV, int ST, int OFF>
+struct DFTs<1, INV, ST, OFF> {
+  __device__ __forceinline__ static void run(double2*) {}
+};
+
+template <bool INV, int ST, int OFF>
+struct DFTs<2, INV, ST, OFF> {
+  __device__ __forceinline__ static void run(double2* v) {
+    const double2 a = v[OFF], b = v[OFF + ST];
+    v[OFF] = cadd(a, b);
+    v[OFF + ST] = csub(a, b);
   }
 };
 
-template <bool INV>
-struct Bfly<3, INV> {
-  __device__ __forceinline__ static void run(double2* v, const double2*, int) {
+template <bool INV, int ST, int OFF>
+struct DFTs<3, INV, ST, OFF> {
+  __device__ __forceinline__ static void run(double2* v) {
     const double s3 = 0.86602540378443864676372317075294;
-    const double2 t1 = cadd(v[1], v[2]);
-    const double2 t2 = make_double2(fma(-0.5, t1.x, v[0].x), fma(-0.5, t1.y, v[0].y));
-    const double2 d = csub(v[1], v[2]);
+    const double2 x0 = v[OFF], x1 = v[OFF + ST], x2 = v[OFF + 2 * ST];
+    const double2 t1 = cadd(x1, x2);
+    const double2 t2 = make_double2(fma(-0.5, t1.x, x0.x), fma(-0.5, t1.y, x0.y));
+    const double2 d = csub(x1, x2);
     const double2 t3 = mul_mi<INV>(make_double2(s3 * d.x, s3 * d.y));
-    v[0] = cadd(v[0], t1);
-    v[1] = cadd(t2, t3);
-    v[2] = csub(t2, t3);
+    v[OFF] = cadd(x0, t1);
+    v[OFF + ST] = cadd(t2, t3);
+    v[OFF + 2 * ST] = csub(t2, t3);
   }
 };
 
-template <bool INV>
-struct Bfly<4, INV> {
-  __device__ __forceinline__ static void run(double2* v, const double2*, int) {
-    const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
-    const double2 s13 = cadd(v[1], v[3]), d13 = mul_mi<INV>(csub(v[1], v[3]));
-    v[0] = cadd(s02, s13);
-    v[1] = cadd(d02, d13);
-    v[2] = csub(s02, s13);
-    v[3] = csub(d02, d13);
+template <bool INV, int ST, int OFF>
+struct DFTs<4, INV, ST, OFF> {
+  __device__ __forceinline__ static void run(double2* v) {
+    const double2 x0 = v[OFF], x1 = v[OFF + ST], x2 = v[OFF + 2 * ST], x3 = v[OFF + 3 * ST];
+    const double2 s02 = cadd(x0, x2), d02 = csub(x0, x2);
+    const double2 s13 = cadd(x1, x3), d13 = mul_mi<INV>(csub(x1, x3));
+    v[OFF] = cadd(s02, s13);
+    v[OFF + ST] = cadd(d02, d13);
+    v[OFF + 2 * ST] = csub(s02, s13);
+    v[OFF + 3 * ST] = csub(d02, d13);
   }
 };
 
-template <bool INV>
-struct Bfly<5, INV> {
-  __device__ __forceinline__ static void run(double2* v, const double2*, int) {
+template <bool INV, int ST, int OFF>
+struct DFTs<5, INV, ST, OFF> {
+  __device__ __forceinline__ static void run(double2* v) {
     const double c1 = 0.30901699437494742410229341718282;   // cos(2pi/5)
     const double c2 = -0.80901699437494742410229341718282;  // cos(4pi/5)
     const double s1 = 0.95105651629515357211643933337938;   // sin(2pi/5)
     const double s2 = 0.58778525229247312916870595463907;   // sin(4pi/5)
-    const double2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
-    const double2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
-    const double2 a1 = make_double2(fma(c2, t2.x, fma(c1, t1.x, v[0].x)), fma(c2, t2.y, fma(c1, t1.y, v[0].y)));
-    const double2 a2 = make_double2(fma(c1, t2.x, fma(c2, t1.x, v[0].x)), fma(c1, t2.y, fma(c2, t1.y, v[0].y)));
+    const double2 x0 = v[OFF];
+    const double2 t1 = cadd(v[OFF + ST], v[OFF + 4 * ST]), t2 = cadd(v[OFF + 2 * ST], v[OFF + 3 * ST]);
+    const double2 t3 = csub(v[OFF + ST], v[OFF + 4 * ST]), t4 = csub(v[OFF + 2 * ST], v[OFF + 3 * ST]);
+    const double2 a1 = make_double2(fma(c2, t2.x, fma(c1, t1.x, x0.x)), fma(c2, t2.y, fma(c1, t1.y, x0.y)));
+    const double2 a2 = make_double2(fma(c1, t2.x, fma(c2, t1.x, x0.x)), fma(c1, t2.y, fma(c2, t1.y, x0.y)));
     const double2 b1 = mul_mi<INV>(make_double2(fma(s2, t4.x, s1 * t3.x), fma(s2, t4.y, s1 * t3.y)));
     const double2 b2 = mul_mi<INV>(make_double2(fma(-s1, t4.x, s2 * t3.x), fma(-s1, t4.y, s2 * t3.y)));
-    v[0] = cadd(v[0], cadd(t1, t2));
-    v[1] = cadd(a1, b1);
-    v[4] = csub(a1, b1);
-    v[2] = cadd(a2, b2);
-    v[3] = csub(a2, b2);
+    v[OFF] = cadd(x0, cadd(t1, t2));
+    v[OFF + ST] = cadd(a1, b1);
+    v[OFF + 4 * ST] = csub(a1, b1);
+    v[OFF + 2 * ST] = cadd(a2, b2);
+    v[OFF + 3 * ST] = csub(a2, b2);
   }
 };
 
-template <bool INV>
-struct Bfly<8, INV> {
-  __device__ __forceinline__ static void run(double2* v, const double2* tw, int n_over_r) {
-    const double h = 0.70710678118654752440084436210485;
-    // radix-2 x 4: even/odd split
-    double2 e[4] = {v[0], v[2], v[4], v[6]};
-    double2 o[4] = {v[1], v[3], v[5], v[7]};
-    Bfly<4, INV>::run(e, tw, n_over_r);
-    Bfly<4, INV>::run(o, tw, n_over_r);
-    // o[k] *= w8^k
-    const double2 o1 = o[1], o2 = o[2], o3 = o[3];
-    o[1] = INV ? make_double2(h * (o1.x - o1.y), h * (o1.x + o1.y)) : make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x));
-    o[2] = mul_mi<INV>(o2);
-    o[3] = INV ? make_double2(-h * (o3.x + o3.y), h * (o3.x - o3.y)) : make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      v[k] = cadd(e[k], o[k]);
-      v[k + 4] = csub(e[k], o[k]);
-    }
+template <bool INV, int ST, int OFF>
+struct DFTs<7, INV, ST, OFF> {  // direct form with constant twiddles
+  __device__ __forceinline__ static void run(double2* v) {
+    double2 x[7], o[7];
+    sfor<7>([&](auto jc) { x[decltype(jc)::value] = v[OFF + ST * decltype(jc)::value]; });
+    sfor<7>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      double2 acc = x[0];
+      sfor<6>([&](auto jc) {
+        constexpr int j = decltype(jc)::value + 1;
+        acc = cadd(acc, twc<7, INV, j * k>(x[j]));
+      });
+      o[k] = acc;
+    });
+    sfor<7>([&](auto kc) { v[OFF + ST * decltype(kc)::value] = o[decltype(kc)::value]; });
   }
 };
 
-// One forward DIF stage over `nlines` lines (line stride `ls` elements).
+// ----------------------------------------------------------------- stages
+// Stage twiddles w_L^{k m} = tw[k m tws]: w^1 from the table, higher powers by
+// recurrence (error ~k eps, k < 25).
 template <int R>
 __device__ __forceinline__ void dif_stage(double2* buf, int nlines, int ls, int n, const StageDesc& sd,
                                           const double2* tw, bool half_in, int tid, int nth) {
   const int M = sd.M, L = sd.L, tws = sd.tws;
   const int nbf = n / R;
   const int total = nlines * nbf;
-  const int nr = n / R;
   for (int u = tid; u < total; u += nth) {
     const int line = sd.div_nbf.div(u);
     const int bm = u - line * nbf;
@@ -137,21 +193,31 @@ __device__ __forceinline__ void dif_stage(double2* buf, int nlines, int ls, int 
 #pragma unroll
       for (int i = 0; i < R; ++i) v[i] = base[i * M];
     }
-    Bfly<R, false>::run(v, tw, nr);
-    base[0] = v[0];
-#pragma unroll
-    for (int k = 1; k < R; ++k) base[k * M] = (m == 0) ? v[k] : cmul(v[k], tw[k * m * tws]);
+    DFTs<R, false, 1, 0>::run(v);
+    base[0] = v[out_idx(R, 0)];
+    if (m == 0) {
+      sfor<R - 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value + 1;
+        base[k * M] = v[out_idx(R, k)];
+      });
+    } else {
+      const double2 w1 = tw[m * tws];
+      double2 w = w1;
+      sfor<R - 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value + 1;
+        base[k * M] = cmul(v[out_idx(R, k)], w);
+        if (k + 1 < R) w = cmul(w, w1);
+      });
+    }
   }
 }
 
-// One inverse (adjoint) stage.
 template <int R>
 __device__ __forceinline__ void dit_stage_adj(double2* buf, int nlines, int ls, int n, const StageDesc& sd,
                                               const double2* tw, bool half_out, int tid, int nth) {
   const int M = sd.M, L = sd.L, tws = sd.tws;
   const int nbf = n / R;
   const int total = nlines * nbf;
-  const int nr = n / R;
   for (int u = tid; u < total; u += nth) {
     const int line = sd.div_nbf.div(u);
     const int bm = u - line * nbf;
@@ -160,18 +226,35 @@ __device__ __forceinline__ void dit_stage_adj(double2* buf, int nlines, int ls, 
     double2* base = buf + line * ls + b * L + m;
     double2 v[R];
     v[0] = base[0];
+    if (m == 0) {
 #pragma unroll
-    for (int k = 1; k < R; ++k) v[k] = (m == 0) ? base[k * M] : cmulc(base[k * M], tw[k * m * tws]);
-    Bfly<R, true>::run(v, tw, nr);
-    if (half_out) {
-#pragma unroll
-      for (int i = 0; i < R / 2; ++i) base[i * M] = v[i];
+      for (int k = 1; k < R; ++k) v[k] = base[k * M];
     } else {
+      const double2 w1 = tw[m * tws];
+      double2 w = w1;
 #pragma unroll
-      for (int i = 0; i < R; ++i) base[i * M] = v[i];
+      for (int k = 1; k < R; ++k) {
+        v[k] = cmulc(base[k * M], w);
+        if (k + 1 < R) w = cmul(w, w1);
+      }
+    }
+    DFTs<R, true, 1, 0>::run(v);
+    if (half_out) {
+      sfor<R / 2>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        base[i * M] = v[out_idx(R, i)];
+      });
+    } else {
+      sfor<R>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        base[i * M] = v[out_idx(R, i)];
+      });
     }
   }
 }
+
+// Radices the plans may use (api.cu get_plan chooses among these).
+#define VIE_FFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10)
 
 template <bool INV>
 __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int n, const StageDesc& sd,
@@ -182,12 +265,7 @@ __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int 
     if (INV) dit_stage_adj<R>(buf, nlines, ls, n, sd, tw, prune, tid, nth);  \
     else dif_stage<R>(buf, nlines, ls, n, sd, tw, prune, tid, nth);          \
     break;
-    VIE_CASE(2)
-    VIE_CASE(3)
-    VIE_CASE(4)
-    VIE_CASE(5)
-    VIE_CASE(7)
-    VIE_CASE(8)
+    VIE_FFT_RADICES(VIE_CASE)
 #undef VIE_CASE
     default:
       break;  // plan creation rejects other radices

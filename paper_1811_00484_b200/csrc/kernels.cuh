@@ -28,16 +28,19 @@ constexpr int kRowsPerCta = 8;     // row FFT kernels
 constexpr int kColsPerCta = 8;     // column FFT kernels (128 B segments)
 constexpr int kPencilLines = 24;   // pencil kernel: S * W lines in smem
 constexpr int kThreads = 256;
+constexpr size_t kMaxSmem = 227 * 1024;  // per-CTA dynamic shared memory limit (sm_100a)
 
 size_t row_smem(int m);
 size_t col_smem(int m);
-size_t pencil_smem(int m3, int S);
+size_t pencil_smem(int n3, int S, int NC);  // (size_t)-1 if it does not fit
 size_t decomp_smem(int n3, int rmax);
 
 void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& P1, cudaStream_t st);
 void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& P2, cudaStream_t st);
-void launch_pencil(int kind, int basis, double2* B, const double2* Shat, const Geom& g, const FftPlan& P3,
-                   uint64_t active_mask, cudaStream_t st);
+// Bin: forward slab (after axes 1-2); Bout: output slab (before the axis-2/1
+// inverses); PH: n3-point plan; twm3: w_m3^e table of the m3-point plan.
+void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+                   const FftPlan& PH, const double2* twm3, uint64_t active_mask, cudaStream_t st);
 void launch_col_inv(const double2* B, double2* A, const Geom& g, const FftPlan& P2, cudaStream_t st);
 // Epilogue: y = scale * (IDFT) or the system form (eps != nullptr):
 //   y = (diag ? eps*g_l*xin : 0) - (eps - 1) * inv_v * scale * (IDFT)

@@ -7,7 +7,9 @@
 // the dominant r3 * N_e flops), for all components at once:
 //   k_decomp_z : Z_c[p2][a][g] = sum_b G_c[a,b,g] U2_c[p2,b]        (r^3 per p2)
 //   k_decomp_s : T = U1_c Z_c[p2]  (n1+1 x r3),  S^_c[p2][p1][f3] = T U3_c^T
-// Output layout Shat[p2o][p1o][c][f3o], f3o fastest, read by the pencil kernel.
+// Output layout Shat[p2o][p1o][c][bidx(f3o)], axis 3 branch-major (even
+// octant frequencies 0,2,.. first, then odd 1,3,..) to match the pencil
+// kernel's even/odd half-length branches.
 #include "kernels.cuh"
 
 namespace vie {
@@ -92,14 +94,17 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
 #pragma unroll
           for (int j = 0; j < kQ; ++j) cfma(acc[i][j], tv[i], uv[j]);
       }
+      const int E = geo.n3 / 2 + 1;
 #pragma unroll
       for (int i = 0; i < kQ; ++i) {
         const int p1o = p10 + rq * kQ + i;
         if (rq * kQ + i >= np1) break;
-        double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + p1o) * NC + c) * n3p + f0;
+        double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + p1o) * NC + c) * n3p;
 #pragma unroll
-        for (int j = 0; j < kQ; ++j)
-          if (f0 + j < n3p) dst[j] = acc[i][j];
+        for (int j = 0; j < kQ; ++j) {
+          const int f = f0 + j;
+          if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = acc[i][j];
+        }
       }
     }
   }

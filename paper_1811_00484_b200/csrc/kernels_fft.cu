@@ -16,7 +16,7 @@ namespace {
 __host__ __device__ __forceinline__ int line_stride(int n) { return n + 1; }
 
 // -------------------------------------------------------------------- rows
-__global__ void __launch_bounds__(kThreads) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
+__global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
                                                       int n1, int nrows, FftPlan P) {
   extern __shared__ double2 sm[];
   const int m = P.n;
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kThreads) k_row_fwd(const double2* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_row_inv(const double2* __restrict__ A, double2* __restrict__ y,
+__global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restrict__ A, double2* __restrict__ y,
                                                       int n1, int nrows, int rows_per_comp, int64_t nv, FftPlan P,
                                                       double scale, const double2* __restrict__ eps,
                                                       const double2* __restrict__ xin, double inv_v, int lin,
@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) k_row_inv(const double2* __restrict_
 // -------------------------------------------------------------------- columns
 // A: planes of n2 rows x m1 (row-major, column index fastest) -> B: planes of
 // m2 rows x m1; W consecutive columns per CTA.
-__global__ void __launch_bounds__(kThreads) k_col_fwd(const double2* __restrict__ A, double2* __restrict__ B,
+__global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restrict__ A, double2* __restrict__ B,
                                                       int n2, int m1, FftPlan P) {
   extern __shared__ double2 sm[];
   const int m = P.n;
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(kThreads) k_col_fwd(const double2* __restrict_
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_col_inv(const double2* __restrict__ B, double2* __restrict__ A,
+__global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restrict__ B, double2* __restrict__ A,
                                                       int n2, int m1, FftPlan P) {
   extern __shared__ double2 sm[];
   const int m = P.n;
