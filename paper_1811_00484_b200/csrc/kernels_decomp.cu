@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
   const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major: u3[f + n3p*g]
   for (int e = threadIdx.x; e < r3 * n3p; e += blockDim.x) us[e] = u3[e];
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
-  const int nfq = (n3p + kQ - 1) / kQ;
   for (int p10 = 0; p10 < n1p; p10 += kTP1) {
     const int np1 = min(kTP1, n1p - p10);
     __syncthreads();
@@ -74,27 +73,34 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
       ts[g * kTP1 + i] = acc;
     }
     __syncthreads();
-    const int tiles = (kTP1 / kQ) * nfq;
-    for (int t = threadIdx.x; t < tiles; t += blockDim.x) {
-      const int fq = t % nfq, rq = t / nfq;
+    // warp tile: 4 rows (p1o) x 128 columns (f3o = fb + lane + 32 j): T values
+    // are warp broadcasts, U3 values are read by consecutive lanes (no bank
+    // conflicts), 16 complex accumulators per thread.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    const int nfb = (n3p + 127) / 128;
+    const int wtiles = (kTP1 / kQ) * nfb;
+    const int E = geo.n3 / 2 + 1;
+    for (int t = warp; t < wtiles; t += nwarp) {
+      const int fb = (t % nfb) * 128, rq = t / nfb;
       double2 acc[kQ][kQ];
 #pragma unroll
       for (int i = 0; i < kQ; ++i)
 #pragma unroll
         for (int j = 0; j < kQ; ++j) acc[i][j] = make_double2(0.0, 0.0);
-      const int f0 = fq * kQ;
       for (int g = 0; g < r3; ++g) {
         double2 tv[kQ], uv[kQ];
 #pragma unroll
         for (int i = 0; i < kQ; ++i) tv[i] = ts[g * kTP1 + rq * kQ + i];
 #pragma unroll
-        for (int j = 0; j < kQ; ++j) uv[j] = (f0 + j < n3p) ? us[g * n3p + f0 + j] : make_double2(0.0, 0.0);
+        for (int j = 0; j < kQ; ++j) {
+          const int f = fb + lane + 32 * j;
+          uv[j] = f < n3p ? us[g * n3p + f] : make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int i = 0; i < kQ; ++i)
 #pragma unroll
           for (int j = 0; j < kQ; ++j) cfma(acc[i][j], tv[i], uv[j]);
       }
-      const int E = geo.n3 / 2 + 1;
 #pragma unroll
       for (int i = 0; i < kQ; ++i) {
         const int p1o = p10 + rq * kQ + i;
@@ -102,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
         double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + p1o) * NC + c) * n3p;
 #pragma unroll
         for (int j = 0; j < kQ; ++j) {
-          const int f = f0 + j;
+          const int f = fb + lane + 32 * j;
           if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = acc[i][j];
         }
       }

@@ -15,6 +15,16 @@ namespace {
 // smem carve-up: [plan tables][lines]
 __host__ __device__ __forceinline__ int line_stride(int n) { return n + 1; }
 
+// global -> shared 16-byte copies without register staging (full MLP)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // -------------------------------------------------------------------- rows
 __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
                                                       int n1, int nrows, FftPlan P) {
@@ -29,8 +39,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restri
   const double2* src = x + static_cast<int64_t>(row0) * n1;
   for (int e = threadIdx.x; e < nr * n1; e += blockDim.x) {
     const int r = e / n1, i = e - r * n1;
-    buf[r * ls + i] = src[e];
+    cp_async16(buf + r * ls + i, src + e);
   }
+  cp_async_wait();
   __syncthreads();
   fft_forward(buf, nr, ls, SP, true);
   double2* dst = A + static_cast<int64_t>(row0) * m;
@@ -57,8 +68,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restri
   const double2* src = A + static_cast<int64_t>(row0) * m;
   for (int e = threadIdx.x; e < nr * m; e += blockDim.x) {
     const int r = e / m, pos = e - r * m;
-    buf[r * ls + slot_s[freq_of_pos(pos, n1)]] = src[e];
+    cp_async16(buf + r * ls + slot_s[freq_of_pos(pos, n1)], src + e);
   }
+  cp_async_wait();
   __syncthreads();
   fft_inverse(buf, nr, ls, SP, true);
   double2* dst = y + static_cast<int64_t>(row0) * n1;
@@ -102,8 +114,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restri
   const double2* src = A + plane * n2 * m1 + c0;
   for (int e = threadIdx.x; e < n2 * kColsPerCta; e += blockDim.x) {
     const int j = e / kColsPerCta, w = e - j * kColsPerCta;
-    if (w < wc) buf[w * ls + j] = src[static_cast<int64_t>(j) * m1 + w];
+    if (w < wc) cp_async16(buf + w * ls + j, src + static_cast<int64_t>(j) * m1 + w);
   }
+  cp_async_wait();
   __syncthreads();
   fft_forward(buf, wc, ls, SP, true);
   double2* dst = B + plane * m * m1 + c0;
@@ -128,8 +141,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restri
   const double2* src = B + plane * m * m1 + c0;
   for (int e = threadIdx.x; e < m * kColsPerCta; e += blockDim.x) {
     const int pos = e / kColsPerCta, w = e - pos * kColsPerCta;
-    if (w < wc) buf[w * ls + slot_s[freq_of_pos(pos, n2)]] = src[static_cast<int64_t>(pos) * m1 + w];
+    if (w < wc) cp_async16(buf + w * ls + slot_s[freq_of_pos(pos, n2)], src + static_cast<int64_t>(pos) * m1 + w);
   }
+  cp_async_wait();
   __syncthreads();
   fft_inverse(buf, wc, ls, SP, true);
   double2* dst = A + plane * n2 * m1 + c0;
