@@ -1,0 +1,352 @@
+// vie_b200.hpp -- C++ drop-in over the C ABI (vie_b200.h), mirroring the
+// reference operator API (/root/reference/proj/include/vie, header-only C++):
+//
+//   reference                                  here (namespace vie::b200)
+//   DftService            fft.hpp:13-96        DftService (CUDA device + stream + plans)
+//   hosvd / TuckerForm     decomp.hpp:123-176   TuckerForm (spatial-domain forms)
+//   component_parity       components.hpp:51    component_parity
+//   build_operator_spectra operator.hpp:144     build_operator_spectra (Tucker only)
+//   apply_operator         operator.hpp:273     apply_operator (HosvdDecompress semantics)
+//   apply_system           solver.hpp:183       apply_system
+//   gmres / GmresConfig    solver.hpp:12-142    gmres_system (device-resident GMRES)
+//
+// Same argument meaning and error behaviour: std::invalid_argument where the
+// reference throws it (dim mismatch, missing representation, NoBuffer with a
+// decompress strategy, bad GMRES config, non-finite rhs); std::runtime_error
+// for CUDA failures.  Containers are plain std::vector<std::complex<double>>
+// in the reference layouts (Tensor3: i + n1*(j + n2*k); factors column-major;
+// fields component-major), so no Eigen is needed to use it.
+#ifndef VIE_B200_HPP
+#define VIE_B200_HPP
+
+#include <cuda_runtime_api.h>
+
+#include <array>
+#include <complex>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "vie_b200.h"
+
+namespace vie {
+namespace b200 {
+
+using cplx = std::complex<double>;
+using Index = std::int64_t;
+
+enum class OperatorKind { N = VIE_KIND_N, K = VIE_KIND_K };
+enum class BasisOrder { PWC = VIE_BASIS_PWC, PWL = VIE_BASIS_PWL };
+enum class MatvecStrategy { HosvdDecompress, HosvdLoop };
+enum class ScratchPolicy { WithBuffer, NoBuffer };
+
+inline void check(int rc) {
+  if (rc == VIE_OK) return;
+  if (rc == VIE_EINVAL) throw std::invalid_argument(vie_last_error());
+  throw std::runtime_error(std::string("vie_b200: ") + vie_last_error());
+}
+inline void cuda_check(cudaError_t e) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA: ") + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ containers
+struct Tensor3 {  // tensor.hpp:17-71
+  std::array<Index, 3> dims{0, 0, 0};
+  std::vector<cplx> data;
+  Tensor3() = default;
+  Tensor3(Index n1, Index n2, Index n3) : dims{n1, n2, n3}, data(static_cast<size_t>(n1 * n2 * n3)) {
+    if (n1 < 0 || n2 < 0 || n3 < 0) throw std::invalid_argument("Tensor3: negative dimension");
+  }
+  Index size() const { return static_cast<Index>(data.size()); }
+  cplx& operator()(Index i, Index j, Index k) { return data[static_cast<size_t>(i + dims[0] * (j + dims[1] * k))]; }
+  cplx operator()(Index i, Index j, Index k) const {
+    return data[static_cast<size_t>(i + dims[0] * (j + dims[1] * k))];
+  }
+};
+
+struct FactorMatrix {  // column-major rows x cols (Eigen::MatrixXcd layout)
+  Index rows = 0, cols = 0;
+  std::vector<cplx> data;
+  FactorMatrix() = default;
+  FactorMatrix(Index r, Index c) : rows(r), cols(c), data(static_cast<size_t>(r * c)) {}
+  cplx& operator()(Index i, Index j) { return data[static_cast<size_t>(i + rows * j)]; }
+  cplx operator()(Index i, Index j) const { return data[static_cast<size_t>(i + rows * j)]; }
+};
+
+// Spatial-domain Tucker form as hosvd returns it (decomp.hpp:123-133).
+struct TuckerForm {
+  Tensor3 core;                          // r1 x r2 x r3
+  std::array<FactorMatrix, 3> factors;   // n_q x r_q
+  std::array<Index, 3> ranks{0, 0, 0};
+};
+
+struct KernelComponent {  // components.hpp:26-36 (+ PWL polynomial indices)
+  OperatorKind op = OperatorKind::N;
+  int row_axis = 0;
+  int col_axis = 0;
+  int row_poly = 0;  // l  (PWL: 0 constant, 1..3 linear in x, y, z)
+  int col_poly = 0;  // l'
+};
+
+struct Parity {  // components.hpp:40-44
+  std::array<int, 3> sign{1, 1, 1};
+  int product() const { return sign[0] * sign[1] * sign[2]; }
+};
+
+// Reflection parity of a component (components.hpp:51-65; PWL: DESIGN.md).
+inline Parity component_parity(const KernelComponent& c, BasisOrder order = BasisOrder::PWC) {
+  int nc = 0, nb = 0;
+  check(vie_component_table(static_cast<int>(c.op), static_cast<int>(order), &nc, nullptr, nullptr, &nb, nullptr));
+  std::vector<int> comps(static_cast<size_t>(4 * nc)), par(static_cast<size_t>(3 * nc));
+  check(vie_component_table(static_cast<int>(c.op), static_cast<int>(order), &nc, comps.data(), par.data(), &nb,
+                            nullptr));
+  for (int i = 0; i < nc; ++i) {
+    const int* e = &comps[static_cast<size_t>(4 * i)];
+    if (e[0] == c.row_axis && e[1] == c.col_axis && e[2] == c.row_poly && e[3] == c.col_poly)
+      return Parity{{par[static_cast<size_t>(3 * i)], par[static_cast<size_t>(3 * i + 1)],
+                     par[static_cast<size_t>(3 * i + 2)]}};
+  }
+  throw std::invalid_argument("component_parity: component not in the unique-component table");
+}
+
+// Unique components of (kind, order) in the canonical order (components.hpp:71-92).
+inline std::vector<KernelComponent> unique_components(OperatorKind op, BasisOrder order = BasisOrder::PWC) {
+  int nc = 0, nb = 0;
+  check(vie_component_table(static_cast<int>(op), static_cast<int>(order), &nc, nullptr, nullptr, &nb, nullptr));
+  std::vector<int> comps(static_cast<size_t>(4 * nc));
+  check(vie_component_table(static_cast<int>(op), static_cast<int>(order), &nc, comps.data(), nullptr, &nb,
+                            nullptr));
+  std::vector<KernelComponent> out;
+  for (int i = 0; i < nc; ++i)
+    out.push_back({op, comps[static_cast<size_t>(4 * i)], comps[static_cast<size_t>(4 * i + 1)],
+                   comps[static_cast<size_t>(4 * i + 2)], comps[static_cast<size_t>(4 * i + 3)]});
+  return out;
+}
+
+struct CurrentField {  // grid.hpp:107-136 (PWC: 3 components, PWL: 12, s = 4q + l)
+  BasisOrder order = BasisOrder::PWC;
+  std::vector<Tensor3> comp;
+  CurrentField() = default;
+  explicit CurrentField(const std::array<Index, 3>& d, BasisOrder ord = BasisOrder::PWC) : order(ord) {
+    comp.assign(ord == BasisOrder::PWC ? 3 : 12, Tensor3(d[0], d[1], d[2]));
+  }
+  std::array<Index, 3> dims() const { return comp.at(0).dims; }
+  Index flat_size() const { return static_cast<Index>(comp.size()) * comp.at(0).size(); }
+  std::vector<cplx> to_vector() const {
+    std::vector<cplx> v;
+    v.reserve(static_cast<size_t>(flat_size()));
+    for (const auto& t : comp) v.insert(v.end(), t.data.begin(), t.data.end());
+    return v;
+  }
+  static CurrentField from_vector(const std::vector<cplx>& v, const std::array<Index, 3>& d,
+                                  BasisOrder ord = BasisOrder::PWC) {
+    CurrentField f(d, ord);
+    const size_t n = static_cast<size_t>(f.comp[0].size());
+    if (v.size() != n * f.comp.size()) throw std::invalid_argument("CurrentField: vector size mismatch");
+    for (size_t q = 0; q < f.comp.size(); ++q)
+      std::copy(v.begin() + static_cast<long>(q * n), v.begin() + static_cast<long>((q + 1) * n),
+                f.comp[q].data.begin());
+    return f;
+  }
+};
+
+// ------------------------------------------------------------------ device RAII
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t bytes) : bytes_(bytes) { cuda_check(cudaMalloc(&p_, bytes)); }
+  ~DeviceBuffer() {
+    if (p_) cudaFree(p_);
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), bytes_(o.bytes_) { o.p_ = nullptr; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    if (this != &o) {
+      if (p_) cudaFree(p_);
+      p_ = o.p_;
+      bytes_ = o.bytes_;
+      o.p_ = nullptr;
+    }
+    return *this;
+  }
+  double* get() const { return static_cast<double*>(p_); }
+  void upload(const void* h, size_t bytes) { cuda_check(cudaMemcpy(p_, h, bytes, cudaMemcpyHostToDevice)); }
+  void download(void* h, size_t bytes) const { cuda_check(cudaMemcpy(h, p_, bytes, cudaMemcpyDeviceToHost)); }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+class DftService {  // fft.hpp DftService: here the CUDA context, stream and plan cache
+ public:
+  explicit DftService(int device = 0) { check(vie_ctx_create(&ctx_, device)); }
+  ~DftService() { vie_ctx_destroy(ctx_); }
+  DftService(const DftService&) = delete;
+  DftService& operator=(const DftService&) = delete;
+  vie_ctx handle() const { return ctx_; }
+
+ private:
+  vie_ctx ctx_ = nullptr;
+};
+
+struct ApplyWorkspace {};  // the device workspace lives in the operator (operator.hpp:181-187)
+
+class EmbeddedSpectrum {  // operator.hpp:120-129, Tucker representation only
+ public:
+  EmbeddedSpectrum() = default;
+  EmbeddedSpectrum(vie_op op, OperatorKind k, BasisOrder b, std::array<Index, 3> g)
+      : op_(op), kind(k), order(b), grid_dims(g), embedded_dims{2 * g[0], 2 * g[1], 2 * g[2]} {}
+  ~EmbeddedSpectrum() {
+    if (op_) vie_op_destroy(op_);
+  }
+  EmbeddedSpectrum(const EmbeddedSpectrum&) = delete;
+  EmbeddedSpectrum& operator=(const EmbeddedSpectrum&) = delete;
+  EmbeddedSpectrum(EmbeddedSpectrum&& o) noexcept
+      : op_(o.op_), kind(o.kind), order(o.order), grid_dims(o.grid_dims), embedded_dims(o.embedded_dims) {
+    o.op_ = nullptr;
+  }
+  vie_op handle() const { return op_; }
+  Index n_cur() const { return order == BasisOrder::PWC ? 3 : 12; }
+  Index n_vox() const { return grid_dims[0] * grid_dims[1] * grid_dims[2]; }
+
+ private:
+  vie_op op_ = nullptr;
+
+ public:
+  OperatorKind kind = OperatorKind::N;
+  BasisOrder order = BasisOrder::PWC;
+  std::array<Index, 3> grid_dims{0, 0, 0};
+  std::array<Index, 3> embedded_dims{0, 0, 0};
+};
+
+// build_operator_spectra (operator.hpp:144-177) from spatial Tucker forms: the
+// forms are shipped to the device and transform_factors (embedding + 1D DFT
+// of each factor column, operator.hpp:76-90) runs there.
+inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder order,
+                                               const std::vector<std::pair<KernelComponent, TuckerForm>>& forms,
+                                               DftService& dft) {
+  if (forms.empty()) throw std::invalid_argument("build_operator_spectra: no components");
+  const std::array<Index, 3> grid{forms.front().second.factors[0].rows, forms.front().second.factors[1].rows,
+                                  forms.front().second.factors[2].rows};
+  std::vector<vie_tucker> hs;
+  std::vector<int> comps;
+  struct Guard {
+    std::vector<vie_tucker>& h;
+    ~Guard() {
+      for (auto t : h) vie_tucker_destroy(t);
+    }
+  } guard{hs};
+  for (const auto& [comp, f] : forms) {
+    if (comp.op != kind) throw std::invalid_argument("build_operator_spectra: component of another operator");
+    const Parity p = component_parity(comp, order);
+    const Index r[3] = {f.factors[0].cols, f.factors[1].cols, f.factors[2].cols};
+    const int64_t dims[3] = {f.factors[0].rows, f.factors[1].rows, f.factors[2].rows};
+    if (dims[0] != grid[0] || dims[1] != grid[1] || dims[2] != grid[2])
+      throw std::invalid_argument("build_operator_spectra: inconsistent component dims");
+    if (static_cast<Index>(f.core.data.size()) != r[0] * r[1] * r[2])
+      throw std::invalid_argument("build_operator_spectra: core size does not match the factor ranks");
+    const int64_t ranks[3] = {r[0], r[1], r[2]};
+    vie_tucker t = nullptr;
+    check(vie_tucker_from_factors(dft.handle(), dims, ranks, reinterpret_cast<const double*>(f.core.data.data()),
+                                  reinterpret_cast<const double*>(f.factors[0].data.data()),
+                                  reinterpret_cast<const double*>(f.factors[1].data.data()),
+                                  reinterpret_cast<const double*>(f.factors[2].data.data()), p.sign.data(), 0, &t));
+    hs.push_back(t);
+    comps.insert(comps.end(), {comp.row_axis, comp.col_axis, comp.row_poly, comp.col_poly});
+  }
+  const int64_t g[3] = {grid[0], grid[1], grid[2]};
+  vie_op op = nullptr;
+  check(vie_op_create(dft.handle(), static_cast<int>(kind), static_cast<int>(order), g, static_cast<int>(hs.size()),
+                      comps.data(), hs.data(), &op));
+  return EmbeddedSpectrum(op, kind, order, grid);
+}
+
+// apply_operator (operator.hpp:273-382).  Host containers in/out; the matvec
+// runs on the device (vie_matvec_host: H2D, matvec, D2H).
+inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentField& x, MatvecStrategy strategy,
+                                   ScratchPolicy policy, ApplyWorkspace* ws, DftService& dft) {
+  (void)ws;
+  (void)dft;
+  if (x.dims() != op.grid_dims || static_cast<Index>(x.comp.size()) != op.n_cur())
+    throw std::invalid_argument("apply_operator: dim mismatch");
+  if (strategy == MatvecStrategy::HosvdDecompress && policy == ScratchPolicy::NoBuffer)
+    throw std::invalid_argument("apply_operator: decompress strategies need ScratchPolicy::WithBuffer");
+  const std::vector<cplx> xv = x.to_vector();
+  std::vector<cplx> yv(xv.size());
+  check(vie_matvec_host(op.handle(), reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yv.data())));
+  return CurrentField::from_vector(yv, op.grid_dims, op.order);
+}
+
+// apply_system (solver.hpp:183-200) with eps_r per voxel (n_vox values) and
+// inv_v = 1 / voxel volume.
+inline CurrentField apply_system(const std::vector<cplx>& eps_r, double inv_v, const EmbeddedSpectrum& op_n,
+                                 const CurrentField& x) {
+  if (x.dims() != op_n.grid_dims || static_cast<Index>(eps_r.size()) != op_n.n_vox())
+    throw std::invalid_argument("apply_system: dim mismatch");
+  const std::vector<cplx> xv = x.to_vector();
+  const size_t bytes = xv.size() * sizeof(cplx);
+  DeviceBuffer dx(bytes), dy(bytes), de(eps_r.size() * sizeof(cplx));
+  dx.upload(xv.data(), bytes);
+  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx));
+  check(vie_system_matvec(op_n.handle(), de.get(), inv_v, dx.get(), dy.get(), 1, nullptr));
+  std::vector<cplx> yv(xv.size());
+  cuda_check(cudaDeviceSynchronize());
+  dy.download(yv.data(), bytes);
+  return CurrentField::from_vector(yv, op_n.grid_dims, op_n.order);
+}
+
+struct GmresConfig {  // solver.hpp:12-16
+  double tolerance = 1e-5;
+  int inner = 50;
+  int outer = 200;
+};
+
+struct GmresResult {  // solver.hpp:18-24
+  std::vector<cplx> solution;
+  std::vector<double> residual_history;
+  double final_relative_residual = 0.0;
+  int iterations = 0;
+  bool converged = false;
+};
+
+// gmres (solver.hpp:34-142) on the apply_system closure of solve_scene
+// (solver.hpp:309-313), device resident.
+inline GmresResult gmres_system(const std::vector<cplx>& eps_r, double inv_v, const EmbeddedSpectrum& op_n,
+                                const std::vector<cplx>& rhs, const GmresConfig& cfg = {},
+                                const std::vector<cplx>* x0 = nullptr) {
+  const size_t n = static_cast<size_t>(op_n.n_cur() * op_n.n_vox());
+  if (rhs.size() != n || static_cast<Index>(eps_r.size()) != op_n.n_vox())
+    throw std::invalid_argument("gmres: size mismatch");
+  if (x0 && x0->size() != n) throw std::invalid_argument("gmres: initial guess size mismatch");
+  const size_t bytes = n * sizeof(cplx);
+  DeviceBuffer db(bytes), dx(bytes), de(eps_r.size() * sizeof(cplx));
+  db.upload(rhs.data(), bytes);
+  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx));
+  DeviceBuffer dx0;
+  if (x0) {
+    dx0 = DeviceBuffer(bytes);
+    dx0.upload(x0->data(), bytes);
+  }
+  GmresResult res;
+  std::vector<double> hist(static_cast<size_t>(cfg.inner) * static_cast<size_t>(cfg.outer) + 1);
+  int it = 0, hl = 0, cv = 0;
+  double fr = 0.0;
+  check(vie_gmres_solve(op_n.handle(), de.get(), inv_v, db.get(), x0 ? dx0.get() : nullptr, cfg.tolerance, cfg.inner,
+                        cfg.outer, dx.get(), &it, &fr, hist.data(), static_cast<int>(hist.size()), &hl, &cv));
+  res.solution.resize(n);
+  dx.download(res.solution.data(), bytes);
+  res.residual_history.assign(hist.begin(), hist.begin() + std::min<long>(hl, static_cast<long>(hist.size())));
+  res.final_relative_residual = fr;
+  res.iterations = it;
+  res.converged = cv != 0;
+  return res;
+}
+
+}  // namespace b200
+}  // namespace vie
+
+#endif  // VIE_B200_HPP

@@ -1,0 +1,244 @@
+// C++ parity tests of the drop-in wrapper (include/vie_b200.hpp), written the
+// way the reference's GTest suites are (test_fft_operator.cpp, test_solver.cpp),
+// with the CPU oracle (oracle/vie_oracle.h, test infrastructure) as checker.
+// Prints one PASS/FAIL line per test; exit code = number of failures.
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <functional>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vie_b200.hpp"
+#include "vie_oracle.h"
+
+using namespace vie::b200;
+
+namespace {
+
+int g_fail = 0;
+
+void run(const char* name, const std::function<void()>& fn) {
+  try {
+    fn();
+    std::printf("PASS %s\n", name);
+  } catch (const std::exception& e) {
+    std::printf("FAIL %s: %s\n", name, e.what());
+    ++g_fail;
+  }
+}
+
+void expect(bool ok, const std::string& msg) {
+  if (!ok) throw std::runtime_error(msg);
+}
+
+// test_util.hpp:17-24 recipe
+FactorMatrix random_matrix(Index rows, Index cols, std::uint64_t seed) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  FactorMatrix m(rows, cols);
+  for (Index j = 0; j < cols; ++j)
+    for (Index i = 0; i < rows; ++i) m(i, j) = cplx(gauss(rng), gauss(rng));
+  return m;
+}
+
+// spatial Tucker form with the parity-zero rows (test_fft_operator.cpp:17-26)
+TuckerForm random_form(const std::array<Index, 3>& d, Index r, const Parity& p, std::uint64_t seed) {
+  TuckerForm f;
+  f.core = Tensor3(r, r, r);
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (auto& v : f.core.data) v = cplx(gauss(rng), gauss(rng));
+  for (int q = 0; q < 3; ++q) {
+    f.factors[q] = random_matrix(d[q], r, seed + 1 + q);
+    if (p.sign[q] < 0)
+      for (Index c = 0; c < r; ++c) f.factors[q](0, c) = 0.0;
+  }
+  f.ranks = {r, r, r};
+  return f;
+}
+
+CurrentField random_field(const std::array<Index, 3>& d, BasisOrder b, std::uint64_t seed) {
+  CurrentField x(d, b);
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  for (auto& t : x.comp)
+    for (auto& v : t.data) v = cplx(gauss(rng), gauss(rng));
+  return x;
+}
+
+double rel(const std::vector<cplx>& a, const std::vector<cplx>& b) {
+  double num = 0, den = 0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    num += std::norm(a[i] - b[i]);
+    den += std::norm(a[i]);
+  }
+  return std::sqrt(num / (den > 0 ? den : 1.0));
+}
+
+struct OracleForms {  // transformed (Fourier) factors for the oracle
+  std::vector<int64_t> ranks;
+  std::vector<std::vector<cplx>> cores, u1, u2, u3;
+  std::vector<const double*> pc, p1, p2, p3;
+};
+
+OracleForms to_oracle(const std::vector<std::pair<KernelComponent, TuckerForm>>& forms, BasisOrder order) {
+  OracleForms o;
+  for (const auto& [comp, f] : forms) {
+    const Parity p = component_parity(comp, order);
+    o.ranks.insert(o.ranks.end(), {f.ranks[0], f.ranks[1], f.ranks[2]});
+    o.cores.push_back(f.core.data);
+    std::vector<cplx>* dst[3] = {nullptr, nullptr, nullptr};
+    o.u1.emplace_back();
+    o.u2.emplace_back();
+    o.u3.emplace_back();
+    dst[0] = &o.u1.back();
+    dst[1] = &o.u2.back();
+    dst[2] = &o.u3.back();
+    for (int q = 0; q < 3; ++q) {
+      const FactorMatrix& u = f.factors[q];
+      dst[q]->resize(static_cast<size_t>(2 * u.rows * u.cols));
+      if (orc_transform_factor(reinterpret_cast<const double*>(u.data.data()), u.rows, u.cols, p.sign[q],
+                               reinterpret_cast<double*>(dst[q]->data())))
+        throw std::runtime_error(orc_last_error());
+    }
+  }
+  for (size_t c = 0; c < o.cores.size(); ++c) {
+    o.pc.push_back(reinterpret_cast<const double*>(o.cores[c].data()));
+    o.p1.push_back(reinterpret_cast<const double*>(o.u1[c].data()));
+    o.p2.push_back(reinterpret_cast<const double*>(o.u2[c].data()));
+    o.p3.push_back(reinterpret_cast<const double*>(o.u3[c].data()));
+  }
+  return o;
+}
+
+std::vector<std::pair<KernelComponent, TuckerForm>> make_family(OperatorKind k, BasisOrder b,
+                                                                 const std::array<Index, 3>& d, Index r,
+                                                                 std::uint64_t seed) {
+  std::vector<std::pair<KernelComponent, TuckerForm>> out;
+  for (const auto& c : unique_components(k, b)) out.emplace_back(c, random_form(d, r, component_parity(c, b), ++seed));
+  return out;
+}
+
+}  // namespace
+
+int main() {
+  DftService dft(0);
+
+  for (auto [k, b] : {std::pair{OperatorKind::N, BasisOrder::PWC}, std::pair{OperatorKind::K, BasisOrder::PWC},
+                      std::pair{OperatorKind::N, BasisOrder::PWL}, std::pair{OperatorKind::K, BasisOrder::PWL}}) {
+    const std::string name = std::string("ApplyOperator.MatchesOracle.") + (k == OperatorKind::N ? "N" : "K") +
+                             (b == BasisOrder::PWC ? "pwc" : "pwl");
+    run(name.c_str(), [&, k = k, b = b] {
+      const std::array<Index, 3> d{3, 4, 5};
+      auto fam = make_family(k, b, d, 3, 30);
+      EmbeddedSpectrum op = build_operator_spectra(k, b, fam, dft);
+      OracleForms of = to_oracle(fam, b);
+      ApplyWorkspace ws;
+      for (int trial = 0; trial < 3; ++trial) {
+        CurrentField x = random_field(d, b, 40 + 3 * trial);
+        CurrentField y = apply_operator(op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, &ws, dft);
+        const std::vector<cplx> xv = x.to_vector();
+        std::vector<cplx> yref(xv.size());
+        const int64_t g[3] = {d[0], d[1], d[2]};
+        if (orc_apply_operator_tucker(static_cast<int>(k), static_cast<int>(b), g, of.ranks.data(), of.pc.data(),
+                                      of.p1.data(), of.p2.data(), of.p3.data(),
+                                      reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yref.data())))
+          throw std::runtime_error(orc_last_error());
+        const double e = rel(yref, y.to_vector());
+        expect(e <= 1e-10, "rel err " + std::to_string(e));
+      }
+    });
+  }
+
+  run("ApplyOperator.ScratchPolicyErrors", [&] {  // test_fft_operator.cpp:265-284
+    const std::array<Index, 3> d{2, 2, 2};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 2, 95);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, fam, dft);
+    CurrentField x = random_field(d, BasisOrder::PWC, 96);
+    bool thrown = false;
+    try {
+      apply_operator(op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::NoBuffer, nullptr, dft);
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    expect(thrown, "NoBuffer with a decompress strategy must throw");
+    thrown = false;
+    try {
+      apply_operator(op, random_field({2, 2, 3}, BasisOrder::PWC, 1), MatvecStrategy::HosvdDecompress,
+                     ScratchPolicy::WithBuffer, nullptr, dft);
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    expect(thrown, "dim mismatch must throw");
+  });
+
+  run("ApplyOperator.ZeroInputGivesZero", [&] {  // test_fft_operator.cpp:121-130
+    const std::array<Index, 3> d{3, 3, 4};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 2, 20);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, fam, dft);
+    CurrentField y = apply_operator(op, CurrentField(d), MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer,
+                                    nullptr, dft);
+    double n = 0;
+    for (auto v : y.to_vector()) n += std::norm(v);
+    expect(n == 0.0, "nonzero output");
+  });
+
+  run("ApplySystem.MatchesOracle", [&] {  // test_solver.cpp:153-180
+    const std::array<Index, 3> d{4, 3, 5};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 3, 17);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, fam, dft);
+    OracleForms of = to_oracle(fam, BasisOrder::PWC);
+    std::vector<cplx> eps(static_cast<size_t>(op.n_vox()));
+    for (size_t i = 0; i < eps.size(); ++i) eps[i] = cplx(2.0 + 0.1 * static_cast<double>(i % 7), -0.3);
+    CurrentField x = random_field(d, BasisOrder::PWC, 20);
+    CurrentField y = apply_system(eps, 0.37, op, x);
+    const std::vector<cplx> xv = x.to_vector();
+    std::vector<cplx> yref(xv.size());
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_apply_system_tucker(0, g, of.ranks.data(), of.pc.data(), of.p1.data(), of.p2.data(), of.p3.data(),
+                                reinterpret_cast<const double*>(eps.data()), 0.37,
+                                reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yref.data())))
+      throw std::runtime_error(orc_last_error());
+    expect(rel(yref, y.to_vector()) <= 1e-10, "rel err");
+  });
+
+  run("Gmres.MatchesOracle", [&] {  // iterations +-1, final residual within 1e-8
+    const std::array<Index, 3> d{5, 4, 4};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 3, 77);
+    for (auto& pr : fam)
+      for (auto& v : pr.second.core.data) v *= 1e-4;
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, fam, dft);
+    OracleForms of = to_oracle(fam, BasisOrder::PWC);
+    std::vector<cplx> eps(static_cast<size_t>(op.n_vox()));
+    for (size_t i = 0; i < eps.size(); ++i) eps[i] = cplx(2.0 + 3.0 * static_cast<double>(i % 5) / 5.0, -0.5);
+    const std::vector<cplx> rhs = random_field(d, BasisOrder::PWC, 78).to_vector();
+    GmresConfig cfg{1e-8, 8, 20};
+    GmresResult r = gmres_system(eps, 1.0, op, rhs, cfg);
+    std::vector<cplx> xref(rhs.size());
+    std::vector<double> hist(200);
+    int it = 0, cv = 0, hl = 0;
+    double fr = 0;
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_gmres_system_tucker(0, g, of.ranks.data(), of.pc.data(), of.p1.data(), of.p2.data(), of.p3.data(),
+                                reinterpret_cast<const double*>(eps.data()), 1.0,
+                                reinterpret_cast<const double*>(rhs.data()), nullptr, 1e-8, 8, 20,
+                                reinterpret_cast<double*>(xref.data()), &it, &cv, &fr, hist.data(), 200, &hl))
+      throw std::runtime_error(orc_last_error());
+    expect(r.converged && cv, "not converged");
+    expect(std::abs(r.iterations - it) <= 1, "iterations " + std::to_string(r.iterations) + " vs " + std::to_string(it));
+    expect(std::abs(r.final_relative_residual - fr) <= 1e-8, "final residual");
+    bool thrown = false;
+    try {
+      gmres_system(eps, 1.0, op, rhs, GmresConfig{1e-5, 0, 1});
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    expect(thrown, "invalid config must throw");
+  });
+
+  std::printf("%d failure(s)\n", g_fail);
+  return g_fail;
+}
