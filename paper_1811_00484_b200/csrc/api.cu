@@ -794,6 +794,17 @@ int vie_op_last_stats(vie_op op, int* launches, double* stage_ms) {
   });
 }
 
+#ifdef VIE_PENCIL_PROFILE
+}  // extern "C"
+namespace vie {
+void pencil_phase_read(unsigned long long* out8, bool reset);
+}
+extern "C" {
+int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
+  return guard([&] { vie::pencil_phase_read(out8, reset != 0); });
+}
+#endif
+
 int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3], double tol,
                         int rule, vie_tucker* out, int64_t ranks_out[3]) {
   (void)ctx; (void)dims; (void)t_host; (void)sign; (void)tol; (void)rule; (void)out; (void)ranks_out;

@@ -27,7 +27,7 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // -------------------------------------------------------------------- rows
 __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
-                                                      int n1, int nrows, FftPlan P) {
+                                                      int n1, int nrows, FftPlan P, FastDiv dn1, FastDiv dm) {
   extern __shared__ double2 sm[];
   const int m = P.n;
   const SmemPlan SP = load_plan(sm, P);
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restri
   const int nr = min(kRowsPerCta, nrows - row0);
   const double2* src = x + static_cast<int64_t>(row0) * n1;
   for (int e = threadIdx.x; e < nr * n1; e += blockDim.x) {
-    const int r = e / n1, i = e - r * n1;
+    const int r = static_cast<int>(dn1.div(e)), i = e - r * n1;
     cp_async16(buf + r * ls + i, src + e);
   }
   cp_async_wait();
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restri
   fft_forward(buf, nr, ls, SP, true);
   double2* dst = A + static_cast<int64_t>(row0) * m;
   for (int e = threadIdx.x; e < nr * m; e += blockDim.x) {
-    const int r = e / m, pos = e - r * m;
+    const int r = static_cast<int>(dm.div(e)), pos = e - r * m;
     dst[e] = buf[r * ls + slot_s[freq_of_pos(pos, n1)]];
   }
 }
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restri
                                                       int n1, int nrows, int rows_per_comp, int64_t nv, FftPlan P,
                                                       double scale, const double2* __restrict__ eps,
                                                       const double2* __restrict__ xin, double inv_v, int lin,
-                                                      int diag) {
+                                                      int diag, FastDiv dn1, FastDiv dm, FastDiv drpc) {
   extern __shared__ double2 sm[];
   const int m = P.n;
   const SmemPlan SP = load_plan(sm, P);
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restri
   const int nr = min(kRowsPerCta, nrows - row0);
   const double2* src = A + static_cast<int64_t>(row0) * m;
   for (int e = threadIdx.x; e < nr * m; e += blockDim.x) {
-    const int r = e / m, pos = e - r * m;
+    const int r = static_cast<int>(dm.div(e)), pos = e - r * m;
     cp_async16(buf + r * ls + slot_s[freq_of_pos(pos, n1)], src + e);
   }
   cp_async_wait();
@@ -75,14 +75,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restri
   fft_inverse(buf, nr, ls, SP, true);
   double2* dst = y + static_cast<int64_t>(row0) * n1;
   for (int e = threadIdx.x; e < nr * n1; e += blockDim.x) {
-    const int r = e / n1, i = e - r * n1;
+    const int r = static_cast<int>(dn1.div(e)), i = e - r * n1;
     const double2 v = cscale(buf[r * ls + i], scale);
     if (eps == nullptr) {
       dst[e] = v;
     } else {
       // apply_system (solver.hpp:191-198): y = eps*x - chi*inv_v*nx
       const int row = row0 + r;
-      const int t = row / rows_per_comp;
+      const int t = static_cast<int>(drpc.div(row));
       const int64_t vox = static_cast<int64_t>(row - t * rows_per_comp) * n1 + i;
       const double2 ep = eps[vox];
       const double2 chv = make_double2((ep.x - 1.0) * inv_v, ep.y * inv_v);
@@ -170,7 +170,10 @@ void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& 
   const int nrows = g.S * g.n2 * g.n3;
   const size_t sm = row_smem(g.m1);
   set_smem(reinterpret_cast<const void*>(k_row_fwd), sm);
-  k_row_fwd<<<(nrows + kRowsPerCta - 1) / kRowsPerCta, kThreads, sm, st>>>(x, A, g.n1, nrows, P1);
+  FastDiv dn1, dm;
+  dn1.init(static_cast<uint32_t>(g.n1));
+  dm.init(static_cast<uint32_t>(g.m1));
+  k_row_fwd<<<(nrows + kRowsPerCta - 1) / kRowsPerCta, kThreads, sm, st>>>(x, A, g.n1, nrows, P1, dn1, dm);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -180,8 +183,12 @@ void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& 
   const size_t sm = row_smem(g.m1);
   set_smem(reinterpret_cast<const void*>(k_row_inv), sm);
   const int64_t nv = static_cast<int64_t>(g.n1) * g.n2 * g.n3;
+  FastDiv dn1, dm, drpc;
+  dn1.init(static_cast<uint32_t>(g.n1));
+  dm.init(static_cast<uint32_t>(g.m1));
+  drpc.init(static_cast<uint32_t>(g.n2 * g.n3));
   k_row_inv<<<(nrows + kRowsPerCta - 1) / kRowsPerCta, kThreads, sm, st>>>(
-      A, y, g.n1, nrows, g.n2 * g.n3, nv, P1, scale, eps, xin, inv_v, basis == 1 ? 1 : 0, diag);
+      A, y, g.n1, nrows, g.n2 * g.n3, nv, P1, scale, eps, xin, inv_v, basis == 1 ? 1 : 0, diag, dn1, dm, drpc);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

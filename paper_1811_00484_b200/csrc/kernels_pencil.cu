@@ -89,14 +89,39 @@ struct PencilArgs {
   Geom g;
   FftPlan PH;           // n3-point plan (branch transforms)
   int P1P;              // axis-1 mirror pairs per CTA
+  int P2N;              // axis-2 positions per CTA (1 or 2)
+  int NBUF;             // spectrum chunk buffers (1 or 2)
   int CF;               // octant frequencies per spectrum chunk
   uint64_t active;
+  FastDiv div_n3;       // element index -> (line, k) without runtime division
+  FastDiv div_cf;
+  FastDiv div_nc;
 };
 
-constexpr int kPencilThreads = 512;  // 16 warps: the CTA owns the SM (smem), so it must hide latency itself
+// Launch shapes: THREADS x MINB CTAs per SM.  P2N axis-2 positions per CTA
+// (2 = full mirror group, Ŝ read once; 1 = half group, the axis-2 mirror CTA is
+// the next blockIdx.x and re-reads Ŝ from L2).  NBUF spectrum chunk buffers.
+#ifdef VIE_PENCIL_PROFILE
+__device__ unsigned long long g_pencil_phase[8];
+#define VIE_PHASE(i)                                                   \
+  do {                                                                 \
+    if (threadIdx.x == 0) {                                            \
+      const long long t_ = clock64();                                  \
+      atomicAdd(&g_pencil_phase[i], static_cast<unsigned long long>(t_ - t_last)); \
+      t_last = t_;                                                     \
+    }                                                                  \
+  } while (0)
+#else
+#define VIE_PHASE(i) \
+  do {               \
+  } while (0)
+#endif
 
-template <int KIND, int BASIS>
-__global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
+template <int KIND, int BASIS, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
+#ifdef VIE_PENCIL_PROFILE
+  long long t_last = clock64();
+#endif
   constexpr int S = TableDims<KIND, BASIS>::S;
   constexpr int NB = TableDims<KIND, BASIS>::NB;
   constexpr int NC = TableDims<KIND, BASIS>::NC;
@@ -105,21 +130,25 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
   extern __shared__ double2 sm[];
   const Geom& g = a.g;
   const int n1 = g.n1, n2 = g.n2, n3 = g.n3, m1 = g.m1, m2 = g.m2, m3 = g.m3;
-  const int P1P = a.P1P, CF = a.CF;
-  const int NP = 4 * P1P;  // pencils: [p2sel][w], w < 2*P1P
+  const int P1P = a.P1P, CF = a.CF, P2N = a.P2N, NBUF = a.NBUF;
   const int W = 2 * P1P;
+  const int NP = P2N * W;  // pencils: [p2sel][w], w < W  (powers of two)
+  const int lgW = __ffs(W) - 1, lgNP = __ffs(NP) - 1;
   const int ls = line_stride(n3);
   const SmemPlan SP = load_plan(sm, a.PH);
   double2* twb = sm + plan_smem_elems(n3);  // w_m3^k, k < n3
-  double2* shb = twb + n3;                  // 2 x [P1P][NC][CF]
+  double2* shb = twb + n3;                  // NBUF x [P1P][NC][CF]
   const int chunk_elems = P1P * NC * CF;
-  double2* buf = shb + 2 * chunk_elems;     // [S][NP] lines of ls
+  double2* buf = shb + NBUF * chunk_elems;  // [S][NP] lines of ls
   for (int e = threadIdx.x; e < n3; e += blockDim.x) twb[e] = a.twm3[e];
 
+  // blockIdx.x runs over axis-1 groups: neighbouring CTAs read neighbouring
+  // 32-byte segments of every pencil row, so L2 sectors fetched from DRAM are
+  // fully used (the transposed order measured 2.8x the DRAM reads).
   const int c0 = blockIdx.x * W;  // first axis-1 position
   const int q0 = c0 >> 1;         // tile octant row of axis 1
-  const int j = blockIdx.y;       // axis-2 position pair (2j, 2j+1)
-  const int f2t = freq_of_pos(2 * j, n2);
+  const int pos2_0 = blockIdx.y * P2N;  // first axis-2 position (pair 2j, 2j+1 when P2N = 2)
+  const int f2t = freq_of_pos(pos2_0, n2);
   const int p2o_tile = f2t > n2 ? m2 - f2t : f2t;
   const int n3p = n3 + 1;
   const int E = n3 / 2 + 1;            // even octant frequencies 0,2,..
@@ -132,12 +161,13 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
     const int nbo = b ? O : E;
     const int nchunks = (nbo + CF - 1) / CF;
     auto issue_chunk = [&](int ci) {
-      double2* dst = shb + (ci & 1) * chunk_elems;
+      double2* dst = shb + (ci % NBUF) * chunk_elems;
       const int u0 = ci * CF;
       for (int e = threadIdx.x; e < chunk_elems; e += blockDim.x) {
-        const int ul = e % CF;
-        const int rc = e / CF;
-        const int c = rc % NC, tr = rc / NC;
+        const int rc = static_cast<int>(a.div_cf.div(e));
+        const int ul = e - rc * CF;
+        const int tr = static_cast<int>(a.div_nc.div(rc));
+        const int c = rc - tr * NC;
         const int p1o = q0 + tr;
         if (p1o <= n1 && u0 + ul < nbo)
           cp_async16(dst + e, a.Shat + ((static_cast<int64_t>(p2o_tile) * (n1 + 1) + p1o) * NC + c) * n3p +
@@ -149,34 +179,41 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
 
     // ---- load the pencils (k < n3) with cp.async (no register staging)
     for (int e = threadIdx.x; e < S * n3 * NP; e += blockDim.x) {
-      const int w = e % W;
-      const int r = e / W;
-      const int p2sel = r & 1;
-      const int sk = r >> 1;
-      const int s = sk / n3, k = sk - s * n3;
-      const int pos1 = c0 + w, pos2 = 2 * j + p2sel;
-      double2* dst = buf + (s * NP + p2sel * W + w) * ls + k;
+      const int p = e & (NP - 1);  // NP, W are powers of two
+      const int w = p & (W - 1);
+      const int p2sel = p >> lgW;
+      const int sk = e >> lgNP;
+      const int s = static_cast<int>(a.div_n3.div(sk)), k = sk - s * n3;
+      const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
+      double2* dst = buf + (s * NP + p) * ls + k;
       if (pos1 < m1) cp_async16(dst, a.Bin + s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1);
       else *dst = make_double2(0.0, 0.0);
     }
     cp_async_commit();
     cp_async_wait_all();  // also lands spectrum chunk 0 (committed earlier)
     __syncthreads();
+    VIE_PHASE(0);
     if (b) {  // branch twiddle w_m3^{k} (odd frequencies)
       for (int e = threadIdx.x; e < S * NP * n3; e += blockDim.x) {
-        const int line = e / n3, k = e - line * n3;
+        const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
         buf[line * ls + k] = cmul(buf[line * ls + k], twb[k]);
       }
     }
     __syncthreads();
+    VIE_PHASE(1);
     fft_forward(buf, S * NP, ls, SP, false);
+    VIE_PHASE(2);
 
     // ---- Hadamard over the branch's octant frequencies, chunk by chunk
     for (int ci = 0; ci < nchunks; ++ci) {
+      if (NBUF == 1 && ci > 0) {
+        __syncthreads();  // chunk ci-1 consumers done before its buffer is refilled
+        issue_chunk(ci);
+      }
       cp_async_wait_all();
-      __syncthreads();  // chunk ci visible; chunk ci-1 consumers done
-      if (ci + 1 < nchunks) issue_chunk(ci + 1);
-      const double2* shc = shb + (ci & 1) * chunk_elems;
+      __syncthreads();  // chunk ci visible; (NBUF 2) chunk ci-1 consumers done
+      if (NBUF == 2 && ci + 1 < nchunks) issue_chunk(ci + 1);
+      const double2* shc = shb + (ci % NBUF) * chunk_elems;
       // work unit = (spectral point, target half); threads [0, items) take
       // half 0, [items, 2 items) half 1 (warp-uniform halves)
       const int items = CF * NP * 2;
@@ -188,11 +225,11 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
         // lanes: mirror pair (mir) x pencil x frequency, frequency slowest
         const int mir = it & 1;
         const int rest = it >> 1;
-        const int p = rest % NP;
-        const int ul = rest / NP;
+        const int p = rest & (NP - 1);
+        const int ul = rest >> lgNP;
         const int u = ci * CF + ul;
         const int f3o = 2 * u + b;
-        const int w = p % W, p2sel = p / W;
+        const int w = p & (W - 1), p2sel = p >> lgW;
         const int pos1 = c0 + w;
         const bool valid = unit < units && u < nbo && !(mir && (f3o == 0 || f3o == n3)) && pos1 < m1;
         double2 xh[S];
@@ -202,7 +239,7 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
           const int f1 = freq_of_pos(pos1, n1);
           m1flag = f1 > n1;
           p1o = m1flag ? m1 - f1 : f1;
-          const int f2 = freq_of_pos(2 * j + p2sel, n2);
+          const int f2 = freq_of_pos(pos2_0 + p2sel, n2);
           m2flag = f2 > n2;
           p2o = m2flag ? m2 - f2 : f2;
           const int f3 = mir ? m3 - f3o : f3o;
@@ -238,39 +275,64 @@ __global__ void __launch_bounds__(kPencilThreads, 1) k_pencil(PencilArgs a) {
       }
     }
     __syncthreads();
+    VIE_PHASE(3);
     fft_inverse(buf, S * NP, ls, SP, false);
+    VIE_PHASE(4);
 
     // ---- store / accumulate the cropped output pencils
     for (int e = threadIdx.x; e < S * n3 * NP; e += blockDim.x) {
-      const int w = e % W;
-      const int r = e / W;
-      const int p2sel = r & 1;
-      const int sk = r >> 1;
-      const int s = sk / n3, k = sk - s * n3;
-      const int pos1 = c0 + w, pos2 = 2 * j + p2sel;
+      const int p = e & (NP - 1);
+      const int w = p & (W - 1);
+      const int p2sel = p >> lgW;
+      const int sk = e >> lgNP;
+      const int s = static_cast<int>(a.div_n3.div(sk)), k = sk - s * n3;
+      const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
       if (pos1 >= m1) continue;
       double2* out = a.Bout + s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1;
-      const double2 v = buf[(s * NP + p2sel * W + w) * ls + k];
+      const double2 v = buf[(s * NP + p) * ls + k];
       if (b == 0) *out = v;
       else *out = cadd(*out, cmulc(v, twb[k]));
     }
     __syncthreads();
+    VIE_PHASE(5);
   }
 }
 
 int pencil_p1pairs(int S) { return S >= 12 ? 1 : (S >= 6 ? 2 : 4); }
 
-size_t pencil_smem_cf(int n3, int S, int NC, int CF) {
-  const int P1P = pencil_p1pairs(S);
-  const size_t e = static_cast<size_t>(plan_smem_elems(n3)) + n3 + 2ull * P1P * NC * CF +
-                   static_cast<size_t>(S) * 4 * P1P * line_stride(n3);
+struct PencilShape {
+  int P1P, P2N, NBUF, CF;
+};
+
+size_t pencil_smem_shape(int n3, int S, int NC, const PencilShape& sh) {
+  const size_t e = static_cast<size_t>(plan_smem_elems(n3)) + n3 +
+                   static_cast<size_t>(sh.NBUF) * sh.P1P * NC * sh.CF +
+                   static_cast<size_t>(S) * 2 * sh.P1P * sh.P2N * line_stride(n3);
   return e * sizeof(double2);
 }
 
-int pencil_cf(int n3, int S, int NC) {
-  for (int cf : {32, 16, 8})
-    if (pencil_smem_cf(n3, S, NC, cf) <= kMaxSmem) return cf;
-  return 0;
+// Two 256-thread CTAs per SM (half mirror group, one chunk buffer) when they
+// fit in half the SM's shared memory; else one 512-thread full-group CTA.
+constexpr size_t kHalfSmSmem = 112 * 1024;
+
+bool pencil_shape(int n3, int S, int NC, PencilShape& sh, bool& two_per_sm) {
+  const int P1P = pencil_p1pairs(S);
+  // measured (r1, C4 PWL): full group 36.5 ms < two half-group CTAs per SM 44 ms
+  for (int cf : {32, 16, 8}) {
+    sh = PencilShape{P1P, 2, 2, cf};
+    if (pencil_smem_shape(n3, S, NC, sh) <= kMaxSmem) {
+      two_per_sm = false;
+      return true;
+    }
+  }
+  for (int cf : {32, 28, 24, 20, 16}) {
+    sh = PencilShape{P1P, 1, 1, cf};
+    if (pencil_smem_shape(n3, S, NC, sh) <= kHalfSmSmem) {
+      two_per_sm = true;
+      return true;
+    }
+  }
+  return false;
 }
 
 template <int KIND, int BASIS>
@@ -278,21 +340,45 @@ void launch_pencil_t(const double2* Bin, double2* Bout, const double2* Shat, con
                      const double2* twm3, uint64_t active, cudaStream_t st) {
   constexpr int S = TableDims<KIND, BASIS>::S;
   constexpr int NC = TableDims<KIND, BASIS>::NC;
-  PencilArgs a{Bin, Bout, Shat, twm3, g, PH, pencil_p1pairs(S), pencil_cf(g.n3, S, NC), active};
-  const size_t sm = pencil_smem_cf(g.n3, S, NC, a.CF);
-  auto fn = k_pencil<KIND, BASIS>;
-  VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sm)));
-  dim3 grid((g.n1 + a.P1P - 1) / a.P1P, g.n2);
-  fn<<<grid, kPencilThreads, sm, st>>>(a);
+  PencilShape sh{};
+  bool two = false;
+  if (!pencil_shape(g.n3, S, NC, sh, two)) throw std::invalid_argument("pencil kernel: grid edge n3 too large");
+  PencilArgs a{Bin, Bout, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}};
+  a.div_n3.init(static_cast<uint32_t>(g.n3));
+  a.div_cf.init(static_cast<uint32_t>(sh.CF));
+  a.div_nc.init(static_cast<uint32_t>(NC));
+  const size_t smem = pencil_smem_shape(g.n3, S, NC, sh);
+  dim3 grid((g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P), g.m2 / sh.P2N);
+  if (two) {
+    auto fn = k_pencil<KIND, BASIS, 256, 2>;
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    fn<<<grid, 256, smem, st>>>(a);
+  } else {
+    auto fn = k_pencil<KIND, BASIS, 512, 1>;
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    fn<<<grid, 512, smem, st>>>(a);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
 }  // namespace
 
+#ifdef VIE_PENCIL_PROFILE
+void pencil_phase_read(unsigned long long* out8, bool reset) {
+  cudaMemcpyFromSymbol(out8, g_pencil_phase, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_pencil_phase, z, sizeof(z));
+  }
+}
+#endif
+
 size_t pencil_smem(int n3, int S, int NC) {
-  const int cf = pencil_cf(n3, S, NC);
-  return cf ? pencil_smem_cf(n3, S, NC, cf) : static_cast<size_t>(-1);
+  PencilShape sh{};
+  bool two = false;
+  return pencil_shape(n3, S, NC, sh, two) ? pencil_smem_shape(n3, S, NC, sh) : static_cast<size_t>(-1);
 }
 
 void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
