@@ -108,7 +108,8 @@ struct vie_op_s {
   double2* Shat = nullptr;
   double2* A = nullptr;
   double2* B = nullptr;
-  double2* Bo = nullptr;  // pencil output slab
+  double2* Bo = nullptr;   // pencil output slab (even axis-3 frequencies)
+  double2* Bo1 = nullptr;  // pencil output slab (odd axis-3 frequencies)
   int64_t ws_bytes = 0;
   FftPlan P1{}, P2{}, P3{}, PH{};
   // host-buffer staging (vie_matvec_host)
@@ -128,7 +129,7 @@ struct vie_op_s {
   cudaEvent_t ev[8] = {};
   ~vie_op_s() {
     for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
-                    static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo),
+                    static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(V),
                     static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
@@ -271,9 +272,9 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   mark();
   vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
   mark();
-  vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->PH, op->P3.tw, op->active, st);
+  vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st);
   mark();
-  vie::launch_col_inv(op->Bo, op->A, g, op->P2, st);
+  vie::launch_col_inv(op->Bo, nullptr, op->A, g, op->P2, st);
   mark();
   // reference inverse3 divides by N_e (fft.hpp:34-37)
   vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);

@@ -39,9 +39,11 @@ void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& 
 void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& P2, cudaStream_t st);
 // Bin: forward slab (after axes 1-2); Bout: output slab (before the axis-2/1
 // inverses); PH: n3-point plan; twm3: w_m3^e table of the m3-point plan.
-void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
-                   const FftPlan& PH, const double2* twm3, uint64_t active_mask, cudaStream_t st);
-void launch_col_inv(const double2* B, double2* A, const Geom& g, const FftPlan& P2, cudaStream_t st);
+void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat,
+                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active_mask, cudaStream_t st);
+// B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
+void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,
+                    cudaStream_t st);
 // Epilogue: y = scale * (IDFT) or the system form (eps != nullptr):
 //   y = (diag ? eps*g_l*xin : 0) - (eps - 1) * inv_v * scale * (IDFT)
 void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& P1, double scale,

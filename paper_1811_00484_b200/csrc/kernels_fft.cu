@@ -126,8 +126,9 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restri
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restrict__ B, double2* __restrict__ A,
-                                                      int n2, int m1, FftPlan P) {
+__global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restrict__ B,
+                                                         const double2* __restrict__ B1, double2* __restrict__ A,
+                                                         int n2, int m1, FftPlan P) {
   extern __shared__ double2 sm[];
   const int m = P.n;
   const SmemPlan SP = load_plan(sm, P);
@@ -144,6 +145,16 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restri
     if (w < wc) cp_async16(buf + w * ls + slot_s[freq_of_pos(pos, n2)], src + static_cast<int64_t>(pos) * m1 + w);
   }
   cp_async_wait();
+  if (B1) {  // add the second slab (same element mapping: each thread owns its cp.async targets)
+    const double2* src1 = B1 + plane * m * m1 + c0;
+    for (int e = threadIdx.x; e < m * kColsPerCta; e += blockDim.x) {
+      const int pos = e / kColsPerCta, w = e - pos * kColsPerCta;
+      if (w < wc) {
+        double2* d = buf + w * ls + slot_s[freq_of_pos(pos, n2)];
+        *d = cadd(*d, src1[static_cast<int64_t>(pos) * m1 + w]);
+      }
+    }
+  }
   __syncthreads();
   fft_inverse(buf, wc, ls, SP, true);
   double2* dst = A + plane * n2 * m1 + c0;
@@ -200,11 +211,12 @@ void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& 
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_col_inv(const double2* B, double2* A, const Geom& g, const FftPlan& P2, cudaStream_t st) {
+void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,
+                    cudaStream_t st) {
   const size_t sm = col_smem(g.m2);
   set_smem(reinterpret_cast<const void*>(k_col_inv), sm);
   dim3 grid((g.m1 + kColsPerCta - 1) / kColsPerCta, g.S * g.n3);
-  k_col_inv<<<grid, kThreads, sm, st>>>(B, A, g.n2, g.m1, P2);
+  k_col_inv<<<grid, kThreads, sm, st>>>(B, B1, A, g.n2, g.m1, P2);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -19,6 +19,8 @@
 // Hadamard = apply_operator's component loop + mac_elementwise
 // (operator.hpp:303-364) fused over all components: x^ read once per point,
 // y^_t = sum_blocks coef * sign * S^_c * x^_s kept in registers.
+#include <cooperative_groups.h>
+
 #include <utility>
 
 #include "fft.cuh"
@@ -83,7 +85,8 @@ __device__ __forceinline__ void had_all(std::integer_sequence<int, Bs...>, doubl
 
 struct PencilArgs {
   const double2* Bin;
-  double2* Bout;
+  double2* Bout;   // branch 0 output slab
+  double2* Bout1;  // branch 1 output slab (conj-twiddled); summed by the axis-2 inverse pass
   const double2* Shat;
   const double2* twm3;  // w_m3^e, e < m3 (full-length plan table)
   Geom g;
@@ -145,7 +148,8 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   // blockIdx.x runs over axis-1 groups: neighbouring CTAs read neighbouring
   // 32-byte segments of every pencil row, so L2 sectors fetched from DRAM are
   // fully used (the transposed order measured 2.8x the DRAM reads).
-  const int c0 = blockIdx.x * W;  // first axis-1 position
+  const int b = blockIdx.x & 1;        // axis-3 branch (even / odd frequencies)
+  const int c0 = (blockIdx.x >> 1) * W;  // first axis-1 position
   const int q0 = c0 >> 1;         // tile octant row of axis 1
   const int pos2_0 = blockIdx.y * P2N;  // first axis-2 position (pair 2j, 2j+1 when P2N = 2)
   const int f2t = freq_of_pos(pos2_0, n2);
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   const int64_t kstride = static_cast<int64_t>(m2) * m1;
   const int64_t sstride = kstride * n3;
 
-  for (int b = 0; b < 2; ++b) {
+  {
     // ---- prefetch spectrum chunk 0 of this branch (lands during the FFT)
     const int nbo = b ? O : E;
     const int nchunks = (nbo + CF - 1) / CF;
@@ -279,21 +283,26 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
     fft_inverse(buf, S * NP, ls, SP, false);
     VIE_PHASE(4);
 
-    // ---- store / accumulate the cropped output pencils
-    for (int e = threadIdx.x; e < S * n3 * NP; e += blockDim.x) {
-      const int p = e & (NP - 1);
-      const int w = p & (W - 1);
-      const int p2sel = p >> lgW;
-      const int sk = e >> lgNP;
-      const int s = static_cast<int>(a.div_n3.div(sk)), k = sk - s * n3;
+    // ---- combine the two branches through DSMEM and store the cropped pencils:
+    // y[n] = A_0[n] + conj(w_m3^n) A_1[n]; CTA b of the cluster writes half
+    // of the lines, reading the partner branch from the partner's smem.
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();  // both branches' inverse transforms done
+    const double2* rbuf = cluster.map_shared_rank(buf, b ^ 1);
+    const int nlines = S * NP;
+    const int l0 = b ? nlines / 2 : 0, l1 = b ? nlines : nlines / 2;
+    for (int e = l0 * n3 + threadIdx.x; e < l1 * n3; e += blockDim.x) {
+      const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
+      const int s = line >> lgNP, p = line & (NP - 1);
+      const int w = p & (W - 1), p2sel = p >> lgW;
       const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
       if (pos1 >= m1) continue;
-      double2* out = a.Bout + s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1;
-      const double2 v = buf[(s * NP + p) * ls + k];
-      if (b == 0) *out = v;
-      else *out = cadd(*out, cmulc(v, twb[k]));
+      const double2 own = buf[line * ls + k], rem = rbuf[line * ls + k];
+      const double2 a0 = b ? rem : own, a1 = b ? own : rem;
+      a.Bout[s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1] = cadd(a0, cmulc(a1, twb[k]));
     }
-    __syncthreads();
+    cluster.sync();  // partner finished reading this CTA's smem
     VIE_PHASE(5);
   }
 }
@@ -336,29 +345,43 @@ bool pencil_shape(int n3, int S, int NC, PencilShape& sh, bool& two_per_sm) {
 }
 
 template <int KIND, int BASIS>
-void launch_pencil_t(const double2* Bin, double2* Bout, const double2* Shat, const Geom& g, const FftPlan& PH,
+void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat, const Geom& g,
+                     const FftPlan& PH,
                      const double2* twm3, uint64_t active, cudaStream_t st) {
   constexpr int S = TableDims<KIND, BASIS>::S;
   constexpr int NC = TableDims<KIND, BASIS>::NC;
   PencilShape sh{};
   bool two = false;
   if (!pencil_shape(g.n3, S, NC, sh, two)) throw std::invalid_argument("pencil kernel: grid edge n3 too large");
-  PencilArgs a{Bin, Bout, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}};
+  PencilArgs a{Bin, Bout, Bout1, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}};
   a.div_n3.init(static_cast<uint32_t>(g.n3));
   a.div_cf.init(static_cast<uint32_t>(sh.CF));
   a.div_nc.init(static_cast<uint32_t>(NC));
   const size_t smem = pencil_smem_shape(g.n3, S, NC, sh);
-  dim3 grid((g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P), g.m2 / sh.P2N);
+  dim3 grid(2 * ((g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P)), g.m2 / sh.P2N);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // the two axis-3 branches of a group
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
   if (two) {
     auto fn = k_pencil<KIND, BASIS, 256, 2>;
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    fn<<<grid, 256, smem, st>>>(a);
+    cfg.blockDim = dim3(256);
+    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
   } else {
     auto fn = k_pencil<KIND, BASIS, 512, 1>;
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    fn<<<grid, 512, smem, st>>>(a);
+    cfg.blockDim = dim3(512);
+    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
@@ -381,12 +404,12 @@ size_t pencil_smem(int n3, int S, int NC) {
   return pencil_shape(n3, S, NC, sh, two) ? pencil_smem_shape(n3, S, NC, sh) : static_cast<size_t>(-1);
 }
 
-void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
-                   const FftPlan& PH, const double2* twm3, uint64_t active, cudaStream_t st) {
-  if (kind == 0 && basis == 0) launch_pencil_t<0, 0>(Bin, Bout, Shat, g, PH, twm3, active, st);
-  else if (kind == 1 && basis == 0) launch_pencil_t<1, 0>(Bin, Bout, Shat, g, PH, twm3, active, st);
-  else if (kind == 0 && basis == 1) launch_pencil_t<0, 1>(Bin, Bout, Shat, g, PH, twm3, active, st);
-  else launch_pencil_t<1, 1>(Bin, Bout, Shat, g, PH, twm3, active, st);
+void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat,
+                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active, cudaStream_t st) {
+  if (kind == 0 && basis == 0) launch_pencil_t<0, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
+  else if (kind == 1 && basis == 0) launch_pencil_t<1, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
+  else if (kind == 0 && basis == 1) launch_pencil_t<0, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
+  else launch_pencil_t<1, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
 }
 
 }  // namespace vie
