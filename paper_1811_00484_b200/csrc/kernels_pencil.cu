@@ -56,31 +56,44 @@ constexpr bool first_in_half(int B, int TH, int HALF) {
 
 // Block B of the table, all indices compile-time constants; only blocks whose
 // target is in [HALF*TH, HALF*TH + TH) (target split across two threads).
-template <int KIND, int BASIS, int B, int S, int TH, int HALF>
+__device__ __forceinline__ double2 flip_sign(double2 v, unsigned long long sbit) {
+  // branch-free negation: xor of the IEEE sign bits (integer pipe)
+  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ static_cast<long long>(sbit)),
+                      __longlong_as_double(__double_as_longlong(v.y) ^ static_cast<long long>(sbit)));
+}
+
+// Block B of the table, all indices compile-time constants; only blocks whose
+// target is in [HALF*TH, HALF*TH + TH) (target split across two threads).
+// ALL = every component active (no per-component branch: lets the compiler
+// schedule spectrum loads and FMAs across components).
+template <int KIND, int BASIS, int B, int S, int TH, int HALF, bool ALL>
 __device__ __forceinline__ void had_block(double2 (&yh)[TH], const double2 (&xh)[S], double2& sh,
-                                          const double2* sh_base, int cstride, uint64_t active, int m1flag,
-                                          int m2flag, int mir) {
+                                          const double2* sh_base, int cstride, uint64_t active,
+                                          unsigned long long f1, unsigned long long f2, unsigned long long f3) {
   constexpr BlockT blk = Tab<KIND, BASIS>::value.blocks[B];
   if constexpr (blk.t / TH == HALF) {
     constexpr bool first = first_in_half<KIND, BASIS>(B, TH, HALF);
     constexpr CompT cp = Tab<KIND, BASIS>::value.comps[blk.c];
-    if (!((active >> blk.c) & 1ull)) return;
+    if (!ALL && !((active >> blk.c) & 1ull)) return;
     if (first) {
-      sh = sh_base[blk.c * cstride];
-      const int flip = (cp.p0 < 0 ? m1flag : 0) ^ (cp.p1 < 0 ? m2flag : 0) ^ (cp.p2 < 0 ? mir : 0);
-      if (flip) sh = make_double2(-sh.x, -sh.y);
+      // sign of the mirrored point: product of the odd-axis flags (sign bits)
+      const unsigned long long sbit = (cp.p0 < 0 ? f1 : 0ull) ^ (cp.p1 < 0 ? f2 : 0ull) ^ (cp.p2 < 0 ? f3 : 0ull);
+      sh = flip_sign(sh_base[blk.c * cstride], sbit);
     }
     if (blk.coef > 0) cfma(yh[blk.t - HALF * TH], sh, xh[blk.s]);
     else cfms(yh[blk.t - HALF * TH], sh, xh[blk.s]);
   }
 }
 
-template <int KIND, int BASIS, int S, int TH, int HALF, int... Bs>
+template <int KIND, int BASIS, int S, int TH, int HALF, bool ALL, int... Bs>
 __device__ __forceinline__ void had_all(std::integer_sequence<int, Bs...>, double2 (&yh)[TH], const double2 (&xh)[S],
                                         const double2* sh_base, int cstride, uint64_t active, int m1flag, int m2flag,
                                         int mir) {
   double2 sh = make_double2(0.0, 0.0);
-  (had_block<KIND, BASIS, Bs, S, TH, HALF>(yh, xh, sh, sh_base, cstride, active, m1flag, m2flag, mir), ...);
+  const unsigned long long f1 = static_cast<unsigned long long>(m1flag) << 63;
+  const unsigned long long f2 = static_cast<unsigned long long>(m2flag) << 63;
+  const unsigned long long f3 = static_cast<unsigned long long>(mir) << 63;
+  (had_block<KIND, BASIS, Bs, S, TH, HALF, ALL>(yh, xh, sh, sh_base, cstride, active, f1, f2, f3), ...);
 }
 
 struct PencilArgs {
@@ -120,7 +133,7 @@ __device__ unsigned long long g_pencil_phase[8];
   } while (0)
 #endif
 
-template <int KIND, int BASIS, int THREADS, int MINB>
+template <int KIND, int BASIS, int THREADS, int MINB, bool ALL>
 __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
 #ifdef VIE_PENCIL_PROFILE
   long long t_last = clock64();
@@ -267,11 +280,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
 #pragma unroll
           for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
           if (half == 0) {
-            had_all<KIND, BASIS, S, TH, 0>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride, a.active,
-                                           m1flag, m2flag, mir);
+            had_all<KIND, BASIS, S, TH, 0, ALL>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride,
+                                                a.active, m1flag, m2flag, mir);
           } else if constexpr (TS > 1) {
-            had_all<KIND, BASIS, S, TH, 1>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride, a.active,
-                                           m1flag, m2flag, mir);
+            had_all<KIND, BASIS, S, TH, 1, ALL>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride,
+                                                a.active, m1flag, m2flag, mir);
           }
 #pragma unroll
           for (int t = 0; t < TH; ++t) pl[(half * TH + t) * NP * ls] = yh[t];
@@ -370,18 +383,19 @@ void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const do
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  const bool all = active == ((NC >= 64) ? ~0ull : ((1ull << NC) - 1));
+  auto launch = [&](auto fn, int threads) {
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cfg.blockDim = dim3(threads);
+    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
+  };
   if (two) {
-    auto fn = k_pencil<KIND, BASIS, 256, 2>;
-    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    cfg.blockDim = dim3(256);
-    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
+    if (all) launch(k_pencil<KIND, BASIS, 256, 2, true>, 256);
+    else launch(k_pencil<KIND, BASIS, 256, 2, false>, 256);
   } else {
-    auto fn = k_pencil<KIND, BASIS, 512, 1>;
-    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    cfg.blockDim = dim3(512);
-    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
+    if (all) launch(k_pencil<KIND, BASIS, 512, 1, true>, 512);
+    else launch(k_pencil<KIND, BASIS, 512, 1, false>, 512);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
