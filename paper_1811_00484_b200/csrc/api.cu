@@ -525,7 +525,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       d.off_z = zoff;
       zoff += static_cast<int64_t>(g.n2 + 1) * d.r1 * d.r3;
     }
-    if (vie::decomp_smem(g.n3, op->rmax) > 220 * 1024)
+    if (vie::decomp_smem(g.n3, op->rmax) > vie::kMaxSmem && vie::decomp_mma_smem(g.n1, g.n3, op->rmax) > vie::kMaxSmem)
       throw Invalid("vie_op_create: Tucker rank too large for the decompression tile (rank * (n3 + 1) too big)");
     if (vie::pencil_smem(g.n3, g.S, g.NC) > vie::kMaxSmem) throw Invalid("vie_op_create: grid edge n3 too large");
     op->forms = dev_alloc<double2>(static_cast<size_t>(off));

@@ -34,6 +34,7 @@ size_t row_smem(int m);
 size_t col_smem(int m);
 size_t pencil_smem(int n3, int S, int NC);  // (size_t)-1 if it does not fit
 size_t decomp_smem(int n3, int rmax);
+size_t decomp_mma_smem(int n1, int n3, int rmax);
 
 void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& P1, cudaStream_t st);
 void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& P2, cudaStream_t st);

@@ -16,6 +16,15 @@ namespace vie {
 
 namespace {
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all_d() {
+  asm volatile("cp.async.commit_group;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::);
+}
+
 // CTA per (component, g): stage one core slice G[:,:,g] in smem.
 __global__ void __launch_bounds__(kThreads) k_decomp_z(const double2* __restrict__ forms,
                                                        const CompDev* __restrict__ comps, double2* __restrict__ Z,
@@ -116,6 +125,117 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
   }
 }
 
+// ---------------------------------------------------------------------------
+// Octant decompression on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).
+// CTA = (component c, PP consecutive p2o).  U3_c staged once in smem as the
+// B operand; per p2o: T = U1_c Z_c[p2o] (FMA, 4% of the flops) into smem as the
+// A operand, then S^ = T U3^T as a complex GEMM = 4 real DMMAs per 8x8x4 step.
+// Fragment smem layout [row][Kp] with Kp = 4 (mod 8): conflict-free quarter-warps.
+constexpr int kMmaMC = 64;   // rows (p1o) per T chunk
+constexpr int kMmaPP = 4;    // p2o values per CTA (U3 reuse)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__host__ __device__ __forceinline__ int mma_kp(int r3) {
+  int kp = (r3 + 3) / 4 * 4;
+  if (kp % 8 == 0) kp += 4;
+  return kp;
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __restrict__ forms,
+                                                              const CompDev* __restrict__ comps,
+                                                              const double2* __restrict__ Z,
+                                                              double2* __restrict__ Shat, Geom geo, int NC) {
+  extern __shared__ double2 sm[];
+  const int c = blockIdx.x;
+  const CompDev cd = comps[c];
+  if (!cd.active) return;
+  const int r1 = cd.r1, r3 = cd.r3;
+  const int n1p = geo.n1 + 1, n2p = geo.n2 + 1, n3p = geo.n3 + 1;
+  const int Kp = mma_kp(r3);
+  const int NPad = (n3p + 15) / 16 * 16;
+  double2* us = sm;                                    // [NPad][Kp]  B operand (U3)
+  double2* zs = us + static_cast<int64_t>(NPad) * Kp;  // [r1][r3]
+  double2* ts = zs + r1 * r3;                          // [kMmaMC][Kp] A operand (T chunk)
+  double2* u1s = ts + kMmaMC * Kp;                     // [r1][kMmaMC] U1 rows of the chunk
+  const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major
+  for (int e = threadIdx.x; e < NPad * Kp; e += blockDim.x) {
+    const int n = e / Kp, k = e - n * Kp;
+    if (n < n3p && k < r3) cp_async16(us + e, u3 + n + static_cast<int64_t>(n3p) * k);
+    else us[e] = make_double2(0.0, 0.0);
+  }
+  const double2* u1 = forms + cd.off_u1;  // n1p x r1
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), col / k (B)
+  const int E = geo.n3 / 2 + 1;
+  const int nct = NPad / 16;
+  const int p2end = min(n2p, (blockIdx.y + 1) * kMmaPP);
+  for (int p2o = blockIdx.y * kMmaPP; p2o < p2end; ++p2o) {
+    __syncthreads();  // previous p2o done with zs / ts
+    const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;
+    for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) cp_async16(zs + e, zsrc + e);
+    for (int m0 = 0; m0 < n1p; m0 += kMmaMC) {
+      if (m0) __syncthreads();  // previous chunk's GEMM done with ts / u1s
+      for (int e = threadIdx.x; e < r1 * kMmaMC; e += blockDim.x) {
+        const int a = e / kMmaMC, i = e - a * kMmaMC;
+        if (m0 + i < n1p) cp_async16(u1s + e, u1 + (m0 + i) + static_cast<int64_t>(n1p) * a);
+      }
+      cp_async_wait_all_d();
+      __syncthreads();
+      for (int e = threadIdx.x; e < kMmaMC * Kp; e += blockDim.x) {
+        const int i = e / Kp, g = e - i * Kp;
+        double2 acc = make_double2(0.0, 0.0);
+        if (g < r3 && m0 + i < n1p)
+          for (int a = 0; a < r1; ++a) cfma(acc, u1s[a * kMmaMC + i], zs[a * r3 + g]);
+        ts[e] = acc;
+      }
+      __syncthreads();
+      const int nrt = (min(kMmaMC, n1p - m0) + 15) / 16;
+      for (int t = warp; t < nrt * nct; t += nwarp) {
+        const int rt = t / nct, ct = t - rt * nct;
+        double accr[2][2][2], acci[2][2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
+        const double2* ta = ts + (rt * 16 + fr) * Kp + fk;
+        const double2* ub = us + (ct * 16 + fr) * Kp + fk;
+        for (int k0 = 0; k0 < Kp; k0 += 4) {
+          const double2 a0 = ta[k0], a1 = ta[8 * Kp + k0];
+          const double2 b0 = ub[k0], b1 = ub[8 * Kp + k0];
+          const double2 av[2] = {a0, a1}, bv[2] = {b0, b1};
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(accr[i][j][0], accr[i][j][1], av[i].x, bv[j].x);
+              dmma(accr[i][j][0], accr[i][j][1], -av[i].y, bv[j].y);
+              dmma(acci[i][j][0], acci[i][j][1], av[i].x, bv[j].y);
+              dmma(acci[i][j][0], acci[i][j][1], av[i].y, bv[j].x);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = m0 + rt * 16 + i * 8 + fr;
+          if (row >= n1p) continue;
+          double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + row) * NC + c) * n3p;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int f = ct * 16 + j * 8 + 2 * fk + h;
+              if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = make_double2(accr[i][j][h], acci[i][j][h]);
+            }
+        }
+      }
+    }
+  }
+}
+
 // Factor transform: out[p + (n+1) c] = sum_m e_c[m] w_{2n}^{p m}, p <= n,
 // with e_c the parity embedding of column c (embed_column).
 __global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, int sign,
@@ -138,6 +258,14 @@ __global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, 
 
 }  // namespace
 
+size_t decomp_mma_smem(int n1, int n3, int rmax) {
+  (void)n1;
+  const int kp = mma_kp(rmax);
+  const size_t npad = static_cast<size_t>((n3 + 1 + 15) / 16 * 16);
+  return sizeof(double2) * (npad * kp + static_cast<size_t>(rmax) * rmax + static_cast<size_t>(kMmaMC) * kp +
+                            static_cast<size_t>(rmax) * kMmaMC);
+}
+
 size_t decomp_smem(int n3, int rmax) {
   return sizeof(double2) * (static_cast<size_t>(rmax) * rmax + static_cast<size_t>(rmax) * (n3 + 1) +
                             static_cast<size_t>(rmax) * kTP1);
@@ -151,10 +279,18 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smz)));
   k_decomp_z<<<dim3(g.NC, rmax), kThreads, smz, st>>>(forms, comps_dev, Z, g.n2);
   VIE_CUDA_CHECK(cudaGetLastError());
-  const size_t sms = decomp_smem(g.n3, rmax);
-  VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
-  k_decomp_s<<<dim3(g.NC, g.n2 + 1), kThreads, sms, st>>>(forms, comps_dev, Z, Shat, g, g.NC);
+  const size_t sms = decomp_mma_smem(g.n1, g.n3, rmax);
+  if (sms <= kMaxSmem) {
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s_mma),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
+    k_decomp_s_mma<<<dim3(g.NC, (g.n2 + 1 + kMmaPP - 1) / kMmaPP), kThreads, sms, st>>>(forms, comps_dev, Z, Shat,
+                                                                                      g, g.NC);
+  } else {
+    const size_t smf = decomp_smem(g.n3, rmax);
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smf)));
+    k_decomp_s<<<dim3(g.NC, g.n2 + 1), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
