@@ -145,12 +145,13 @@ namespace {
 // Radix set of the register DFTs (fft.cuh VIE_FFT_RADICES).  Radices are capped
 // at kMaxRadix: larger register DFTs raise register pressure and cut the warps
 // per SM below what the shared-memory passes need to hide latency (ncu r1).
-const int kRadices[] = {10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES
+const int kRadices[] = {20, 16, 15, 12, 10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES(_WIDE)
 constexpr int kMaxRadix = 10;
 
 // Fewest stages, then smallest largest radix; first radix even when the
 // transform is pad/crop pruned (half_in / half_out).
-bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::vector<int>& best) {
+bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::vector<int>& best,
+                 int maxr = kMaxRadix) {
   if (n == 1) {
     if (best.empty() || cur.size() < best.size() ||
         (cur.size() == best.size() && *std::max_element(cur.begin(), cur.end()) <
@@ -161,23 +162,26 @@ bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::
   if (depth == 0) return false;
   bool any = false;
   for (int r : kRadices) {
-    if (r > kMaxRadix || n % r) continue;
+    if (r > maxr || n % r) continue;
+    if (r > 10 && r != 12 && r != 15 && r != 16 && r != 20) continue;  // VIE_FFT_RADICES_WIDE
     if (even_first && cur.empty() && (r & 1)) continue;
     cur.push_back(r);
-    any |= factor_plan(n / r, even_first, depth - 1, cur, best);
+    any |= factor_plan(n / r, even_first, depth - 1, cur, best, maxr);
     cur.pop_back();
   }
   return any;
 }
 
-const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true) {
-  const int key = pruned ? n : -n;
+// wide = plan for the pencil kernel (radices up to 20, VIE_FFT_RADICES_WIDE)
+const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = false) {
+  const int key = (pruned ? n : -n) * (wide ? 4096 : 1);
   std::lock_guard<std::mutex> lk(ctx->mu);
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) return it->second->plan;
   if (n < 1 || (pruned && (n & 1))) throw Invalid("FFT plan: embedded length must be even");
   std::vector<int> rad, cur;
-  for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth) factor_plan(n, pruned, depth, cur, rad);
+  for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth)
+    factor_plan(n, pruned, depth, cur, rad, wide ? 20 : kMaxRadix);
   if (n > 1 && rad.empty())
     throw Invalid("FFT plan: length " + std::to_string(n) + " has a prime factor > 7");
   auto h = std::make_unique<PlanHolder>();
@@ -556,7 +560,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P1 = get_plan(ctx, g.m1);
     op->P2 = get_plan(ctx, g.m2);
     op->P3 = get_plan(ctx, g.m3);
-    op->PH = get_plan(ctx, g.n3, false);
+    op->PH = get_plan(ctx, g.n3, false, true);
     *out = op.release();
   });
 }

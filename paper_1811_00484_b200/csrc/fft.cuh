@@ -253,10 +253,14 @@ __device__ __forceinline__ void dit_stage_adj(double2* buf, int nlines, int ls, 
   }
 }
 
-// Radices the plans may use (api.cu get_plan chooses among these).
+// Radices the plans may use (api.cu get_plan chooses among these).  Small set
+// (<= 10, low register pressure) for the occupancy-bound row/column passes;
+// wide set (two-stage plans, fewer smem passes) for the pencil kernel, which
+// owns its SM and has 128 registers per thread.
 #define VIE_FFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10)
+#define VIE_FFT_RADICES_WIDE(X) VIE_FFT_RADICES(X) X(12) X(15) X(16) X(20)
 
-template <bool INV>
+template <bool INV, bool WIDE = false>
 __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int n, const StageDesc& sd,
                                           const double2* tw, bool prune, int tid, int nth) {
   switch (sd.radix) {
@@ -268,6 +272,22 @@ __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int 
     VIE_FFT_RADICES(VIE_CASE)
 #undef VIE_CASE
     default:
+      if constexpr (WIDE) {
+        switch (sd.radix) {
+#define VIE_CASE(R)                                                          \
+  case R:                                                                    \
+    if (INV) dit_stage_adj<R>(buf, nlines, ls, n, sd, tw, prune, tid, nth);  \
+    else dif_stage<R>(buf, nlines, ls, n, sd, tw, prune, tid, nth);          \
+    break;
+          VIE_CASE(12)
+          VIE_CASE(15)
+          VIE_CASE(16)
+          VIE_CASE(20)
+#undef VIE_CASE
+          default:
+            break;
+        }
+      }
       break;  // plan creation rejects other radices
   }
 }
@@ -302,19 +322,21 @@ __device__ __forceinline__ SmemPlan load_plan(double2* sm, const FftPlan& P) {
 }
 
 // Full forward transform of `nlines` lines in smem (digit-reversed output).
+template <bool WIDE = false>
 __device__ __forceinline__ void fft_forward(double2* buf, int nlines, int ls, const SmemPlan& P, bool half_in) {
   const int tid = threadIdx.x, nth = blockDim.x;
   for (int s = 0; s < P.nst; ++s) {
-    run_stage<false>(buf, nlines, ls, P.n, P.st[s], P.tw, half_in && s == 0, tid, nth);
+    run_stage<false, WIDE>(buf, nlines, ls, P.n, P.st[s], P.tw, half_in && s == 0, tid, nth);
     __syncthreads();
   }
 }
 
 // Full inverse transform (digit-reversed input, natural unnormalised output).
+template <bool WIDE = false>
 __device__ __forceinline__ void fft_inverse(double2* buf, int nlines, int ls, const SmemPlan& P, bool half_out) {
   const int tid = threadIdx.x, nth = blockDim.x;
   for (int s = P.nst - 1; s >= 0; --s) {
-    run_stage<true>(buf, nlines, ls, P.n, P.st[s], P.tw, half_out && s == 0, tid, nth);
+    run_stage<true, WIDE>(buf, nlines, ls, P.n, P.st[s], P.tw, half_out && s == 0, tid, nth);
     __syncthreads();
   }
 }

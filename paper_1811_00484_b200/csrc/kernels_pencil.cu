@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
     }
     __syncthreads();
     VIE_PHASE(1);
-    fft_forward(buf, S * NP, ls, SP, false);
+    fft_forward<true>(buf, S * NP, ls, SP, false);
     VIE_PHASE(2);
 
     // ---- Hadamard over the branch's octant frequencies, chunk by chunk
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
     }
     __syncthreads();
     VIE_PHASE(3);
-    fft_inverse(buf, S * NP, ls, SP, false);
+    fft_inverse<true>(buf, S * NP, ls, SP, false);
     VIE_PHASE(4);
 
     // ---- combine the two branches through DSMEM and store the cropped pencils:
@@ -305,15 +305,30 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
     const double2* rbuf = cluster.map_shared_rank(buf, b ^ 1);
     const int nlines = S * NP;
     const int l0 = b ? nlines / 2 : 0, l1 = b ? nlines : nlines / 2;
-    for (int e = l0 * n3 + threadIdx.x; e < l1 * n3; e += blockDim.x) {
-      const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
-      const int s = line >> lgNP, p = line & (NP - 1);
-      const int w = p & (W - 1), p2sel = p >> lgW;
-      const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
-      if (pos1 >= m1) continue;
-      const double2 own = buf[line * ls + k], rem = rbuf[line * ls + k];
-      const double2 a0 = b ? rem : own, a1 = b ? own : rem;
-      a.Bout[s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1] = cadd(a0, cmulc(a1, twb[k]));
+    constexpr int U = 4;  // remote (DSMEM) loads issued before use
+    for (int e0 = l0 * n3 + threadIdx.x; e0 < l1 * n3; e0 += U * blockDim.x) {
+      double2 own[U], rem[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = e0 + q * blockDim.x;
+        if (e < l1 * n3) {
+          const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
+          own[q] = buf[line * ls + k];
+          rem[q] = rbuf[line * ls + k];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int e = e0 + q * blockDim.x;
+        if (e >= l1 * n3) break;
+        const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
+        const int s = line >> lgNP, p = line & (NP - 1);
+        const int w = p & (W - 1), p2sel = p >> lgW;
+        const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
+        if (pos1 >= m1) continue;
+        const double2 a0 = b ? rem[q] : own[q], a1 = b ? own[q] : rem[q];
+        a.Bout[s * sstride + k * kstride + static_cast<int64_t>(pos2) * m1 + pos1] = cadd(a0, cmulc(a1, twb[k]));
+      }
     }
     cluster.sync();  // partner finished reading this CTA's smem
     VIE_PHASE(5);
