@@ -265,6 +265,48 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder ord
   return EmbeddedSpectrum(op, kind, order, grid);
 }
 
+enum class TruncationRule { SigmaMax = VIE_RULE_SIGMA_MAX, Energy = VIE_RULE_ENERGY };
+
+struct SpectrumBuildOptions {  // operator.hpp:131-139 (Tucker representation only)
+  double tol = 1e-8;
+  TruncationRule rule = TruncationRule::Energy;
+  BasisOrder order = BasisOrder::PWC;
+};
+
+// build_operator_spectra (operator.hpp:144-177) from SPATIAL defining tensors,
+// exactly the reference signature: each component is compressed by
+// tucker_compress (hosvd + transform_factors) and kept only as a Tucker form.
+inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind,
+                                               const std::vector<std::pair<KernelComponent, Tensor3>>& tensors,
+                                               const SpectrumBuildOptions& opts, DftService& dft) {
+  if (tensors.empty()) throw std::invalid_argument("build_operator_spectra: no components");
+  const std::array<Index, 3> grid = tensors.front().second.dims;
+  std::vector<vie_tucker> hs;
+  std::vector<int> comps;
+  struct Guard {
+    std::vector<vie_tucker>& h;
+    ~Guard() {
+      for (auto t : h) vie_tucker_destroy(t);
+    }
+  } guard{hs};
+  for (const auto& [comp, t] : tensors) {
+    if (t.dims != grid) throw std::invalid_argument("build_operator_spectra: inconsistent component dims");
+    const Parity p = component_parity(comp, opts.order);
+    const int64_t dims[3] = {grid[0], grid[1], grid[2]};
+    int64_t ranks[3] = {0, 0, 0};
+    vie_tucker h = nullptr;
+    check(vie_tucker_compress(dft.handle(), dims, reinterpret_cast<const double*>(t.data.data()), p.sign.data(),
+                              opts.tol, static_cast<int>(opts.rule), &h, ranks));
+    hs.push_back(h);
+    comps.insert(comps.end(), {comp.row_axis, comp.col_axis, comp.row_poly, comp.col_poly});
+  }
+  const int64_t g[3] = {grid[0], grid[1], grid[2]};
+  vie_op op = nullptr;
+  check(vie_op_create(dft.handle(), static_cast<int>(kind), static_cast<int>(opts.order), g,
+                      static_cast<int>(hs.size()), comps.data(), hs.data(), &op));
+  return EmbeddedSpectrum(op, kind, opts.order, grid);
+}
+
 // apply_operator (operator.hpp:273-382).  Host containers in/out; the matvec
 // runs on the device (vie_matvec_host: H2D, matvec, D2H).
 inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentField& x, MatvecStrategy strategy,

@@ -9,7 +9,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvie_b200.so")
-SOURCES = ["api.cu", "kernels_fft.cu", "kernels_pencil.cu", "kernels_decomp.cu", "kernels_blas.cu"]
+SOURCES = ["api.cu", "kernels_fft.cu", "kernels_pencil.cu", "kernels_decomp.cu", "kernels_blas.cu",
+           "kernels_hosvd.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "kernels.cuh", "twiddles_gen.cuh"]
 
 NVCC_FLAGS = [

@@ -256,6 +256,111 @@ void host_table(int kind, int basis, std::vector<HComp>& cs, std::vector<HBlock>
   else throw Invalid("component table: kind must be N/K and basis PWC/PWL");
 }
 
+// RAII pool of scratch device buffers
+struct DevPool {
+  std::vector<void*> p;
+  ~DevPool() {
+    for (void* x : p) dev_free(x);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    T* x = dev_alloc<T>(n);
+    p.push_back(x);
+    return x;
+  }
+};
+
+// ---------------------------------------------------------------- hosvd (host parts)
+// truncation_rank (decomp.hpp:72-103)
+int64_t truncation_rank_host(const std::vector<double>& s, double tol, int rule) {
+  const int64_t n = static_cast<int64_t>(s.size());
+  if (n == 0) return 0;
+  const double smax = s[0];
+  if (smax <= 0.0) return 0;
+  if (rule == VIE_RULE_SIGMA_MAX) {
+    const double threshold = (tol / std::sqrt(3.0)) * smax;
+    int64_t r = 0;
+    for (int64_t j = 0; j < n; ++j)
+      if (s[static_cast<size_t>(j)] > 0.0 && s[static_cast<size_t>(j)] >= threshold - 1e-14 * smax) r = j + 1;
+    return r;
+  }
+  double total = 0.0;
+  for (double x : s) total += x * x;
+  const double budget = (tol / std::sqrt(3.0)) * std::sqrt(total);
+  const double budget2 = budget * budget;
+  double tail = 0.0;
+  int64_t r = n;
+  while (r > 0) {
+    const double cand = tail + s[static_cast<size_t>(r - 1)] * s[static_cast<size_t>(r - 1)];
+    if (cand <= budget2 || s[static_cast<size_t>(r - 1)] == 0.0) {
+      tail = cand;
+      --r;
+    } else {
+      break;
+    }
+  }
+  return r;
+}
+
+// Cyclic Jacobi eigendecomposition of a Hermitian n x n matrix (col-major):
+// eigenvalues descending in lam, eigenvectors in the columns of V.  Rotation
+// J = [[c, s e^{i phi}], [-s e^{-i phi}, c]] zeroes a_pq = |a_pq| e^{i phi}.
+void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::vector<cd>& V) {
+  auto A = [&](int i, int j) -> cd& { return a[static_cast<size_t>(i) + static_cast<size_t>(n) * j]; };
+  std::vector<cd> v(static_cast<size_t>(n) * n, cd(0.0));
+  for (int i = 0; i < n; ++i) v[static_cast<size_t>(i) * (n + 1)] = 1.0;
+  double fro = 0.0;
+  for (const cd& x : a) fro += std::norm(x);
+  fro = std::sqrt(fro);
+  for (int sweep = 0; sweep < 60 && fro > 0.0; ++sweep) {
+    double off = 0.0;
+    for (int q = 1; q < n; ++q)
+      for (int p = 0; p < q; ++p) off += std::norm(A(p, q));
+    if (std::sqrt(2.0 * off) <= 1e-15 * fro) break;
+    for (int p = 0; p < n - 1; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const cd apq = A(p, q);
+        const double mag = std::abs(apq);
+        if (mag <= 1e-300 || mag <= 1e-18 * fro) continue;
+        const double tau = (A(q, q).real() - A(p, p).real()) / (2.0 * mag);
+        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
+        const cd ph = apq / mag;
+        const cd jpq = s * ph, jqp = -s * std::conj(ph);
+        for (int k = 0; k < n; ++k) {  // A <- A J (columns p, q)
+          const cd akp = A(k, p), akq = A(k, q);
+          A(k, p) = akp * c + akq * jqp;
+          A(k, q) = akp * jpq + akq * c;
+        }
+        for (int k = 0; k < n; ++k) {  // A <- J^H A (rows p, q)
+          const cd apk = A(p, k), aqk = A(q, k);
+          A(p, k) = c * apk + std::conj(jqp) * aqk;
+          A(q, k) = std::conj(jpq) * apk + c * aqk;
+        }
+        A(p, q) = 0.0;
+        A(q, p) = 0.0;
+        for (int k = 0; k < n; ++k) {  // V <- V J
+          cd& vkp = v[static_cast<size_t>(k) + static_cast<size_t>(n) * p];
+          cd& vkq = v[static_cast<size_t>(k) + static_cast<size_t>(n) * q];
+          const cd x = vkp, y = vkq;
+          vkp = x * c + y * jqp;
+          vkq = x * jpq + y * c;
+        }
+      }
+  }
+  std::vector<int> order(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) order[static_cast<size_t>(i)] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return A(x, x).real() > A(y, y).real(); });
+  lam.resize(static_cast<size_t>(n));
+  V.assign(static_cast<size_t>(n) * n, cd(0.0));
+  for (int k = 0; k < n; ++k) {
+    const int o = order[static_cast<size_t>(k)];
+    lam[static_cast<size_t>(k)] = A(o, o).real();
+    for (int i = 0; i < n; ++i)
+      V[static_cast<size_t>(i) + static_cast<size_t>(n) * k] = v[static_cast<size_t>(i) + static_cast<size_t>(n) * o];
+  }
+}
+
 // ---------------------------------------------------------------- matvec
 void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const double2* eps, double inv_v,
                 int diag) {
@@ -812,9 +917,83 @@ int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
 
 int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3], double tol,
                         int rule, vie_tucker* out, int64_t ranks_out[3]) {
-  (void)ctx; (void)dims; (void)t_host; (void)sign; (void)tol; (void)rule; (void)out; (void)ranks_out;
-  g_err = "vie_tucker_compress: not implemented in this build";
-  return VIE_EINVAL;
+  return guard([&] {
+    if (!ctx || !dims || !t_host || !sign || !out) throw Invalid("tucker_compress: null argument");
+    for (int q = 0; q < 3; ++q) {
+      if (dims[q] < 1) throw Invalid("hosvd: degenerate tensor dimensions");
+      if (sign[q] != 1 && sign[q] != -1) throw Invalid("tucker_compress: sign must be +-1");
+    }
+    if (!(tol >= 0.0)) throw Invalid("truncated_svd: tol must be >= 0");
+    if (rule != VIE_RULE_SIGMA_MAX && rule != VIE_RULE_ENERGY) throw Invalid("tucker_compress: bad rule");
+    if (dims[0] > 4096 || dims[1] > 4096 || dims[2] > 4096) throw Invalid("tucker_compress: dims too large");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    const int64_t nv = dims[0] * dims[1] * dims[2];
+    check_cplx_finite_host(t_host, static_cast<size_t>(nv), "tucker_compress: tensor");
+    cudaStream_t st = ctx->stream;
+    DevPool dev;
+    double2* dt = dev.alloc<double2>(static_cast<size_t>(nv));
+    VIE_CUDA_CHECK(cudaMemcpy(dt, t_host, sizeof(double2) * nv, cudaMemcpyHostToDevice));
+    // per mode: Gram on the device, Hermitian Jacobi eigendecomposition on the host
+    // (sigma_k = sqrt(lambda_k): the left singular pairs of the unfolding), rank
+    // by truncation_rank (decomp.hpp:72-103), U_q = leading eigenvectors.
+    std::vector<cd> U[3];
+    int64_t rk[3];
+    for (int q = 0; q < 3; ++q) {
+      const int n = static_cast<int>(dims[q]);
+      double2* dG = dev.alloc<double2>(static_cast<size_t>(n) * n);
+      vie::launch_gram(dt, dims, q + 1, dG, st);
+      std::vector<cd> G(static_cast<size_t>(n) * n);
+      VIE_CUDA_CHECK(cudaMemcpyAsync(G.data(), dG, sizeof(double2) * G.size(), cudaMemcpyDeviceToHost, st));
+      VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+      std::vector<double> lam;
+      std::vector<cd> V;
+      herm_eig_jacobi(G, n, lam, V);
+      std::vector<double> sig(static_cast<size_t>(n));
+      for (int k = 0; k < n; ++k) sig[static_cast<size_t>(k)] = std::sqrt(std::max(lam[static_cast<size_t>(k)], 0.0));
+      int64_t r = truncation_rank_host(sig, tol, rule);
+      const bool zero = r == 0;
+      if (zero) r = 1;  // rank-0 form == zero spectrum; keep one (zeroed) column
+      rk[q] = r;
+      U[q].assign(static_cast<size_t>(n * r), cd(0.0));
+      for (int64_t c = 0; c < r; ++c)
+        for (int i = 0; i < n; ++i) U[q][static_cast<size_t>(i + n * c)] = zero ? cd(0.0) : V[static_cast<size_t>(i + n * c)];
+      if (sign[q] < 0) {  // odd axis: the offset-0 row is zero (components.hpp:46-50)
+        double nrm = 0.0, row0 = 0.0;
+        for (int64_t c = 0; c < r; ++c) {
+          row0 += std::norm(U[q][static_cast<size_t>(n * c)]);
+          for (int i = 0; i < n; ++i) nrm += std::norm(U[q][static_cast<size_t>(i + n * c)]);
+        }
+        if (row0 > 1e-20 * std::max(nrm, 1e-300))
+          throw Invalid("tucker_compress: odd-parity component has a nonzero offset-0 plane");
+        for (int64_t c = 0; c < r; ++c) U[q][static_cast<size_t>(n * c)] = 0.0;
+      }
+    }
+    // core = t x1 U1^H x2 U2^H x3 U3^H (decomp.hpp:171-174), on the device
+    int64_t d[3] = {dims[0], dims[1], dims[2]};
+    const double2* cur = dt;
+    for (int q = 0; q < 3; ++q) {
+      double2* dU = dev.alloc<double2>(U[q].size());
+      VIE_CUDA_CHECK(cudaMemcpyAsync(dU, U[q].data(), sizeof(double2) * U[q].size(), cudaMemcpyHostToDevice, st));
+      int64_t od[3] = {d[0], d[1], d[2]};
+      od[q] = rk[q];
+      double2* nxt = dev.alloc<double2>(static_cast<size_t>(od[0] * od[1] * od[2]));
+      vie::launch_mode_product_h(cur, d, q + 1, dU, static_cast<int>(rk[q]), nxt, st);
+      cur = nxt;
+      d[0] = od[0];
+      d[1] = od[1];
+      d[2] = od[2];
+    }
+    std::vector<cd> core(static_cast<size_t>(rk[0] * rk[1] * rk[2]));
+    VIE_CUDA_CHECK(cudaMemcpyAsync(core.data(), cur, sizeof(double2) * core.size(), cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    const int rc = vie_tucker_from_factors(ctx, dims, rk, reinterpret_cast<const double*>(core.data()),
+                                           reinterpret_cast<const double*>(U[0].data()),
+                                           reinterpret_cast<const double*>(U[1].data()),
+                                           reinterpret_cast<const double*>(U[2].data()), sign, 0, out);
+    if (rc != VIE_OK) throw Invalid(g_err);
+    if (ranks_out)
+      for (int q = 0; q < 3; ++q) ranks_out[q] = rk[q];
+  });
 }
 
 }  // extern "C"

@@ -58,6 +58,13 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
 void launch_factor_transform(const double2* u, int n, int r, int sign, const double2* tw2n, double2* out,
                              cudaStream_t st);
 
+// ---- tucker_compress (hosvd) device parts
+// G (nq x nq, col-major) = M_q M_q^H of the mode-q unfolding (mode 1..3)
+void launch_gram(const double2* t, const int64_t dims[3], int mode, double2* G, cudaStream_t st);
+// out = in x_mode U^H (U: n_mode x r col-major)
+void launch_mode_product_h(const double2* in, const int64_t dims[3], int mode, const double2* U, int r,
+                           double2* out, cudaStream_t st);
+
 // ---- BLAS-1 for GMRES (deterministic two-level reductions) ----
 struct RedBuf {
   double2* partials;       // kRedBlocks entries

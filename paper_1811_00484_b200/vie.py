@@ -146,12 +146,33 @@ class TuckerForm:
     def handle(self):
         return self._h
 
+    @classmethod
+    def _from_handle(cls, dft, h, dims, ranks, sign):
+        obj = cls.__new__(cls)
+        obj._h, obj._dft = h, dft
+        obj.dims, obj.ranks, obj.sign = tuple(dims), tuple(ranks), tuple(sign)
+        return obj
+
     def __del__(self):
         try:
             if self._h:
                 lib().vie_tucker_destroy(self._h)
         except Exception:
             pass
+
+
+def tucker_compress(dft: DftService, t, dims, sign, tol: float = 1e-8, rule: int = RULE_ENERGY) -> TuckerForm:
+    """hosvd + transform_factors (decomp.hpp:160-176, operator.hpp:76-90) of a spatial
+    Toeplitz-defining tensor (flat, reference layout); returns the device form."""
+    t = _cplx(np.asarray(t).reshape(-1, order="F") if np.asarray(t).ndim == 3 else t).reshape(-1)
+    if t.size != int(np.prod(dims)):
+        raise ValueError("tucker_compress: tensor size does not match dims")
+    h = C.c_void_p()
+    ranks = (C.c_int64 * 3)()
+    _check(lib().vie_tucker_compress(dft.handle, _i64(dims), t.ctypes.data_as(_dp),
+                                     (C.c_int * 3)(*[int(x) for x in sign]), C.c_double(tol), int(rule),
+                                     C.byref(h), ranks))
+    return TuckerForm._from_handle(dft, h, dims, [ranks[0], ranks[1], ranks[2]], sign)
 
 
 @dataclass

@@ -153,6 +153,51 @@ int main() {
     });
   }
 
+  run("BuildOperatorSpectra.FromTensors.ErrorTracksTolerance", [&] {  // test_fft_operator.cpp:192-209
+    const std::array<Index, 3> d{4, 4, 4};
+    std::vector<std::pair<KernelComponent, Tensor3>> tensors;
+    std::vector<std::vector<cplx>> spec;  // oracle dense spectra
+    std::uint64_t seed = 70;
+    for (const auto& c : unique_components(OperatorKind::N)) {
+      // rank-2 separable component with parity-zero rows (make_component_tensor)
+      const Parity p = component_parity(c);
+      Tensor3 t(d[0], d[1], d[2]);
+      ++seed;
+      FactorMatrix f[3];
+      for (int q = 0; q < 3; ++q) {
+        f[q] = random_matrix(d[q], 2, seed + 7 * q);
+        if (p.sign[q] < 0)
+          for (Index l = 0; l < 2; ++l) f[q](0, l) = 0.0;
+      }
+      for (Index k = 0; k < d[2]; ++k)
+        for (Index j = 0; j < d[1]; ++j)
+          for (Index i = 0; i < d[0]; ++i)
+            for (Index l = 0; l < 2; ++l) t(i, j, k) += f[0](i, l) * f[1](j, l) * f[2](k, l);
+      tensors.emplace_back(c, t);
+      std::vector<cplx> sp(static_cast<size_t>(8 * t.size()));
+      const int64_t dims[3] = {d[0], d[1], d[2]};
+      if (orc_dense_spectrum(reinterpret_cast<const double*>(t.data.data()), dims, p.sign.data(),
+                             reinterpret_cast<double*>(sp.data())))
+        throw std::runtime_error(orc_last_error());
+      spec.push_back(std::move(sp));
+    }
+    SpectrumBuildOptions opts;
+    opts.tol = 1e-4;
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, tensors, opts, dft);
+    CurrentField x = random_field(d, BasisOrder::PWC, 71);
+    CurrentField y = apply_operator(op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, nullptr, dft);
+    std::vector<const double*> sp;
+    for (auto& v : spec) sp.push_back(reinterpret_cast<const double*>(v.data()));
+    const std::vector<cplx> xv = x.to_vector();
+    std::vector<cplx> yref(xv.size());
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_apply_operator_dense(0, 0, g, sp.data(), reinterpret_cast<const double*>(xv.data()),
+                                 reinterpret_cast<double*>(yref.data())))
+      throw std::runtime_error(orc_last_error());
+    const double e = rel(yref, y.to_vector());
+    expect(e < 10 * opts.tol, "rel err " + std::to_string(e));
+  });
+
   run("ApplyOperator.ScratchPolicyErrors", [&] {  // test_fft_operator.cpp:265-284
     const std::array<Index, 3> d{2, 2, 2};
     auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 2, 95);
