@@ -145,8 +145,12 @@ namespace {
 // Radix set of the register DFTs (fft.cuh VIE_FFT_RADICES).  Radices are capped
 // at kMaxRadix: larger register DFTs raise register pressure and cut the warps
 // per SM below what the shared-memory passes need to hide latency (ncu r1).
-const int kRadices[] = {20, 16, 15, 12, 10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES(_WIDE)
+const int kRadices[] = {24, 20, 16, 15, 12, 10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES(_WIDE)
 constexpr int kMaxRadix = 10;
+#ifndef VIE_WIDE_PASSES
+#define VIE_WIDE_PASSES 1
+#endif
+constexpr bool kWidePasses = VIE_WIDE_PASSES;  // two-stage plans for the row/column passes
 
 // Fewest stages, then smallest largest radix; first radix even when the
 // transform is pad/crop pruned (half_in / half_out).
@@ -163,7 +167,7 @@ bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::
   bool any = false;
   for (int r : kRadices) {
     if (r > maxr || n % r) continue;
-    if (r > 10 && r != 12 && r != 15 && r != 16 && r != 20) continue;  // VIE_FFT_RADICES_WIDE
+    if (r > 10 && r != 12 && r != 15 && r != 16 && r != 20 && r != 24) continue;  // VIE_FFT_RADICES_WIDE
     if (even_first && cur.empty() && (r & 1)) continue;
     cur.push_back(r);
     any |= factor_plan(n / r, even_first, depth - 1, cur, best, maxr);
@@ -181,7 +185,7 @@ const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = fals
   if (n < 1 || (pruned && (n & 1))) throw Invalid("FFT plan: embedded length must be even");
   std::vector<int> rad, cur;
   for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth)
-    factor_plan(n, pruned, depth, cur, rad, wide ? 20 : kMaxRadix);
+    factor_plan(n, pruned, depth, cur, rad, wide ? 24 : kMaxRadix);
   if (n > 1 && rad.empty())
     throw Invalid("FFT plan: length " + std::to_string(n) + " has a prime factor > 7");
   auto h = std::make_unique<PlanHolder>();
@@ -662,8 +666,8 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->B = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
     op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
     op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 10 * nv);
-    op->P1 = get_plan(ctx, g.m1);
-    op->P2 = get_plan(ctx, g.m2);
+    op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
+    op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
     op->PH = get_plan(ctx, g.n3, false, true);
     *out = op.release();

@@ -258,7 +258,7 @@ __device__ __forceinline__ void dit_stage_adj(double2* buf, int nlines, int ls, 
 // wide set (two-stage plans, fewer smem passes) for the pencil kernel, which
 // owns its SM and has 128 registers per thread.
 #define VIE_FFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10)
-#define VIE_FFT_RADICES_WIDE(X) VIE_FFT_RADICES(X) X(12) X(15) X(16) X(20)
+#define VIE_FFT_RADICES_WIDE(X) VIE_FFT_RADICES(X) X(12) X(15) X(16) X(20) X(24)
 
 template <bool INV, bool WIDE = false>
 __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int n, const StageDesc& sd,
@@ -283,6 +283,7 @@ __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int 
           VIE_CASE(15)
           VIE_CASE(16)
           VIE_CASE(20)
+          VIE_CASE(24)
 #undef VIE_CASE
           default:
             break;

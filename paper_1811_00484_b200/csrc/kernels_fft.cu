@@ -26,7 +26,7 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // -------------------------------------------------------------------- rows
-__global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
+__global__ void __launch_bounds__(kThreads, 2) k_row_fwd(const double2* __restrict__ x, double2* __restrict__ A,
                                                       int n1, int nrows, FftPlan P, FastDiv dn1, FastDiv dm) {
   extern __shared__ double2 sm[];
   const int m = P.n;
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restri
   }
   cp_async_wait();
   __syncthreads();
-  fft_forward(buf, nr, ls, SP, true);
+  fft_forward<true>(buf, nr, ls, SP, true);
   double2* dst = A + static_cast<int64_t>(row0) * m;
   for (int e = threadIdx.x; e < nr * m; e += blockDim.x) {
     const int r = static_cast<int>(dm.div(e)), pos = e - r * m;
@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_fwd(const double2* __restri
   }
 }
 
-__global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restrict__ A, double2* __restrict__ y,
+__global__ void __launch_bounds__(kThreads, 2) k_row_inv(const double2* __restrict__ A, double2* __restrict__ y,
                                                       int n1, int nrows, int rows_per_comp, int64_t nv, FftPlan P,
                                                       double scale, const double2* __restrict__ eps,
                                                       const double2* __restrict__ xin, double inv_v, int lin,
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_row_inv(const double2* __restri
   }
   cp_async_wait();
   __syncthreads();
-  fft_inverse(buf, nr, ls, SP, true);
+  fft_inverse<true>(buf, nr, ls, SP, true);
   double2* dst = y + static_cast<int64_t>(row0) * n1;
   for (int e = threadIdx.x; e < nr * n1; e += blockDim.x) {
     const int r = static_cast<int>(dn1.div(e)), i = e - r * n1;
