@@ -122,6 +122,10 @@ struct vie_op_s {
   double2* scal = nullptr;  // device scalars
   double2* red_partials = nullptr;
   unsigned int* red_counter = nullptr;
+  // side stream: the x-independent decompression runs concurrently with the
+  // forward FFT passes (and with the H2D copy of vie_matvec_host)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   // stats
   int profiling = 0;
   int last_launches = 0;
@@ -136,6 +140,9 @@ struct vie_op_s {
       dev_free(p);
     for (auto& e : ev)
       if (e) cudaEventDestroy(e);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (side) cudaStreamDestroy(side);
   }
 };
 
@@ -366,11 +373,19 @@ void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::v
 }
 
 // ---------------------------------------------------------------- matvec
+// Launch the decompression on the side stream after all work queued on `st`.
+void fork_decomp(vie_op op, cudaStream_t st) {
+  VIE_CUDA_CHECK(cudaEventRecord(op->ev_fork, st));
+  VIE_CUDA_CHECK(cudaStreamWaitEvent(op->side, op->ev_fork, 0));
+  vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, op->g, op->rmax, op->side);
+  VIE_CUDA_CHECK(cudaEventRecord(op->ev_join, op->side));
+}
+
 void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const double2* eps, double inv_v,
-                int diag) {
+                int diag, bool decomp_forked = false) {
   const Geom& g = op->g;
   const double ne = 8.0 * g.n1 * static_cast<double>(g.n2) * g.n3;
-  if (op->profiling) {
+  if (op->profiling) {  // serial launches so every stage gets its own event interval
     for (auto& e : op->ev)
       if (!e) VIE_CUDA_CHECK(cudaEventCreate(&e));
     VIE_CUDA_CHECK(cudaEventRecord(op->ev[0], st));
@@ -379,11 +394,18 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   auto mark = [&] {
     if (op->profiling) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
   };
+  const bool overlap = !op->profiling;
+  if (overlap && !decomp_forked) fork_decomp(op, st);
   vie::launch_row_fwd(x, op->A, g, op->P1, st);
   mark();
   vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
   mark();
-  vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
+  if (overlap) {
+    VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
+  } else {
+    if (decomp_forked) VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
+    else vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
+  }
   mark();
   vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st);
   mark();
@@ -670,6 +692,11 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
     op->PH = get_plan(ctx, g.n3, false, true);
+    int prio_lo = 0, prio_hi = 0;  // high priority: decompression CTAs are dispatched before FFT-pass CTAs
+    VIE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+    VIE_CUDA_CHECK(cudaStreamCreateWithPriority(&op->side, cudaStreamNonBlocking, prio_hi));
+    VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
+    VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
     *out = op.release();
   });
 }
@@ -710,8 +737,9 @@ int vie_matvec_host(vie_op op, const double* x_host, double* y_host) {
     if (!op->hx) op->hx = dev_alloc<double2>(static_cast<size_t>(n));
     if (!op->hy) op->hy = dev_alloc<double2>(static_cast<size_t>(n));
     cudaStream_t st = op->ctx->stream;
+    fork_decomp(op, st);  // decompression overlaps the H2D copy
     VIE_CUDA_CHECK(cudaMemcpyAsync(op->hx, x_host, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
-    run_matvec(op, op->hx, op->hy, st, nullptr, 0.0, 0);
+    run_matvec(op, op->hx, op->hy, st, nullptr, 0.0, 0, true);
     VIE_CUDA_CHECK(cudaMemcpyAsync(y_host, op->hy, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
   });
