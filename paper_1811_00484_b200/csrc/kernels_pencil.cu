@@ -352,24 +352,33 @@ size_t pencil_smem_shape(int n3, int S, int NC, const PencilShape& sh) {
 // fit in half the SM's shared memory; else one 512-thread full-group CTA.
 constexpr size_t kHalfSmSmem = 112 * 1024;
 
+#ifndef VIE_PENCIL_HALF_FIRST
+#define VIE_PENCIL_HALF_FIRST 1
+#endif
+
 bool pencil_shape(int n3, int S, int NC, PencilShape& sh, bool& two_per_sm) {
   const int P1P = pencil_p1pairs(S);
-  // measured (r1, C4 PWL): full group 36.5 ms < two half-group CTAs per SM 44 ms
-  for (int cf : {32, 16, 8}) {
-    sh = PencilShape{P1P, 2, 2, cf};
-    if (pencil_smem_shape(n3, S, NC, sh) <= kMaxSmem) {
-      two_per_sm = false;
-      return true;
+  auto full = [&]() {
+    for (int cf : {32, 16, 8}) {
+      sh = PencilShape{P1P, 2, 2, cf};
+      if (pencil_smem_shape(n3, S, NC, sh) <= kMaxSmem) {
+        two_per_sm = false;
+        return true;
+      }
     }
-  }
-  for (int cf : {32, 28, 24, 20, 16}) {
-    sh = PencilShape{P1P, 1, 1, cf};
-    if (pencil_smem_shape(n3, S, NC, sh) <= kHalfSmSmem) {
-      two_per_sm = true;
-      return true;
+    return false;
+  };
+  auto half = [&]() {
+    for (int cf : {32, 28, 24, 20, 16}) {
+      sh = PencilShape{P1P, 1, 1, cf};
+      if (pencil_smem_shape(n3, S, NC, sh) <= kHalfSmSmem) {
+        two_per_sm = true;
+        return true;
+      }
     }
-  }
-  return false;
+    return false;
+  };
+  return VIE_PENCIL_HALF_FIRST ? (half() || full()) : (full() || half());
 }
 
 template <int KIND, int BASIS>
