@@ -66,12 +66,23 @@ __device__ __forceinline__ double2 flip_sign(double2 v, unsigned long long sbit)
 // target is in [HALF*TH, HALF*TH + TH) (target split across two threads).
 // ALL = every component active (no per-component branch: lets the compiler
 // schedule spectrum loads and FMAs across components).
-template <int KIND, int BASIS, int B, int S, int TH, int HALF, bool ALL>
+// Component groups: the spectrum is streamed NG groups of CG components at a
+// time (double-buffered cp.async) while y^ stays in registers.
+template <int NC>
+constexpr int n_groups() {
+  return NC >= 16 ? 3 : 1;
+}
+template <int NC>
+constexpr int group_size() {
+  return (NC + n_groups<NC>() - 1) / n_groups<NC>();
+}
+
+template <int KIND, int BASIS, int B, int S, int TH, int HALF, bool ALL, int GRP, int CG>
 __device__ __forceinline__ void had_block(double2 (&yh)[TH], const double2 (&xh)[S], double2& sh,
                                           const double2* sh_base, int cstride, uint64_t active,
                                           unsigned long long f1, unsigned long long f2, unsigned long long f3) {
   constexpr BlockT blk = Tab<KIND, BASIS>::value.blocks[B];
-  if constexpr (blk.t / TH == HALF) {
+  if constexpr (blk.t / TH == HALF && blk.c / CG == GRP) {
     constexpr bool first = first_in_half<KIND, BASIS>(B, TH, HALF);
     constexpr CompT cp = Tab<KIND, BASIS>::value.comps[blk.c];
     if (!ALL && !((active >> blk.c) & 1ull)) return;
@@ -85,7 +96,7 @@ __device__ __forceinline__ void had_block(double2 (&yh)[TH], const double2 (&xh)
   }
 }
 
-template <int KIND, int BASIS, int S, int TH, int HALF, bool ALL, int... Bs>
+template <int KIND, int BASIS, int S, int TH, int HALF, bool ALL, int GRP, int CG, int... Bs>
 __device__ __forceinline__ void had_all(std::integer_sequence<int, Bs...>, double2 (&yh)[TH], const double2 (&xh)[S],
                                         const double2* sh_base, int cstride, uint64_t active, int m1flag, int m2flag,
                                         int mir) {
@@ -93,7 +104,12 @@ __device__ __forceinline__ void had_all(std::integer_sequence<int, Bs...>, doubl
   const unsigned long long f1 = static_cast<unsigned long long>(m1flag) << 63;
   const unsigned long long f2 = static_cast<unsigned long long>(m2flag) << 63;
   const unsigned long long f3 = static_cast<unsigned long long>(mir) << 63;
-  (had_block<KIND, BASIS, Bs, S, TH, HALF, ALL>(yh, xh, sh, sh_base, cstride, active, f1, f2, f3), ...);
+  (had_block<KIND, BASIS, Bs, S, TH, HALF, ALL, GRP, CG>(yh, xh, sh, sh_base, cstride, active, f1, f2, f3), ...);
+}
+
+template <int... Is, class F>
+__device__ __forceinline__ void sfor_g(std::integer_sequence<int, Is...>, F&& f) {
+  (f(std::integral_constant<int, Is>{}), ...);
 }
 
 struct PencilArgs {
@@ -146,16 +162,18 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   extern __shared__ double2 sm[];
   const Geom& g = a.g;
   const int n1 = g.n1, n2 = g.n2, n3 = g.n3, m1 = g.m1, m2 = g.m2, m3 = g.m3;
-  const int P1P = a.P1P, CF = a.CF, P2N = a.P2N, NBUF = a.NBUF;
+  constexpr int NG = n_groups<NC>();
+  constexpr int CG = group_size<NC>();
+  const int P1P = a.P1P, CF = a.CF, P2N = a.P2N;
   const int W = 2 * P1P;
   const int NP = P2N * W;  // pencils: [p2sel][w], w < W  (powers of two)
   const int lgW = __ffs(W) - 1, lgNP = __ffs(NP) - 1;
   const int ls = line_stride(n3);
   const SmemPlan SP = load_plan(sm, a.PH);
   double2* twb = sm + plan_smem_elems(n3);  // w_m3^k, k < n3
-  double2* shb = twb + n3;                  // NBUF x [P1P][NC][CF]
-  const int chunk_elems = P1P * NC * CF;
-  double2* buf = shb + NBUF * chunk_elems;  // [S][NP] lines of ls
+  double2* shb = twb + n3;                  // 2 x [P1P][CG][CF] spectrum sub-chunks
+  const int chunk_elems = P1P * CG * CF;
+  double2* buf = shb + 2 * chunk_elems;     // [S][NP] lines of ls
   for (int e = threadIdx.x; e < n3; e += blockDim.x) twb[e] = a.twm3[e];
 
   // blockIdx.x runs over axis-1 groups: neighbouring CTAs read neighbouring
@@ -174,19 +192,22 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   const int64_t sstride = kstride * n3;
 
   {
-    // ---- prefetch spectrum chunk 0 of this branch (lands during the FFT)
+    // ---- spectrum sub-chunks q = round * NG + group: CF octant frequencies x
+    // CG components; sub-chunk 0 is prefetched so it lands during the FFT
     const int nbo = b ? O : E;
-    const int nchunks = (nbo + CF - 1) / CF;
-    auto issue_chunk = [&](int ci) {
-      double2* dst = shb + (ci % NBUF) * chunk_elems;
-      const int u0 = ci * CF;
+    const int nrounds = (nbo + CF - 1) / CF;
+    const int nsub = nrounds * NG;
+    auto issue_chunk = [&](int q) {
+      double2* dst = shb + (q & 1) * chunk_elems;
+      const int r = q / NG, grp = q - r * NG;
+      const int u0 = r * CF;
       for (int e = threadIdx.x; e < chunk_elems; e += blockDim.x) {
         const int rc = static_cast<int>(a.div_cf.div(e));
         const int ul = e - rc * CF;
-        const int tr = static_cast<int>(a.div_nc.div(rc));
-        const int c = rc - tr * NC;
+        const int tr = static_cast<int>(a.div_nc.div(rc));  // div_nc divides by CG
+        const int c = grp * CG + (rc - tr * CG);
         const int p1o = q0 + tr;
-        if (p1o <= n1 && u0 + ul < nbo)
+        if (c < NC && p1o <= n1 && u0 + ul < nbo)
           cp_async16(dst + e, a.Shat + ((static_cast<int64_t>(p2o_tile) * (n1 + 1) + p1o) * NC + c) * n3p +
                                   b * E + u0 + ul);
       }
@@ -221,74 +242,72 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
     fft_forward<true>(buf, S * NP, ls, SP, false);
     VIE_PHASE(2);
 
-    // ---- Hadamard over the branch's octant frequencies, chunk by chunk
-    for (int ci = 0; ci < nchunks; ++ci) {
-      if (NBUF == 1 && ci > 0) {
-        __syncthreads();  // chunk ci-1 consumers done before its buffer is refilled
-        issue_chunk(ci);
-      }
-      cp_async_wait_all();
-      __syncthreads();  // chunk ci visible; (NBUF 2) chunk ci-1 consumers done
-      if (NBUF == 2 && ci + 1 < nchunks) issue_chunk(ci + 1);
-      const double2* shc = shb + (ci % NBUF) * chunk_elems;
-      // work unit = (spectral point, target half); threads [0, items) take
-      // half 0, [items, 2 items) half 1 (warp-uniform halves)
-      const int items = CF * NP * 2;
-      const int units = items * TS;
-      for (int u0 = 0; u0 < units; u0 += blockDim.x) {
-        const int unit = u0 + threadIdx.x;
-        const int half = unit >= items ? 1 : 0;
-        const int it = unit - half * items;
-        // lanes: mirror pair (mir) x pencil x frequency, frequency slowest
-        const int mir = it & 1;
-        const int rest = it >> 1;
-        const int p = rest & (NP - 1);
-        const int ul = rest >> lgNP;
-        const int u = ci * CF + ul;
-        const int f3o = 2 * u + b;
-        const int w = p & (W - 1), p2sel = p >> lgW;
-        const int pos1 = c0 + w;
-        const bool valid = unit < units && u < nbo && !(mir && (f3o == 0 || f3o == n3)) && pos1 < m1;
-        double2 xh[S];
-        double2* pl = buf;
-        int m1flag = 0, m2flag = 0, p1o = 0, p2o = 0;
-        if (valid) {
-          const int f1 = freq_of_pos(pos1, n1);
-          m1flag = f1 > n1;
-          p1o = m1flag ? m1 - f1 : f1;
-          const int f2 = freq_of_pos(pos2_0 + p2sel, n2);
-          m2flag = f2 > n2;
-          p2o = m2flag ? m2 - f2 : f2;
-          const int f3 = mir ? m3 - f3o : f3o;
-          pl = buf + p * ls + SP.slot[(f3 - b) >> 1];
+    // ---- Hadamard: one spectral point (x one target half) per thread per
+    // round; x^ and y^ in registers for the whole round while the spectrum of
+    // the round streams in NG component groups (next group prefetched).
+    // lanes: mirror pair (mir) x pencil x frequency (slowest)
+    const int items = CF * NP * 2;
+    for (int r = 0; r < nrounds; ++r) {
+      const int unit = threadIdx.x;
+      const int half = unit >= items ? 1 : 0;
+      const int it = unit - half * items;
+      const int mir = it & 1;
+      const int rest = it >> 1;
+      const int p = rest & (NP - 1);
+      const int ul = rest >> lgNP;
+      const int u = r * CF + ul;
+      const int f3o = 2 * u + b;
+      const int w = p & (W - 1), p2sel = p >> lgW;
+      const int pos1 = c0 + w;
+      const bool valid = unit < items * TS && u < nbo && !(mir && (f3o == 0 || f3o == n3)) && pos1 < m1;
+      double2 xh[S], yh[TH];
+      double2* pl = buf;
+      int m1flag = 0, m2flag = 0, p1o = 0, p2o = 0, tr = 0;
+      bool in_tile = false;
+      if (valid) {
+        const int f1 = freq_of_pos(pos1, n1);
+        m1flag = f1 > n1;
+        p1o = m1flag ? m1 - f1 : f1;
+        const int f2 = freq_of_pos(pos2_0 + p2sel, n2);
+        m2flag = f2 > n2;
+        p2o = m2flag ? m2 - f2 : f2;
+        const int f3 = mir ? m3 - f3o : f3o;
+        pl = buf + p * ls + SP.slot[(f3 - b) >> 1];
 #pragma unroll
-          for (int s = 0; s < S; ++s) xh[s] = pl[s * NP * ls];
-        }
-        if (TS > 1) __syncthreads();  // both halves read x^ before either overwrites it
+        for (int s = 0; s < S; ++s) xh[s] = pl[s * NP * ls];
+        tr = p1o - q0;
+        in_tile = p2o == p2o_tile && tr >= 0 && tr < P1P;
+      }
+#pragma unroll
+      for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
+      sfor_g(std::make_integer_sequence<int, NG>{}, [&](auto gc) {
+        constexpr int GRP = decltype(gc)::value;
+        const int q = r * NG + GRP;
+        cp_async_wait_all();
+        __syncthreads();  // sub-chunk q visible; all threads done with q-1 (and with x^ reads of this round)
+        if (q + 1 < nsub) issue_chunk(q + 1);
         if (valid) {
           const double2* sh_base;
           int cstride;
-          const int tr = p1o - q0;
-          if (p2o == p2o_tile && tr >= 0 && tr < P1P) {
-            sh_base = shc + (tr * NC) * CF + ul;
+          if (in_tile) {  // smem sub-chunk [tr][c - GRP*CG][ul]
+            sh_base = shb + (q & 1) * chunk_elems + (tr * CG - GRP * CG) * CF + ul;
             cstride = CF;
           } else {  // boundary pencils (frequencies 0 / n of a pair) outside the tile
             sh_base = a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + p1o) * NC) * n3p + b * E + u;
             cstride = n3p;
           }
-          double2 yh[TH];
-#pragma unroll
-          for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
           if (half == 0) {
-            had_all<KIND, BASIS, S, TH, 0, ALL>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride,
-                                                a.active, m1flag, m2flag, mir);
+            had_all<KIND, BASIS, S, TH, 0, ALL, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base,
+                                                         cstride, a.active, m1flag, m2flag, mir);
           } else if constexpr (TS > 1) {
-            had_all<KIND, BASIS, S, TH, 1, ALL>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, cstride,
-                                                a.active, m1flag, m2flag, mir);
+            had_all<KIND, BASIS, S, TH, 1, ALL, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base,
+                                                         cstride, a.active, m1flag, m2flag, mir);
           }
-#pragma unroll
-          for (int t = 0; t < TH; ++t) pl[(half * TH + t) * NP * ls] = yh[t];
         }
+      });
+      if (valid) {
+#pragma unroll
+        for (int t = 0; t < TH; ++t) pl[(half * TH + t) * NP * ls] = yh[t];
       }
     }
     __syncthreads();
@@ -342,14 +361,15 @@ struct PencilShape {
 };
 
 size_t pencil_smem_shape(int n3, int S, int NC, const PencilShape& sh) {
-  const size_t e = static_cast<size_t>(plan_smem_elems(n3)) + n3 +
-                   static_cast<size_t>(sh.NBUF) * sh.P1P * NC * sh.CF +
+  const int cg = NC >= 16 ? (NC + 2) / 3 : NC;  // group_size<NC>()
+  const size_t e = static_cast<size_t>(plan_smem_elems(n3)) + n3 + 2ull * sh.P1P * cg * sh.CF +
                    static_cast<size_t>(S) * 2 * sh.P1P * sh.P2N * line_stride(n3);
   return e * sizeof(double2);
 }
 
-// Two 256-thread CTAs per SM (half mirror group, one chunk buffer) when they
-// fit in half the SM's shared memory; else one 512-thread full-group CTA.
+// Two 256-thread CTAs per SM (half mirror group) when they fit in half the
+// SM's shared memory; else one 512-thread full-group CTA.  CF is set so a
+// round gives every thread one (point, target half): CF = threads / (NP 2 TS).
 constexpr size_t kHalfSmSmem = 112 * 1024;
 
 #ifndef VIE_PENCIL_HALF_FIRST
@@ -358,25 +378,16 @@ constexpr size_t kHalfSmSmem = 112 * 1024;
 
 bool pencil_shape(int n3, int S, int NC, PencilShape& sh, bool& two_per_sm) {
   const int P1P = pencil_p1pairs(S);
+  const int TS = S >= 12 ? 2 : 1;
   auto full = [&]() {
-    for (int cf : {32, 16, 8}) {
-      sh = PencilShape{P1P, 2, 2, cf};
-      if (pencil_smem_shape(n3, S, NC, sh) <= kMaxSmem) {
-        two_per_sm = false;
-        return true;
-      }
-    }
-    return false;
+    sh = PencilShape{P1P, 2, 2, 512 / (4 * P1P * 2 * TS)};
+    two_per_sm = false;
+    return pencil_smem_shape(n3, S, NC, sh) <= kMaxSmem;
   };
   auto half = [&]() {
-    for (int cf : {32, 28, 24, 20, 16}) {
-      sh = PencilShape{P1P, 1, 1, cf};
-      if (pencil_smem_shape(n3, S, NC, sh) <= kHalfSmSmem) {
-        two_per_sm = true;
-        return true;
-      }
-    }
-    return false;
+    sh = PencilShape{P1P, 1, 2, 256 / (2 * P1P * 2 * TS)};
+    two_per_sm = true;
+    return pencil_smem_shape(n3, S, NC, sh) <= kHalfSmSmem;
   };
   return VIE_PENCIL_HALF_FIRST ? (half() || full()) : (full() || half());
 }
@@ -393,7 +404,7 @@ void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const do
   PencilArgs a{Bin, Bout, Bout1, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}};
   a.div_n3.init(static_cast<uint32_t>(g.n3));
   a.div_cf.init(static_cast<uint32_t>(sh.CF));
-  a.div_nc.init(static_cast<uint32_t>(NC));
+  a.div_nc.init(static_cast<uint32_t>(group_size<NC>()));
   const size_t smem = pencil_smem_shape(g.n3, S, NC, sh);
   dim3 grid(2 * ((g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P)), g.m2 / sh.P2N);
   cudaLaunchConfig_t cfg = {};
