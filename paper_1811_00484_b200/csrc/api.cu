@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -66,6 +67,7 @@ struct PlanHolder {
   double2* tw = nullptr;
   int* slot = nullptr;
   vie::StageDesc* st = nullptr;
+  std::vector<int> radices;
   ~PlanHolder() {
     dev_free(tw);
     dev_free(slot);
@@ -112,6 +114,8 @@ struct vie_op_s {
   double2* Bo1 = nullptr;  // pencil output slab (odd axis-3 frequencies)
   int64_t ws_bytes = 0;
   FftPlan P1{}, P2{}, P3{}, PH{};
+  vie::Pass2 Q1{}, Q2{};           // register-staged two-stage row / column passes
+  bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
   // host-buffer staging (vie_matvec_host)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -158,6 +162,14 @@ constexpr int kMaxRadix = 10;
 #define VIE_WIDE_PASSES 1
 #endif
 constexpr bool kWidePasses = VIE_WIDE_PASSES;  // two-stage plans for the row/column passes
+#ifndef VIE_PASS2
+#define VIE_PASS2 1
+#endif
+constexpr bool kPass2 = VIE_PASS2;  // register-staged passes (kernels_fft2.cu)
+int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
 
 // Fewest stages, then smallest largest radix; first radix even when the
 // transform is pad/crop pruned (half_in / half_out).
@@ -184,11 +196,15 @@ bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::
 }
 
 // wide = plan for the pencil kernel (radices up to 20, VIE_FFT_RADICES_WIDE)
-const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = false) {
+const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = false,
+                        std::vector<int>* radices = nullptr) {
   const int key = (pruned ? n : -n) * (wide ? 4096 : 1);
   std::lock_guard<std::mutex> lk(ctx->mu);
   auto it = ctx->plans.find(key);
-  if (it != ctx->plans.end()) return it->second->plan;
+  if (it != ctx->plans.end()) {
+    if (radices) *radices = it->second->radices;
+    return it->second->plan;
+  }
   if (n < 1 || (pruned && (n & 1))) throw Invalid("FFT plan: embedded length must be even");
   std::vector<int> rad, cur;
   for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth)
@@ -196,6 +212,8 @@ const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = fals
   if (n > 1 && rad.empty())
     throw Invalid("FFT plan: length " + std::to_string(n) + " has a prime factor > 7");
   auto h = std::make_unique<PlanHolder>();
+  h->radices = rad;
+  if (radices) *radices = rad;
   FftPlan& P = h->plan;
   P.n = n;
   P.nst = static_cast<int>(rad.size());
@@ -396,9 +414,11 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   };
   const bool overlap = !op->profiling;
   if (overlap && !decomp_forked) fork_decomp(op, st);
-  vie::launch_row_fwd(x, op->A, g, op->P1, st);
+  if (op->q1) vie::launch_row_fwd2(x, op->A, g, op->Q1, st);
+  else vie::launch_row_fwd(x, op->A, g, op->P1, st);
   mark();
-  vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
+  if (op->q2) vie::launch_col_fwd2(op->A, op->B, g, op->Q2, st);
+  else vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
   mark();
   if (overlap) {
     VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
@@ -409,10 +429,12 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   mark();
   vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st);
   mark();
-  vie::launch_col_inv(op->Bo, nullptr, op->A, g, op->P2, st);
+  if (op->q2) vie::launch_col_inv2(op->Bo, op->A, g, op->Q2, st);
+  else vie::launch_col_inv(op->Bo, nullptr, op->A, g, op->P2, st);
   mark();
   // reference inverse3 divides by N_e (fft.hpp:34-37)
-  vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+  if (op->q1) vie::launch_row_inv2(op->A, y, g, op->Q1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+  else vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
   mark();
   op->last_launches = 7;
   if (op->profiling) {
@@ -691,6 +713,13 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
+    if (kPass2) {  // register-staged passes when the axis has a <= 2-stage wide plan
+      std::vector<int> r1, r2;
+      const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1);
+      const FftPlan& W2 = get_plan(ctx, g.m2, true, true, &r2);
+      op->q1 = vie::pass2_init(op->Q1, g.m1, r1.data(), static_cast<int>(r1.size()), W1.tw, env_int("VIE_ROW_LINES", 0));
+      op->q2 = vie::pass2_init(op->Q2, g.m2, r2.data(), static_cast<int>(r2.size()), W2.tw, 0);
+    }
     op->PH = get_plan(ctx, g.n3, false, true);
     int prio_lo = 0, prio_hi = 0;  // high priority: decompression CTAs are dispatched before FFT-pass CTAs
     VIE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));

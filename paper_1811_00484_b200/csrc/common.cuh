@@ -89,6 +89,11 @@ __host__ __device__ __forceinline__ int freq_of_pos(int P, int n) {
   if (P == 1) return n;
   return (P & 1) ? 2 * n - (P >> 1) : (P >> 1);
 }
+__host__ __device__ __forceinline__ int pos_of_freq(int f, int n) {
+  if (f == 0) return 0;
+  if (f == n) return 1;
+  return f < n ? 2 * f : 2 * (2 * n - f) + 1;
+}
 
 // ---------------------------------------------------------------- tables
 // Component tables (product-side implementation; the oracle has its own).

@@ -45,6 +45,23 @@ void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, doubl
 // B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
 void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,
                     cudaStream_t st);
+// Register-staged passes (kernels_fft2.cu) for axes with m = R0 * R1 (or
+// m = R0), R0 even: one shared-memory round trip per pass.
+struct Pass2 {
+  int m, n;     // embedded / grid length
+  int R0, R1;   // radices (R1 == 1: single stage)
+  int R1p, ls;  // padded block length (odd) and smem line stride (odd)
+  int lines;    // rows per CTA (row passes)
+  const double2* tw;  // w_m^e
+  FastDiv dR0, dR1;
+};
+bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw, int row_lines);
+void launch_row_fwd2(const double2* x, double2* A, const Geom& g, const Pass2& P, cudaStream_t st);
+void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st);
+void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st);
+void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P, double scale, const double2* eps,
+                     const double2* xin, double inv_v, int basis, int diag, cudaStream_t st);
+
 // Epilogue: y = scale * (IDFT) or the system form (eps != nullptr):
 //   y = (diag ? eps*g_l*xin : 0) - (eps - 1) * inv_v * scale * (IDFT)
 void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& P1, double scale,
