@@ -116,6 +116,7 @@ struct vie_op_s {
   FftPlan P1{}, P2{}, P3{}, PH{};
   vie::Pass2 Q1{}, Q2{};           // register-staged two-stage row / column passes
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
+  bool pencil2 = false;         // compile-time-shaped pencil kernel for this n3
   // host-buffer staging (vie_matvec_host)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -165,7 +166,11 @@ constexpr bool kWidePasses = VIE_WIDE_PASSES;  // two-stage plans for the row/co
 #ifndef VIE_PASS2
 #define VIE_PASS2 1
 #endif
-constexpr bool kPass2 = VIE_PASS2;  // register-staged passes (kernels_fft2.cu)
+constexpr bool kPass2 = VIE_PASS2;
+#ifndef VIE_PENCIL2
+#define VIE_PENCIL2 1
+#endif
+constexpr bool kPencil2 = VIE_PENCIL2;  // kernels_pencil2.cu when n3 has a compiled shape  // register-staged passes (kernels_fft2.cu)
 int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -427,7 +432,13 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
     else vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
   }
   mark();
-  vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st);
+  if (op->pencil2) {  // compile-time-shaped kernel + the axis-1 edge group on the generic one
+    vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st,
+                       1);
+    vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+  } else {
+    vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st);
+  }
   mark();
   if (op->q2) vie::launch_col_inv2(op->Bo, op->A, g, op->Q2, st);
   else vie::launch_col_inv(op->Bo, nullptr, op->A, g, op->P2, st);
@@ -713,6 +724,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
+    op->pencil2 = kPencil2 && vie::pencil2_supported(op->kind, op->basis, g.n3, op->active, g.NC);
     if (kPass2) {  // register-staged passes when the axis has a <= 2-stage wide plan
       std::vector<int> r1, r2;
       const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1);

@@ -41,7 +41,15 @@ void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& 
 // Bin: forward slab (after axes 1-2); Bout: output slab (before the axis-2/1
 // inverses); PH: n3-point plan; twm3: w_m3^e table of the m3-point plan.
 void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat,
-                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active_mask, cudaStream_t st);
+                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active_mask, cudaStream_t st,
+                   int groups = 0);  // groups > 0: only the first `groups` axis-1 pair groups (edge pencils)
+// Compile-time-shaped pencil kernel (kernels_pencil2.cu) for n3 = R0 * R1 in
+// its shape list and all components active; handles every axis-1 group but
+// the first (frequencies 0 and n1 pair differently), which launch_pencil
+// covers with groups = 1.  Returns false (nothing launched) if unsupported.
+bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
+void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+                    const double2* twm3, cudaStream_t st);
 // B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
 void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,
                     cudaStream_t st);

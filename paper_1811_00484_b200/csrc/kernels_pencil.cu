@@ -24,11 +24,14 @@
 #include <utility>
 
 #include "fft.cuh"
+#include "hadamard.cuh"
 #include "kernels.cuh"
 
 namespace vie {
 
 namespace {
+
+using namespace had;
 
 __host__ __device__ __forceinline__ int line_stride(int n) { return n + 1; }
 
@@ -38,79 +41,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
-
-template <int KIND, int BASIS>
-struct Tab {
-  static constexpr Table<KIND, BASIS> value = make_table<KIND, BASIS>();
-};
-
-// First block of component c (of block B) whose target lies in this half.
-template <int KIND, int BASIS>
-constexpr bool first_in_half(int B, int TH, int HALF) {
-  const auto& tb = Tab<KIND, BASIS>::value;
-  const int c = tb.blocks[B].c;
-  for (int b = B - 1; b >= 0 && tb.blocks[b].c == c; --b)
-    if (tb.blocks[b].t / TH == HALF) return false;
-  return true;
-}
-
-// Block B of the table, all indices compile-time constants; only blocks whose
-// target is in [HALF*TH, HALF*TH + TH) (target split across two threads).
-__device__ __forceinline__ double2 flip_sign(double2 v, unsigned long long sbit) {
-  // branch-free negation: xor of the IEEE sign bits (integer pipe)
-  return make_double2(__longlong_as_double(__double_as_longlong(v.x) ^ static_cast<long long>(sbit)),
-                      __longlong_as_double(__double_as_longlong(v.y) ^ static_cast<long long>(sbit)));
-}
-
-// Block B of the table, all indices compile-time constants; only blocks whose
-// target is in [HALF*TH, HALF*TH + TH) (target split across two threads).
-// ALL = every component active (no per-component branch: lets the compiler
-// schedule spectrum loads and FMAs across components).
-// Component groups: the spectrum is streamed NG groups of CG components at a
-// time (double-buffered cp.async) while y^ stays in registers.
-template <int NC>
-constexpr int n_groups() {
-  return NC >= 16 ? 3 : 1;
-}
-template <int NC>
-constexpr int group_size() {
-  return (NC + n_groups<NC>() - 1) / n_groups<NC>();
-}
-
-template <int KIND, int BASIS, int B, int S, int TH, int HALF, bool ALL, int GRP, int CG>
-__device__ __forceinline__ void had_block(double2 (&yh)[TH], const double2 (&xh)[S], double2& sh,
-                                          const double2* sh_base, int cstride, uint64_t active,
-                                          unsigned long long f1, unsigned long long f2, unsigned long long f3) {
-  constexpr BlockT blk = Tab<KIND, BASIS>::value.blocks[B];
-  if constexpr (blk.t / TH == HALF && blk.c / CG == GRP) {
-    constexpr bool first = first_in_half<KIND, BASIS>(B, TH, HALF);
-    constexpr CompT cp = Tab<KIND, BASIS>::value.comps[blk.c];
-    if (!ALL && !((active >> blk.c) & 1ull)) return;
-    if (first) {
-      // sign of the mirrored point: product of the odd-axis flags (sign bits)
-      const unsigned long long sbit = (cp.p0 < 0 ? f1 : 0ull) ^ (cp.p1 < 0 ? f2 : 0ull) ^ (cp.p2 < 0 ? f3 : 0ull);
-      sh = flip_sign(sh_base[blk.c * cstride], sbit);
-    }
-    if (blk.coef > 0) cfma(yh[blk.t - HALF * TH], sh, xh[blk.s]);
-    else cfms(yh[blk.t - HALF * TH], sh, xh[blk.s]);
-  }
-}
-
-template <int KIND, int BASIS, int S, int TH, int HALF, bool ALL, int GRP, int CG, int... Bs>
-__device__ __forceinline__ void had_all(std::integer_sequence<int, Bs...>, double2 (&yh)[TH], const double2 (&xh)[S],
-                                        const double2* sh_base, int cstride, uint64_t active, int m1flag, int m2flag,
-                                        int mir) {
-  double2 sh = make_double2(0.0, 0.0);
-  const unsigned long long f1 = static_cast<unsigned long long>(m1flag) << 63;
-  const unsigned long long f2 = static_cast<unsigned long long>(m2flag) << 63;
-  const unsigned long long f3 = static_cast<unsigned long long>(mir) << 63;
-  (had_block<KIND, BASIS, Bs, S, TH, HALF, ALL, GRP, CG>(yh, xh, sh, sh_base, cstride, active, f1, f2, f3), ...);
-}
-
-template <int... Is, class F>
-__device__ __forceinline__ void sfor_g(std::integer_sequence<int, Is...>, F&& f) {
-  (f(std::integral_constant<int, Is>{}), ...);
-}
 
 struct PencilArgs {
   const double2* Bin;
@@ -395,7 +325,7 @@ bool pencil_shape(int n3, int S, int NC, PencilShape& sh, bool& two_per_sm) {
 template <int KIND, int BASIS>
 void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat, const Geom& g,
                      const FftPlan& PH,
-                     const double2* twm3, uint64_t active, cudaStream_t st) {
+                     const double2* twm3, uint64_t active, int groups, cudaStream_t st) {
   constexpr int S = TableDims<KIND, BASIS>::S;
   constexpr int NC = TableDims<KIND, BASIS>::NC;
   PencilShape sh{};
@@ -406,7 +336,8 @@ void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const do
   a.div_cf.init(static_cast<uint32_t>(sh.CF));
   a.div_nc.init(static_cast<uint32_t>(group_size<NC>()));
   const size_t smem = pencil_smem_shape(g.n3, S, NC, sh);
-  dim3 grid(2 * ((g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P)), g.m2 / sh.P2N);
+  const int all_groups = (g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P);
+  dim3 grid(2 * (groups > 0 ? std::min(groups, all_groups) : all_groups), g.m2 / sh.P2N);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.dynamicSmemBytes = smem;
@@ -454,11 +385,12 @@ size_t pencil_smem(int n3, int S, int NC) {
 }
 
 void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, double2* Bout1, const double2* Shat,
-                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active, cudaStream_t st) {
-  if (kind == 0 && basis == 0) launch_pencil_t<0, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
-  else if (kind == 1 && basis == 0) launch_pencil_t<1, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
-  else if (kind == 0 && basis == 1) launch_pencil_t<0, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
-  else launch_pencil_t<1, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, st);
+                   const Geom& g, const FftPlan& PH, const double2* twm3, uint64_t active, cudaStream_t st,
+                   int groups) {
+  if (kind == 0 && basis == 0) launch_pencil_t<0, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, groups, st);
+  else if (kind == 1 && basis == 0) launch_pencil_t<1, 0>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, groups, st);
+  else if (kind == 0 && basis == 1) launch_pencil_t<0, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, groups, st);
+  else launch_pencil_t<1, 1>(Bin, Bout, Bout1, Shat, g, PH, twm3, active, groups, st);
 }
 
 }  // namespace vie

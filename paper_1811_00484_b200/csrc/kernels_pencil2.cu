@@ -1,0 +1,400 @@
+// kernels_pencil2.cu -- compile-time-shaped fused axis-3 FFT + Hadamard + IFFT.
+//
+// Same math as kernels_pencil.cu (read its header first): a 2-CTA cluster
+// owns P1P axis-1 mirror pairs at one axis-2 position, CTA b of the cluster
+// the even (b = 0) / odd (b = 1) axis-3 frequencies as a length-n3 branch
+// transform, and the octant spectrum S^ is read once per mirror group.  What
+// differs is the schedule, shaped for n3 = R0 * R1 known at compile time:
+//
+//  * forward stage 0 (radix R0) runs straight from global memory in
+//    registers -- no staging copy, and the odd branch's input twiddle
+//    w_m3^{n} folds into compile-time constants w_{2 R0}^{i} on the inputs plus
+//    the stage twiddle w_m3^{m'(2k+b)} on the outputs; stage 1 (radix R1) is
+//    one in-place smem pass;
+//  * the spectrum streams in component-group chunks through 1-D bulk copies
+//    (cp.async.bulk, one per component run, issued by one thread) on an
+//    mbarrier full/empty ring -- no per-element address arithmetic;
+//  * every spectrum offset in the unrolled block table is an immediate;
+//  * the inverse stage 1 is one in-place smem pass; the inverse stage 0 is
+//    fused with the branch combine y[n] = A_0[n] + conj(w_m3^n) A_1[n]: CTA b
+//    reads both branches' lines of its half (the partner's through DSMEM),
+//    runs both radix-R0 adjoints in registers and stores y to global.
+#include <cooperative_groups.h>
+
+#include <utility>
+
+#include "fft.cuh"
+#include "hadamard.cuh"
+#include "kernels.cuh"
+
+namespace vie {
+
+namespace {
+
+using namespace had;
+
+// ---------------------------------------------------------------- mbarrier / bulk copy
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  while (!mbar_try(b, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int p1pairs(int S) { return S >= 12 ? 1 : (S >= 6 ? 2 : 4); }  // = kernels_pencil.cu pencil_p1pairs
+
+template <int KIND, int BASIS, int R0, int R1>
+struct Shape2 {
+  static constexpr int S = TableDims<KIND, BASIS>::S;
+  static constexpr int NB = TableDims<KIND, BASIS>::NB;
+  static constexpr int NC = TableDims<KIND, BASIS>::NC;
+  static constexpr int THREADS = 256;
+  static constexpr int WARPS = THREADS / 32;
+  static constexpr int TS = S >= 12 ? 2 : 1;  // threads per spectral point (target halves)
+  static constexpr int TH = S / TS;
+  static constexpr int P1P = p1pairs(S);
+  static constexpr int NP = 2 * P1P;  // pencils (axis-1 positions) per CTA
+  static constexpr int LINES = S * NP;
+  static constexpr int HL = LINES / 2;  // lines combined + stored by each CTA of the pair
+  static constexpr int N3 = R0 * R1;
+  static constexpr int LS = N3 | 1;  // odd line stride: lanes over lines hit distinct banks
+  static constexpr int CF = THREADS / (NP * 2 * TS);  // octant frequencies per chunk
+  static constexpr int NG = n_groups<NC>();
+  static constexpr int CG = group_size<NC>();
+  static constexpr int CHUNK = P1P * CG * CF;  // double2 per chunk buffer
+  static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
+  static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
+  static constexpr size_t smem_bytes = 64 + sizeof(double2) * (2 * CHUNK + static_cast<size_t>(LINES) * LS);
+  static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
+  static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
+};
+
+struct Pencil2Args {
+  const double2* Bin;
+  double2* Bout;
+  const double2* Shat;
+  const double2* twm3;  // w_m3^e, e < m3
+  int n1, n2, m1, m2, m3;
+  int64_t kstride, sstride;  // m1 m2, m1 m2 n3
+};
+
+// the slot of branch frequency phi = k0 + R0 k1 after the two forward stages
+template <int R0, int R1>
+__device__ __forceinline__ int slot_of(int phi) {
+  const int k0 = phi % R0, k1 = phi / R0;
+  return k0 * R1 + k1;
+}
+
+template <int KIND, int BASIS, int R0, int R1>
+__global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
+  using SH = Shape2<KIND, BASIS, R0, R1>;
+  constexpr int S = SH::S, NB = SH::NB, NC = SH::NC, TS = SH::TS, TH = SH::TH, P1P = SH::P1P, NP = SH::NP;
+  constexpr int LINES = SH::LINES, HL = SH::HL, N3 = SH::N3, LS = SH::LS, CF = SH::CF, NG = SH::NG, CG = SH::CG;
+  constexpr int CHUNK = SH::CHUNK, E = SH::E, O = SH::O;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);  // [2]
+  uint64_t* empty = full + 2;                           // [2]
+  double2* chunk = reinterpret_cast<double2*>(smraw + 64);
+  double2* buf = chunk + 2 * CHUNK;  // [LINES][LS]
+
+  const int tid = threadIdx.x;
+  const int b = blockIdx.x & 1;                     // axis-3 branch = rank in the cluster
+  const int c0 = 2 * P1P * (1 + (blockIdx.x >> 1));  // first axis-1 position (group 0 is the edge launch)
+  const int q0 = c0 >> 1;                           // octant row of pair 0
+  const int pos2 = blockIdx.y;
+  const int n1 = a.n1, n2 = a.n2, m1 = a.m1;
+  const int f2 = freq_of_pos(pos2, n2);
+  const int m2flag = f2 > n2;
+  const int p2o = m2flag ? a.m2 - f2 : f2;
+  constexpr int n3p = N3 + 1;
+  const int nbo = b ? O : E;
+  const int nrounds = (nbo + CF - 1) / CF;
+  const int nsub = nrounds * NG;
+
+  // ---- spectrum chunk q = round * NG + group -> buffer q & 1 (bulk copies)
+  auto issue_chunk = [&](int q) {
+    const int r = q / NG, grp = q - r * NG;
+    const int u0 = r * CF;
+    const int cnt = min(CF, nbo - u0);
+    const int cend = min(CG, NC - grp * CG);
+    int rows = 0;
+    for (int tr = 0; tr < P1P; ++tr) rows += (q0 + tr <= n1) ? 1 : 0;
+    uint64_t* bar = full + (q & 1);
+    mbar_expect_tx(bar, static_cast<uint32_t>(rows * cend * cnt * sizeof(double2)));
+    double2* dst = chunk + (q & 1) * CHUNK;
+    for (int tr = 0; tr < rows; ++tr) {
+      const double2* src =
+          a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + q0 + tr) * NC + grp * CG) * n3p + b * E + u0;
+      for (int cl = 0; cl < cend; ++cl)
+        bulk_g2s(dst + (tr * CG + cl) * CF, src + cl * n3p, static_cast<uint32_t>(cnt * sizeof(double2)), bar);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(full, 1);
+    mbar_init(full + 1, 1);
+    mbar_init(empty, SH::WARPS);
+    mbar_init(empty + 1, SH::WARPS);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    issue_chunk(0);
+    if (nsub > 1) issue_chunk(1);
+  }
+
+  // ---- forward stage 0 (radix R0) from global, branch + stage twiddles folded
+  for (int u = tid; u < LINES * R1; u += SH::THREADS) {
+    const int line = u % LINES, mp = u / LINES;
+    const int s = line / NP, p = line % NP;
+    const int pos1 = c0 + p;
+    double2* dst = buf + line * LS + mp;
+    if (pos1 >= m1) {
+#pragma unroll
+      for (int k = 0; k < R0; ++k) dst[k * R1] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
+                         static_cast<int64_t>(pos2) * m1 + pos1;
+    const int64_t step = static_cast<int64_t>(R1) * a.kstride;
+    double2 v[R0];
+#pragma unroll
+    for (int i = 0; i < R0; ++i) v[i] = src[i * step];
+    if (b) {
+      sfor<R0 - 1>([&](auto ic) {
+        constexpr int i = decltype(ic)::value + 1;
+        v[i] = twc<2 * R0, false, i>(v[i]);  // w_m3^{i R1} = w_{2 R0}^i
+      });
+    }
+    DFTs<R0, false, 1, 0>::run(v);
+    // output k: w_m3^{mp (2k + b)}
+    const double2 wstep = __ldg(a.twm3 + 2 * mp);
+    double2 w = b ? __ldg(a.twm3 + mp) : make_double2(1.0, 0.0);
+    sfor<R0>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      dst[k * R1] = (k == 0 && !b) ? v[out_idx(R0, 0)] : cmul(v[out_idx(R0, k)], w);
+      if (k + 1 < R0) w = cmul(w, wstep);
+    });
+  }
+  __syncthreads();
+  // ---- forward stage 1 (radix R1), in place
+  for (int u = tid; u < LINES * R0; u += SH::THREADS) {
+    const int line = u % LINES, k0 = u / LINES;
+    double2* p = buf + line * LS + k0 * R1;
+    double2 v[R1];
+#pragma unroll
+    for (int i = 0; i < R1; ++i) v[i] = p[i];
+    DFTs<R1, false, 1, 0>::run(v);
+    sfor<R1>([&](auto kc) {
+      constexpr int k = decltype(kc)::value;
+      p[k] = v[out_idx(R1, k)];
+    });
+  }
+  __syncthreads();
+
+  // ---- Hadamard: one (point, target half) per thread per round
+  {
+    constexpr int ITEMS = CF * NP * 2;
+    const int half = TS > 1 ? (tid >= ITEMS ? 1 : 0) : 0;
+    const int it = tid - half * ITEMS;
+    const int mir = it & 1;
+    const int p = (it >> 1) % NP;
+    const int ul = (it >> 1) / NP;
+    const int pos1 = c0 + p;
+    const int m1flag = pos1 & 1;  // positions 2j, 2j+1 hold frequencies j, m1 - j (j >= 1)
+    const int tr = p >> 1;
+    const int lane = tid & 31;
+    for (int r = 0; r < nrounds; ++r) {
+      const int u = r * CF + ul;
+      const int f3o = 2 * u + b;
+      const bool valid = u < nbo && !(mir && (f3o == 0 || f3o == N3)) && pos1 < m1;
+      const int phi = mir ? N3 - u - b : u;
+      double2* pl = buf + p * LS + slot_of<R0, R1>(valid ? phi : 0);
+      double2 xh[S], yh[TH];
+      if (valid) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) xh[s] = pl[s * NP * LS];
+      }
+#pragma unroll
+      for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
+      sfor_g(std::make_integer_sequence<int, NG>{}, [&](auto gc) {
+        constexpr int GRP = decltype(gc)::value;
+        const int q = r * NG + GRP;
+        const int bi = q & 1;
+        mbar_wait(full + bi, (q >> 1) & 1);
+        if (valid) {
+          const double2* sh_base = chunk + bi * CHUNK + (tr * CG - GRP * CG) * CF + ul;
+          if (half == 0) {
+            had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
+                                                          ~0ull, m1flag, m2flag, mir);
+          } else if constexpr (TS > 1) {
+            had_all<KIND, BASIS, S, TH, 1, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
+                                                          ~0ull, m1flag, m2flag, mir);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + bi);
+        if (tid == 0 && q + 2 < nsub) {
+          mbar_wait(empty + bi, (q >> 1) & 1);  // every warp is done with buffer bi
+          issue_chunk(q + 2);
+        }
+      });
+      __syncthreads();  // all x^ of this round read before any y^ overwrites them
+      if (valid) {
+#pragma unroll
+        for (int t = 0; t < TH; ++t) pl[(half * TH + t) * NP * LS] = yh[t];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- inverse stage 1 (adjoint of radix R1), in place
+  for (int u = tid; u < LINES * R0; u += SH::THREADS) {
+    const int line = u % LINES, k0 = u / LINES;
+    double2* p = buf + line * LS + k0 * R1;
+    double2 v[R1];
+#pragma unroll
+    for (int k = 0; k < R1; ++k) v[k] = p[k];
+    DFTs<R1, true, 1, 0>::run(v);
+    sfor<R1>([&](auto ic) {
+      constexpr int i = decltype(ic)::value;
+      p[i] = v[out_idx(R1, i)];
+    });
+  }
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();  // both branches' stage-1 adjoints visible cluster-wide
+  {
+    const double2* own = buf;
+    const double2* rem = cluster.map_shared_rank(buf, b ^ 1);
+    const double2* X0 = b ? rem : own;
+    const double2* X1 = b ? own : rem;
+    for (int u = tid; u < HL * R1; u += SH::THREADS) {
+      const int line = b * HL + u % HL, mp = u / HL;
+      const int s = line / NP, p = line % NP;
+      const int pos1 = c0 + p;
+      if (pos1 >= m1) continue;
+      const int off = line * LS + mp;
+      const double2 wstep = __ldg(a.twm3 + 2 * mp);
+      // branch 1: inputs * conj(w_m3^{mp (2k + 1)}), outputs * conj(w_{2 R0}^i)
+      double2 v1[R0];
+      {
+        double2 w = __ldg(a.twm3 + mp);
+#pragma unroll
+        for (int k = 0; k < R0; ++k) {
+          v1[k] = cmulc(X1[off + k * R1], w);
+          if (k + 1 < R0) w = cmul(w, wstep);
+        }
+      }
+      DFTs<R0, true, 1, 0>::run(v1);
+      double2 v0[R0];
+      v0[0] = X0[off];
+      {
+        double2 w = wstep;
+#pragma unroll
+        for (int k = 1; k < R0; ++k) {
+          v0[k] = cmulc(X0[off + k * R1], w);
+          if (k + 1 < R0) w = cmul(w, wstep);
+        }
+      }
+      DFTs<R0, true, 1, 0>::run(v0);
+      double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
+                     static_cast<int64_t>(pos2) * m1 + pos1;
+      const int64_t step = static_cast<int64_t>(R1) * a.kstride;
+      sfor<R0>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        dst[i * step] = cadd(v0[out_idx(R0, i)], twc<2 * R0, true, i>(v1[out_idx(R0, i)]));
+      });
+    }
+  }
+  cluster.sync();  // the partner finished reading this CTA's lines
+}
+
+#define VIE_PENCIL2_SHAPES(X) X(10, 20) X(10, 10) X(8, 8) X(4, 8)
+
+template <int KIND, int BASIS>
+bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g, const double2* twm3,
+               cudaStream_t st, bool dry) {
+  auto go = [&](auto fn, size_t smem, int P1P) {
+    if (dry) return true;
+    const int groups = (g.m1 + 2 * P1P - 1) / (2 * P1P);
+    if (groups <= 1) return true;  // the edge launch covers everything
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3,
+                  static_cast<int64_t>(g.m1) * g.m2, static_cast<int64_t>(g.m1) * g.m2 * g.n3};
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (groups - 1), g.m2);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
+    VIE_CUDA_CHECK(cudaGetLastError());
+    return true;
+  };
+#define VIE_CASE(A, B)                                                                   \
+  if (n3 == (A) * (B)) {                                                                 \
+    using SH = Shape2<KIND, BASIS, A, B>;                                                \
+    if (SH::smem_bytes > 113 * 1024) return false;                                       \
+    return go(k_pencil2<KIND, BASIS, A, B>, SH::smem_bytes, SH::P1P);                    \
+  }
+  VIE_PENCIL2_SHAPES(VIE_CASE)
+#undef VIE_CASE
+  return false;
+}
+
+bool dispatch2(int kind, int basis, int n3, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+               const double2* twm3, cudaStream_t st, bool dry) {
+  if (kind == 0 && basis == 0) return launch2_t<0, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry);
+  if (kind == 1 && basis == 0) return launch2_t<1, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry);
+  if (kind == 0 && basis == 1) return launch2_t<0, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry);
+  return launch2_t<1, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry);
+}
+
+}  // namespace
+
+bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC) {
+  const uint64_t all = NC >= 64 ? ~0ull : ((1ull << NC) - 1);
+  if (active_mask != all) return false;
+  Geom g{};
+  return dispatch2(kind, basis, n3, nullptr, nullptr, nullptr, g, nullptr, nullptr, true);
+}
+
+void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+                    const double2* twm3, cudaStream_t st) {
+  dispatch2(kind, basis, g.n3, Bin, Bout, Shat, g, twm3, st, false);
+}
+
+}  // namespace vie

@@ -73,6 +73,23 @@ def test_matvec_matches_oracle(vie, dft, orc, kind, basis, dims, rank):
         assert rel(y_ref, y) <= MATVEC_TOL, (kind, basis, dims)
 
 
+# n3 with a compile-time pencil shape (kernels_pencil2.cu: 32 = 4x8, 64 = 8x8, 100 = 10x10):
+# odd/even axis-1 edges, partial last pair group (PWC packs 4 pairs per CTA), m1 = 2
+# (edge launch only), both kinds and bases.
+PENCIL2_CASES = [
+    (N, PWL, (3, 4, 32), 3), (K, PWL, (4, 3, 100), 3), (N, PWC, (5, 3, 64), 4), (K, PWC, (6, 2, 32), 3),
+    (N, PWC, (1, 2, 32), 2), (N, PWL, (7, 5, 64), 3), (N, PWC, (9, 4, 100), 3), (K, PWL, (2, 6, 64), 2),
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", PENCIL2_CASES)
+def test_matvec_pencil2_shapes(vie, dft, orc, kind, basis, dims, rank):
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 11 + sum(dims))
+    x = random_field(basis, dims, 77)
+    y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+    assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims)
+
+
 def test_matvec_c1_cube_pwl(vie, dft, orc):
     # BASELINE configs[0]: 32^3 PWL grid, r = 25 (CPU-runnable reference case)
     dims = (32, 32, 32)
