@@ -44,9 +44,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
 __device__ __forceinline__ bool mbar_try(uint64_t* b, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -77,7 +74,7 @@ struct Shape2 {
   static constexpr int NC = TableDims<KIND, BASIS>::NC;
   static constexpr int THREADS = 256;
   static constexpr int WARPS = THREADS / 32;
-  static constexpr int TS = S >= 12 ? 2 : 1;  // threads per spectral point (target halves)
+  static constexpr int TS = 1;  // one thread per spectral point, all targets: no x^/y^ hazard between threads
   static constexpr int TH = S / TS;
   static constexpr int P1P = p1pairs(S);
   static constexpr int NP = 2 * P1P;  // pencils (axis-1 positions) per CTA
@@ -86,12 +83,16 @@ struct Shape2 {
   static constexpr int N3 = R0 * R1;
   static constexpr int LS = N3 | 1;  // odd line stride: lanes over lines hit distinct banks
   static constexpr int CF = THREADS / (NP * 2 * TS);  // octant frequencies per chunk
-  static constexpr int NG = n_groups<NC>();
-  static constexpr int CG = group_size<NC>();
+  static constexpr int CHUNK_BUDGET = 640;            // double2 per chunk buffer (10 KB)
+  static constexpr int CG0 = CHUNK_BUDGET / (P1P * CF) > 0 ? CHUNK_BUDGET / (P1P * CF) : 1;
+  static constexpr int NG = (NC + CG0 - 1) / CG0;  // component groups per round
+  static constexpr int CG = (NC + NG - 1) / NG;
+  static constexpr int NU0 = (LINES * R1 + THREADS - 1) / THREADS;  // forward stage-0 units per thread
   static constexpr int CHUNK = P1P * CG * CF;  // double2 per chunk buffer
   static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
   static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
   static constexpr size_t smem_bytes = 64 + sizeof(double2) * (2 * CHUNK + static_cast<size_t>(LINES) * LS);
+  static_assert(HL * R1 <= THREADS, "one combine unit per thread");
   static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
   static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
 };
@@ -115,12 +116,12 @@ __device__ __forceinline__ int slot_of(int phi) {
 template <int KIND, int BASIS, int R0, int R1>
 __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   using SH = Shape2<KIND, BASIS, R0, R1>;
-  constexpr int S = SH::S, NB = SH::NB, NC = SH::NC, TS = SH::TS, TH = SH::TH, P1P = SH::P1P, NP = SH::NP;
+  constexpr int S = SH::S, NB = SH::NB, NC = SH::NC, TH = SH::TH, P1P = SH::P1P, NP = SH::NP;
   constexpr int LINES = SH::LINES, HL = SH::HL, N3 = SH::N3, LS = SH::LS, CF = SH::CF, NG = SH::NG, CG = SH::CG;
   constexpr int CHUNK = SH::CHUNK, E = SH::E, O = SH::O;
   extern __shared__ __align__(16) unsigned char smraw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);  // [2]
-  uint64_t* empty = full + 2;                           // [2]
+  unsigned* cnt = reinterpret_cast<unsigned*>(full + 2);  // [2] warps done with each chunk buffer
   double2* chunk = reinterpret_cast<double2*>(smraw + 64);
   double2* buf = chunk + 2 * CHUNK;  // [LINES][LS]
 
@@ -142,65 +143,72 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   auto issue_chunk = [&](int q) {
     const int r = q / NG, grp = q - r * NG;
     const int u0 = r * CF;
-    const int cnt = min(CF, nbo - u0);
+    const int nf = min(CF, nbo - u0);
     const int cend = min(CG, NC - grp * CG);
     int rows = 0;
     for (int tr = 0; tr < P1P; ++tr) rows += (q0 + tr <= n1) ? 1 : 0;
     uint64_t* bar = full + (q & 1);
-    mbar_expect_tx(bar, static_cast<uint32_t>(rows * cend * cnt * sizeof(double2)));
+    mbar_expect_tx(bar, static_cast<uint32_t>(rows * cend * nf * sizeof(double2)));
     double2* dst = chunk + (q & 1) * CHUNK;
     for (int tr = 0; tr < rows; ++tr) {
       const double2* src =
           a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + q0 + tr) * NC + grp * CG) * n3p + b * E + u0;
       for (int cl = 0; cl < cend; ++cl)
-        bulk_g2s(dst + (tr * CG + cl) * CF, src + cl * n3p, static_cast<uint32_t>(cnt * sizeof(double2)), bar);
+        bulk_g2s(dst + (tr * CG + cl) * CF, src + cl * n3p, static_cast<uint32_t>(nf * sizeof(double2)), bar);
     }
   };
+  // ---- forward stage 0 loads first (NU0 units per thread, all loads in flight)
+  double2 v0[SH::NU0][R0];
+#pragma unroll
+  for (int j = 0; j < SH::NU0; ++j) {
+    const int u = tid + j * SH::THREADS;
+    const int line = u % LINES, mp = u / LINES;
+    const int s = line / NP, p = line % NP;
+    if (u < LINES * R1 && c0 + p < m1) {
+      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
+                           static_cast<int64_t>(pos2) * m1 + c0 + p;
+      const int64_t step = static_cast<int64_t>(R1) * a.kstride;
+#pragma unroll
+      for (int i = 0; i < R0; ++i) v0[j][i] = src[i * step];
+    } else {
+#pragma unroll
+      for (int i = 0; i < R0; ++i) v0[j][i] = make_double2(0.0, 0.0);
+    }
+  }
   if (tid == 0) {
     mbar_init(full, 1);
     mbar_init(full + 1, 1);
-    mbar_init(empty, SH::WARPS);
-    mbar_init(empty + 1, SH::WARPS);
+    cnt[0] = 0u;
+    cnt[1] = 0u;
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0) {
     issue_chunk(0);
     if (nsub > 1) issue_chunk(1);
   }
-
-  // ---- forward stage 0 (radix R0) from global, branch + stage twiddles folded
-  for (int u = tid; u < LINES * R1; u += SH::THREADS) {
-    const int line = u % LINES, mp = u / LINES;
-    const int s = line / NP, p = line % NP;
-    const int pos1 = c0 + p;
-    double2* dst = buf + line * LS + mp;
-    if (pos1 >= m1) {
+  // ---- forward stage 0 (radix R0): branch twiddle on the inputs, w_m3^{mp (2k + b)} on the outputs
 #pragma unroll
-      for (int k = 0; k < R0; ++k) dst[k * R1] = make_double2(0.0, 0.0);
-      continue;
-    }
-    const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
-                         static_cast<int64_t>(pos2) * m1 + pos1;
-    const int64_t step = static_cast<int64_t>(R1) * a.kstride;
-    double2 v[R0];
-#pragma unroll
-    for (int i = 0; i < R0; ++i) v[i] = src[i * step];
-    if (b) {
-      sfor<R0 - 1>([&](auto ic) {
-        constexpr int i = decltype(ic)::value + 1;
-        v[i] = twc<2 * R0, false, i>(v[i]);  // w_m3^{i R1} = w_{2 R0}^i
+  for (int j = 0; j < SH::NU0; ++j) {
+    const int u = tid + j * SH::THREADS;
+    if (u < LINES * R1) {
+      const int line = u % LINES, mp = u / LINES;
+      double2* dst = buf + line * LS + mp;
+      double2(&v)[R0] = v0[j];
+      if (b) {
+        sfor<R0 - 1>([&](auto ic) {
+          constexpr int i = decltype(ic)::value + 1;
+          v[i] = twc<2 * R0, false, i>(v[i]);  // w_m3^{i R1} = w_{2 R0}^i
+        });
+      }
+      DFTs<R0, false, 1, 0>::run(v);
+      const double2 wstep = __ldg(a.twm3 + 2 * mp);
+      double2 w = b ? __ldg(a.twm3 + mp) : wstep;
+      dst[0] = b ? cmul(v[out_idx(R0, 0)], w) : v[out_idx(R0, 0)];
+      if (b) w = cmul(w, wstep);
+      sfor<R0 - 1>([&](auto kc) {
+        constexpr int k = decltype(kc)::value + 1;
+        dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+        if (k + 1 < R0) w = cmul(w, wstep);
       });
     }
-    DFTs<R0, false, 1, 0>::run(v);
-    // output k: w_m3^{mp (2k + b)}
-    const double2 wstep = __ldg(a.twm3 + 2 * mp);
-    double2 w = b ? __ldg(a.twm3 + mp) : make_double2(1.0, 0.0);
-    sfor<R0>([&](auto kc) {
-      constexpr int k = decltype(kc)::value;
-      dst[k * R1] = (k == 0 && !b) ? v[out_idx(R0, 0)] : cmul(v[out_idx(R0, k)], w);
-      if (k + 1 < R0) w = cmul(w, wstep);
-    });
   }
   __syncthreads();
   // ---- forward stage 1 (radix R1), in place
@@ -218,14 +226,13 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   }
   __syncthreads();
 
-  // ---- Hadamard: one (point, target half) per thread per round
+  // ---- Hadamard: one spectral point (all targets) per thread per round; the
+  // last warp done with a chunk refills its buffer (no thread ever waits on
+  // the others inside the loop)
   {
-    constexpr int ITEMS = CF * NP * 2;
-    const int half = TS > 1 ? (tid >= ITEMS ? 1 : 0) : 0;
-    const int it = tid - half * ITEMS;
-    const int mir = it & 1;
-    const int p = (it >> 1) % NP;
-    const int ul = (it >> 1) / NP;
+    const int mir = tid & 1;
+    const int p = (tid >> 1) % NP;
+    const int ul = (tid >> 1) / NP;
     const int pos1 = c0 + p;
     const int m1flag = pos1 & 1;  // positions 2j, 2j+1 hold frequencies j, m1 - j (j >= 1)
     const int tr = p >> 1;
@@ -250,25 +257,25 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
         mbar_wait(full + bi, (q >> 1) & 1);
         if (valid) {
           const double2* sh_base = chunk + bi * CHUNK + (tr * CG - GRP * CG) * CF + ul;
-          if (half == 0) {
-            had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
-                                                          ~0ull, m1flag, m2flag, mir);
-          } else if constexpr (TS > 1) {
-            had_all<KIND, BASIS, S, TH, 1, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
-                                                          ~0ull, m1flag, m2flag, mir);
-          }
+          had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
+                                                        ~0ull, m1flag, m2flag, mir);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty + bi);
-        if (tid == 0 && q + 2 < nsub) {
-          mbar_wait(empty + bi, (q >> 1) & 1);  // every warp is done with buffer bi
-          issue_chunk(q + 2);
+        if (lane == 0) {
+          __threadfence_block();  // this warp's reads of buffer bi are done
+          if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {
+            cnt[bi] = 0u;
+            __threadfence_block();
+            if (q + 2 < nsub) {
+              asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+              issue_chunk(q + 2);
+            }
+          }
         }
       });
-      __syncthreads();  // all x^ of this round read before any y^ overwrites them
       if (valid) {
 #pragma unroll
-        for (int t = 0; t < TH; ++t) pl[(half * TH + t) * NP * LS] = yh[t];
+        for (int t = 0; t < TH; ++t) pl[t * NP * LS] = yh[t];
       }
     }
   }
@@ -286,53 +293,49 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       p[i] = v[out_idx(R1, i)];
     });
   }
-  namespace cg = cooperative_groups;
-  cg::cluster_group cluster = cg::this_cluster();
-  cluster.sync();  // both branches' stage-1 adjoints visible cluster-wide
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  __syncthreads();
+  // ---- inverse stage 0 (adjoint of radix R0) of both branches + combine; own branch first,
+  // the partner's (DSMEM) once the cluster barrier completes
   {
-    const double2* own = buf;
-    const double2* rem = cluster.map_shared_rank(buf, b ^ 1);
-    const double2* X0 = b ? rem : own;
-    const double2* X1 = b ? own : rem;
-    for (int u = tid; u < HL * R1; u += SH::THREADS) {
-      const int line = b * HL + u % HL, mp = u / HL;
-      const int s = line / NP, p = line % NP;
-      const int pos1 = c0 + p;
-      if (pos1 >= m1) continue;
-      const int off = line * LS + mp;
-      const double2 wstep = __ldg(a.twm3 + 2 * mp);
-      // branch 1: inputs * conj(w_m3^{mp (2k + 1)}), outputs * conj(w_{2 R0}^i)
-      double2 v1[R0];
-      {
-        double2 w = __ldg(a.twm3 + mp);
+    const int line = b * HL + tid % HL, mp = tid / HL;
+    const int s = line / NP, p = line % NP;
+    const bool act = tid < HL * R1 && c0 + p < m1;
+    const int off = line * LS + mp;
+    const double2 wstep = __ldg(a.twm3 + 2 * min(mp, R1 - 1));
+    const double2 w1 = __ldg(a.twm3 + min(mp, R1 - 1));
+    // branch br: inputs * conj(w_m3^{mp (2k + br)}), then the radix-R0 adjoint
+    auto branch = [&](const double2* X, int br, double2(&v)[R0]) {
+      double2 w = br ? w1 : wstep;
+      v[0] = br ? cmulc(X[off], w) : X[off];
+      if (br) w = cmul(w, wstep);
 #pragma unroll
-        for (int k = 0; k < R0; ++k) {
-          v1[k] = cmulc(X1[off + k * R1], w);
-          if (k + 1 < R0) w = cmul(w, wstep);
-        }
+      for (int k = 1; k < R0; ++k) {
+        v[k] = cmulc(X[off + k * R1], w);
+        if (k + 1 < R0) w = cmul(w, wstep);
       }
-      DFTs<R0, true, 1, 0>::run(v1);
-      double2 v0[R0];
-      v0[0] = X0[off];
-      {
-        double2 w = wstep;
-#pragma unroll
-        for (int k = 1; k < R0; ++k) {
-          v0[k] = cmulc(X0[off + k * R1], w);
-          if (k + 1 < R0) w = cmul(w, wstep);
-        }
-      }
-      DFTs<R0, true, 1, 0>::run(v0);
+      DFTs<R0, true, 1, 0>::run(v);
+    };
+    double2 vo[R0], vr[R0];
+    if (act) branch(buf, b, vo);
+    namespace cg = cooperative_groups;
+    const double2* rem = cg::this_cluster().map_shared_rank(buf, b ^ 1);
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (act) branch(rem, b ^ 1, vr);
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // done reading the partner
+    if (act) {
       double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
-                     static_cast<int64_t>(pos2) * m1 + pos1;
+                     static_cast<int64_t>(pos2) * m1 + c0 + p;
       const int64_t step = static_cast<int64_t>(R1) * a.kstride;
       sfor<R0>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        dst[i * step] = cadd(v0[out_idx(R0, i)], twc<2 * R0, true, i>(v1[out_idx(R0, i)]));
+        const double2 y0 = b ? vr[out_idx(R0, i)] : vo[out_idx(R0, i)];
+        const double2 y1 = b ? vo[out_idx(R0, i)] : vr[out_idx(R0, i)];
+        dst[i * step] = cadd(y0, twc<2 * R0, true, i>(y1));
       });
     }
+    asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // the partner finished reading this CTA
   }
-  cluster.sync();  // the partner finished reading this CTA's lines
 }
 
 #define VIE_PENCIL2_SHAPES(X) X(10, 20) X(10, 10) X(8, 8) X(4, 8)
