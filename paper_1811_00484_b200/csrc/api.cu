@@ -170,7 +170,8 @@ constexpr bool kPass2 = VIE_PASS2;
 #ifndef VIE_PENCIL2
 #define VIE_PENCIL2 1
 #endif
-constexpr bool kPencil2 = VIE_PENCIL2;  // kernels_pencil2.cu when n3 has a compiled shape  // register-staged passes (kernels_fft2.cu)
+constexpr bool kPencil2 = VIE_PENCIL2;
+constexpr int kSlabPad = 0;  // elements appended to each m1 x m2 slab plane (see Geom::bps)  // kernels_pencil2.cu when n3 has a compiled shape  // register-staged passes (kernels_fft2.cu)
 int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -651,6 +652,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     g.m3 = 2 * g.n3;
     g.S = basis == 0 ? 3 : 12;
     g.NC = static_cast<int>(cs.size());
+    g.bps = static_cast<int64_t>(g.m1) * g.m2 + env_int("VIE_BPAD", kSlabPad);
     op->comps_host.assign(cs.size(), CompDev{1, 1, 1, 0, 0, 0, 0, 0, 0});
     std::vector<const vie_tucker_s*> byc(cs.size(), nullptr);
     for (int i = 0; i < ncomp; ++i) {
@@ -718,9 +720,9 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->Z = dev_alloc<double2>(static_cast<size_t>(std::max<int64_t>(zoff, 1)));
     op->Shat = dev_alloc<double2>(static_cast<size_t>(noct * g.NC));
     op->A = dev_alloc<double2>(static_cast<size_t>(g.S * 2 * nv));
-    op->B = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
-    op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * 4 * nv));
-    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 10 * nv);
+    op->B = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
+    op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
+    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 2 * nv + 2 * g.S * g.n3 * g.bps);
     op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);

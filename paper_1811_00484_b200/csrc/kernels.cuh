@@ -21,6 +21,8 @@ struct Geom {
   int m1, m2, m3;  // embedded (2n)
   int S;           // current components (sources = targets)
   int NC;          // canonical component count
+  int64_t bps;     // plane stride of the spectral slabs B, Bo (m1 m2 + pad: spreads the pencil
+                   // kernel's 3 MB-strided accesses over DRAM channels)
 };
 
 // Tuning constants.

@@ -135,7 +135,7 @@ constexpr int kMmaMC = 64;   // rows (p1o) per T chunk
 constexpr int kMmaPP = 4;    // p2o values per CTA (U3 reuse)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -208,13 +208,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
           const double2 a0 = ta[k0], a1 = ta[8 * Kp + k0];
           const double2 b0 = ub[k0], b1 = ub[8 * Kp + k0];
           const double2 av[2] = {a0, a1}, bv[2] = {b0, b1};
+          // 8 independent accumulators, each touched once per pass: dependent DMMAs 8 apart
 #pragma unroll
           for (int i = 0; i < 2; ++i)
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
               dmma(accr[i][j][0], accr[i][j][1], av[i].x, bv[j].x);
-              dmma(accr[i][j][0], accr[i][j][1], -av[i].y, bv[j].y);
               dmma(acci[i][j][0], acci[i][j][1], av[i].x, bv[j].y);
+            }
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+              dmma(accr[i][j][0], accr[i][j][1], -av[i].y, bv[j].y);
               dmma(acci[i][j][0], acci[i][j][1], av[i].y, bv[j].x);
             }
         }

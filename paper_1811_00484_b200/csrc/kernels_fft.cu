@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_row_inv(const double2* __restri
 // A: planes of n2 rows x m1 (row-major, column index fastest) -> B: planes of
 // m2 rows x m1; W consecutive columns per CTA.
 __global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restrict__ A, double2* __restrict__ B,
-                                                      int n2, int m1, FftPlan P) {
+                                                      int n2, int m1, FftPlan P, int64_t bps) {
   extern __shared__ double2 sm[];
   const int m = P.n;
   const SmemPlan SP = load_plan(sm, P);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restri
   cp_async_wait();
   __syncthreads();
   fft_forward(buf, wc, ls, SP, true);
-  double2* dst = B + plane * m * m1 + c0;
+  double2* dst = B + plane * bps + c0;
   for (int e = threadIdx.x; e < m * kColsPerCta; e += blockDim.x) {
     const int pos = e / kColsPerCta, w = e - pos * kColsPerCta;
     if (w < wc) dst[static_cast<int64_t>(pos) * m1 + w] = buf[w * ls + slot_s[freq_of_pos(pos, n2)]];
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_fwd(const double2* __restri
 
 __global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restrict__ B,
                                                          const double2* __restrict__ B1, double2* __restrict__ A,
-                                                         int n2, int m1, FftPlan P) {
+                                                         int n2, int m1, FftPlan P, int64_t bps) {
   extern __shared__ double2 sm[];
   const int m = P.n;
   const SmemPlan SP = load_plan(sm, P);
@@ -139,14 +139,14 @@ __global__ void __launch_bounds__(kThreads, 3) k_col_inv(const double2* __restri
   const int c0 = blockIdx.x * kColsPerCta;
   const int wc = min(kColsPerCta, m1 - c0);
   const int64_t plane = blockIdx.y;
-  const double2* src = B + plane * m * m1 + c0;
+  const double2* src = B + plane * bps + c0;
   for (int e = threadIdx.x; e < m * kColsPerCta; e += blockDim.x) {
     const int pos = e / kColsPerCta, w = e - pos * kColsPerCta;
     if (w < wc) cp_async16(buf + w * ls + slot_s[freq_of_pos(pos, n2)], src + static_cast<int64_t>(pos) * m1 + w);
   }
   cp_async_wait();
   if (B1) {  // add the second slab (same element mapping: each thread owns its cp.async targets)
-    const double2* src1 = B1 + plane * m * m1 + c0;
+    const double2* src1 = B1 + plane * bps + c0;
     for (int e = threadIdx.x; e < m * kColsPerCta; e += blockDim.x) {
       const int pos = e / kColsPerCta, w = e - pos * kColsPerCta;
       if (w < wc) {
@@ -207,7 +207,7 @@ void launch_col_fwd(const double2* A, double2* B, const Geom& g, const FftPlan& 
   const size_t sm = col_smem(g.m2);
   set_smem(reinterpret_cast<const void*>(k_col_fwd), sm);
   dim3 grid((g.m1 + kColsPerCta - 1) / kColsPerCta, g.S * g.n3);
-  k_col_fwd<<<grid, kThreads, sm, st>>>(A, B, g.n2, g.m1, P2);
+  k_col_fwd<<<grid, kThreads, sm, st>>>(A, B, g.n2, g.m1, P2, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -216,7 +216,7 @@ void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom&
   const size_t sm = col_smem(g.m2);
   set_smem(reinterpret_cast<const void*>(k_col_inv), sm);
   dim3 grid((g.m1 + kColsPerCta - 1) / kColsPerCta, g.S * g.n3);
-  k_col_inv<<<grid, kThreads, sm, st>>>(B, B1, A, g.n2, g.m1, P2);
+  k_col_inv<<<grid, kThreads, sm, st>>>(B, B1, A, g.n2, g.m1, P2, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

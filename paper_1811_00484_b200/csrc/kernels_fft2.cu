@@ -234,14 +234,14 @@ static_assert((kCW & (kCW - 1)) == 0, "column tile must be a power of two");
 constexpr int kLgCW = kCW == 8 ? 3 : (kCW == 4 ? 2 : (kCW == 16 ? 4 : 0));
 
 __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
-                                                     Pass2 P) {
+                                                     Pass2 P, int64_t bps) {
   extern __shared__ double2 buf[];
-  const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
+  const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
   const int wc = min(kCW, m1 - c0);
   const int64_t plane = blockIdx.y;
   const double2* src = A + plane * n * m1 + c0;
-  double2* dst = B + plane * m * m1 + c0;
+  double2* dst = B + plane * bps + c0;
   if (R1 == 1) {
     const int w = threadIdx.x;
     if (w < wc)
@@ -279,13 +279,13 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
 }
 
 __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
-                                                     Pass2 P) {
+                                                     Pass2 P, int64_t bps) {
   extern __shared__ double2 buf[];
-  const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
+  const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
   const int wc = min(kCW, m1 - c0);
   const int64_t plane = blockIdx.y;
-  const double2* src = B + plane * m * m1 + c0;
+  const double2* src = B + plane * bps + c0;
   double2* dst = A + plane * n * m1 + c0;
   if (R1 == 1) {
     const int w = threadIdx.x;
@@ -380,7 +380,7 @@ void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P
   if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2), sm);
   dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.n3);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.m1, P);
+  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -389,7 +389,7 @@ void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P
   if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2), sm);
   dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.n3);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.m1, P);
+  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   const int n3p = n3 + 1;
   const int E = n3 / 2 + 1;            // even octant frequencies 0,2,..
   const int O = (n3 + 1) / 2;          // odd octant frequencies 1,3,..
-  const int64_t kstride = static_cast<int64_t>(m2) * m1;
+  const int64_t kstride = g.bps;
   const int64_t sstride = kstride * n3;
 
   {

@@ -27,6 +27,14 @@
 #include "hadamard.cuh"
 #include "kernels.cuh"
 
+#ifndef VIE_P2_NBUF
+#define VIE_P2_NBUF 2
+#endif
+#ifndef VIE_P2_ABL
+#define VIE_P2_ABL 0  // ablation bits (timing experiments only): 1 no Hadamard FMAs, 2 no spectrum stream,
+                     // 4 no pencil loads, 8 no stores, 16 no DSMEM reads
+#endif
+
 namespace vie {
 
 namespace {
@@ -87,11 +95,11 @@ struct Shape2 {
   static constexpr int CG0 = CHUNK_BUDGET / (P1P * CF) > 0 ? CHUNK_BUDGET / (P1P * CF) : 1;
   static constexpr int NG = (NC + CG0 - 1) / CG0;  // component groups per round
   static constexpr int CG = (NC + NG - 1) / NG;
-  static constexpr int NU0 = (LINES * R1 + THREADS - 1) / THREADS;  // forward stage-0 units per thread
   static constexpr int CHUNK = P1P * CG * CF;  // double2 per chunk buffer
   static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
   static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
-  static constexpr size_t smem_bytes = 64 + sizeof(double2) * (2 * CHUNK + static_cast<size_t>(LINES) * LS);
+  static constexpr int NBUF = VIE_P2_NBUF;     // chunk ring depth
+  static constexpr size_t smem_bytes = 64 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS);
   static_assert(HL * R1 <= THREADS, "one combine unit per thread");
   static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
   static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
@@ -103,7 +111,7 @@ struct Pencil2Args {
   const double2* Shat;
   const double2* twm3;  // w_m3^e, e < m3
   int n1, n2, m1, m2, m3;
-  int64_t kstride, sstride;  // m1 m2, m1 m2 n3
+  int64_t kstride, sstride;  // bps, bps n3 (padded slab planes)
 };
 
 // the slot of branch frequency phi = k0 + R0 k1 after the two forward stages
@@ -120,10 +128,11 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   constexpr int LINES = SH::LINES, HL = SH::HL, N3 = SH::N3, LS = SH::LS, CF = SH::CF, NG = SH::NG, CG = SH::CG;
   constexpr int CHUNK = SH::CHUNK, E = SH::E, O = SH::O;
   extern __shared__ __align__(16) unsigned char smraw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);  // [2]
-  unsigned* cnt = reinterpret_cast<unsigned*>(full + 2);  // [2] warps done with each chunk buffer
+  constexpr int NBUF = SH::NBUF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smraw);  // [NBUF]
+  unsigned* cnt = reinterpret_cast<unsigned*>(full + NBUF);  // [NBUF] warps done with each chunk buffer
   double2* chunk = reinterpret_cast<double2*>(smraw + 64);
-  double2* buf = chunk + 2 * CHUNK;  // [LINES][LS]
+  double2* buf = chunk + NBUF * CHUNK;  // [LINES][LS]
 
   const int tid = threadIdx.x;
   const int b = blockIdx.x & 1;                     // axis-3 branch = rank in the cluster
@@ -139,7 +148,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   const int nrounds = (nbo + CF - 1) / CF;
   const int nsub = nrounds * NG;
 
-  // ---- spectrum chunk q = round * NG + group -> buffer q & 1 (bulk copies)
+  // ---- spectrum chunk q = round * NG + group -> buffer q % NBUF (bulk copies)
   auto issue_chunk = [&](int q) {
     const int r = q / NG, grp = q - r * NG;
     const int u0 = r * CF;
@@ -147,9 +156,9 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
     const int cend = min(CG, NC - grp * CG);
     int rows = 0;
     for (int tr = 0; tr < P1P; ++tr) rows += (q0 + tr <= n1) ? 1 : 0;
-    uint64_t* bar = full + (q & 1);
+    uint64_t* bar = full + q % NBUF;
     mbar_expect_tx(bar, static_cast<uint32_t>(rows * cend * nf * sizeof(double2)));
-    double2* dst = chunk + (q & 1) * CHUNK;
+    double2* dst = chunk + (q % NBUF) * CHUNK;
     for (int tr = 0; tr < rows; ++tr) {
       const double2* src =
           a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + q0 + tr) * NC + grp * CG) * n3p + b * E + u0;
@@ -157,60 +166,78 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
         bulk_g2s(dst + (tr * CG + cl) * CF, src + cl * n3p, static_cast<uint32_t>(nf * sizeof(double2)), bar);
     }
   };
-  // ---- forward stage 0 loads first (NU0 units per thread, all loads in flight)
-  double2 v0[SH::NU0][R0];
-#pragma unroll
-  for (int j = 0; j < SH::NU0; ++j) {
-    const int u = tid + j * SH::THREADS;
-    const int line = u % LINES, mp = u / LINES;
-    const int s = line / NP, p = line % NP;
-    if (u < LINES * R1 && c0 + p < m1) {
-      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
+  // ---- forward stage 0 (radix R0) for BOTH branches of this CTA's half of the lines:
+  // the pencils are read from global once per cluster, branch b' of the stage-0
+  // outputs goes to CTA b' (the partner's half through DSMEM stores)
+  namespace cg = cooperative_groups;
+  double2* const rbuf = cg::this_cluster().map_shared_rank(buf, b ^ 1);  // the partner's lines
+  double2* const buf_b0 = b ? rbuf : buf;                                 // branch 0 / branch 1 owners
+  double2* const buf_b1 = b ? buf : rbuf;
+  const int line0 = b * HL + tid % HL, mp0 = tid / HL;
+  const bool act0 = tid < HL * R1;
+  double2 xin[R0];
+  {
+    const int s = line0 / NP, p = line0 % NP;
+    if (act0 && c0 + p < m1 && !(VIE_P2_ABL & 4)) {
+      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp0) * a.kstride +
                            static_cast<int64_t>(pos2) * m1 + c0 + p;
       const int64_t step = static_cast<int64_t>(R1) * a.kstride;
 #pragma unroll
-      for (int i = 0; i < R0; ++i) v0[j][i] = src[i * step];
+      for (int i = 0; i < R0; ++i) xin[i] = src[i * step];
     } else {
 #pragma unroll
-      for (int i = 0; i < R0; ++i) v0[j][i] = make_double2(0.0, 0.0);
+      for (int i = 0; i < R0; ++i) xin[i] = make_double2(0.0, 0.0);
     }
   }
   if (tid == 0) {
-    mbar_init(full, 1);
-    mbar_init(full + 1, 1);
-    cnt[0] = 0u;
-    cnt[1] = 0u;
+    for (int i = 0; i < NBUF; ++i) {
+      mbar_init(full + i, 1);
+      cnt[i] = 0u;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    issue_chunk(0);
-    if (nsub > 1) issue_chunk(1);
+    if (!(VIE_P2_ABL & 2)) {
+      issue_chunk(0);
+      for (int i = 1; i < NBUF && i < nsub; ++i) issue_chunk(i);
+    }
   }
-  // ---- forward stage 0 (radix R0): branch twiddle on the inputs, w_m3^{mp (2k + b)} on the outputs
+  // the partner may still be starting up: its smem is written only after this barrier
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  const double2 wstep0 = __ldg(a.twm3 + 2 * mp0);
+  double2 v[R0];
 #pragma unroll
-  for (int j = 0; j < SH::NU0; ++j) {
-    const int u = tid + j * SH::THREADS;
-    if (u < LINES * R1) {
-      const int line = u % LINES, mp = u / LINES;
-      double2* dst = buf + line * LS + mp;
-      double2(&v)[R0] = v0[j];
-      if (b) {
-        sfor<R0 - 1>([&](auto ic) {
-          constexpr int i = decltype(ic)::value + 1;
-          v[i] = twc<2 * R0, false, i>(v[i]);  // w_m3^{i R1} = w_{2 R0}^i
-        });
-      }
-      DFTs<R0, false, 1, 0>::run(v);
-      const double2 wstep = __ldg(a.twm3 + 2 * mp);
-      double2 w = b ? __ldg(a.twm3 + mp) : wstep;
-      dst[0] = b ? cmul(v[out_idx(R0, 0)], w) : v[out_idx(R0, 0)];
-      if (b) w = cmul(w, wstep);
+  for (int i = 0; i < R0; ++i) v[i] = xin[i];
+  if (act0) DFTs<R0, false, 1, 0>::run(v);  // branch 0: outputs * w_m3^{2 k mp}
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
+  if (act0) {
+    {
+      double2* dst = buf_b0 + line0 * LS + mp0;
+      double2 w = wstep0;
+      dst[0] = v[out_idx(R0, 0)];
       sfor<R0 - 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value + 1;
         dst[k * R1] = cmul(v[out_idx(R0, k)], w);
-        if (k + 1 < R0) w = cmul(w, wstep);
+        if (k + 1 < R0) w = cmul(w, wstep0);
+      });
+    }
+    v[0] = xin[0];  // branch 1: inputs * w_{2 R0}^i, outputs * w_m3^{mp (2k + 1)}
+    sfor<R0 - 1>([&](auto ic) {
+      constexpr int i = decltype(ic)::value + 1;
+      v[i] = twc<2 * R0, false, i>(xin[i]);
+    });
+    DFTs<R0, false, 1, 0>::run(v);
+    {
+      double2* dst = buf_b1 + line0 * LS + mp0;
+      double2 w = __ldg(a.twm3 + mp0);
+      sfor<R0>([&](auto kc) {
+        constexpr int k = decltype(kc)::value;
+        dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+        if (k + 1 < R0) w = cmul(w, wstep0);
       });
     }
   }
-  __syncthreads();
+  // every stage-0 output (own and partner's) visible before stage 1
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   // ---- forward stage 1 (radix R1), in place
   for (int u = tid; u < LINES * R0; u += SH::THREADS) {
     const int line = u % LINES, k0 = u / LINES;
@@ -253,9 +280,9 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       sfor_g(std::make_integer_sequence<int, NG>{}, [&](auto gc) {
         constexpr int GRP = decltype(gc)::value;
         const int q = r * NG + GRP;
-        const int bi = q & 1;
-        mbar_wait(full + bi, (q >> 1) & 1);
-        if (valid) {
+        const int bi = q % NBUF;
+        if (!(VIE_P2_ABL & 2)) mbar_wait(full + bi, (q / NBUF) & 1);
+        if (valid && !(VIE_P2_ABL & 1)) {
           const double2* sh_base = chunk + bi * CHUNK + (tr * CG - GRP * CG) * CF + ul;
           had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
                                                         ~0ull, m1flag, m2flag, mir);
@@ -266,9 +293,9 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
           if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {
             cnt[bi] = 0u;
             __threadfence_block();
-            if (q + 2 < nsub) {
+            if (q + NBUF < nsub && !(VIE_P2_ABL & 2)) {
               asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-              issue_chunk(q + 2);
+              issue_chunk(q + NBUF);
             }
           }
         }
@@ -318,12 +345,11 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
     };
     double2 vo[R0], vr[R0];
     if (act) branch(buf, b, vo);
-    namespace cg = cooperative_groups;
-    const double2* rem = cg::this_cluster().map_shared_rank(buf, b ^ 1);
+    const double2* rem = rbuf;
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-    if (act) branch(rem, b ^ 1, vr);
+    if (act) branch((VIE_P2_ABL & 16) ? buf : rem, b ^ 1, vr);
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // done reading the partner
-    if (act) {
+    if (act && !(VIE_P2_ABL & 8)) {
       double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
                      static_cast<int64_t>(pos2) * m1 + c0 + p;
       const int64_t step = static_cast<int64_t>(R1) * a.kstride;
@@ -350,7 +376,7 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3,
-                  static_cast<int64_t>(g.m1) * g.m2, static_cast<int64_t>(g.m1) * g.m2 * g.n3};
+                  g.bps, g.bps * g.n3};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (groups - 1), g.m2);
     cfg.blockDim = dim3(256);

@@ -22,7 +22,7 @@ from typing import Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvie_b200.so")
+LIB_PATH = os.environ.get("VIE_LIB_PATH") or os.path.join(_HERE, "libvie_b200.so")  # override: ablation builds
 
 KIND_N, KIND_K = 0, 1
 PWC, PWL = 0, 1
