@@ -186,12 +186,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
       }
       cp_async_wait_all_d();
       __syncthreads();
-      for (int e = threadIdx.x; e < kMmaMC * Kp; e += blockDim.x) {
-        const int i = e / Kp, g = e - i * Kp;
-        double2 acc = make_double2(0.0, 0.0);
-        if (g < r3 && m0 + i < n1p)
-          for (int a = 0; a < r1; ++a) cfma(acc, u1s[a * kMmaMC + i], zs[a * r3 + g]);
-        ts[e] = acc;
+      {
+        // T chunk = U1 rows x Z: lane -> column g (Z value reused over 8 rows), warp -> rows
+        // i = warp + 8 q (U1 value broadcast), 8 independent accumulator chains per thread
+        static_assert(kThreads == 256 && kMmaMC == 64, "T-chunk thread map");
+        for (int g = lane; g < Kp; g += 32) {
+          double2 acc[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = make_double2(0.0, 0.0);
+          if (g < r3) {
+            for (int a = 0; a < r1; ++a) {
+              const double2 z = zs[a * r3 + g];
+#pragma unroll
+              for (int q = 0; q < 8; ++q) cfma(acc[q], u1s[a * kMmaMC + warp + 8 * q], z);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = warp + 8 * q;
+            ts[i * Kp + g] = (m0 + i < n1p) ? acc[q] : make_double2(0.0, 0.0);
+          }
+        }
       }
       __syncthreads();
       const int nrt = (min(kMmaMC, n1p - m0) + 15) / 16;
@@ -230,12 +245,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
           if (row >= n1p) continue;
           double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + row) * NC + c) * n3p;
 #pragma unroll
-          for (int j = 0; j < 2; ++j)
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const int f = ct * 16 + j * 8 + 2 * fk + h;
-              if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = make_double2(accr[i][j][h], acci[i][j][h]);
-            }
+          for (int j = 0; j < 2; ++j) {
+            // columns f = 2 hb + h: even f (h = 0) at hb, odd f at E + hb (branch-major)
+            const int hb = ct * 8 + j * 4 + fk;
+            if (2 * hb < n3p) dst[hb] = make_double2(accr[i][j][0], acci[i][j][0]);
+            if (2 * hb + 1 < n3p) dst[E + hb] = make_double2(accr[i][j][1], acci[i][j][1]);
+          }
         }
       }
     }
