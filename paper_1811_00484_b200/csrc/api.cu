@@ -117,6 +117,7 @@ struct vie_op_s {
   vie::Pass2 Q1{}, Q2{};           // register-staged two-stage row / column passes
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
   bool pencil2 = false;         // compile-time-shaped pencil kernel for this n3
+  int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
   // host-buffer staging (vie_matvec_host)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -419,12 +420,14 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
     if (op->profiling) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
   };
   const bool overlap = !op->profiling;
-  if (overlap && !decomp_forked) fork_decomp(op, st);
+  if (overlap && !decomp_forked && op->fork_after == 0) fork_decomp(op, st);
   if (op->q1) vie::launch_row_fwd2(x, op->A, g, op->Q1, st);
   else vie::launch_row_fwd(x, op->A, g, op->P1, st);
+  if (overlap && !decomp_forked && op->fork_after == 1) fork_decomp(op, st);
   mark();
   if (op->q2) vie::launch_col_fwd2(op->A, op->B, g, op->Q2, st);
   else vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
+  if (overlap && !decomp_forked && op->fork_after >= 2) fork_decomp(op, st);
   mark();
   if (overlap) {
     VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
@@ -737,7 +740,9 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->PH = get_plan(ctx, g.n3, false, true);
     int prio_lo = 0, prio_hi = 0;  // high priority: decompression CTAs are dispatched before FFT-pass CTAs
     VIE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
-    VIE_CUDA_CHECK(cudaStreamCreateWithPriority(&op->side, cudaStreamNonBlocking, prio_hi));
+    VIE_CUDA_CHECK(cudaStreamCreateWithPriority(&op->side, cudaStreamNonBlocking,
+                                                env_int("VIE_SIDE_PRIO", 1) ? prio_hi : prio_lo));
+    op->fork_after = env_int("VIE_FORK_AFTER", 0);
     VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_fork, cudaEventDisableTiming));
     VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_join, cudaEventDisableTiming));
     *out = op.release();
@@ -983,10 +988,14 @@ int vie_op_last_stats(vie_op op, int* launches, double* stage_ms) {
 }  // extern "C"
 namespace vie {
 void pencil_phase_read(unsigned long long* out8, bool reset);
+void pencil2_phase_read(unsigned long long* out8, bool reset);
 }
 extern "C" {
 int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
   return guard([&] { vie::pencil_phase_read(out8, reset != 0); });
+}
+int vie_debug_pencil2_phases(unsigned long long* out8, int reset) {
+  return guard([&] { vie::pencil2_phase_read(out8, reset != 0); });
 }
 #endif
 

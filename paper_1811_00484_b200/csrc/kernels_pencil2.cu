@@ -11,16 +11,18 @@
 //    w_m3^{n} folds into compile-time constants w_{2 R0}^{i} on the inputs plus
 //    the stage twiddle w_m3^{m'(2k+b)} on the outputs; stage 1 (radix R1) is
 //    one in-place smem pass;
-//  * the spectrum streams in component-group chunks through 1-D bulk copies
-//    (cp.async.bulk, one per component run, issued by one thread) on an
-//    mbarrier full/empty ring -- no per-element address arithmetic;
+//  * the spectrum streams in component-group chunks, one 3-D TMA tensor copy
+//    per chunk (cp.async.bulk.tensor), on an mbarrier ring refilled by the last
+//    warp done with a buffer -- no per-element address arithmetic;
 //  * every spectrum offset in the unrolled block table is an immediate;
 //  * the inverse stage 1 is one in-place smem pass; the inverse stage 0 is
 //    fused with the branch combine y[n] = A_0[n] + conj(w_m3^n) A_1[n]: CTA b
 //    reads both branches' lines of its half (the partner's through DSMEM),
 //    runs both radix-R0 adjoints in registers and stores y to global.
 #include <cooperative_groups.h>
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 
+#include <array>
 #include <utility>
 
 #include "fft.cuh"
@@ -29,6 +31,9 @@
 
 #ifndef VIE_P2_NBUF
 #define VIE_P2_NBUF 2
+#endif
+#ifndef VIE_P2_SIGNSPLIT
+#define VIE_P2_SIGNSPLIT 1  // mirror signs on x^ / y^ instead of every spectrum value
 #endif
 #ifndef VIE_P2_ABL
 #define VIE_P2_ABL 0  // ablation bits (timing experiments only): 1 no Hadamard FMAs, 2 no spectrum stream,
@@ -65,11 +70,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   while (!mbar_try(b, parity)) {
   }
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+// 3-D tiled TMA load of one spectrum chunk (box [P1P][CG][2 CF doubles]) into smem
+__device__ __forceinline__ void tma_chunk(void* dst, const CUtensorMap* tmap, int x, int y, int z, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
       : "memory");
 }
 
@@ -99,7 +105,7 @@ struct Shape2 {
   static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
   static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
   static constexpr int NBUF = VIE_P2_NBUF;     // chunk ring depth
-  static constexpr size_t smem_bytes = 64 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS);
+  static constexpr size_t smem_bytes = 128 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS);
   static_assert(HL * R1 <= THREADS, "one combine unit per thread");
   static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
   static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
@@ -114,6 +120,22 @@ struct Pencil2Args {
   int64_t kstride, sstride;  // bps, bps n3 (padded slab planes)
 };
 
+#ifdef VIE_PENCIL_PROFILE
+__device__ unsigned long long g_p2_phase[8];
+#define P2_PHASE(i)                                                                   \
+  do {                                                                                \
+    if (threadIdx.x == 0) {                                                           \
+      const long long t_ = clock64();                                                 \
+      atomicAdd(&g_p2_phase[i], static_cast<unsigned long long>(t_ - t_last));        \
+      t_last = t_;                                                                    \
+    }                                                                                 \
+  } while (0)
+#else
+#define P2_PHASE(i) \
+  do {              \
+  } while (0)
+#endif
+
 // the slot of branch frequency phi = k0 + R0 k1 after the two forward stages
 template <int R0, int R1>
 __device__ __forceinline__ int slot_of(int phi) {
@@ -122,16 +144,19 @@ __device__ __forceinline__ int slot_of(int phi) {
 }
 
 template <int KIND, int BASIS, int R0, int R1>
-__global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
+__global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_constant__ CUtensorMap tmap) {
   using SH = Shape2<KIND, BASIS, R0, R1>;
-  constexpr int S = SH::S, NB = SH::NB, NC = SH::NC, TH = SH::TH, P1P = SH::P1P, NP = SH::NP;
+#ifdef VIE_PENCIL_PROFILE
+  long long t_last = clock64();
+#endif
+  constexpr int S = SH::S, NB = SH::NB, TH = SH::TH, P1P = SH::P1P, NP = SH::NP;
   constexpr int LINES = SH::LINES, HL = SH::HL, N3 = SH::N3, LS = SH::LS, CF = SH::CF, NG = SH::NG, CG = SH::CG;
   constexpr int CHUNK = SH::CHUNK, E = SH::E, O = SH::O;
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   constexpr int NBUF = SH::NBUF;
   uint64_t* full = reinterpret_cast<uint64_t*>(smraw);  // [NBUF]
   unsigned* cnt = reinterpret_cast<unsigned*>(full + NBUF);  // [NBUF] warps done with each chunk buffer
-  double2* chunk = reinterpret_cast<double2*>(smraw + 64);
+  double2* chunk = reinterpret_cast<double2*>(smraw + 128);  // TMA destinations: 128-byte aligned
   double2* buf = chunk + NBUF * CHUNK;  // [LINES][LS]
 
   const int tid = threadIdx.x;
@@ -143,28 +168,18 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   const int f2 = freq_of_pos(pos2, n2);
   const int m2flag = f2 > n2;
   const int p2o = m2flag ? a.m2 - f2 : f2;
-  constexpr int n3p = N3 + 1;
   const int nbo = b ? O : E;
   const int nrounds = (nbo + CF - 1) / CF;
   const int nsub = nrounds * NG;
 
   // ---- spectrum chunk q = round * NG + group -> buffer q % NBUF (bulk copies)
+  // one TMA tensor copy per chunk: rows (p2o, q0 .. q0 + P1P), components grp*CG .., the
+  // round's CF frequencies of branch b (out-of-range rows/components zero-filled)
   auto issue_chunk = [&](int q) {
     const int r = q / NG, grp = q - r * NG;
-    const int u0 = r * CF;
-    const int nf = min(CF, nbo - u0);
-    const int cend = min(CG, NC - grp * CG);
-    int rows = 0;
-    for (int tr = 0; tr < P1P; ++tr) rows += (q0 + tr <= n1) ? 1 : 0;
     uint64_t* bar = full + q % NBUF;
-    mbar_expect_tx(bar, static_cast<uint32_t>(rows * cend * nf * sizeof(double2)));
-    double2* dst = chunk + (q % NBUF) * CHUNK;
-    for (int tr = 0; tr < rows; ++tr) {
-      const double2* src =
-          a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + q0 + tr) * NC + grp * CG) * n3p + b * E + u0;
-      for (int cl = 0; cl < cend; ++cl)
-        bulk_g2s(dst + (tr * CG + cl) * CF, src + cl * n3p, static_cast<uint32_t>(nf * sizeof(double2)), bar);
-    }
+    mbar_expect_tx(bar, static_cast<uint32_t>(CHUNK * sizeof(double2)));
+    tma_chunk(chunk + (q % NBUF) * CHUNK, &tmap, 2 * (b * E + r * CF), grp * CG, p2o * (n1 + 1) + q0, bar);
   };
   // ---- forward stage 0 (radix R0) for BOTH branches of this CTA's half of the lines:
   // the pencils are read from global once per cluster, branch b' of the stage-0
@@ -195,11 +210,10 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       cnt[i] = 0u;
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    if (!(VIE_P2_ABL & 2)) {
-      issue_chunk(0);
-      for (int i = 1; i < NBUF && i < nsub; ++i) issue_chunk(i);
-    }
+    if (!(VIE_P2_ABL & 2))
+      for (int i = 0; i < NBUF && i < nsub; ++i) issue_chunk(i);
   }
+  P2_PHASE(0);
   // the partner may still be starting up: its smem is written only after this barrier
   asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
   const double2 wstep0 = __ldg(a.twm3 + 2 * mp0);
@@ -238,6 +252,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   // every stage-0 output (own and partner's) visible before stage 1
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  P2_PHASE(1);
   // ---- forward stage 1 (radix R1), in place
   for (int u = tid; u < LINES * R0; u += SH::THREADS) {
     const int line = u % LINES, k0 = u / LINES;
@@ -253,6 +268,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
   }
   __syncthreads();
 
+  P2_PHASE(2);
   // ---- Hadamard: one spectral point (all targets) per thread per round; the
   // last warp done with a chunk refills its buffer (no thread ever waits on
   // the others inside the loop)
@@ -271,9 +287,12 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       const int phi = mir ? N3 - u - b : u;
       double2* pl = buf + p * LS + slot_of<R0, R1>(valid ? phi : 0);
       double2 xh[S], yh[TH];
+      constexpr auto SG = Signs<KIND, BASIS>::value;
+      const int sbits = m1flag | (m2flag << 1) | (mir << 2);
       if (valid) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) xh[s] = pl[s * NP * LS];
+        for (int s = 0; s < S; ++s)
+          xh[s] = VIE_P2_SIGNSPLIT ? flip_sign(pl[s * NP * LS], pattern_sign(SG.pi[s] ^ SG.G, sbits)) : pl[s * NP * LS];
       }
 #pragma unroll
       for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
@@ -284,13 +303,16 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
         if (!(VIE_P2_ABL & 2)) mbar_wait(full + bi, (q / NBUF) & 1);
         if (valid && !(VIE_P2_ABL & 1)) {
           const double2* sh_base = chunk + bi * CHUNK + (tr * CG - GRP * CG) * CF + ul;
-          had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
-                                                        ~0ull, m1flag, m2flag, mir);
+          if constexpr (VIE_P2_SIGNSPLIT)
+            had_all_ns<KIND, BASIS, S, TH, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF);
+          else
+            had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
+                                                          ~0ull, m1flag, m2flag, mir);
         }
         __syncwarp();
         if (lane == 0) {
           __threadfence_block();  // this warp's reads of buffer bi are done
-          if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {
+          if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {  // the last warp out refills the buffer
             cnt[bi] = 0u;
             __threadfence_block();
             if (q + NBUF < nsub && !(VIE_P2_ABL & 2)) {
@@ -302,11 +324,13 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       });
       if (valid) {
 #pragma unroll
-        for (int t = 0; t < TH; ++t) pl[t * NP * LS] = yh[t];
+        for (int t = 0; t < TH; ++t)
+          pl[t * NP * LS] = VIE_P2_SIGNSPLIT ? flip_sign(yh[t], pattern_sign(SG.pi[t], sbits)) : yh[t];
       }
     }
   }
   __syncthreads();
+  P2_PHASE(3);
   // ---- inverse stage 1 (adjoint of radix R1), in place
   for (int u = tid; u < LINES * R0; u += SH::THREADS) {
     const int line = u % LINES, k0 = u / LINES;
@@ -345,8 +369,10 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
     };
     double2 vo[R0], vr[R0];
     if (act) branch(buf, b, vo);
+    P2_PHASE(4);
     const double2* rem = rbuf;
     asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    P2_PHASE(5);
     if (act) branch((VIE_P2_ABL & 16) ? buf : rem, b ^ 1, vr);
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // done reading the partner
     if (act && !(VIE_P2_ABL & 8)) {
@@ -361,7 +387,34 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
       });
     }
     asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // the partner finished reading this CTA
+    P2_PHASE(6);
   }
+}
+
+// Spectrum slab as a 3-D tensor of doubles: [(n2+1)(n1+1) rows][NC components][2 (n3+1)]
+void encode_spectrum_map(CUtensorMap* map, const double2* Shat, const Geom& g, const std::array<int, 3>& box) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    VIE_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess)
+      throw CudaError(cudaErrorNotSupported, "cuTensorMapEncodeTiled entry point", __FILE__, __LINE__);
+    return reinterpret_cast<Encode>(fn);
+  }();
+  const cuuint64_t n3p = static_cast<cuuint64_t>(g.n3) + 1;
+  const cuuint64_t dims[3] = {2 * n3p, static_cast<cuuint64_t>(g.NC),
+                              static_cast<cuuint64_t>(g.n1 + 1) * static_cast<cuuint64_t>(g.n2 + 1)};
+  const cuuint64_t strides[2] = {n3p * sizeof(double2), n3p * sizeof(double2) * g.NC};
+  const cuuint32_t boxd[3] = {static_cast<cuuint32_t>(box[0]), static_cast<cuuint32_t>(box[1]),
+                              static_cast<cuuint32_t>(box[2])};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(Shat), dims, strides, boxd,
+                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError(cudaErrorInvalidValue, "cuTensorMapEncodeTiled", __FILE__, __LINE__);
 }
 
 #define VIE_PENCIL2_SHAPES(X) X(10, 20) X(10, 10) X(8, 8) X(4, 8)
@@ -369,7 +422,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a) {
 template <int KIND, int BASIS>
 bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g, const double2* twm3,
                cudaStream_t st, bool dry) {
-  auto go = [&](auto fn, size_t smem, int P1P) {
+  auto go = [&](auto fn, size_t smem, int P1P, std::array<int, 3> box) {
     if (dry) return true;
     const int groups = (g.m1 + 2 * P1P - 1) / (2 * P1P);
     if (groups <= 1) return true;  // the edge launch covers everything
@@ -377,6 +430,8 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3,
                   g.bps, g.bps * g.n3};
+    CUtensorMap tmap;
+    encode_spectrum_map(&tmap, Shat, g, box);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (groups - 1), g.m2);
     cfg.blockDim = dim3(256);
@@ -389,7 +444,7 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a));
+    VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a, tmap));
     VIE_CUDA_CHECK(cudaGetLastError());
     return true;
   };
@@ -397,7 +452,7 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
   if (n3 == (A) * (B)) {                                                                 \
     using SH = Shape2<KIND, BASIS, A, B>;                                                \
     if (SH::smem_bytes > 113 * 1024) return false;                                       \
-    return go(k_pencil2<KIND, BASIS, A, B>, SH::smem_bytes, SH::P1P);                    \
+    return go(k_pencil2<KIND, BASIS, A, B>, SH::smem_bytes, SH::P1P, {2 * SH::CF, SH::CG, SH::P1P}); \
   }
   VIE_PENCIL2_SHAPES(VIE_CASE)
 #undef VIE_CASE
@@ -413,6 +468,16 @@ bool dispatch2(int kind, int basis, int n3, const double2* Bin, double2* Bout, c
 }
 
 }  // namespace
+
+#ifdef VIE_PENCIL_PROFILE
+void pencil2_phase_read(unsigned long long* out8, bool reset) {
+  cudaMemcpyFromSymbol(out8, g_p2_phase, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_p2_phase, z, sizeof(z));
+  }
+}
+#endif
 
 bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC) {
   const uint64_t all = NC >= 64 ? ~0ull : ((1ull << NC) - 1);
