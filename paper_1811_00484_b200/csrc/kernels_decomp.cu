@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
 // Octant decompression on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64).
 // CTA = (component c, PP consecutive p2o).  U3_c staged once in smem as the
 // B operand; per p2o: T = U1_c Z_c[p2o] (FMA, 4% of the flops) into smem as the
-// A operand, then S^ = T U3^T as a complex GEMM = 4 real DMMAs per 8x8x4 step.
+// A operand, then S^ = T U3^T as a complex GEMM = 3 real DMMAs per 8x8x4 step (Gauss).
 // Fragment smem layout [row][Kp] with Kp = 4 (mod 8): conflict-free quarter-warps.
 constexpr int kMmaMC = 64;   // rows (p1o) per T chunk
 constexpr int kMmaPP = 4;    // p2o values per CTA (U3 reuse)
@@ -212,33 +212,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
       const int nrt = (min(kMmaMC, n1p - m0) + 15) / 16;
       for (int t = warp; t < nrt * nct; t += nwarp) {
         const int rt = t / nct, ct = t - rt * nct;
+        // 3-multiplication complex product (Gauss): P1 = Ar Br, P2 = Ai Bi,
+        // P3 = (Ar + Ai)(Br + Bi); re = P1 - P2, im = P3 - P1 - P2 -> 3 DMMAs per step
+        double p1[2][2][2], p2[2][2][2], p3[2][2][2];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) p1[i][j][0] = p1[i][j][1] = p2[i][j][0] = p2[i][j][1] = p3[i][j][0] = p3[i][j][1] = 0.0;
+        const double2* ta = ts + (rt * 16 + fr) * Kp + fk;
+        const double2* ub = us + (ct * 16 + fr) * Kp + fk;
+        for (int k0 = 0; k0 < Kp; k0 += 4) {
+          const double2 av[2] = {ta[k0], ta[8 * Kp + k0]};
+          const double2 bv[2] = {ub[k0], ub[8 * Kp + k0]};
+          const double as[2] = {av[0].x + av[0].y, av[1].x + av[1].y};
+          const double bs[2] = {bv[0].x + bv[0].y, bv[1].x + bv[1].y};
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma(p1[i][j][0], p1[i][j][1], av[i].x, bv[j].x);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma(p2[i][j][0], p2[i][j][1], av[i].y, bv[j].y);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
+        }
         double accr[2][2][2], acci[2][2][2];
 #pragma unroll
         for (int i = 0; i < 2; ++i)
 #pragma unroll
-          for (int j = 0; j < 2; ++j) accr[i][j][0] = accr[i][j][1] = acci[i][j][0] = acci[i][j][1] = 0.0;
-        const double2* ta = ts + (rt * 16 + fr) * Kp + fk;
-        const double2* ub = us + (ct * 16 + fr) * Kp + fk;
-        for (int k0 = 0; k0 < Kp; k0 += 4) {
-          const double2 a0 = ta[k0], a1 = ta[8 * Kp + k0];
-          const double2 b0 = ub[k0], b1 = ub[8 * Kp + k0];
-          const double2 av[2] = {a0, a1}, bv[2] = {b0, b1};
-          // 8 independent accumulators, each touched once per pass: dependent DMMAs 8 apart
+          for (int j = 0; j < 2; ++j)
 #pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              dmma(accr[i][j][0], accr[i][j][1], av[i].x, bv[j].x);
-              dmma(acci[i][j][0], acci[i][j][1], av[i].x, bv[j].y);
+            for (int h = 0; h < 2; ++h) {
+              accr[i][j][h] = p1[i][j][h] - p2[i][j][h];
+              acci[i][j][h] = p3[i][j][h] - p1[i][j][h] - p2[i][j][h];
             }
-#pragma unroll
-          for (int i = 0; i < 2; ++i)
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              dmma(accr[i][j][0], accr[i][j][1], -av[i].y, bv[j].y);
-              dmma(acci[i][j][0], acci[i][j][1], av[i].y, bv[j].x);
-            }
-        }
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int row = m0 + rt * 16 + i * 8 + fr;
