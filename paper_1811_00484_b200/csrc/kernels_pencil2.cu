@@ -309,12 +309,12 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
             had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
                                                           ~0ull, m1flag, m2flag, mir);
         }
+        // every Hadamard read of buffer bi has returned (its FMAs were issued), so the
+        // warp can sign off without a fence; the last warp out refills the buffer
         __syncwarp();
         if (lane == 0) {
-          __threadfence_block();  // this warp's reads of buffer bi are done
-          if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {  // the last warp out refills the buffer
+          if (atomicAdd(cnt + bi, 1u) == SH::WARPS - 1) {
             cnt[bi] = 0u;
-            __threadfence_block();
             if (q + NBUF < nsub && !(VIE_P2_ABL & 2)) {
               asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
               issue_chunk(q + NBUF);
