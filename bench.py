@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import subprocess
 import sys
@@ -74,11 +75,26 @@ STAGES = ["row_fwd", "col_fwd", "decomp", "pencil", "col_inv", "row_inv"]
 
 
 def flops_model(grid, basis, nc, rank):
+    """Algorithmic FP64 flops.  Complex MAC = 8 flops; a length-N complex FFT is
+    credited the conventional 5 N log2 N (pad/crop pruning not credited)."""
     n1, n2, n3 = grid
+    m1, m2, m3 = 2 * n1, 2 * n2, 2 * n3
+    S = 3 if basis == 0 else 12
     noct = (n1 + 1) * (n2 + 1) * (n3 + 1)
     nb = 9 if basis == 0 else 144
     ne = 8 * n1 * n2 * n3
-    return {"decomp": 8.0 * nc * rank * noct, "hadamard": 8.0 * nb * ne}
+    fft = lambda lines, n: 5.0 * lines * n * math.log2(n)
+    return {
+        "decomp": 8.0 * nc * rank * noct + 8.0 * nc * rank * rank * (n1 + 1) * (n2 + 1),
+        "hadamard": 8.0 * nb * ne,
+        # per kernel
+        "row_fwd": fft(S * n2 * n3, m1), "col_fwd": fft(S * m1 * n3, m2),
+        "pencil": 8.0 * nb * ne + 2 * fft(S * m1 * m2, m3),
+        "col_inv": fft(S * m1 * n3, m2), "row_inv": fft(S * n2 * n3, m1),
+    }
+
+
+FP64_PEAK_TFLOPS = 37.1  # measured DMMA m8n8k4 = DFMA peak on this pool (profiles/r1_fp64_peak.txt)
 
 
 # ----------------------------------------------------------------------- clocks
@@ -326,7 +342,14 @@ def run_b200(args):
                              "frac": bm["matvec_staged"] / (ms * 1e-3) / 1e9 / peak},
             "stage_ms": {k: round(float(v), 4) for k, v in zip(STAGES, stage_ms)},
             "fp64_gflop": {k: v / 1e9 for k, v in fl.items()},
-            "gpu_launches": 7 * args.steps,
+            # the pencil kernel is FP64-pipe bound (168 GFLOP vs 24 GB at C4): the FP64 roofline
+            "roofline_fp64": {"bound": "fp64", "kernel": dom, "achieved": fl[dom] / (stage_ms[STAGES.index(dom)] * 1e-3) / 1e12,
+                              "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": fl[dom] / (stage_ms[STAGES.index(dom)] * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                              "per_kernel_tflops": {k: fl[k] / (stage_ms[STAGES.index(k)] * 1e-3) / 1e12
+                                                    for k in STAGES if k in fl},
+                              "peak_kind": "measured (scripts/fp64_peak.cu)"},
+            "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,

@@ -451,7 +451,8 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   if (op->q1) vie::launch_row_inv2(op->A, y, g, op->Q1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
   else vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
   mark();
-  op->last_launches = 7;
+  // row, column, (decomp_z + decomp), pencil (+ edge), column, row
+  op->last_launches = 7 + (op->pencil2 ? 1 : 0);
   if (op->profiling) {
     VIE_CUDA_CHECK(cudaEventSynchronize(op->ev[k - 1]));
     for (int i = 1; i < k; ++i) {

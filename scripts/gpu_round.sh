@@ -8,4 +8,4 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
 $CMD > gpurun_out/plain.json 2> gpurun_out/plain.err && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > /dev/null 2>&1; echo ncu1=$?
-ncu --set full --clock-control none --import-source on -k regex:"k_pencil|k_decomp_s_mma|k_col_fwd|k_row_fwd" -s 8 -c 4 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
+ncu --set full --clock-control none --import-source on -k regex:"k_pencil2|k_decomp_s_mma|k_col_fwd2|k_row_fwd2|k_col_inv2|k_row_inv2" -s 10 -c 6 -o gpurun_out/prof_full $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2=$?
