@@ -91,6 +91,11 @@ int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_by
 int vie_matvec(vie_op op, const double* x, double* y, void* stream);
 /* Same call with HOST buffers (H2D, matvec, D2H) -- the reference-facing call. */
 int vie_matvec_host(vie_op op, const double* x_host, double* y_host);
+/* `count` independent applications with HOST buffers, pipelined: the H2D copy of
+ * x_host[i+1] and the D2H copy of y_host[i-1] overlap the matvec of x_host[i]
+ * (copy streams + two device slots per direction).  Pinned host buffers are
+ * needed for the overlap.  Results are those of count vie_matvec_host calls. */
+int vie_matvec_host_batch(vie_op op, int64_t count, const double* const* x_host, double* const* y_host);
 
 /* apply_system (solver.hpp:183-200): y = eps_r*g*x - (eps_r - 1)*inv_v*(N x)
  * with g = 1 (PWC; PWL constant) or 1/12 (PWL linear), eps_r: n_vox complex.

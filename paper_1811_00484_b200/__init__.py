@@ -4,9 +4,9 @@ The compute lives in libvie_b200.so (hand-written sm_100a CUDA behind the C ABI
 in include/vie_b200.h); ``vie`` mirrors the reference operator API over it.
 """
 from .vie import (KIND_K, KIND_N, PWC, PWL, DftService, EmbeddedSpectrum, GmresConfig, GmresResult, TuckerForm,
-                  VieError, apply_operator, apply_system, build_operator_spectra, component_table, gmres, lib,
+                  VieError, apply_operator, apply_operator_batch, apply_system, build_operator_spectra, component_table, gmres, lib,
                   ncur, tucker_compress, RULE_ENERGY, RULE_SIGMA_MAX)
 
 __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "GmresConfig", "GmresResult",
-           "TuckerForm", "VieError", "apply_operator", "apply_system", "build_operator_spectra",
+           "TuckerForm", "VieError", "apply_operator", "apply_operator_batch", "apply_system", "build_operator_spectra",
            "component_table", "gmres", "lib", "ncur", "tucker_compress", "RULE_ENERGY", "RULE_SIGMA_MAX"]

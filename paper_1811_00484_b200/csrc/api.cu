@@ -118,9 +118,13 @@ struct vie_op_s {
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
   bool pencil2 = false;         // compile-time-shaped pencil kernel for this n3
   int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
-  // host-buffer staging (vie_matvec_host)
+  // host-buffer staging (vie_matvec_host; the batch call double-buffers with hx2 / hy2)
   double2* hx = nullptr;
   double2* hy = nullptr;
+  double2* hx2 = nullptr;
+  double2* hy2 = nullptr;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_h2d[2] = {}, ev_done[2] = {}, ev_d2h[2] = {};
   // GMRES state
   int g_inner = 0;
   double2* V = nullptr;
@@ -140,7 +144,8 @@ struct vie_op_s {
   ~vie_op_s() {
     for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
                     static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
-                    static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(V),
+                    static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(hx2), static_cast<void*>(hy2),
+                    static_cast<void*>(V),
                     static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
       dev_free(p);
@@ -148,7 +153,12 @@ struct vie_op_s {
       if (e) cudaEventDestroy(e);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t e : {ev_h2d[i], ev_done[i], ev_d2h[i]})
+        if (e) cudaEventDestroy(e);
     if (side) cudaStreamDestroy(side);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
   }
 };
 
@@ -790,6 +800,44 @@ int vie_matvec_host(vie_op op, const double* x_host, double* y_host) {
     VIE_CUDA_CHECK(cudaMemcpyAsync(op->hx, x_host, sizeof(double2) * n, cudaMemcpyHostToDevice, st));
     run_matvec(op, op->hx, op->hy, st, nullptr, 0.0, 0, true);
     VIE_CUDA_CHECK(cudaMemcpyAsync(y_host, op->hy, sizeof(double2) * n, cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int vie_matvec_host_batch(vie_op op, int64_t count, const double* const* x_host, double* const* y_host) {
+  return guard([&] {
+    if (!op || count < 0 || (count > 0 && (!x_host || !y_host))) throw Invalid("apply_operator: null argument");
+    for (int64_t i = 0; i < count; ++i)
+      if (!x_host[i] || !y_host[i]) throw Invalid("apply_operator: null argument");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    const int64_t n = static_cast<int64_t>(op->g.S) * op->g.n1 * op->g.n2 * op->g.n3;
+    const size_t bytes = sizeof(double2) * static_cast<size_t>(n);
+    for (double2** p : {&op->hx, &op->hy, &op->hx2, &op->hy2})
+      if (!*p) *p = dev_alloc<double2>(static_cast<size_t>(n));
+    if (!op->s_h2d) VIE_CUDA_CHECK(cudaStreamCreateWithFlags(&op->s_h2d, cudaStreamNonBlocking));
+    if (!op->s_d2h) VIE_CUDA_CHECK(cudaStreamCreateWithFlags(&op->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i)
+      for (cudaEvent_t* e : {&op->ev_h2d[i], &op->ev_done[i], &op->ev_d2h[i]})
+        if (!*e) VIE_CUDA_CHECK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    double2* dx[2] = {op->hx, op->hx2};
+    double2* dy[2] = {op->hy, op->hy2};
+    cudaStream_t st = op->ctx->stream;
+    // three-stage pipeline: H2D(i+1) and D2H(i-1) on their own copy streams overlap
+    // matvec(i); two device slots per direction, each reused once its consumer is done
+    for (int64_t i = 0; i < count; ++i) {
+      const int sl = static_cast<int>(i & 1);
+      if (i >= 2) VIE_CUDA_CHECK(cudaStreamWaitEvent(op->s_h2d, op->ev_done[sl], 0));  // matvec(i-2) read dx[sl]
+      VIE_CUDA_CHECK(cudaMemcpyAsync(dx[sl], x_host[i], bytes, cudaMemcpyHostToDevice, op->s_h2d));
+      VIE_CUDA_CHECK(cudaEventRecord(op->ev_h2d[sl], op->s_h2d));
+      VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_h2d[sl], 0));
+      if (i >= 2) VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_d2h[sl], 0));  // D2H(i-2) drained dy[sl]
+      run_matvec(op, dx[sl], dy[sl], st, nullptr, 0.0, 0);
+      VIE_CUDA_CHECK(cudaEventRecord(op->ev_done[sl], st));
+      VIE_CUDA_CHECK(cudaStreamWaitEvent(op->s_d2h, op->ev_done[sl], 0));
+      VIE_CUDA_CHECK(cudaMemcpyAsync(y_host[i], dy[sl], bytes, cudaMemcpyDeviceToHost, op->s_d2h));
+      VIE_CUDA_CHECK(cudaEventRecord(op->ev_d2h[sl], op->s_d2h));
+    }
+    VIE_CUDA_CHECK(cudaStreamSynchronize(op->s_d2h));
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
   });
 }

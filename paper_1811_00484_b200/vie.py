@@ -53,6 +53,7 @@ def lib() -> C.CDLL:
                                         C.c_void_p]
         L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_matvec_host_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.vie_gmres_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_double,
                                       C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                       _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
@@ -286,6 +287,26 @@ def apply_operator(op: EmbeddedSpectrum, x, strategy: str = "hosvd_decompress", 
     y = out if out is not None else torch.empty_like(x)
     _check(lib().vie_matvec(op.handle, x.data_ptr(), y.data_ptr(), _stream_handle(stream, x.device)))
     return y
+
+
+def apply_operator_batch(op: EmbeddedSpectrum, xs, ys=None):
+    """Independent applications y_i = A x_i of HOST vectors (numpy complex128 or CPU
+    torch tensors, pinned for copy/compute overlap), pipelined on the device
+    (vie_matvec_host_batch): the copies of neighbouring vectors overlap each matvec."""
+    xs = list(xs)
+    n = op.n_cur * op.n_vox
+    ptr = lambda a: a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
+    for x in xs:
+        if (x.numel() if hasattr(x, "numel") else x.size) != n:
+            raise ValueError("apply_operator: dim mismatch")
+    if ys is None:
+        ys = [np.empty(n, dtype=np.complex128) for _ in xs]
+    if len(ys) != len(xs):
+        raise ValueError("apply_operator: dim mismatch")
+    xp = (C.c_void_p * max(1, len(xs)))(*[ptr(x) for x in xs])
+    yp = (C.c_void_p * max(1, len(ys)))(*[ptr(y) for y in ys])
+    _check(lib().vie_matvec_host_batch(op.handle, len(xs), xp, yp))
+    return ys
 
 
 def apply_system(eps_r, inv_v: float, op: EmbeddedSpectrum, x, out=None, diag_term: bool = True, stream=None):

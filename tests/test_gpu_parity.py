@@ -117,6 +117,22 @@ def test_matvec_mixed_ranks_and_host_path(vie, dft, orc):
     assert rel(y_ref, vie.apply_operator(op, x)) <= MATVEC_TOL  # host-buffer C-ABI call
 
 
+def test_host_batch_matches_single_calls(vie, dft, orc):
+    # vie_matvec_host_batch: pipelined copies, results identical to one call per vector
+    import torch
+
+    dims = (5, 6, 4)
+    op, oforms, _, _ = make_ops(vie, dft, orc, N, PWL, dims, 3, 5)
+    xs = [random_field(PWL, dims, 40 + i) for i in range(5)]
+    xp = [torch.from_numpy(x.copy()).pin_memory() for x in xs]
+    yp = [torch.empty_like(x).pin_memory() for x in xp]
+    vie.apply_operator_batch(op, xp, yp)
+    for x, y in zip(xs, yp):
+        assert np.array_equal(vie.apply_operator(op, x), y.numpy())
+    assert rel(orc.apply_operator_tucker(N, PWL, dims, oforms, xs[3]), yp[3].numpy()) <= MATVEC_TOL
+    assert vie.apply_operator_batch(op, []) == []
+
+
 @pytest.mark.parametrize("basis", [PWC, PWL])
 def test_component_sharding_sums_to_full(vie, dft, orc, basis):
     # components sharded over "ranks": partial outputs add up to the full matvec
