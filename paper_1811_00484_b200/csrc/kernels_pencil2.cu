@@ -23,6 +23,8 @@
 #include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point)
 
 #include <array>
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 #include "fft.cuh"
@@ -34,6 +36,21 @@
 #endif
 #ifndef VIE_P2_SIGNSPLIT
 #define VIE_P2_SIGNSPLIT 1  // mirror signs on x^ / y^ instead of every spectrum value
+#endif
+#ifndef VIE_P2_LDMODE
+#define VIE_P2_LDMODE 0  // stage-0 pencil loads: 0 default, 1 .cg, 2 .cs
+#endif
+#ifndef VIE_P2_STMODE
+#define VIE_P2_STMODE 0  // output stores: 0 default, 1 .cg, 2 .cs
+#endif
+#ifndef VIE_P2_TWLDG
+#define VIE_P2_TWLDG 0  // stage twiddles from the (L1-resident) table instead of recurrences
+#endif
+#ifndef VIE_P2_CHUNK
+#define VIE_P2_CHUNK 640  // spectrum chunk budget (double2): 10 KB
+#endif
+#ifndef VIE_P2_EXTRA
+#define VIE_P2_EXTRA 0
 #endif
 #ifndef VIE_P2_ABL
 #define VIE_P2_ABL 0  // ablation bits (timing experiments only): 1 no Hadamard FMAs, 2 no spectrum stream,
@@ -97,7 +114,7 @@ struct Shape2 {
   static constexpr int N3 = R0 * R1;
   static constexpr int LS = N3 | 1;  // odd line stride: lanes over lines hit distinct banks
   static constexpr int CF = THREADS / (NP * 2 * TS);  // octant frequencies per chunk
-  static constexpr int CHUNK_BUDGET = 640;            // double2 per chunk buffer (10 KB)
+  static constexpr int CHUNK_BUDGET = VIE_P2_CHUNK;   // double2 per chunk buffer
   static constexpr int CG0 = CHUNK_BUDGET / (P1P * CF) > 0 ? CHUNK_BUDGET / (P1P * CF) : 1;
   static constexpr int NG = (NC + CG0 - 1) / CG0;  // component groups per round
   static constexpr int CG = (NC + NG - 1) / NG;
@@ -105,7 +122,7 @@ struct Shape2 {
   static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
   static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
   static constexpr int NBUF = VIE_P2_NBUF;     // chunk ring depth
-  static constexpr size_t smem_bytes = 128 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS);
+  static constexpr size_t smem_bytes = 128 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS + VIE_P2_EXTRA);
   static_assert(HL * R1 <= THREADS, "one combine unit per thread");
   static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
   static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
@@ -198,7 +215,15 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
                            static_cast<int64_t>(pos2) * m1 + c0 + p;
       const int64_t step = static_cast<int64_t>(R1) * a.kstride;
 #pragma unroll
-      for (int i = 0; i < R0; ++i) xin[i] = src[i * step];
+      for (int i = 0; i < R0; ++i) {
+#if VIE_P2_LDMODE == 1
+        xin[i] = __ldcg(src + i * step);
+#elif VIE_P2_LDMODE == 2
+        xin[i] = __ldcs(src + i * step);
+#else
+        xin[i] = src[i * step];
+#endif
+      }
     } else {
 #pragma unroll
       for (int i = 0; i < R0; ++i) xin[i] = make_double2(0.0, 0.0);
@@ -229,8 +254,12 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       dst[0] = v[out_idx(R0, 0)];
       sfor<R0 - 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value + 1;
-        dst[k * R1] = cmul(v[out_idx(R0, k)], w);
-        if (k + 1 < R0) w = cmul(w, wstep0);
+        if constexpr (VIE_P2_TWLDG) {
+          dst[k * R1] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * 2 * k));
+        } else {
+          dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+          if (k + 1 < R0) w = cmul(w, wstep0);
+        }
       });
     }
     v[0] = xin[0];  // branch 1: inputs * w_{2 R0}^i, outputs * w_m3^{mp (2k + 1)}
@@ -244,8 +273,12 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       double2 w = __ldg(a.twm3 + mp0);
       sfor<R0>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        dst[k * R1] = cmul(v[out_idx(R0, k)], w);
-        if (k + 1 < R0) w = cmul(w, wstep0);
+        if constexpr (VIE_P2_TWLDG) {
+          dst[k * R1] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * (2 * k + 1)));
+        } else {
+          dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+          if (k + 1 < R0) w = cmul(w, wstep0);
+        }
       });
     }
   }
@@ -357,13 +390,20 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     const double2 w1 = __ldg(a.twm3 + min(mp, R1 - 1));
     // branch br: inputs * conj(w_m3^{mp (2k + br)}), then the radix-R0 adjoint
     auto branch = [&](const double2* X, int br, double2(&v)[R0]) {
-      double2 w = br ? w1 : wstep;
-      v[0] = br ? cmulc(X[off], w) : X[off];
-      if (br) w = cmul(w, wstep);
+      if constexpr (VIE_P2_TWLDG) {
+        const int mpc = min(mp, R1 - 1);
+        v[0] = br ? cmulc(X[off], w1) : X[off];
 #pragma unroll
-      for (int k = 1; k < R0; ++k) {
-        v[k] = cmulc(X[off + k * R1], w);
-        if (k + 1 < R0) w = cmul(w, wstep);
+        for (int k = 1; k < R0; ++k) v[k] = cmulc(X[off + k * R1], __ldg(a.twm3 + mpc * (2 * k + br)));
+      } else {
+        double2 w = br ? w1 : wstep;
+        v[0] = br ? cmulc(X[off], w) : X[off];
+        if (br) w = cmul(w, wstep);
+#pragma unroll
+        for (int k = 1; k < R0; ++k) {
+          v[k] = cmulc(X[off + k * R1], w);
+          if (k + 1 < R0) w = cmul(w, wstep);
+        }
       }
       DFTs<R0, true, 1, 0>::run(v);
     };
@@ -383,7 +423,13 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
         constexpr int i = decltype(ic)::value;
         const double2 y0 = b ? vr[out_idx(R0, i)] : vo[out_idx(R0, i)];
         const double2 y1 = b ? vo[out_idx(R0, i)] : vr[out_idx(R0, i)];
+#if VIE_P2_STMODE == 1
+        __stcg(dst + i * step, cadd(y0, twc<2 * R0, true, i>(y1)));
+#elif VIE_P2_STMODE == 2
+        __stcs(dst + i * step, cadd(y0, twc<2 * R0, true, i>(y1)));
+#else
         dst[i * step] = cadd(y0, twc<2 * R0, true, i>(y1));
+#endif
       });
     }
     asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // the partner finished reading this CTA
@@ -444,6 +490,12 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    if (std::getenv("VIE_DEBUG_OCC")) {
+      int nb = 0, ncl = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, 256, smem);
+      cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg);
+      fprintf(stderr, "pencil2 smem %zu: blocks/SM %d, active clusters %d\n", smem, nb, ncl);
+    }
     VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a, tmap));
     VIE_CUDA_CHECK(cudaGetLastError());
     return true;
