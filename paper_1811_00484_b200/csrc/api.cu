@@ -182,7 +182,6 @@ constexpr bool kPass2 = VIE_PASS2;
 #define VIE_PENCIL2 1
 #endif
 constexpr bool kPencil2 = VIE_PENCIL2;
-constexpr int kSlabPad = 0;  // elements appended to each m1 x m2 slab plane (see Geom::bps)  // kernels_pencil2.cu when n3 has a compiled shape  // register-staged passes (kernels_fft2.cu)
 int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -666,7 +665,10 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     g.m3 = 2 * g.n3;
     g.S = basis == 0 ? 3 : 12;
     g.NC = static_cast<int>(cs.size());
-    g.bps = static_cast<int64_t>(g.m1) * g.m2 + env_int("VIE_BPAD", kSlabPad);
+    g.nk = g.n3;  // one slab block (vie_op_set_partition re-blocks for the slab-decomposed matvec)
+    g.np2 = g.m2;
+    g.p2off = 0;
+    g.bps = static_cast<int64_t>(g.m1) * g.m2;
     op->comps_host.assign(cs.size(), CompDev{1, 1, 1, 0, 0, 0, 0, 0, 0});
     std::vector<const vie_tucker_s*> byc(cs.size(), nullptr);
     for (int i = 0; i < ncomp; ++i) {

@@ -21,8 +21,15 @@ struct Geom {
   int m1, m2, m3;  // embedded (2n)
   int S;           // current components (sources = targets)
   int NC;          // canonical component count
-  int64_t bps;     // plane stride of the spectral slabs B, Bo (m1 m2 + pad: spreads the pencil
-                   // kernel's 3 MB-strided accesses over DRAM channels)
+  // Spectral slabs B, Bo (after the axis-1/2 FFTs) are blocked for the slab-decomposed
+  // multi-GPU matvec: [block][s][k in block][axis-2 row in block][pos1]
+  // with blocks of nk k-planes (forward/inverse passes: the block = destination rank of
+  // the axis-2 rows, q = pos2 / np2) or of np2 axis-2 rows (pencil stage: the block = source
+  // rank of the k-planes, r = k / nk).  One GPU: nk = n3, np2 = m2, p2off = 0, one block.
+  int nk;          // k-planes per block
+  int np2;         // axis-2 rows per block
+  int p2off;       // first global axis-2 position of this rank's pencil rows
+  int64_t bps;     // plane stride = np2 * m1
 };
 
 // Tuning constants.
@@ -77,8 +84,10 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
 void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& P1, double scale,
                     const double2* eps, const double2* xin, double inv_v, int basis, int diag, cudaStream_t st);
 
+// Octant spectra rows p2o in [p2lo, p2hi) (p2hi < 0: all n2 + 1 rows); with_z: also Z = core x2 U2
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
-                   double2* Shat, const Geom& g, int rmax, cudaStream_t st);
+                   double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo = 0, int p2hi = -1,
+                   bool with_z = true);
 
 // transform_factors on device: spatial factor (n x r, col-major) -> octant rows
 // (n+1) x r of the DFT of the parity embedding (operator.hpp:64-90).

@@ -55,12 +55,12 @@ constexpr int kQ = 4;     // micro-tile 4 x 4
 __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict__ forms,
                                                        const CompDev* __restrict__ comps,
                                                        const double2* __restrict__ Z, double2* __restrict__ Shat,
-                                                       Geom geo, int NC) {
+                                                       Geom geo, int NC, int p2lo) {
   extern __shared__ double2 sm[];
   const int c = blockIdx.x;
   const CompDev cd = comps[c];
   if (!cd.active) return;
-  const int p2o = blockIdx.y;
+  const int p2o = p2lo + blockIdx.y;
   const int r1 = cd.r1, r3 = cd.r3;
   const int n1p = geo.n1 + 1, n3p = geo.n3 + 1;
   double2* zs = sm;                                   // r1 x r3   zs[a*r3 + g]
@@ -149,13 +149,14 @@ __host__ __device__ __forceinline__ int mma_kp(int r3) {
 __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __restrict__ forms,
                                                               const CompDev* __restrict__ comps,
                                                               const double2* __restrict__ Z,
-                                                              double2* __restrict__ Shat, Geom geo, int NC) {
+                                                              double2* __restrict__ Shat, Geom geo, int NC, int p2lo,
+                                                              int p2hi) {
   extern __shared__ double2 sm[];
   const int c = blockIdx.x;
   const CompDev cd = comps[c];
   if (!cd.active) return;
   const int r1 = cd.r1, r3 = cd.r3;
-  const int n1p = geo.n1 + 1, n2p = geo.n2 + 1, n3p = geo.n3 + 1;
+  const int n1p = geo.n1 + 1, n3p = geo.n3 + 1;
   const int Kp = mma_kp(r3);
   const int NPad = (n3p + 15) / 16 * 16;
   double2* us = sm;                                    // [NPad][Kp]  B operand (U3)
@@ -173,8 +174,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
   const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), col / k (B)
   const int E = geo.n3 / 2 + 1;
   const int nct = NPad / 16;
-  const int p2end = min(n2p, (blockIdx.y + 1) * kMmaPP);
-  for (int p2o = blockIdx.y * kMmaPP; p2o < p2end; ++p2o) {
+  const int p2end = min(p2hi, p2lo + (static_cast<int>(blockIdx.y) + 1) * kMmaPP);
+  for (int p2o = p2lo + blockIdx.y * kMmaPP; p2o < p2end; ++p2o) {
     __syncthreads();  // previous p2o done with zs / ts
     const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;
     for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) cp_async16(zs + e, zsrc + e);
@@ -303,24 +304,28 @@ size_t decomp_smem(int n3, int rmax) {
 }
 
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
-                   double2* Shat, const Geom& g, int rmax, cudaStream_t st) {
+                   double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo, int p2hi, bool with_z) {
   (void)comps_host;
+  if (p2hi < 0) p2hi = g.n2 + 1;
+  if (p2hi <= p2lo) return;
   const size_t smz = sizeof(double2) * static_cast<size_t>(rmax) * rmax;
   VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_z),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smz)));
-  k_decomp_z<<<dim3(g.NC, rmax), kThreads, smz, st>>>(forms, comps_dev, Z, g.n2);
-  VIE_CUDA_CHECK(cudaGetLastError());
+  if (with_z) {
+    k_decomp_z<<<dim3(g.NC, rmax), kThreads, smz, st>>>(forms, comps_dev, Z, g.n2);
+    VIE_CUDA_CHECK(cudaGetLastError());
+  }
   const size_t sms = decomp_mma_smem(g.n1, g.n3, rmax);
   if (sms <= kMaxSmem) {
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s_mma),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
-    k_decomp_s_mma<<<dim3(g.NC, (g.n2 + 1 + kMmaPP - 1) / kMmaPP), kThreads, sms, st>>>(forms, comps_dev, Z, Shat,
-                                                                                      g, g.NC);
+    k_decomp_s_mma<<<dim3(g.NC, (p2hi - p2lo + kMmaPP - 1) / kMmaPP), kThreads, sms, st>>>(
+        forms, comps_dev, Z, Shat, g, g.NC, p2lo, p2hi);
   } else {
     const size_t smf = decomp_smem(g.n3, rmax);
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smf)));
-    k_decomp_s<<<dim3(g.NC, g.n2 + 1), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC);
+    k_decomp_s<<<dim3(g.NC, p2hi - p2lo), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC, p2lo);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }

@@ -229,12 +229,21 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
 // -------------------------------------------------------------------- columns
 // A: planes of n2 rows x m1 -> B: planes of m2 rows x m1 (mirror-paired rows);
 // kColsPerCta consecutive columns per CTA, lanes over columns (128 B segments).
+// offset of axis-2 position pos in a blocked slab (Geom): block q = pos / np2
+template <bool BLOCKED>
+__device__ __forceinline__ int64_t slab_row(int pos, int m1, const FastDiv& dnp2, int64_t blk) {
+  if constexpr (!BLOCKED) return static_cast<int64_t>(pos) * m1;  // single block (one GPU)
+  const int q = static_cast<int>(dnp2.div(static_cast<uint32_t>(pos)));
+  return q * blk + static_cast<int64_t>(pos - q * static_cast<int>(dnp2.d)) * m1;
+}
+
 constexpr int kCW = kColsPerCta;
 static_assert((kCW & (kCW - 1)) == 0, "column tile must be a power of two");
 constexpr int kLgCW = kCW == 8 ? 3 : (kCW == 4 ? 2 : (kCW == 16 ? 4 : 0));
 
+template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
-                                                     Pass2 P, int64_t bps) {
+                                                     Pass2 P, int64_t bps, FastDiv dnp2, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
@@ -248,7 +257,7 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
       even_dispatch(R0, [&](auto rc) {
         fwd_first<decltype(rc)::value>(
             0, P.tw, [&](int i) { return src[static_cast<int64_t>(i) * m1 + w]; },
-            [&](int k, double2 v) { dst[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w] = v; });
+            [&](int k, double2 v) { dst[slab_row<BLOCKED>(pos_of_freq(k, n), m1, dnp2, blk) + w] = v; });
       });
     return;
   }
@@ -273,13 +282,14 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
     radix_dispatch(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, false>(
           [&](int i) { return b[i]; },
-          [&](int k, double2 v) { d[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1] = v; });
+          [&](int k, double2 v) { d[slab_row<BLOCKED>(pos_of_freq(bk + R0 * k, n), m1, dnp2, blk)] = v; });
     });
   }
 }
 
+template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
-                                                     Pass2 P, int64_t bps) {
+                                                     Pass2 P, int64_t bps, FastDiv dnp2, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     if (w < wc)
       even_dispatch(R0, [&](auto rc) {
         inv_last<decltype(rc)::value>(
-            0, P.tw, [&](int k) { return src[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w]; },
+            0, P.tw, [&](int k) { return src[slab_row<BLOCKED>(pos_of_freq(k, n), m1, dnp2, blk) + w]; },
             [&](int i, double2 v) { dst[static_cast<int64_t>(i) * m1 + w] = v; });
       });
     return;
@@ -305,7 +315,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     double2* b = buf + w * ls + bk * R1p;
     radix_dispatch(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, true>(
-          [&](int k) { return s[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1]; },
+          [&](int k) { return s[slab_row<BLOCKED>(pos_of_freq(bk + R0 * k, n), m1, dnp2, blk)]; },
           [&](int i, double2 v) { b[i] = v; });
     });
   }
@@ -377,19 +387,35 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
 
 void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st) {
   const size_t sm = pass2_smem(P, kCW);
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2), sm);
-  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.n3);
+  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps);
+  FastDiv dnp2;
+  dnp2.init(static_cast<uint32_t>(g.np2));
+  const int64_t blk = g.bps * g.S * g.nk;
+  if (g.np2 == g.m2) {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2<false>), sm);
+    k_col_fwd2<false><<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps, dnp2, blk);
+  } else {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2<true>), sm);
+    k_col_fwd2<true><<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps, dnp2, blk);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st) {
   const size_t sm = pass2_smem(P, kCW);
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2), sm);
-  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.n3);
+  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps);
+  FastDiv dnp2;
+  dnp2.init(static_cast<uint32_t>(g.np2));
+  const int64_t blk = g.bps * g.S * g.nk;
+  if (g.np2 == g.m2) {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2<false>), sm);
+    k_col_inv2<false><<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps, dnp2, blk);
+  } else {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2<true>), sm);
+    k_col_inv2<true><<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps, dnp2, blk);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -37,20 +37,11 @@
 #ifndef VIE_P2_SIGNSPLIT
 #define VIE_P2_SIGNSPLIT 1  // mirror signs on x^ / y^ instead of every spectrum value
 #endif
-#ifndef VIE_P2_LDMODE
-#define VIE_P2_LDMODE 0  // stage-0 pencil loads: 0 default, 1 .cg, 2 .cs
-#endif
-#ifndef VIE_P2_STMODE
-#define VIE_P2_STMODE 0  // output stores: 0 default, 1 .cg, 2 .cs
-#endif
 #ifndef VIE_P2_TWLDG
 #define VIE_P2_TWLDG 0  // stage twiddles from the (L1-resident) table instead of recurrences
 #endif
 #ifndef VIE_P2_CHUNK
 #define VIE_P2_CHUNK 640  // spectrum chunk budget (double2): 10 KB
-#endif
-#ifndef VIE_P2_EXTRA
-#define VIE_P2_EXTRA 0
 #endif
 #ifndef VIE_P2_ABL
 #define VIE_P2_ABL 0  // ablation bits (timing experiments only): 1 no Hadamard FMAs, 2 no spectrum stream,
@@ -122,7 +113,7 @@ struct Shape2 {
   static constexpr int E = N3 / 2 + 1;         // even octant frequencies (branch 0)
   static constexpr int O = (N3 + 1) / 2;       // odd octant frequencies (branch 1)
   static constexpr int NBUF = VIE_P2_NBUF;     // chunk ring depth
-  static constexpr size_t smem_bytes = 128 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS + VIE_P2_EXTRA);
+  static constexpr size_t smem_bytes = 128 + sizeof(double2) * (NBUF * CHUNK + static_cast<size_t>(LINES) * LS);
   static_assert(HL * R1 <= THREADS, "one combine unit per thread");
   static_assert(LINES % 2 == 0 && (NP & (NP - 1)) == 0, "pencil tile shape");
   static_assert(CF * NP * 2 * TS == THREADS, "one (point, target half) per thread per round");
@@ -134,7 +125,9 @@ struct Pencil2Args {
   const double2* Shat;
   const double2* twm3;  // w_m3^e, e < m3
   int n1, n2, m1, m2, m3;
-  int64_t kstride, sstride;  // bps, bps n3 (padded slab planes)
+  int64_t kstride, sstride;  // plane stride bps, current stride nk * bps (Geom)
+  int nk, p2off;
+  FastDiv dnk;
 };
 
 #ifdef VIE_PENCIL_PROFILE
@@ -180,7 +173,13 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   const int b = blockIdx.x & 1;                     // axis-3 branch = rank in the cluster
   const int c0 = 2 * P1P * (1 + (blockIdx.x >> 1));  // first axis-1 position (group 0 is the edge launch)
   const int q0 = c0 >> 1;                           // octant row of pair 0
-  const int pos2 = blockIdx.y;
+  const int pos2l = blockIdx.y;          // axis-2 row of this rank's slab block
+  const int pos2 = a.p2off + pos2l;      // global axis-2 position
+  // slab offset of k-plane k: block r = k / nk of the k-planes (one block on one GPU)
+  auto koff = [&](int k) -> int64_t {
+    const int r = static_cast<int>(a.dnk.div(static_cast<uint32_t>(k)));
+    return static_cast<int64_t>(k + r * (SH::S - 1) * a.nk) * a.kstride;
+  };
   const int n1 = a.n1, n2 = a.n2, m1 = a.m1;
   const int f2 = freq_of_pos(pos2, n2);
   const int m2flag = f2 > n2;
@@ -211,19 +210,9 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   {
     const int s = line0 / NP, p = line0 % NP;
     if (act0 && c0 + p < m1 && !(VIE_P2_ABL & 4)) {
-      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(mp0) * a.kstride +
-                           static_cast<int64_t>(pos2) * m1 + c0 + p;
-      const int64_t step = static_cast<int64_t>(R1) * a.kstride;
+      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(pos2l) * m1 + c0 + p;
 #pragma unroll
-      for (int i = 0; i < R0; ++i) {
-#if VIE_P2_LDMODE == 1
-        xin[i] = __ldcg(src + i * step);
-#elif VIE_P2_LDMODE == 2
-        xin[i] = __ldcs(src + i * step);
-#else
-        xin[i] = src[i * step];
-#endif
-      }
+      for (int i = 0; i < R0; ++i) xin[i] = src[koff(mp0 + i * R1)];
     } else {
 #pragma unroll
       for (int i = 0; i < R0; ++i) xin[i] = make_double2(0.0, 0.0);
@@ -416,20 +405,12 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     if (act) branch((VIE_P2_ABL & 16) ? buf : rem, b ^ 1, vr);
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // done reading the partner
     if (act && !(VIE_P2_ABL & 8)) {
-      double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(mp) * a.kstride +
-                     static_cast<int64_t>(pos2) * m1 + c0 + p;
-      const int64_t step = static_cast<int64_t>(R1) * a.kstride;
+      double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(pos2l) * m1 + c0 + p;
       sfor<R0>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         const double2 y0 = b ? vr[out_idx(R0, i)] : vo[out_idx(R0, i)];
         const double2 y1 = b ? vo[out_idx(R0, i)] : vr[out_idx(R0, i)];
-#if VIE_P2_STMODE == 1
-        __stcg(dst + i * step, cadd(y0, twc<2 * R0, true, i>(y1)));
-#elif VIE_P2_STMODE == 2
-        __stcs(dst + i * step, cadd(y0, twc<2 * R0, true, i>(y1)));
-#else
-        dst[i * step] = cadd(y0, twc<2 * R0, true, i>(y1));
-#endif
+        dst[koff(mp + i * R1)] = cadd(y0, twc<2 * R0, true, i>(y1));
       });
     }
     asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");  // the partner finished reading this CTA
@@ -474,12 +455,12 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     if (groups <= 1) return true;  // the edge launch covers everything
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3,
-                  g.bps, g.bps * g.n3};
+    Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3, g.bps, g.bps * g.nk, g.nk, g.p2off, {}};
+    a.dnk.init(static_cast<uint32_t>(g.nk));
     CUtensorMap tmap;
     encode_spectrum_map(&tmap, Shat, g, box);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (groups - 1), g.m2);
+    cfg.gridDim = dim3(2 * (groups - 1), g.np2);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
