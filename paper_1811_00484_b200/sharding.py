@@ -45,3 +45,98 @@ def sharded_apply_system(eps_r, inv_v, op, x, out=None, group=None, stream=None)
     rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
     y = apply_system(eps_r, inv_v, op, x, out=out, diag_term=(rank == 0), stream=stream)
     return allreduce_sum_(y, group)
+
+
+# ----------------------------------------------------------------------------
+# Slab decomposition (recommended partition): rank r owns the
+# z-planes [r nk, (r+1) nk) of x and y and the axis-2 spectral rows
+# [r np2, (r+1) np2) of the pencil stage.  One matvec = local axis-1/2 FFTs ->
+# all-to-all -> decompression of the rank's octant rows + fused axis-3 FFT /
+# Hadamard / IFFT -> all-to-all back -> local inverse axis-2/1 FFTs.  The
+# exchanged buffers are blocked by rank (vie_slab_* in include/vie_b200.h), so
+# each exchange is one equal-split all_to_all_single (NCCL over NVLink).
+
+
+def slab_planes(n3: int, rank: int, world: int) -> tuple[int, int]:
+    """z-planes [k0, k0 + nk) owned by `rank` (n3 divisible by world)."""
+    if world < 1 or not (0 <= rank < world) or n3 % world:
+        raise ValueError("slab_planes: n3 must split evenly over the ranks")
+    nk = n3 // world
+    return rank * nk, nk
+
+
+def local_slab(x, S: int, n3: int, nv_plane: int, rank: int, world: int):
+    """This rank's z-slab of a global current vector [s][k][j][i] (torch or numpy)."""
+    k0, nk = slab_planes(n3, rank, world)
+    return x.reshape(S, n3, nv_plane)[:, k0:k0 + nk].reshape(-1)
+
+
+class SlabMatvec:
+    """apply_operator / apply_system of a slab-partitioned operator on this rank.
+
+    ``exchange(recv, send)`` defaults to torch.distributed.all_to_all_single over
+    ``group``; tests emulate it for several ranks in one process."""
+
+    def __init__(self, op, rank: int, world: int, group=None, exchange=None):
+        import ctypes as C
+
+        import torch
+
+        from .vie import _check, lib
+
+        self.op, self.rank, self.world, self.group = op, rank, world, group
+        L = lib()
+        _check(L.vie_op_set_partition(op.handle, world, rank))
+        xe, se, k0, nk = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(L.vie_slab_info(op.handle, C.byref(xe), C.byref(se), C.byref(k0), C.byref(nk)))
+        self.x_elems, self.slab_elems, self.k0, self.nk = xe.value, se.value, k0.value, nk.value
+        mk = lambda: torch.empty(self.slab_elems, dtype=torch.complex128, device="cuda")
+        self.send, self.recv, self.out, self.back = mk(), mk(), mk(), mk()
+        self._exchange = exchange
+
+    def exchange(self, recv, send):
+        if self._exchange is not None:
+            return self._exchange(recv, send)
+        if self.world == 1:
+            recv.copy_(send)
+            return recv
+        import torch.distributed as dist
+
+        dist.all_to_all_single(recv, send, group=self.group)
+        return recv
+
+    # the three stages (also used separately by the emulation test); kernels run on
+    # torch's current stream so they order with the collectives
+    def forward(self, x_local, stream=None):
+        from .vie import _check, _stream_handle, lib
+
+        _check(lib().vie_slab_forward(self.op.handle, x_local.data_ptr(), self.send.data_ptr(),
+                                      _stream_handle(stream, x_local.device)))
+
+    def pencil(self, stream=None):
+        from .vie import _check, _stream_handle, lib
+
+        _check(lib().vie_slab_pencil(self.op.handle, self.recv.data_ptr(), self.out.data_ptr(),
+                                     _stream_handle(stream, self.recv.device)))
+
+    def inverse(self, y_local, eps_local=None, inv_v=0.0, x_local=None, diag=True, stream=None):
+        from .vie import _check, _stream_handle, lib
+
+        _check(lib().vie_slab_inverse(self.op.handle, self.back.data_ptr(), y_local.data_ptr(),
+                                      None if eps_local is None else eps_local.data_ptr(), float(inv_v),
+                                      None if x_local is None else x_local.data_ptr(), int(bool(diag)),
+                                      _stream_handle(stream, y_local.device)))
+
+    def apply(self, x_local, out=None, eps_local=None, inv_v=0.0, diag=True):
+        """y_local = (A x)_local (or the system matvec with eps_local); x_local: CUDA complex128."""
+        import torch
+
+        if x_local.numel() != self.x_elems or x_local.dtype != torch.complex128 or not x_local.is_cuda:
+            raise ValueError("slab apply: x_local must be this rank's CUDA complex128 z-slab")
+        y = out if out is not None else torch.empty_like(x_local)
+        self.forward(x_local)
+        self.exchange(self.recv, self.send)
+        self.pencil()
+        self.exchange(self.back, self.out)
+        self.inverse(y, eps_local, inv_v, x_local if eps_local is not None else None, diag)
+        return y

@@ -54,6 +54,12 @@ def lib() -> C.CDLL:
         L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_matvec_host_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.vie_op_set_partition.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        L.vie_slab_info.argtypes = [C.c_void_p] + [C.POINTER(C.c_int64)] * 4
+        L.vie_slab_forward.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_slab_pencil.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_slab_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                       C.c_int, C.c_void_p]
         L.vie_gmres_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_double,
                                       C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
                                       _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
