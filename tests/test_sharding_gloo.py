@@ -79,3 +79,74 @@ def test_shard_assignment_partitions():
             assert got == list(range(nc))
     with pytest.raises(ValueError):
         shard_components(6, 2, 2)
+
+
+# --------------------------------------------------------------------------
+# Slab decomposition host logic (vie_slab_* dataflow) with real gloo all-to-alls:
+# the per-rank stages are numpy stand-ins for the three C-ABI stages using the same
+# rank-blocked exchange layout [rank][s][k in block][axis-2 row in block][axis-1].
+def _slab_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import oracle as orc
+    from paper_1811_00484_b200.sharding import local_slab, slab_planes
+    from tests.helpers import fourier_forms, random_field, spatial_tucker_forms
+
+    kind, basis, dims = 0, 0, (3, 6, 6)
+    n1, n2, n3 = dims
+    m1, m2, m3 = 2 * n1, 2 * n2, 2 * n3
+    S = 3
+    spatial, par = spatial_tucker_forms(kind, basis, dims, 2, 4)
+    forms = fourier_forms(spatial, par)
+    _, _, blocks = orc.component_table(kind, basis)
+    spec = [orc.decompress_tucker((m1, m2, m3), f).reshape(m3, m2, m1) for f in forms]
+    x = random_field(basis, dims, 8)
+    k0, nk = slab_planes(n3, rank, world)
+    np2 = m2 // world
+    xl = local_slab(x, S, n3, n1 * n2, rank, world).reshape(S, nk, n2, n1)
+    # stage 1: axis-1/2 FFTs of the local z-slab, blocked by destination rank
+    xa = np.zeros((S, nk, m2, m1), complex)
+    xa[:, :, :n2, :n1] = xl
+    xa = np.fft.fft2(xa, axes=(2, 3))
+    send = np.stack([xa[:, :, qq * np2:(qq + 1) * np2, :] for qq in range(world)]).reshape(-1)
+    recv = torch.empty(send.size, dtype=torch.complex128)
+    dist.all_to_all_single(recv, torch.from_numpy(send))
+    # stage 2: this rank's axis-2 rows, all k: axis-3 FFT, Hadamard, IFFT, crop
+    blk = recv.numpy().reshape(world, S, nk, np2, m1)
+    xp = np.zeros((S, m3, np2, m1), complex)
+    xp[:, :n3] = blk.transpose(1, 0, 2, 3, 4).reshape(S, n3, np2, m1)
+    xp = np.fft.fft(xp, axis=1)
+    rows = slice(rank * np2, (rank + 1) * np2)
+    yp = np.zeros_like(xp)
+    for t, s_, c, coef in blocks:
+        yp[t] += coef * spec[c][:, rows, :] * xp[s_]
+    yp = np.fft.ifft(yp, axis=1)[:, :n3]
+    out = np.stack([yp[:, r * nk:(r + 1) * nk] for r in range(world)]).reshape(-1)
+    back = torch.empty(out.size, dtype=torch.complex128)
+    dist.all_to_all_single(back, torch.from_numpy(out))
+    # stage 3: inverse axis-2/1 FFTs of the local z-slab, crop
+    ya = back.numpy().reshape(world, S, nk, np2, m1).transpose(1, 2, 0, 3, 4).reshape(S, nk, m2, m1)
+    yl = np.fft.ifft2(ya, axes=(2, 3))[:, :, :n2, :n1]
+    gathered = [torch.empty(yl.size, dtype=torch.complex128) for _ in range(world)]
+    dist.all_gather(gathered, torch.from_numpy(np.ascontiguousarray(yl).reshape(-1)))
+    if rank == 0:
+        y = np.concatenate([g.numpy().reshape(S, nk, n1 * n2) for g in gathered], axis=1).reshape(-1)
+        ref = orc.apply_operator_tucker(kind, basis, dims, forms, x)
+        q.put(np.linalg.norm(y - ref) / np.linalg.norm(ref))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_decomposition_exchange_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    err = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert err < 1e-12
