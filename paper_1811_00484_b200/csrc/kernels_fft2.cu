@@ -359,7 +359,7 @@ bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw,
   P.dR0.init(static_cast<uint32_t>(R0));
   P.dR1.init(static_cast<uint32_t>(R1));
   const int widest = std::max(R0, R1);
-  P.lines = R1 == 1 ? 64 : std::max(1, (row_lines > 0 ? row_lines : 160 / widest));  // 8 rows at m = 400 (measured best)
+  P.lines = R1 == 1 ? 64 : std::max(1, (row_lines > 0 ? row_lines : 120 / widest));  // 6 rows at m = 400 (measured best)
   return true;
 }
 
