@@ -116,7 +116,7 @@ struct vie_op_s {
   FftPlan P1{}, P2{}, P3{}, PH{};
   vie::Pass2 Q1{}, Q2{};           // register-staged two-stage row / column passes
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
-  bool pencil2 = false;         // compile-time-shaped pencil kernel for this n3
+  bool pencil2 = false;         // compile-time-shaped two-branch pencil kernel for this n3
   int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
   // slab decomposition (vie_op_set_partition): this rank's z-planes [k0, k0 + nk) and
   // axis-2 rows [p2off, p2off + np2) of the spectral slabs
@@ -186,6 +186,7 @@ constexpr bool kPass2 = VIE_PASS2;
 #define VIE_PENCIL2 1
 #endif
 constexpr bool kPencil2 = VIE_PENCIL2;
+
 int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -670,6 +671,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     g.m3 = 2 * g.n3;
     g.S = basis == 0 ? 3 : 12;
     g.NC = static_cast<int>(cs.size());
+    g.snat = 0;
     g.nk = g.n3;  // one slab block (vie_op_set_partition re-blocks for the slab-decomposed matvec)
     g.np2 = g.m2;
     g.p2off = 0;

@@ -30,6 +30,7 @@ struct Geom {
   int np2;         // axis-2 rows per block
   int p2off;       // first global axis-2 position of this rank's pencil rows
   int64_t bps;     // plane stride = np2 * m1
+  int snat;        // octant spectra f3o order: 0 branch-major (even, then odd: kernels_pencil/2), 1 natural (pencil3)
 };
 
 // Tuning constants.
@@ -57,6 +58,7 @@ void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, doubl
 // the first (frequencies 0 and n1 pair differently), which launch_pencil
 // covers with groups = 1.  Returns false (nothing launched) if unsupported.
 bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
+
 void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
                     const double2* twm3, cudaStream_t st);
 // B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
