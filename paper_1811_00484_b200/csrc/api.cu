@@ -431,10 +431,15 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
     VIE_CUDA_CHECK(cudaEventRecord(op->ev[0], st));
   }
   int k = 1;
+  // profiling 1: serial stages, one event interval each; 2: the normal overlapped
+  // schedule with events after the column pass, after the decompression join and at the end
   auto mark = [&] {
-    if (op->profiling) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
+    if (op->profiling == 1) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
   };
-  const bool overlap = !op->profiling;
+  auto mark2 = [&] {
+    if (op->profiling == 2) VIE_CUDA_CHECK(cudaEventRecord(op->ev[k++], st));
+  };
+  const bool overlap = op->profiling != 1;
   if (overlap && !decomp_forked && op->fork_after == 0) fork_decomp(op, st);
   if (op->q1) vie::launch_row_fwd2(x, op->A, g, op->Q1, st);
   else vie::launch_row_fwd(x, op->A, g, op->P1, st);
@@ -444,8 +449,10 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   else vie::launch_col_fwd(op->A, op->B, g, op->P2, st);
   if (overlap && !decomp_forked && op->fork_after >= 2) fork_decomp(op, st);
   mark();
+  mark2();
   if (overlap) {
     VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
+    mark2();
   } else {
     if (decomp_forked) VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
     else vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
@@ -466,6 +473,7 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   if (op->q1) vie::launch_row_inv2(op->A, y, g, op->Q1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
   else vie::launch_row_inv(op->A, y, g, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
   mark();
+  mark2();
   // row, column, (decomp_z + decomp), pencil (+ edge), column, row
   op->last_launches = 7 + (op->pencil2 ? 1 : 0);
   if (op->profiling) {
@@ -1142,7 +1150,7 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
 int vie_op_set_profiling(vie_op op, int enable) {
   return guard([&] {
     if (!op) throw Invalid("vie_op_set_profiling: null operator");
-    op->profiling = enable ? 1 : 0;
+    op->profiling = enable == 2 ? 2 : (enable ? 1 : 0);
   });
 }
 

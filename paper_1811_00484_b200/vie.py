@@ -209,8 +209,10 @@ class EmbeddedSpectrum:
         _check(lib().vie_op_info(self.handle, None, None, C.byref(ws)))
         return ws.value
 
-    def set_profiling(self, on: bool):
-        _check(lib().vie_op_set_profiling(self.handle, int(bool(on))))
+    def set_profiling(self, on):
+        """True/1: serial stages with per-kernel event times; 2: the overlapped schedule with
+        events after the forward passes, after the decompression join and at the end."""
+        _check(lib().vie_op_set_profiling(self.handle, 2 if on == 2 else int(bool(on))))
 
     def last_stats(self):
         n = C.c_int()
