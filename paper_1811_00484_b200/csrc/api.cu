@@ -679,7 +679,6 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     g.m3 = 2 * g.n3;
     g.S = basis == 0 ? 3 : 12;
     g.NC = static_cast<int>(cs.size());
-    g.snat = 0;
     g.nk = g.n3;  // one slab block (vie_op_set_partition re-blocks for the slab-decomposed matvec)
     g.np2 = g.m2;
     g.p2off = 0;

@@ -30,7 +30,6 @@ struct Geom {
   int np2;         // axis-2 rows per block
   int p2off;       // first global axis-2 position of this rank's pencil rows
   int64_t bps;     // plane stride = np2 * m1
-  int snat;        // octant spectra f3o order: 0 branch-major (even, then odd: kernels_pencil/2), 1 natural (pencil3)
 };
 
 // Tuning constants.

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
 #pragma unroll
         for (int j = 0; j < kQ; ++j) {
           const int f = fb + lane + 32 * j;
-          if (f < n3p) dst[geo.snat ? f : ((f & 1) ? E + (f >> 1) : (f >> 1))] = acc[i][j];
+          if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = acc[i][j];
         }
       }
     }
@@ -259,8 +259,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
           for (int j = 0; j < 2; ++j) {
             // columns f = 2 hb + h: even f (h = 0) at hb, odd f at E + hb (branch-major)
             const int hb = ct * 8 + j * 4 + fk;
-            if (2 * hb < n3p) dst[geo.snat ? 2 * hb : hb] = make_double2(accr[i][j][0], acci[i][j][0]);
-            if (2 * hb + 1 < n3p) dst[geo.snat ? 2 * hb + 1 : E + hb] = make_double2(accr[i][j][1], acci[i][j][1]);
+            if (2 * hb < n3p) dst[hb] = make_double2(accr[i][j][0], acci[i][j][0]);
+            if (2 * hb + 1 < n3p) dst[E + hb] = make_double2(accr[i][j][1], acci[i][j][1]);
           }
         }
       }
