@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
 // Fragment smem layout [row][Kp] with Kp = 4 (mod 8): conflict-free quarter-warps.
 constexpr int kMmaMC = 64;   // rows (p1o) per T chunk
 constexpr int kMmaPP = 4;    // p2o values per CTA (U3 reuse)
+constexpr int kZS = 34;      // Z row stride (== 2 mod 8: conflict-free B fragments over k)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -158,17 +159,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
   const int r1 = cd.r1, r3 = cd.r3;
   const int n1p = geo.n1 + 1, n3p = geo.n3 + 1;
   const int Kp = mma_kp(r3);
+  const int KA = mma_kp(r1);  // T = U1 Z inner dimension (padded)
   const int NPad = (n3p + 15) / 16 * 16;
   double2* us = sm;                                    // [NPad][Kp]  B operand (U3)
-  double2* zs = us + static_cast<int64_t>(NPad) * Kp;  // [r1][r3]
-  double2* ts = zs + r1 * r3;                          // [kMmaMC][Kp] A operand (T chunk)
-  double2* u1s = ts + kMmaMC * Kp;                     // [r1][kMmaMC] U1 rows of the chunk
+  double2* zs = us + static_cast<int64_t>(NPad) * Kp;  // [KA][kZS]   B operand of T (Z, zero padded)
+  double2* ts = zs + KA * kZS;                         // [kMmaMC][Kp] A operand (T chunk)
+  double2* u1s = ts + kMmaMC * Kp;                     // [kMmaMC][KA] A operand of T (U1 rows)
   const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major
   for (int e = threadIdx.x; e < NPad * Kp; e += blockDim.x) {
     const int n = e / Kp, k = e - n * Kp;
     if (n < n3p && k < r3) cp_async16(us + e, u3 + n + static_cast<int64_t>(n3p) * k);
     else us[e] = make_double2(0.0, 0.0);
   }
+  for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) zs[e] = make_double2(0.0, 0.0);  // pads
+  for (int e = threadIdx.x; e < kMmaMC * KA; e += blockDim.x) u1s[e] = make_double2(0.0, 0.0);
+  __syncthreads();
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), col / k (B)
@@ -178,35 +183,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
   for (int p2o = p2lo + blockIdx.y * kMmaPP; p2o < p2end; ++p2o) {
     __syncthreads();  // previous p2o done with zs / ts
     const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;
-    for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) cp_async16(zs + e, zsrc + e);
+    for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) {
+      const int a = e / r3, gcol = e - a * r3;
+      cp_async16(zs + a * kZS + gcol, zsrc + e);
+    }
     for (int m0 = 0; m0 < n1p; m0 += kMmaMC) {
       if (m0) __syncthreads();  // previous chunk's GEMM done with ts / u1s
       for (int e = threadIdx.x; e < r1 * kMmaMC; e += blockDim.x) {
         const int a = e / kMmaMC, i = e - a * kMmaMC;
-        if (m0 + i < n1p) cp_async16(u1s + e, u1 + (m0 + i) + static_cast<int64_t>(n1p) * a);
+        if (m0 + i < n1p) cp_async16(u1s + i * KA + a, u1 + (m0 + i) + static_cast<int64_t>(n1p) * a);
       }
       cp_async_wait_all_d();
       __syncthreads();
       {
-        // T chunk = U1 rows x Z: lane -> column g (Z value reused over 8 rows), warp -> rows
-        // i = warp + 8 q (U1 value broadcast), 8 independent accumulator chains per thread
-        static_assert(kThreads == 256 && kMmaMC == 64, "T-chunk thread map");
-        for (int g = lane; g < Kp; g += 32) {
-          double2 acc[8];
+        // T chunk = U1 rows x Z on the tensor cores: one 16 x 16 tile per warp
+        // (kMmaMC / 16 row tiles x 2 column tiles of the <= 32 Z columns), 3M product
+        static_assert(kMmaMC / 16 * 2 == kThreads / 32, "one T tile per warp");
+        const int rt = warp >> 1, ct = warp & 1;
+        double p1[2][2][2] = {}, p2[2][2][2] = {}, p3[2][2][2] = {};
+        const double2* ta = u1s + (rt * 16 + fr) * KA + fk;
+        const double2* zb = zs + fk * kZS + ct * 16 + fr;
+        for (int k0 = 0; k0 < KA; k0 += 4) {
+          const double2 av[2] = {ta[k0], ta[8 * KA + k0]};
+          const double2 bv[2] = {zb[k0 * kZS], zb[k0 * kZS + 8]};
+          const double as[2] = {av[0].x + av[0].y, av[1].x + av[1].y};
+          const double bs[2] = {bv[0].x + bv[0].y, bv[1].x + bv[1].y};
 #pragma unroll
-          for (int q = 0; q < 8; ++q) acc[q] = make_double2(0.0, 0.0);
-          if (g < r3) {
-            for (int a = 0; a < r1; ++a) {
-              const double2 z = zs[a * r3 + g];
+          for (int i = 0; i < 2; ++i)
 #pragma unroll
-              for (int q = 0; q < 8; ++q) cfma(acc[q], u1s[a * kMmaMC + warp + 8 * q], z);
+            for (int j = 0; j < 2; ++j) dmma(p1[i][j][0], p1[i][j][1], av[i].x, bv[j].x);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma(p2[i][j][0], p2[i][j][1], av[i].y, bv[j].y);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dmma(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int row = rt * 16 + i * 8 + fr;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int col = ct * 16 + j * 8 + 2 * fk + h;
+              if (col < Kp)
+                ts[row * Kp + col] = make_double2(p1[i][j][h] - p2[i][j][h], p3[i][j][h] - p1[i][j][h] - p2[i][j][h]);
             }
-          }
-#pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const int i = warp + 8 * q;
-            ts[i * Kp + g] = (m0 + i < n1p) ? acc[q] : make_double2(0.0, 0.0);
-          }
         }
       }
       __syncthreads();
@@ -292,10 +317,11 @@ __global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, 
 
 size_t decomp_mma_smem(int n1, int n3, int rmax) {
   (void)n1;
+  if (rmax > 28) return static_cast<size_t>(-1);  // T tiles cover <= 32 columns, Kp <= 28 (else the FMA kernel)
   const int kp = mma_kp(rmax);
   const size_t npad = static_cast<size_t>((n3 + 1 + 15) / 16 * 16);
-  return sizeof(double2) * (npad * kp + static_cast<size_t>(rmax) * rmax + static_cast<size_t>(kMmaMC) * kp +
-                            static_cast<size_t>(rmax) * kMmaMC);
+  return sizeof(double2) * (npad * kp + static_cast<size_t>(kp) * kZS + static_cast<size_t>(kMmaMC) * kp +
+                            static_cast<size_t>(kMmaMC) * kp);
 }
 
 size_t decomp_smem(int n3, int rmax) {
