@@ -164,7 +164,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
   double2* us = sm;                                    // [NPad][Kp]  B operand (U3)
   double2* zs = us + static_cast<int64_t>(NPad) * Kp;  // [KA][kZS]   B operand of T (Z, zero padded)
   double2* ts = zs + KA * kZS;                         // [kMmaMC][Kp] A operand (T chunk)
-  double2* u1s = ts + kMmaMC * Kp;                     // [kMmaMC][KA] A operand of T (U1 rows)
+  const int NPad1 = (n1p + 15) / 16 * 16;
+  double2* u1s = ts + kMmaMC * Kp;                     // [NPad1][KA] A operand of T: all of U1, staged once
   const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major
   for (int e = threadIdx.x; e < NPad * Kp; e += blockDim.x) {
     const int n = e / Kp, k = e - n * Kp;
@@ -172,38 +173,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
     else us[e] = make_double2(0.0, 0.0);
   }
   for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) zs[e] = make_double2(0.0, 0.0);  // pads
-  for (int e = threadIdx.x; e < kMmaMC * KA; e += blockDim.x) u1s[e] = make_double2(0.0, 0.0);
-  __syncthreads();
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
-  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), col / k (B)
-  const int E = geo.n3 / 2 + 1;
-  const int nct = NPad / 16;
-  const int p2end = min(p2hi, p2lo + (static_cast<int>(blockIdx.y) + 1) * kMmaPP);
-  for (int p2o = p2lo + blockIdx.y * kMmaPP; p2o < p2end; ++p2o) {
-    __syncthreads();  // previous p2o done with zs / ts
+  for (int e = threadIdx.x; e < NPad1 * KA; e += blockDim.x) {
+    const int a = e / NPad1, i = e - a * NPad1;  // i fastest: coalesced column reads
+    if (a < KA) {
+      if (i < n1p && a < r1) cp_async16(u1s + i * KA + a, u1 + i + static_cast<int64_t>(n1p) * a);
+      else u1s[i * KA + a] = make_double2(0.0, 0.0);
+    }
+  }
+  auto load_z = [&](int p2o) {
     const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;
     for (int e = threadIdx.x; e < r1 * r3; e += blockDim.x) {
       const int a = e / r3, gcol = e - a * r3;
       cp_async16(zs + a * kZS + gcol, zsrc + e);
     }
+  };
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), col / k (B)
+  const int E = geo.n3 / 2 + 1;
+  const int nct = NPad / 16;
+  const int p2end = min(p2hi, p2lo + (static_cast<int>(blockIdx.y) + 1) * kMmaPP);
+  const int p2beg = p2lo + blockIdx.y * kMmaPP;
+  if (p2beg < p2end) load_z(p2beg);
+  for (int p2o = p2beg; p2o < p2end; ++p2o) {
+    cp_async_wait_all_d();  // U3, U1 (first p2o) and this p2o's Z landed
+    __syncthreads();
     for (int m0 = 0; m0 < n1p; m0 += kMmaMC) {
-      if (m0) __syncthreads();  // previous chunk's GEMM done with ts / u1s
-      for (int e = threadIdx.x; e < r1 * kMmaMC; e += blockDim.x) {
-        const int a = e / kMmaMC, i = e - a * kMmaMC;
-        if (m0 + i < n1p) cp_async16(u1s + i * KA + a, u1 + (m0 + i) + static_cast<int64_t>(n1p) * a);
-      }
-      cp_async_wait_all_d();
-      __syncthreads();
+      if (m0) __syncthreads();  // previous chunk's GEMM done with ts
       {
         // T chunk = U1 rows x Z on the tensor cores: one 16 x 16 tile per warp
         // (kMmaMC / 16 row tiles x 2 column tiles of the <= 32 Z columns), 3M product
         static_assert(kMmaMC / 16 * 2 == kThreads / 32, "one T tile per warp");
         const int rt = warp >> 1, ct = warp & 1;
+        const bool tile_ok = m0 + rt * 16 < NPad1;  // rows past U1's padded end are never used
         double p1[2][2][2] = {}, p2[2][2][2] = {}, p3[2][2][2] = {};
-        const double2* ta = u1s + (rt * 16 + fr) * KA + fk;
+        const double2* ta = u1s + (m0 + rt * 16 + fr) * KA + fk;
         const double2* zb = zs + fk * kZS + ct * 16 + fr;
-        for (int k0 = 0; k0 < KA; k0 += 4) {
+        for (int k0 = 0; tile_ok && k0 < KA; k0 += 4) {
           const double2 av[2] = {ta[k0], ta[8 * KA + k0]};
           const double2 bv[2] = {zb[k0 * kZS], zb[k0 * kZS + 8]};
           const double as[2] = {av[0].x + av[0].y, av[1].x + av[1].y};
@@ -235,6 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
         }
       }
       __syncthreads();
+      if (m0 + kMmaMC >= n1p && p2o + 1 < p2end) load_z(p2o + 1);  // zs free: lands during the GEMM
       const int nrt = (min(kMmaMC, n1p - m0) + 15) / 16;
       for (int t = warp; t < nrt * nct; t += nwarp) {
         const int rt = t / nct, ct = t - rt * nct;
@@ -316,12 +323,12 @@ __global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, 
 }  // namespace
 
 size_t decomp_mma_smem(int n1, int n3, int rmax) {
-  (void)n1;
   if (rmax > 28) return static_cast<size_t>(-1);  // T tiles cover <= 32 columns, Kp <= 28 (else the FMA kernel)
   const int kp = mma_kp(rmax);
   const size_t npad = static_cast<size_t>((n3 + 1 + 15) / 16 * 16);
+  const size_t npad1 = static_cast<size_t>((n1 + 1 + 15) / 16 * 16);
   return sizeof(double2) * (npad * kp + static_cast<size_t>(kp) * kZS + static_cast<size_t>(kMmaMC) * kp +
-                            static_cast<size_t>(kMmaMC) * kp);
+                            npad1 * kp);
 }
 
 size_t decomp_smem(int n3, int rmax) {
