@@ -132,7 +132,10 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
 // A operand, then S^ = T U3^T as a complex GEMM = 3 real DMMAs per 8x8x4 step (Gauss).
 // Fragment smem layout [row][Kp] with Kp = 4 (mod 8): conflict-free quarter-warps.
 constexpr int kMmaMC = 64;   // rows (p1o) per T chunk
-constexpr int kMmaPP = 4;    // p2o values per CTA (U3 reuse)
+#ifndef VIE_DECOMP_PP
+#define VIE_DECOMP_PP 4
+#endif
+constexpr int kMmaPP = VIE_DECOMP_PP;  // p2o values per CTA (U3 / U1 staging reuse)
 constexpr int kZS = 34;      // Z row stride (== 2 mod 8: conflict-free B fragments over k)
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
