@@ -90,6 +90,25 @@ def test_matvec_pencil2_shapes(vie, dft, orc, kind, basis, dims, rank):
     assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims)
 
 
+# kernel-path coverage: rank > 28 (FMA decompression fallback), an axis length without a
+# two-stage plan (m = 250 = 2 x 5^3: generic multi-stage passes), and n3 without a compiled
+# pencil shape (generic pencil kernel)
+PATH_CASES = [
+    (N, PWC, (6, 5, 7), 30),     # rank 30: k_decomp_s (FMA) instead of the DMMA kernel
+    (N, PWC, (125, 4, 3), 2),    # m1 = 250: generic row passes (three-stage plan)
+    (N, PWL, (4, 125, 3), 2),    # m2 = 250: generic column passes
+    (K, PWL, (3, 4, 9), 3),      # n3 = 9: no compiled pencil shape, generic pencil kernel
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", PATH_CASES)
+def test_matvec_kernel_paths(vie, dft, orc, kind, basis, dims, rank):
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 31 + sum(dims))
+    x = random_field(basis, dims, 5)
+    y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+    assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims, rank)
+
+
 def test_matvec_c1_cube_pwl(vie, dft, orc):
     # BASELINE configs[0]: 32^3 PWL grid, r = 25 (CPU-runnable reference case)
     dims = (32, 32, 32)
