@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--config", default="head_1mm", choices=sorted(CONFIGS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
     return ap.parse_args()
 
 
@@ -217,6 +218,63 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ solve time
+def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=200):
+    """Solve time (north star: matvecs/s AND solve time): restarted GMRES(50) to 1e-6 on
+    the PWL system at 64^3 (BASELINE configs[1]), device resident (vie_gmres_solve).
+    Synthetic rank-25 forms are scaled so |(eps - 1) N| ~ 0.2 min|eps g| (a well-posed
+    perturbation of the PWL Gram term); eps = 1 + U(1,5) - i U(0,1)."""
+    from tests.helpers import spatial_tucker_forms
+
+    grid, basis, r = (64, 64, 64), 1, 25
+    S = vie.ncur(basis)
+    nv = int(np.prod(grid))
+    comps, _, _ = vie.component_table(0, basis)
+    spatial, par = spatial_tucker_forms(0, basis, grid, r, 4321)
+
+    def build(scale):
+        forms = [vie.TuckerForm(dft, grid, spatial[c][0] * scale, spatial[c][1], par[c]) for c in range(len(comps))]
+        return vie.build_operator_spectra(0, basis, grid, comps, forms, dft), forms
+
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(S * nv, dtype=torch.complex128, device="cuda", generator=g)
+    op1, _ = build(1.0)
+    rho = float(torch.linalg.vector_norm(vie.apply_operator(op1, x)) / torch.linalg.vector_norm(x))
+    del op1
+    scale = 0.2 * (2.0 / 12.0) / (5.0 * max(rho, 1e-300))  # max|eps - 1| = 5, min|eps g| = 2/12
+    op, forms = build(scale)
+    rng = np.random.default_rng(5)
+    eps = torch.from_numpy(1 + rng.uniform(1, 5, nv) - 1j * rng.uniform(0, 1, nv)).cuda()
+    rhs = torch.randn(S * nv, dtype=torch.complex128, device="cuda", generator=g)
+    cfg = vie.GmresConfig(tol, inner, outer)
+    vie.gmres(op, eps, 1.0, rhs, vie.GmresConfig(tol, 2, 1))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = vie.gmres(op, eps, 1.0, rhs, cfg)
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    out = {"config": "cube_64: 64^3 PWL N system (BASELINE configs[1]), 60 components rank 25, synthetic",
+           "solver": f"restarted GMRES({inner}) to {tol}, device resident (vie_gmres_solve)",
+           "iterations": res.iterations, "converged": res.converged,
+           "final_relative_residual": res.final_relative_residual, "seconds": t,
+           "ms_per_iteration": 1e3 * t / max(res.iterations, 1)}
+    if with_cpu:  # the oracle's GMRES on the same system, bounded: 2 iterations, per-iteration time
+        from oracle import oracle as orc
+        from tests.helpers import fourier_forms
+
+        scaled = [(core * scale, us) for core, us in spatial]
+        of = fourier_forms(scaled, par)
+        orc.set_threads(os.cpu_count() or 1)
+        t0 = time.perf_counter()
+        ref = orc.gmres_system_tucker(basis, grid, of, eps.cpu().numpy(), 1.0, rhs.cpu().numpy(), tol=tol,
+                                      inner=2, outer=1)
+        tc = (time.perf_counter() - t0) / max(ref.iterations, 1)
+        out["cpu_oracle_ms_per_iteration"] = 1e3 * tc
+        out["cpu_oracle_cores"] = os.cpu_count() or 1
+        out["cpu_oracle_solve_seconds_estimate"] = tc * res.iterations
+    return out
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args):
     import torch
@@ -365,6 +423,10 @@ def run_b200(args):
         cpu = {"value": v, "unit": "matvecs/s", "cores": threads, "kind": "port", "sample": info["sample"],
                "detail": info}
 
+    solve = None
+    if rank == 0 and world == 1 and not args.no_solve:
+        solve = gmres_solve_bench(vie, dft, torch, with_cpu=not args.no_cpu_baseline)
+
     fl = flops_model(grid, basis, nc, r)
     if rank == 0:
         line = {
@@ -398,6 +460,7 @@ def run_b200(args):
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "gmres_solve": solve,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:
