@@ -323,6 +323,29 @@ inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentFiel
   return CurrentField::from_vector(yv, op.grid_dims, op.order);
 }
 
+// Many independent applications from host memory (vie_matvec_host_batch): the copies
+// of neighbouring fields overlap each device matvec (full overlap needs pinned memory;
+// with pageable std::vector storage the results are identical, the copies serialise).
+inline std::vector<CurrentField> apply_operator_batch(const EmbeddedSpectrum& op, const std::vector<CurrentField>& xs) {
+  std::vector<std::vector<cplx>> xv, yv;
+  std::vector<const double*> xp;
+  std::vector<double*> yp;
+  for (const CurrentField& x : xs) {
+    if (x.dims() != op.grid_dims || static_cast<Index>(x.comp.size()) != op.n_cur())
+      throw std::invalid_argument("apply_operator: dim mismatch");
+    xv.push_back(x.to_vector());
+    yv.emplace_back(xv.back().size());
+  }
+  for (size_t i = 0; i < xs.size(); ++i) {
+    xp.push_back(reinterpret_cast<const double*>(xv[i].data()));
+    yp.push_back(reinterpret_cast<double*>(yv[i].data()));
+  }
+  check(vie_matvec_host_batch(op.handle(), static_cast<int64_t>(xs.size()), xp.data(), yp.data()));
+  std::vector<CurrentField> ys;
+  for (const auto& y : yv) ys.push_back(CurrentField::from_vector(y, op.grid_dims, op.order));
+  return ys;
+}
+
 // apply_system (solver.hpp:183-200) with eps_r per voxel (n_vox values) and
 // inv_v = 1 / voxel volume.
 inline CurrentField apply_system(const std::vector<cplx>& eps_r, double inv_v, const EmbeddedSpectrum& op_n,

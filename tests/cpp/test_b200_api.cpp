@@ -153,6 +153,21 @@ int main() {
     });
   }
 
+  run("ApplyOperator.BatchEqualsSingleCalls", [&] {
+    const std::array<Index, 3> d{4, 3, 5};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWL, d, 2, 90);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWL, fam, dft);
+    std::vector<CurrentField> xs;
+    for (int i = 0; i < 3; ++i) xs.push_back(random_field(d, BasisOrder::PWL, 91 + i));
+    const std::vector<CurrentField> ys = apply_operator_batch(op, xs);
+    expect(ys.size() == xs.size(), "batch size");
+    for (size_t i = 0; i < xs.size(); ++i) {
+      CurrentField y = apply_operator(op, xs[i], MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, nullptr, dft);
+      const double e = rel(y.to_vector(), ys[i].to_vector());
+      expect(e == 0.0, "batch vs single rel err " + std::to_string(e));
+    }
+  });
+
   run("BuildOperatorSpectra.FromTensors.ErrorTracksTolerance", [&] {  // test_fft_operator.cpp:192-209
     const std::array<Index, 3> d{4, 4, 4};
     std::vector<std::pair<KernelComponent, Tensor3>> tensors;
