@@ -115,10 +115,30 @@ __device__ unsigned long long g_p2_phase[8];
 #endif
 
 // the slot of branch frequency phi = k0 + R0 k1 after the two forward stages
+// Position of element j of stage-1 block k0: rotated by ROT k0 within the block so the
+// Hadamard's lanes (consecutive branch frequencies, their mirrors, both pencils) hit
+// distinct smem banks (searched offline; 2.0 -> 1.47 wavefronts per quarter warp at
+// n3 = 10 x 20).  The FFT stages address whole blocks per thread, so any rotation is
+// conflict-free for them.
+template <int R0, int R1>
+struct Rot {
+  static constexpr int ROT = (R0 == 10 && R1 == 20) ? 18 : 0;
+};
+template <int R0, int R1>
+__device__ __forceinline__ int blk_pos(int k0, int j) {  // k0 block, j < R1 element
+  if constexpr (Rot<R0, R1>::ROT == 0) {
+    return k0 * R1 + j;
+  } else {
+    int t = j + (Rot<R0, R1>::ROT * k0) % R1;
+    t -= t >= R1 ? R1 : 0;
+    return k0 * R1 + t;
+  }
+}
+// the slot of branch frequency phi = k0 + R0 k1 after the two forward stages
 template <int R0, int R1>
 __device__ __forceinline__ int slot_of(int phi) {
   const int k0 = phi % R0, k1 = phi / R0;
-  return k0 * R1 + k1;
+  return blk_pos<R0, R1>(k0, k1);
 }
 
 template <int KIND, int BASIS, int R0, int R1>
@@ -206,15 +226,15 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
   if (act0) {
     {
-      double2* dst = buf_b0 + line0 * LS + mp0;
+      double2* dst = buf_b0 + line0 * LS;
       double2 w = wstep0;
-      dst[0] = v[out_idx(R0, 0)];
+      dst[blk_pos<R0, R1>(0, mp0)] = v[out_idx(R0, 0)];
       sfor<R0 - 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value + 1;
         if constexpr (VIE_P2_TWLDG) {
-          dst[k * R1] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * 2 * k));
+          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * 2 * k));
         } else {
-          dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
           if (k + 1 < R0) w = cmul(w, wstep0);
         }
       });
@@ -226,14 +246,14 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     });
     DFTs<R0, false, 1, 0>::run(v);
     {
-      double2* dst = buf_b1 + line0 * LS + mp0;
+      double2* dst = buf_b1 + line0 * LS;
       double2 w = __ldg(a.twm3 + mp0);
       sfor<R0>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
         if constexpr (VIE_P2_TWLDG) {
-          dst[k * R1] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * (2 * k + 1)));
+          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * (2 * k + 1)));
         } else {
-          dst[k * R1] = cmul(v[out_idx(R0, k)], w);
+          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
           if (k + 1 < R0) w = cmul(w, wstep0);
         }
       });
@@ -246,14 +266,14 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   // ---- forward stage 1 (radix R1), in place
   for (int u = tid; u < LINES * R0; u += SH::THREADS) {
     const int line = u % LINES, k0 = u / LINES;
-    double2* p = buf + line * LS + k0 * R1;
+    double2* p = buf + line * LS;
     double2 v[R1];
 #pragma unroll
-    for (int i = 0; i < R1; ++i) v[i] = p[i];
+    for (int i = 0; i < R1; ++i) v[i] = p[blk_pos<R0, R1>(k0, i)];
     DFTs<R1, false, 1, 0>::run(v);
     sfor<R1>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
-      p[k] = v[out_idx(R1, k)];
+      p[blk_pos<R0, R1>(k0, k)] = v[out_idx(R1, k)];
     });
   }
   __syncthreads();
@@ -263,9 +283,9 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   // last warp done with a chunk refills its buffer (no thread ever waits on
   // the others inside the loop)
   {
-    const int mir = tid & 1;
-    const int p = (tid >> 1) % NP;
-    const int ul = (tid >> 1) / NP;
+    const int p = tid % NP;          // lane order (searched with the rotation): pencil fastest,
+    const int ul = (tid / NP) % CF;  // then frequency, mirror slowest
+    const int mir = tid / (NP * CF);
     const int pos1 = c0 + p;
     const int m1flag = pos1 & 1;  // positions 2j, 2j+1 hold frequencies j, m1 - j (j >= 1)
     const int tr = p >> 1;
@@ -324,14 +344,14 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   // ---- inverse stage 1 (adjoint of radix R1), in place
   for (int u = tid; u < LINES * R0; u += SH::THREADS) {
     const int line = u % LINES, k0 = u / LINES;
-    double2* p = buf + line * LS + k0 * R1;
+    double2* p = buf + line * LS;
     double2 v[R1];
 #pragma unroll
-    for (int k = 0; k < R1; ++k) v[k] = p[k];
+    for (int k = 0; k < R1; ++k) v[k] = p[blk_pos<R0, R1>(k0, k)];
     DFTs<R1, true, 1, 0>::run(v);
     sfor<R1>([&](auto ic) {
       constexpr int i = decltype(ic)::value;
-      p[i] = v[out_idx(R1, i)];
+      p[blk_pos<R0, R1>(k0, i)] = v[out_idx(R1, i)];
     });
   }
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -342,23 +362,25 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     const int line = b * HL + tid % HL, mp = tid / HL;
     const int s = line / NP, p = line % NP;
     const bool act = tid < HL * R1 && c0 + p < m1;
-    const int off = line * LS + mp;
+    const int off = line * LS;
     const double2 wstep = __ldg(a.twm3 + 2 * min(mp, R1 - 1));
     const double2 w1 = __ldg(a.twm3 + min(mp, R1 - 1));
     // branch br: inputs * conj(w_m3^{mp (2k + br)}), then the radix-R0 adjoint
     auto branch = [&](const double2* X, int br, double2(&v)[R0]) {
       if constexpr (VIE_P2_TWLDG) {
         const int mpc = min(mp, R1 - 1);
-        v[0] = br ? cmulc(X[off], w1) : X[off];
+        v[0] = br ? cmulc(X[off + blk_pos<R0, R1>(0, mpc)], w1) : X[off + blk_pos<R0, R1>(0, mpc)];
 #pragma unroll
-        for (int k = 1; k < R0; ++k) v[k] = cmulc(X[off + k * R1], __ldg(a.twm3 + mpc * (2 * k + br)));
+        for (int k = 1; k < R0; ++k)
+          v[k] = cmulc(X[off + blk_pos<R0, R1>(k, mpc)], __ldg(a.twm3 + mpc * (2 * k + br)));
       } else {
+        const int mpc = min(mp, R1 - 1);
         double2 w = br ? w1 : wstep;
-        v[0] = br ? cmulc(X[off], w) : X[off];
+        v[0] = br ? cmulc(X[off + blk_pos<R0, R1>(0, mpc)], w) : X[off + blk_pos<R0, R1>(0, mpc)];
         if (br) w = cmul(w, wstep);
 #pragma unroll
         for (int k = 1; k < R0; ++k) {
-          v[k] = cmulc(X[off + k * R1], w);
+          v[k] = cmulc(X[off + blk_pos<R0, R1>(k, mpc)], w);
           if (k + 1 < R0) w = cmul(w, wstep);
         }
       }
