@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--slab", action="store_true", help="slab-decomposed path even on 1 GPU (exercise it)")
     return ap.parse_args()
 
 
@@ -302,7 +303,7 @@ def run_b200(args):
     nc = len(comps)
     # N > 1: slab decomposition (z-planes / axis-2 spectral rows, two NCCL all-to-alls per
     # matvec) when the grid splits evenly, else component sharding + NCCL all-reduce
-    slab = world > 1 and grid[2] % world == 0 and grid[1] % world == 0
+    slab = (world > 1 or args.slab) and grid[2] % world == 0 and grid[1] % world == 0
     mine = list(range(nc)) if (world == 1 or slab) else [c for c in range(nc) if c % world == rank]
     dft = vie.DftService(local)
     spatial, par = spatial_tucker_forms(0, basis, grid, r, 1234)
