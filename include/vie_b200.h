@@ -115,24 +115,25 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
 /* Timing helpers for the bench: number of kernels the last vie_matvec
  * launched, and per-stage device times (ms) of the last vie_matvec when
  * profiling was enabled with vie_op_set_profiling(op, 1).                   */
-/* ---- slab-decomposed matvec (multi-GPU; SURVEY 8(e) recommended partition) ----
+/* ---- slab-decomposed matvec (multi-GPU) ----
  * Rank r of R owns the z-planes [r nk, (r+1) nk) of x and y (nk = n3 / R) and the
- * axis-2 spectral rows [r np2, (r+1) np2) (np2 = 2 n2 / R) of the pencil stage.  One
- * matvec = slab_forward -> all-to-all (equal chunks of slab_elems / R) -> slab_pencil ->
- * all-to-all -> slab_inverse.  The exchanged buffers are blocked
- * [rank][s][k in block][axis-2 row in block][axis-1 position] so that the chunk for
- * rank q is contiguous (the caller runs the collective, e.g. NCCL all_to_all).
- * With R = 1 the three stages are vie_matvec split in three.                     */
+ * axis-1 spectral positions [r W, (r+1) W) (W = 2 n1 / R, whole pencil groups) of the
+ * axis-2 / axis-3 stages.  One matvec = slab_forward (axis-1 FFTs) -> all-to-all (equal
+ * chunks of slab_elems / R) -> slab_pencil (axis-2 FFTs, decompression of the rank's
+ * octant rows, fused axis-3 FFT / Hadamard / IFFT, inverse axis-2 FFTs) -> all-to-all ->
+ * slab_inverse (inverse axis-1 FFTs).  The exchanged buffers are blocked
+ * [rank][s][k in block][j][w < W] so the chunk for rank q is contiguous (the caller runs
+ * the collective, e.g. NCCL all_to_all).  With R = 1 the stages are vie_matvec in three. */
 int vie_op_set_partition(vie_op op, int nranks, int rank);
-/* x_elems = S n1 n2 nk (local x / y), slab_elems = S nk 2n2 2n1 (each exchange buffer),
+/* x_elems = S n1 n2 nk (local x / y), slab_elems = S nk n2 2n1 (each exchange buffer),
  * k0 = first z-plane of this rank, nk = z-planes per rank                         */
 int vie_slab_info(vie_op op, int64_t* x_elems, int64_t* slab_elems, int64_t* k0, int64_t* nk);
-/* axis-1/2 FFTs of the local z-slab x_local -> send (blocked by destination rank)  */
+/* axis-1 FFTs of the local z-slab x_local -> send (blocked by destination rank)      */
 int vie_slab_forward(vie_op op, const double* x_local, double* send, void* stream);
-/* decompression of this rank's octant rows + fused axis-3 FFT / Hadamard / IFFT:
- * recv (blocked by source rank) -> out (same blocking)                             */
+/* axis-2 FFTs of the rank's positions, decompression of its octant rows, fused
+ * axis-3 FFT / Hadamard / IFFT, inverse axis-2 FFTs: recv -> out (blocked by rank)   */
 int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream);
-/* inverse axis-2/1 FFTs, crop, 1/N_e -> y_local; with eps_local the apply_system
+/* inverse axis-1 FFTs, crop, 1/N_e -> y_local; with eps_local the apply_system
  * epilogue y = eps g x - (eps - 1) inv_v (N x) (x_local needed when diag_term)       */
 int vie_slab_inverse(vie_op op, const double* back, double* y_local, const double* eps_local, double inv_v,
                      const double* x_local, int diag_term, void* stream);

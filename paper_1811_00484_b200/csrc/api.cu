@@ -119,9 +119,8 @@ struct vie_op_s {
   bool pencil2 = false;         // compile-time-shaped two-branch pencil kernel for this n3
   int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
   // slab decomposition (vie_op_set_partition): this rank's z-planes [k0, k0 + nk) and
-  // axis-2 rows [p2off, p2off + np2) of the spectral slabs
+  // axis-1 positions [p1off, p1off + W) (Geom)
   int nranks = 1, rank = 0;
-  double2* As = nullptr;  // local axis-1 slab (S m1 n2 nk)
   // host-buffer staging (vie_matvec_host; the batch call double-buffers with hx2 / hy2)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -149,7 +148,7 @@ struct vie_op_s {
     for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
                     static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(hx2), static_cast<void*>(hy2),
-                    static_cast<void*>(V), static_cast<void*>(As),
+                    static_cast<void*>(V),
                     static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
       dev_free(p);
@@ -680,8 +679,8 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     g.S = basis == 0 ? 3 : 12;
     g.NC = static_cast<int>(cs.size());
     g.nk = g.n3;  // one slab block (vie_op_set_partition re-blocks for the slab-decomposed matvec)
-    g.np2 = g.m2;
-    g.p2off = 0;
+    g.W = g.m1;
+    g.p1off = 0;
     g.bps = static_cast<int64_t>(g.m1) * g.m2;
     op->comps_host.assign(cs.size(), CompDev{1, 1, 1, 0, 0, 0, 0, 0, 0});
     std::vector<const vie_tucker_s*> byc(cs.size(), nullptr);
@@ -805,34 +804,26 @@ int vie_matvec(vie_op op, const double* x, double* y, void* stream) {
 }
 
 // ---------------------------------------------------------------- slab decomposition
-namespace {
-Geom slab_geom_local(const vie_op op) {  // the rank's z-slab as a grid for the row/column passes
-  Geom gl = op->g;
-  gl.n3 = op->g.nk;
-  gl.m3 = 2 * op->g.nk;
-  return gl;
-}
-}  // namespace
 
 int vie_op_set_partition(vie_op op, int nranks, int rank) {
   return guard([&] {
     if (!op) throw Invalid("set_partition: null operator");
     if (nranks < 1 || rank < 0 || rank >= nranks) throw Invalid("set_partition: bad rank / size");
     Geom& g = op->g;
+    const int group = 2 * (g.S >= 12 ? 1 : (g.S >= 6 ? 2 : 4));  // axis-1 positions per pencil group (kernels_pencil.cu pencil_p1pairs)
     if (g.n3 % nranks) throw Invalid("set_partition: n3 must be divisible by the number of ranks");
-    if (g.m2 % (2 * nranks)) throw Invalid("set_partition: 2*n2 must split into an even number of rows per rank");
+    if (g.m1 % nranks || (g.m1 / nranks) % group)
+      throw Invalid("set_partition: 2*n1 must split into whole pencil groups per rank");
     if (nranks > 1 && !(op->q1 && op->q2))
-      throw Invalid("set_partition: axis lengths need two-stage plans for the blocked slab passes");
+      throw Invalid("set_partition: axis lengths need two-stage plans for the slab passes");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     VIE_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
     op->nranks = nranks;
     op->rank = rank;
     g.nk = g.n3 / nranks;
-    g.np2 = g.m2 / nranks;
-    g.p2off = rank * g.np2;
-    g.bps = static_cast<int64_t>(g.np2) * g.m1;
-    dev_free(op->As);
-    op->As = dev_alloc<double2>(static_cast<size_t>(g.S) * g.m1 * g.n2 * g.nk);
+    g.W = g.m1 / nranks;
+    g.p1off = rank * g.W;
+    g.bps = static_cast<int64_t>(g.m2) * g.W;
   });
 }
 
@@ -841,55 +832,69 @@ int vie_slab_info(vie_op op, int64_t* x_elems, int64_t* slab_elems, int64_t* k0,
     if (!op) throw Invalid("slab_info: null operator");
     const Geom& g = op->g;
     if (x_elems) *x_elems = static_cast<int64_t>(g.S) * g.n1 * g.n2 * g.nk;
-    if (slab_elems) *slab_elems = static_cast<int64_t>(g.S) * g.nk * g.m2 * g.m1;
+    if (slab_elems) *slab_elems = static_cast<int64_t>(g.S) * g.nk * g.n2 * g.m1;
     if (k0) *k0 = static_cast<int64_t>(op->rank) * g.nk;
     if (nk) *nk = g.nk;
   });
 }
 
+namespace {
+Geom slab_geom_rows(const vie_op op) {  // the rank's z-slab for the axis-1 passes
+  Geom gl = op->g;
+  gl.n3 = op->g.nk;
+  gl.m3 = 2 * op->g.nk;
+  return gl;
+}
+Geom slab_geom_cols(const vie_op op) {  // all k-planes (blocked by source rank) of the rank's W columns
+  Geom gc = op->g;
+  gc.nk = op->g.n3;
+  return gc;
+}
+}  // namespace
+
 int vie_slab_forward(vie_op op, const double* x_local, double* send, void* stream) {
   return guard([&] {
     if (!op || !x_local || !send) throw Invalid("slab_forward: null argument");
-    if (!op->As) throw Invalid("slab_forward: call vie_op_set_partition first");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     cudaStream_t st = pick_stream(op, stream);
-    const Geom gl = slab_geom_local(op);
+    const Geom gl = slab_geom_rows(op);
     const double2* x = reinterpret_cast<const double2*>(x_local);
-    double2* B = reinterpret_cast<double2*>(send);
-    if (op->q1) vie::launch_row_fwd2(x, op->As, gl, op->Q1, st);
-    else vie::launch_row_fwd(x, op->As, gl, op->P1, st);
-    if (op->q2) vie::launch_col_fwd2(op->As, B, gl, op->Q2, st);
-    else vie::launch_col_fwd(op->As, B, gl, op->P2, st);
+    double2* A = reinterpret_cast<double2*>(send);  // [q][s][k][j][W] (blocked by pencil rank)
+    if (op->q1) vie::launch_row_fwd2(x, A, gl, op->Q1, st);
+    else vie::launch_row_fwd(x, A, gl, op->P1, st);
   });
 }
 
 int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
   return guard([&] {
     if (!op || !recv || !out) throw Invalid("slab_pencil: null argument");
-    if (!op->As) throw Invalid("slab_pencil: call vie_op_set_partition first");
     if (recv == out) throw Invalid("slab_pencil: recv and out must not alias");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     cudaStream_t st = pick_stream(op, stream);
     const Geom& g = op->g;
-    // octant spectra rows of this rank's axis-2 positions: pairs (2j, 2j+1) -> row j,
-    // positions 0, 1 -> rows 0 and n2
-    const int lo = g.p2off / 2, hi = (g.p2off + g.np2) / 2;
-    if (op->nranks == 1) {
-      vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
-    } else {
-      vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, lo, hi);
-      if (g.p2off == 0)
-        vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, g.n2,
-                           g.n2 + 1, false);
-    }
-    const double2* Bin = reinterpret_cast<const double2*>(recv);
-    double2* Bout = reinterpret_cast<double2*>(out);
+    const Geom gc = slab_geom_cols(op);
+    // axis-2 FFTs of the rank's W columns over all k-planes: recv -> B
+    if (op->q2) vie::launch_col_fwd2(reinterpret_cast<const double2*>(recv), op->B, gc, op->Q2, st);
+    else vie::launch_col_fwd(reinterpret_cast<const double2*>(recv), op->B, gc, op->P2, st);
+    // octant spectra rows of this rank's axis-1 positions: pairs (2j, 2j+1) -> row j,
+    // positions 0, 1 -> rows 0 and n1
+    const int lo = g.p1off / 2, hi = (g.p1off + g.W) / 2;
+    vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
+                       true, lo, hi);
+    if (g.p1off == 0)
+      vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
+                         false, g.n1, g.n1 + 1);
     if (op->pencil2) {
-      vie::launch_pencil(op->kind, op->basis, Bin, Bout, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st, 1);
-      vie::launch_pencil2(op->kind, op->basis, Bin, Bout, op->Shat, g, op->P3.tw, st);
+      if (g.p1off == 0)
+        vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
+                           st, 1);
+      vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
     } else {
-      vie::launch_pencil(op->kind, op->basis, Bin, Bout, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st);
+      vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st);
     }
+    // inverse axis-2 FFTs: Bo -> out (blocked by z-slab rank)
+    if (op->q2) vie::launch_col_inv2(op->Bo, reinterpret_cast<double2*>(out), gc, op->Q2, st);
+    else vie::launch_col_inv(op->Bo, nullptr, reinterpret_cast<double2*>(out), gc, op->P2, st);
   });
 }
 
@@ -897,23 +902,20 @@ int vie_slab_inverse(vie_op op, const double* back, double* y_local, const doubl
                      const double* x_local, int diag_term, void* stream) {
   return guard([&] {
     if (!op || !back || !y_local) throw Invalid("slab_inverse: null argument");
-    if (!op->As) throw Invalid("slab_inverse: call vie_op_set_partition first");
     if (eps_local && op->kind != VIE_KIND_N) throw Invalid("apply_system: needs the N operator");
     if (eps_local && diag_term && !x_local) throw Invalid("apply_system: null argument");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     cudaStream_t st = pick_stream(op, stream);
-    const Geom gl = slab_geom_local(op);
+    const Geom gl = slab_geom_rows(op);
     const double ne = 8.0 * op->g.n1 * static_cast<double>(op->g.n2) * op->g.n3;  // global N_e
-    const double2* B = reinterpret_cast<const double2*>(back);
+    const double2* A = reinterpret_cast<const double2*>(back);
     double2* y = reinterpret_cast<double2*>(y_local);
-    if (op->q2) vie::launch_col_inv2(B, op->As, gl, op->Q2, st);
-    else vie::launch_col_inv(B, nullptr, op->As, gl, op->P2, st);
     const double2* eps = reinterpret_cast<const double2*>(eps_local);
     const double2* xin = reinterpret_cast<const double2*>(x_local);
     if (op->q1)
-      vie::launch_row_inv2(op->As, y, gl, op->Q1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
+      vie::launch_row_inv2(A, y, gl, op->Q1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
     else
-      vie::launch_row_inv(op->As, y, gl, op->P1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
+      vie::launch_row_inv(A, y, gl, op->P1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
   });
 }
 

@@ -21,15 +21,16 @@ struct Geom {
   int m1, m2, m3;  // embedded (2n)
   int S;           // current components (sources = targets)
   int NC;          // canonical component count
-  // Spectral slabs B, Bo (after the axis-1/2 FFTs) are blocked for the slab-decomposed
-  // multi-GPU matvec: [block][s][k in block][axis-2 row in block][pos1]
-  // with blocks of nk k-planes (forward/inverse passes: the block = destination rank of
-  // the axis-2 rows, q = pos2 / np2) or of np2 axis-2 rows (pencil stage: the block = source
-  // rank of the k-planes, r = k / nk).  One GPU: nk = n3, np2 = m2, p2off = 0, one block.
+  // Slab decomposition (multi-GPU): rank r of R owns the z-planes
+  // [r nk, (r+1) nk) for the axis-1 passes and the axis-1 positions [p1off, p1off + W) for
+  // the axis-2 passes, the decomposition rows and the pencil stage.  The exchanged slabs
+  // (after the axis-1 FFT) are blocked [rank][s][k in block][j][w < W]; the spectral slabs
+  // B, Bo of the pencil stage are [r][s][k in block][pos2][w < W] (block r = k / nk).
+  // One GPU: nk = n3, W = m1, p1off = 0, a single block.
   int nk;          // k-planes per block
-  int np2;         // axis-2 rows per block
-  int p2off;       // first global axis-2 position of this rank's pencil rows
-  int64_t bps;     // plane stride = np2 * m1
+  int W;           // axis-1 positions per rank (row length of the exchanged / spectral slabs)
+  int p1off;       // first global axis-1 position of this rank's W
+  int64_t bps;     // plane stride of B, Bo = m2 * W
 };
 
 // Tuning constants.
@@ -85,10 +86,11 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
 void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& P1, double scale,
                     const double2* eps, const double2* xin, double inv_v, int basis, int diag, cudaStream_t st);
 
-// Octant spectra rows p2o in [p2lo, p2hi) (p2hi < 0: all n2 + 1 rows); with_z: also Z = core x2 U2
+// Octant spectra rows p2o in [p2lo, p2hi) x p1o in [p1lo, p1hi) (hi < 0: all rows);
+// with_z: also Z = core x2 U2
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
                    double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo = 0, int p2hi = -1,
-                   bool with_z = true);
+                   bool with_z = true, int p1lo = 0, int p1hi = -1);
 
 // transform_factors on device: spatial factor (n x r, col-major) -> octant rows
 // (n+1) x r of the DFT of the parity embedding (operator.hpp:64-90).

@@ -55,7 +55,7 @@ constexpr int kQ = 4;     // micro-tile 4 x 4
 __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict__ forms,
                                                        const CompDev* __restrict__ comps,
                                                        const double2* __restrict__ Z, double2* __restrict__ Shat,
-                                                       Geom geo, int NC, int p2lo) {
+                                                       Geom geo, int NC, int p2lo, int p1lo, int p1hi) {
   extern __shared__ double2 sm[];
   const int c = blockIdx.x;
   const CompDev cd = comps[c];
@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
   const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major: u3[f + n3p*g]
   for (int e = threadIdx.x; e < r3 * n3p; e += blockDim.x) us[e] = u3[e];
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
-  for (int p10 = 0; p10 < n1p; p10 += kTP1) {
-    const int np1 = min(kTP1, n1p - p10);
+  for (int p10 = p1lo; p10 < p1hi; p10 += kTP1) {
+    const int np1 = min(kTP1, p1hi - p10);
     __syncthreads();
     for (int e = threadIdx.x; e < kTP1 * r3; e += blockDim.x) {
       const int i = e % kTP1, g = e / kTP1;
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
                                                               const CompDev* __restrict__ comps,
                                                               const double2* __restrict__ Z,
                                                               double2* __restrict__ Shat, Geom geo, int NC, int p2lo,
-                                                              int p2hi) {
+                                                              int p2hi, int p1lo, int p1hi) {
   extern __shared__ double2 sm[];
   const int c = blockIdx.x;
   const CompDev cd = comps[c];
@@ -201,8 +201,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
   for (int p2o = p2beg; p2o < p2end; ++p2o) {
     cp_async_wait_all_d();  // U3, U1 (first p2o) and this p2o's Z landed
     __syncthreads();
-    for (int m0 = 0; m0 < n1p; m0 += kMmaMC) {
-      if (m0) __syncthreads();  // previous chunk's GEMM done with ts
+    const int m0beg = p1lo / 16 * 16;  // chunks start on a 16-row tile (rows < p1lo are not stored)
+    for (int m0 = m0beg; m0 < p1hi; m0 += kMmaMC) {
+      if (m0 > m0beg) __syncthreads();  // previous chunk's GEMM done with ts
       {
         // T chunk = U1 rows x Z on the tensor cores: one 16 x 16 tile per warp
         // (kMmaMC / 16 row tiles x 2 column tiles of the <= 32 Z columns), 3M product
@@ -244,8 +245,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
         }
       }
       __syncthreads();
-      if (m0 + kMmaMC >= n1p && p2o + 1 < p2end) load_z(p2o + 1);  // zs free: lands during the GEMM
-      const int nrt = (min(kMmaMC, n1p - m0) + 15) / 16;
+      if (m0 + kMmaMC >= p1hi && p2o + 1 < p2end) load_z(p2o + 1);  // zs free: lands during the GEMM
+      const int nrt = (min(kMmaMC, p1hi - m0) + 15) / 16;
       for (int t = warp; t < nrt * nct; t += nwarp) {
         const int rt = t / nct, ct = t - rt * nct;
         // 3-multiplication complex product (Gauss): P1 = Ar Br, P2 = Ai Bi,
@@ -288,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_decomp_s_mma(const double2* __r
 #pragma unroll
         for (int i = 0; i < 2; ++i) {
           const int row = m0 + rt * 16 + i * 8 + fr;
-          if (row >= n1p) continue;
+          if (row >= p1hi || row < p1lo) continue;
           double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + row) * NC + c) * n3p;
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
@@ -340,10 +341,12 @@ size_t decomp_smem(int n3, int rmax) {
 }
 
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
-                   double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo, int p2hi, bool with_z) {
+                   double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo, int p2hi, bool with_z, int p1lo,
+                   int p1hi) {
   (void)comps_host;
   if (p2hi < 0) p2hi = g.n2 + 1;
-  if (p2hi <= p2lo) return;
+  if (p1hi < 0) p1hi = g.n1 + 1;
+  if (p2hi <= p2lo || p1hi <= p1lo) return;
   const size_t smz = sizeof(double2) * static_cast<size_t>(rmax) * rmax;
   VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_z),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smz)));
@@ -356,12 +359,12 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s_mma),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
     k_decomp_s_mma<<<dim3(g.NC, (p2hi - p2lo + kMmaPP - 1) / kMmaPP), kThreads, sms, st>>>(
-        forms, comps_dev, Z, Shat, g, g.NC, p2lo, p2hi);
+        forms, comps_dev, Z, Shat, g, g.NC, p2lo, p2hi, p1lo, p1hi);
   } else {
     const size_t smf = decomp_smem(g.n3, rmax);
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smf)));
-    k_decomp_s<<<dim3(g.NC, p2hi - p2lo), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC, p2lo);
+    k_decomp_s<<<dim3(g.NC, p2hi - p2lo), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC, p2lo, p1lo, p1hi);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }

@@ -120,21 +120,35 @@ __device__ __forceinline__ void inv_last(int mp, const double2* __restrict__ tw,
 }
 
 // -------------------------------------------------------------------- rows
+// Offset of (row, axis-1 position pos) in the spectral row slab A: rows of m on one GPU;
+// blocked by the pencil rank q = pos / W for the slab-decomposed matvec (Geom):
+// [q][row][pos - q W], blocks of nrows * W.
+template <bool BLOCKED>
+__device__ __forceinline__ int64_t arow(int row, int pos, int m, const FastDiv& dW, int64_t blk) {
+  if constexpr (!BLOCKED) {
+    return static_cast<int64_t>(row) * m + pos;
+  } else {
+    const int q = static_cast<int>(dW.div(static_cast<uint32_t>(pos)));
+    const int W = static_cast<int>(dW.d);
+    return q * blk + static_cast<int64_t>(row) * W + (pos - q * W);
+  }
+}
+
 // x: rows of n (voxel order) -> A: rows of m, mirror-paired spectral positions.
+template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__ x, double2* __restrict__ A,
-                                                     int nrows, Pass2 P) {
+                                                     int nrows, Pass2 P, FastDiv dW, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
   const int row0 = blockIdx.x * P.lines;
   const int nr = min(P.lines, nrows - row0);
   const double2* src = x + static_cast<int64_t>(row0) * n;
-  double2* dst = A + static_cast<int64_t>(row0) * m;
   if (R1 == 1) {  // single stage: no shared memory
     for (int r = threadIdx.x; r < nr; r += blockDim.x)
       even_dispatch(R0, [&](auto rc) {
         fwd_first<decltype(rc)::value>(
             0, P.tw, [&](int i) { return src[r * n + i]; },
-            [&](int k, double2 v) { dst[r * m + pos_of_freq(k, n)] = v; });
+            [&](int k, double2 v) { A[arow<BLOCKED>(row0 + r, pos_of_freq(k, n), m, dW, blk)] = v; });
       });
     return;
   }
@@ -152,10 +166,10 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__
   for (int u = threadIdx.x; u < nr * R0; u += blockDim.x) {
     const int r = static_cast<int>(P.dR0.div(u)), bk = u - r * R0;
     const double2* b = buf + r * ls + bk * R1p;
-    double2* d = dst + r * m;
     radix_dispatch(R1, [&](auto rc) {
-      plain_stage<decltype(rc)::value, false>([&](int i) { return b[i]; },
-                                              [&](int k, double2 v) { d[pos_of_freq(bk + R0 * k, n)] = v; });
+      plain_stage<decltype(rc)::value, false>(
+          [&](int i) { return b[i]; },
+          [&](int k, double2 v) { A[arow<BLOCKED>(row0 + r, pos_of_freq(bk + R0 * k, n), m, dW, blk)] = v; });
     });
   }
 }
@@ -186,19 +200,19 @@ struct RowEpi {
   }
 };
 
+template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__ A, double2* __restrict__ y,
-                                                     int nrows, Pass2 P, RowEpi epi) {
+                                                     int nrows, Pass2 P, RowEpi epi, FastDiv dW, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
   const int row0 = blockIdx.x * P.lines;
   const int nr = min(P.lines, nrows - row0);
-  const double2* src = A + static_cast<int64_t>(row0) * m;
   double2* dst = y + static_cast<int64_t>(row0) * n;
   if (R1 == 1) {
     for (int r = threadIdx.x; r < nr; r += blockDim.x)
       even_dispatch(R0, [&](auto rc) {
         inv_last<decltype(rc)::value>(
-            0, P.tw, [&](int k) { return src[r * m + pos_of_freq(k, n)]; },
+            0, P.tw, [&](int k) { return A[arow<BLOCKED>(row0 + r, pos_of_freq(k, n), m, dW, blk)]; },
             [&](int i, double2 v) { dst[r * n + i] = epi(v, row0 + r, i, n); });
       });
     return;
@@ -206,11 +220,11 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
   const int R1p = P.R1p, ls = P.ls;
   for (int u = threadIdx.x; u < nr * R0; u += blockDim.x) {
     const int r = static_cast<int>(P.dR0.div(u)), bk = u - r * R0;
-    const double2* s = src + r * m;
     double2* b = buf + r * ls + bk * R1p;
     radix_dispatch(R1, [&](auto rc) {
-      plain_stage<decltype(rc)::value, true>([&](int k) { return s[pos_of_freq(bk + R0 * k, n)]; },
-                                             [&](int i, double2 v) { b[i] = v; });
+      plain_stage<decltype(rc)::value, true>(
+          [&](int k) { return A[arow<BLOCKED>(row0 + r, pos_of_freq(bk + R0 * k, n), m, dW, blk)]; },
+          [&](int i, double2 v) { b[i] = v; });
     });
   }
   __syncthreads();
@@ -229,21 +243,12 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
 // -------------------------------------------------------------------- columns
 // A: planes of n2 rows x m1 -> B: planes of m2 rows x m1 (mirror-paired rows);
 // kColsPerCta consecutive columns per CTA, lanes over columns (128 B segments).
-// offset of axis-2 position pos in a blocked slab (Geom): block q = pos / np2
-template <bool BLOCKED>
-__device__ __forceinline__ int64_t slab_row(int pos, int m1, const FastDiv& dnp2, int64_t blk) {
-  if constexpr (!BLOCKED) return static_cast<int64_t>(pos) * m1;  // single block (one GPU)
-  const int q = static_cast<int>(dnp2.div(static_cast<uint32_t>(pos)));
-  return q * blk + static_cast<int64_t>(pos - q * static_cast<int>(dnp2.d)) * m1;
-}
-
 constexpr int kCW = kColsPerCta;
 static_assert((kCW & (kCW - 1)) == 0, "column tile must be a power of two");
 constexpr int kLgCW = kCW == 8 ? 3 : (kCW == 4 ? 2 : (kCW == 16 ? 4 : 0));
 
-template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
-                                                     Pass2 P, int64_t bps, FastDiv dnp2, int64_t blk) {
+                                                     Pass2 P, int64_t bps) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
@@ -257,7 +262,7 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
       even_dispatch(R0, [&](auto rc) {
         fwd_first<decltype(rc)::value>(
             0, P.tw, [&](int i) { return src[static_cast<int64_t>(i) * m1 + w]; },
-            [&](int k, double2 v) { dst[slab_row<BLOCKED>(pos_of_freq(k, n), m1, dnp2, blk) + w] = v; });
+            [&](int k, double2 v) { dst[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w] = v; });
       });
     return;
   }
@@ -282,14 +287,13 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
     radix_dispatch(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, false>(
           [&](int i) { return b[i]; },
-          [&](int k, double2 v) { d[slab_row<BLOCKED>(pos_of_freq(bk + R0 * k, n), m1, dnp2, blk)] = v; });
+          [&](int k, double2 v) { d[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1] = v; });
     });
   }
 }
 
-template <bool BLOCKED>
 __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
-                                                     Pass2 P, int64_t bps, FastDiv dnp2, int64_t blk) {
+                                                     Pass2 P, int64_t bps) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
@@ -302,7 +306,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     if (w < wc)
       even_dispatch(R0, [&](auto rc) {
         inv_last<decltype(rc)::value>(
-            0, P.tw, [&](int k) { return src[slab_row<BLOCKED>(pos_of_freq(k, n), m1, dnp2, blk) + w]; },
+            0, P.tw, [&](int k) { return src[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w]; },
             [&](int i, double2 v) { dst[static_cast<int64_t>(i) * m1 + w] = v; });
       });
     return;
@@ -315,7 +319,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     double2* b = buf + w * ls + bk * R1p;
     radix_dispatch(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, true>(
-          [&](int k) { return s[slab_row<BLOCKED>(pos_of_freq(bk + R0 * k, n), m1, dnp2, blk)]; },
+          [&](int k) { return s[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1]; },
           [&](int i, double2 v) { b[i] = v; });
     });
   }
@@ -366,9 +370,17 @@ bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw,
 void launch_row_fwd2(const double2* x, double2* A, const Geom& g, const Pass2& P, cudaStream_t st) {
   const int nrows = g.S * g.n2 * g.n3;
   const size_t sm = pass2_smem(P, P.lines);
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2), sm);
   const int threads = round_threads(P.R1 == 1 ? P.lines : P.lines * std::max(P.R0, P.R1));
-  k_row_fwd2<<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P);
+  FastDiv dW;
+  dW.init(static_cast<uint32_t>(g.W));
+  const int64_t blk = static_cast<int64_t>(nrows) * g.W;
+  if (g.W == g.m1) {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2<false>), sm);
+    k_row_fwd2<false><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P, dW, blk);
+  } else {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2<true>), sm);
+    k_row_fwd2<true><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P, dW, blk);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -376,46 +388,40 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
                      const double2* xin, double inv_v, int basis, int diag, cudaStream_t st) {
   const int nrows = g.S * g.n2 * g.n3;
   const size_t sm = pass2_smem(P, P.lines);
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2), sm);
   RowEpi epi{scale, eps, xin, inv_v, basis == 1 ? 1 : 0, diag, g.n2 * g.n3,
              static_cast<int64_t>(g.n1) * g.n2 * g.n3, {}};
   epi.drpc.init(static_cast<uint32_t>(g.n2 * g.n3));
   const int threads = round_threads(P.R1 == 1 ? P.lines : P.lines * std::max(P.R0, P.R1));
-  k_row_inv2<<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi);
+  FastDiv dW;
+  dW.init(static_cast<uint32_t>(g.W));
+  const int64_t blk = static_cast<int64_t>(nrows) * g.W;
+  if (g.W == g.m1) {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2<false>), sm);
+    k_row_inv2<false><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi, dW, blk);
+  } else {
+    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2<true>), sm);
+    k_row_inv2<true><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi, dW, blk);
+  }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
+// Column passes over the S * nk planes of a Geom, rows of length W (= m1 on one GPU;
+// the rank's axis-1 positions in the slab-decomposed pencil stage).
 void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st) {
   const size_t sm = pass2_smem(P, kCW);
-  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.nk);
+  dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  FastDiv dnp2;
-  dnp2.init(static_cast<uint32_t>(g.np2));
-  const int64_t blk = g.bps * g.S * g.nk;
-  if (g.np2 == g.m2) {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2<false>), sm);
-    k_col_fwd2<false><<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps, dnp2, blk);
-  } else {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2<true>), sm);
-    k_col_fwd2<true><<<grid, threads, sm, st>>>(A, B, g.m1, P, g.bps, dnp2, blk);
-  }
+  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2), sm);
+  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.W, P, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
 void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st) {
   const size_t sm = pass2_smem(P, kCW);
-  dim3 grid((g.m1 + kCW - 1) / kCW, g.S * g.nk);
+  dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  FastDiv dnp2;
-  dnp2.init(static_cast<uint32_t>(g.np2));
-  const int64_t blk = g.bps * g.S * g.nk;
-  if (g.np2 == g.m2) {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2<false>), sm);
-    k_col_inv2<false><<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps, dnp2, blk);
-  } else {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2<true>), sm);
-    k_col_inv2<true><<<grid, threads, sm, st>>>(B, A, g.m1, P, g.bps, dnp2, blk);
-  }
+  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2), sm);
+  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.W, P, g.bps);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -57,6 +57,7 @@ struct PencilArgs {
   uint64_t active;
   FastDiv div_n3;       // element index -> (line, k) without runtime division
   FastDiv div_nk;       // k -> slab block
+  int g0;               // first axis-1 group of this launch
   FastDiv div_cf;
   FastDiv div_nc;
 };
@@ -111,10 +112,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
   // 32-byte segments of every pencil row, so L2 sectors fetched from DRAM are
   // fully used (the transposed order measured 2.8x the DRAM reads).
   const int b = blockIdx.x & 1;        // axis-3 branch (even / odd frequencies)
-  const int c0 = (blockIdx.x >> 1) * W;  // first axis-1 position
+  const int c0 = (a.g0 + (blockIdx.x >> 1)) * W;  // first axis-1 position (global)
   const int q0 = c0 >> 1;         // tile octant row of axis 1
-  const int pos2l_0 = blockIdx.y * P2N;   // first axis-2 row of this rank's slab block
-  const int pos2_0 = g.p2off + pos2l_0;  // global position (pair 2j, 2j+1 when P2N = 2)
+  const int pos2_0 = blockIdx.y * P2N;  // first axis-2 position (pair 2j, 2j+1 when P2N = 2)
   const int f2t = freq_of_pos(pos2_0, n2);
   const int p2o_tile = f2t > n2 ? m2 - f2t : f2t;
   const int n3p = n3 + 1;
@@ -159,9 +159,10 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
       const int p2sel = p >> lgW;
       const int sk = e >> lgNP;
       const int s = static_cast<int>(a.div_n3.div(sk)), k = sk - s * n3;
-      const int pos1 = c0 + w, pos2l = pos2l_0 + p2sel;
+      const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
       double2* dst = buf + (s * NP + p) * ls + k;
-      if (pos1 < m1) cp_async16(dst, a.Bin + s * sstride + koff(k) + static_cast<int64_t>(pos2l) * m1 + pos1);
+      if (pos1 < m1)
+        cp_async16(dst, a.Bin + s * sstride + koff(k) + static_cast<int64_t>(pos2) * g.W + (pos1 - g.p1off));
       else *dst = make_double2(0.0, 0.0);
     }
     cp_async_commit();
@@ -280,10 +281,11 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
         const int line = static_cast<int>(a.div_n3.div(e)), k = e - line * n3;
         const int s = line >> lgNP, p = line & (NP - 1);
         const int w = p & (W - 1), p2sel = p >> lgW;
-        const int pos1 = c0 + w, pos2l = pos2l_0 + p2sel;
+        const int pos1 = c0 + w, pos2 = pos2_0 + p2sel;
         if (pos1 >= m1) continue;
         const double2 a0 = b ? rem[q] : own[q], a1 = b ? own[q] : rem[q];
-        a.Bout[s * sstride + koff(k) + static_cast<int64_t>(pos2l) * m1 + pos1] = cadd(a0, cmulc(a1, twb[k]));
+        a.Bout[s * sstride + koff(k) + static_cast<int64_t>(pos2) * g.W + (pos1 - g.p1off)] =
+            cadd(a0, cmulc(a1, twb[k]));
       }
     }
     cluster.sync();  // partner finished reading this CTA's smem
@@ -338,14 +340,18 @@ void launch_pencil_t(const double2* Bin, double2* Bout, double2* Bout1, const do
   PencilShape sh{};
   bool two = false;
   if (!pencil_shape(g.n3, S, NC, sh, two)) throw std::invalid_argument("pencil kernel: grid edge n3 too large");
-  PencilArgs a{Bin, Bout, Bout1, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}, {}};
+  PencilArgs a{Bin, Bout, Bout1, Shat, twm3, g, PH, sh.P1P, sh.P2N, sh.NBUF, sh.CF, active, {}, {}, {}, {}, 0};
   a.div_n3.init(static_cast<uint32_t>(g.n3));
   a.div_nk.init(static_cast<uint32_t>(g.nk));
   a.div_cf.init(static_cast<uint32_t>(sh.CF));
   a.div_nc.init(static_cast<uint32_t>(group_size<NC>()));
   const size_t smem = pencil_smem_shape(g.n3, S, NC, sh);
-  const int all_groups = (g.m1 + 2 * sh.P1P - 1) / (2 * sh.P1P);
-  dim3 grid(2 * (groups > 0 ? std::min(groups, all_groups) : all_groups), g.np2 / sh.P2N);
+  // this rank's axis-1 groups [g0, g1) (all of them on one GPU); groups > 0: only the first
+  a.g0 = g.p1off / (2 * sh.P1P);
+  const int g1 = (std::min(g.m1, g.p1off + g.W) + 2 * sh.P1P - 1) / (2 * sh.P1P);
+  const int ng = groups > 0 ? std::min(groups, g1 - a.g0) : g1 - a.g0;
+  if (ng <= 0) return;
+  dim3 grid(2 * ng, g.m2 / sh.P2N);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.dynamicSmemBytes = smem;

@@ -94,7 +94,10 @@ struct Pencil2Args {
   const double2* twm3;  // w_m3^e, e < m3
   int n1, n2, m1, m2, m3;
   int64_t kstride, sstride;  // plane stride bps, current stride nk * bps (Geom)
-  int nk, p2off;
+  int nk;      // k-planes per slab block (koff)
+  int W;       // row length of the slabs (axis-1 positions of this rank)
+  int p1off;   // global axis-1 position of slab column 0
+  int gfirst;  // first axis-1 group of this launch
   FastDiv dnk;
 };
 
@@ -159,10 +162,10 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
 
   const int tid = threadIdx.x;
   const int b = blockIdx.x & 1;                     // axis-3 branch = rank in the cluster
-  const int c0 = 2 * P1P * (1 + (blockIdx.x >> 1));  // first axis-1 position (group 0 is the edge launch)
+  const int c0 = 2 * P1P * (a.gfirst + (blockIdx.x >> 1));  // first axis-1 position (group 0 is the edge launch)
+  const int cl0 = c0 - a.p1off;                              // its slab column
   const int q0 = c0 >> 1;                           // octant row of pair 0
-  const int pos2l = blockIdx.y;          // axis-2 row of this rank's slab block
-  const int pos2 = a.p2off + pos2l;      // global axis-2 position
+  const int pos2 = blockIdx.y;  // axis-2 position
   // slab offset of k-plane k: block r = k / nk of the k-planes (one block on one GPU)
   auto koff = [&](int k) -> int64_t {
     const int r = static_cast<int>(a.dnk.div(static_cast<uint32_t>(k)));
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   {
     const int s = line0 / NP, p = line0 % NP;
     if (act0 && c0 + p < m1 && !(VIE_P2_ABL & 4)) {
-      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(pos2l) * m1 + c0 + p;
+      const double2* src = a.Bin + s * a.sstride + static_cast<int64_t>(pos2) * a.W + cl0 + p;
 #pragma unroll
       for (int i = 0; i < R0; ++i) xin[i] = src[koff(mp0 + i * R1)];
     } else {
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     if (act) branch((VIE_P2_ABL & 16) ? buf : rem, b ^ 1, vr);
     asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");  // done reading the partner
     if (act && !(VIE_P2_ABL & 8)) {
-      double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(pos2l) * m1 + c0 + p;
+      double2* dst = a.Bout + s * a.sstride + static_cast<int64_t>(pos2) * a.W + cl0 + p;
       sfor<R0>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         const double2 y0 = b ? vr[out_idx(R0, i)] : vo[out_idx(R0, i)];
@@ -415,16 +418,19 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
                cudaStream_t st, bool dry) {
   auto go = [&](auto fn, size_t smem, int P1P, std::array<int, 3> box) {
     if (dry) return true;
-    const int groups = (g.m1 + 2 * P1P - 1) / (2 * P1P);
-    if (groups <= 1) return true;  // the edge launch covers everything
+    // axis-1 groups of this rank's positions [p1off, p1off + W); group 0 is the edge launch
+    const int glo = std::max(1, g.p1off / (2 * P1P));
+    const int ghi = (std::min(g.m1, g.p1off + g.W) + 2 * P1P - 1) / (2 * P1P);
+    if (ghi <= glo) return true;
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3, g.bps, g.bps * g.nk, g.nk, g.p2off, {}};
+    Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3, g.bps, g.bps * g.nk, g.nk, g.W, g.p1off,
+                  glo, {}};
     a.dnk.init(static_cast<uint32_t>(g.nk));
     CUtensorMap tmap;
     encode_spectrum_map(&tmap, Shat, g, box);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (groups - 1), g.np2);
+    cfg.gridDim = dim3(2 * (ghi - glo), g.m2);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;

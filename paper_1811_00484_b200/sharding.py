@@ -48,12 +48,13 @@ def sharded_apply_system(eps_r, inv_v, op, x, out=None, group=None, stream=None)
 
 
 # ----------------------------------------------------------------------------
-# Slab decomposition (recommended partition): rank r owns the
-# z-planes [r nk, (r+1) nk) of x and y and the axis-2 spectral rows
-# [r np2, (r+1) np2) of the pencil stage.  One matvec = local axis-1/2 FFTs ->
-# all-to-all -> decompression of the rank's octant rows + fused axis-3 FFT /
-# Hadamard / IFFT -> all-to-all back -> local inverse axis-2/1 FFTs.  The
-# exchanged buffers are blocked by rank (vie_slab_* in include/vie_b200.h), so
+# Slab decomposition: rank r owns the z-planes [r nk, (r+1) nk) of x
+# and y for the axis-1 FFTs and the axis-1 positions [r W, (r+1) W) of everything
+# after them (axis-2 FFTs, the decomposition rows, the fused axis-3 pencil stage).
+# One matvec = local axis-1 FFTs -> all-to-all of the axis-1 spectra (2x the input,
+# half of exchanging after the axis-2 FFT too) -> axis-2 FFT + pencil stage + inverse
+# axis-2 FFT on the rank's positions -> all-to-all back -> local inverse axis-1 FFTs.
+# The exchanged buffers are blocked by rank (vie_slab_* in include/vie_b200.h), so
 # each exchange is one equal-split all_to_all_single (NCCL over NVLink).
 
 

@@ -1,4 +1,6 @@
-"""Slab-decomposed multi-GPU matvec, emulated rank by rank on one GPU:
+"""Slab-decomposed multi-GPU matvec: z-slabs for the axis-1 passes, axis-1
+position slabs for the axis-2 passes / decomposition / pencil stage, one all-to-all each
+way after the axis-1 FFT; emulated rank by rank on one GPU:
 every rank's stage runs to completion before the exchange (no rank waits on
 another inside a kernel), the all-to-all is done by chunk copies with the exact
 semantics of torch.distributed.all_to_all_single.  The assembled result must equal
@@ -46,8 +48,8 @@ def _emulate(vie, ops, xg, dims, S, world, eps=None, inv_v=0.0):
 
 
 SLAB_CASES = [
-    (N, PWL, (4, 4, 8), 2, 3), (N, PWL, (4, 4, 8), 4, 3), (N, PWC, (6, 8, 8), 4, 4), (K, PWL, (5, 4, 6), 2, 3),
-    (N, PWL, (3, 4, 32), 4, 3), (N, PWC, (5, 8, 64), 8, 3), (K, PWC, (7, 6, 10), 2, 3), (N, PWC, (4, 4, 4), 1, 2),
+    (N, PWL, (4, 4, 8), 2, 3), (N, PWL, (4, 4, 8), 4, 3), (N, PWC, (16, 8, 8), 4, 4), (K, PWL, (6, 4, 6), 2, 3),
+    (N, PWL, (4, 4, 32), 4, 3), (N, PWC, (32, 3, 64), 8, 3), (K, PWC, (8, 6, 10), 2, 3), (N, PWC, (4, 4, 4), 1, 2),
 ]
 
 
@@ -68,7 +70,7 @@ def test_slab_ranks_assemble_the_single_gpu_matvec(vie, dft, orc, kind, basis, d
 def test_slab_system_matvec(vie, dft, orc):
     import torch
 
-    dims, world = (4, 6, 6), 3
+    dims, world = (6, 4, 6), 3
     x = torch.from_numpy(random_field(PWL, dims, 9)).cuda()
     rng = np.random.default_rng(3)
     eps = torch.from_numpy(1 + rng.random(int(np.prod(dims))) + 0.3j * rng.random(int(np.prod(dims)))).cuda()
@@ -84,12 +86,12 @@ def test_partition_errors_and_guard(vie, dft, orc):
 
     from paper_1811_00484_b200.sharding import SlabMatvec
 
-    dims = (4, 6, 8)
+    dims = (8, 6, 8)
     op = make_ops(vie, dft, orc, N, PWC, dims, 2, 5)[0]
     with pytest.raises(ValueError):
         SlabMatvec(op, 0, 3)  # n3 = 8 not divisible by 3
     with pytest.raises(ValueError):
-        SlabMatvec(op, 0, 4)  # 2 n2 = 12 rows do not split into even blocks of 4 ranks
+        SlabMatvec(op, 0, 4)  # 2 n1 = 16 positions give 4 per rank: not a whole PWC pencil group (8)
     SlabMatvec(op, 1, 2)
     with pytest.raises(ValueError):  # a partitioned operator refuses the unpartitioned matvec
         vie.apply_operator(op, torch.zeros(3 * int(np.prod(dims)), dtype=torch.complex128, device="cuda"))

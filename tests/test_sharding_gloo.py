@@ -93,7 +93,7 @@ def _slab_worker(rank, world, port, q):
     from paper_1811_00484_b200.sharding import local_slab, slab_planes
     from tests.helpers import fourier_forms, random_field, spatial_tucker_forms
 
-    kind, basis, dims = 0, 0, (3, 6, 6)
+    kind, basis, dims = 0, 0, (12, 4, 6)
     n1, n2, n3 = dims
     m1, m2, m3 = 2 * n1, 2 * n2, 2 * n3
     S = 3
@@ -103,31 +103,31 @@ def _slab_worker(rank, world, port, q):
     spec = [orc.decompress_tucker((m1, m2, m3), f).reshape(m3, m2, m1) for f in forms]
     x = random_field(basis, dims, 8)
     k0, nk = slab_planes(n3, rank, world)
-    np2 = m2 // world
+    W = m1 // world
     xl = local_slab(x, S, n3, n1 * n2, rank, world).reshape(S, nk, n2, n1)
-    # stage 1: axis-1/2 FFTs of the local z-slab, blocked by destination rank
-    xa = np.zeros((S, nk, m2, m1), complex)
-    xa[:, :, :n2, :n1] = xl
-    xa = np.fft.fft2(xa, axes=(2, 3))
-    send = np.stack([xa[:, :, qq * np2:(qq + 1) * np2, :] for qq in range(world)]).reshape(-1)
+    # stage 1: axis-1 FFT of the local z-slab, blocked by the destination rank's W positions
+    xa = np.zeros((S, nk, n2, m1), complex)
+    xa[..., :n1] = xl
+    xa = np.fft.fft(xa, axis=3)
+    send = np.stack([xa[..., qq * W:(qq + 1) * W] for qq in range(world)]).reshape(-1)
     recv = torch.empty(send.size, dtype=torch.complex128)
     dist.all_to_all_single(recv, torch.from_numpy(send))
-    # stage 2: this rank's axis-2 rows, all k: axis-3 FFT, Hadamard, IFFT, crop
-    blk = recv.numpy().reshape(world, S, nk, np2, m1)
-    xp = np.zeros((S, m3, np2, m1), complex)
-    xp[:, :n3] = blk.transpose(1, 0, 2, 3, 4).reshape(S, n3, np2, m1)
-    xp = np.fft.fft(xp, axis=1)
-    rows = slice(rank * np2, (rank + 1) * np2)
+    # stage 2: this rank's W positions, all k: axis-2 FFT, axis-3 FFT, Hadamard, inverses
+    blk = recv.numpy().reshape(world, S, nk, n2, W)
+    xp = np.zeros((S, m3, m2, W), complex)
+    xp[:, :n3, :n2] = blk.transpose(1, 0, 2, 3, 4).reshape(S, n3, n2, W)
+    xp = np.fft.fft(np.fft.fft(xp, axis=2), axis=1)
+    cols = slice(rank * W, (rank + 1) * W)
     yp = np.zeros_like(xp)
     for t, s_, c, coef in blocks:
-        yp[t] += coef * spec[c][:, rows, :] * xp[s_]
-    yp = np.fft.ifft(yp, axis=1)[:, :n3]
+        yp[t] += coef * spec[c][:, :, cols] * xp[s_]
+    yp = np.fft.ifft(np.fft.ifft(yp, axis=1)[:, :n3], axis=2)[:, :, :n2]
     out = np.stack([yp[:, r * nk:(r + 1) * nk] for r in range(world)]).reshape(-1)
     back = torch.empty(out.size, dtype=torch.complex128)
     dist.all_to_all_single(back, torch.from_numpy(out))
-    # stage 3: inverse axis-2/1 FFTs of the local z-slab, crop
-    ya = back.numpy().reshape(world, S, nk, np2, m1).transpose(1, 2, 0, 3, 4).reshape(S, nk, m2, m1)
-    yl = np.fft.ifft2(ya, axes=(2, 3))[:, :, :n2, :n1]
+    # stage 3: inverse axis-1 FFT of the local z-slab rows, crop
+    ya = back.numpy().reshape(world, S, nk, n2, W).transpose(1, 2, 3, 0, 4).reshape(S, nk, n2, m1)
+    yl = np.fft.ifft(ya, axis=3)[..., :n1]
     gathered = [torch.empty(yl.size, dtype=torch.complex128) for _ in range(world)]
     dist.all_gather(gathered, torch.from_numpy(np.ascontiguousarray(yl).reshape(-1)))
     if rank == 0:
