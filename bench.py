@@ -303,7 +303,9 @@ def run_b200(args):
     nc = len(comps)
     # N > 1: slab decomposition (z-planes / axis-2 spectral rows, two NCCL all-to-alls per
     # matvec) when the grid splits evenly, else component sharding + NCCL all-reduce
-    slab = (world > 1 or args.slab) and grid[2] % world == 0 and grid[1] % world == 0
+    group = 2 * (1 if S >= 12 else (2 if S >= 6 else 4))  # axis-1 positions per pencil group
+    slab = ((world > 1 or args.slab) and grid[2] % world == 0 and (2 * grid[0]) % world == 0
+            and ((2 * grid[0]) // world) % group == 0)
     mine = list(range(nc)) if (world == 1 or slab) else [c for c in range(nc) if c % world == rank]
     dft = vie.DftService(local)
     spatial, par = spatial_tucker_forms(0, basis, grid, r, 1234)
@@ -439,7 +441,7 @@ def run_b200(args):
                                    f"embedded {tuple(2 * d for d in grid)}, {nc} Tucker components rank {r}, "
                                    f"{S} currents", "grid": list(grid), "basis": "PWL" if basis else "PWC",
                        "rank": r, "components": nc,
-                       "parallelism": (f"slab decomposition x{world} (z-planes / axis-2 rows, NCCL all-to-all)" if slab
+                       "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all)" if slab
                                        else f"components sharded x{world}") if world > 1 else "1 GPU",
                        "l2": "inputs 1.8 GB > 126 MB L2 (no flush needed)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
