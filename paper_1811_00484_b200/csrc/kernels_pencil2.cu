@@ -35,12 +35,6 @@
 #ifndef VIE_P2_NBUF
 #define VIE_P2_NBUF 2
 #endif
-#ifndef VIE_P2_SIGNSPLIT
-#define VIE_P2_SIGNSPLIT 1  // mirror signs on x^ / y^ instead of every spectrum value
-#endif
-#ifndef VIE_P2_TWLDG
-#define VIE_P2_TWLDG 0  // stage twiddles from the (L1-resident) table instead of recurrences
-#endif
 #ifndef VIE_P2_CHUNK
 #define VIE_P2_CHUNK 640  // spectrum chunk budget (double2): 10 KB
 #endif
@@ -234,12 +228,8 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       dst[blk_pos<R0, R1>(0, mp0)] = v[out_idx(R0, 0)];
       sfor<R0 - 1>([&](auto kc) {
         constexpr int k = decltype(kc)::value + 1;
-        if constexpr (VIE_P2_TWLDG) {
-          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * 2 * k));
-        } else {
-          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
-          if (k + 1 < R0) w = cmul(w, wstep0);
-        }
+        dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
+        if (k + 1 < R0) w = cmul(w, wstep0);
       });
     }
     v[0] = xin[0];  // branch 1: inputs * w_{2 R0}^i, outputs * w_m3^{mp (2k + 1)}
@@ -253,12 +243,8 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       double2 w = __ldg(a.twm3 + mp0);
       sfor<R0>([&](auto kc) {
         constexpr int k = decltype(kc)::value;
-        if constexpr (VIE_P2_TWLDG) {
-          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], __ldg(a.twm3 + mp0 * (2 * k + 1)));
-        } else {
-          dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
-          if (k + 1 < R0) w = cmul(w, wstep0);
-        }
+        dst[blk_pos<R0, R1>(k, mp0)] = cmul(v[out_idx(R0, k)], w);
+        if (k + 1 < R0) w = cmul(w, wstep0);
       });
     }
   }
@@ -304,8 +290,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       const int sbits = m1flag | (m2flag << 1) | (mir << 2);
       if (valid) {
 #pragma unroll
-        for (int s = 0; s < S; ++s)
-          xh[s] = VIE_P2_SIGNSPLIT ? flip_sign(pl[s * NP * LS], pattern_sign(SG.pi[s] ^ SG.G, sbits)) : pl[s * NP * LS];
+        for (int s = 0; s < S; ++s) xh[s] = flip_sign(pl[s * NP * LS], pattern_sign(SG.pi[s] ^ SG.G, sbits));
       }
 #pragma unroll
       for (int t = 0; t < TH; ++t) yh[t] = make_double2(0.0, 0.0);
@@ -316,11 +301,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
         if (!(VIE_P2_ABL & 2)) mbar_wait(full + bi, (q / NBUF) & 1);
         if (valid && !(VIE_P2_ABL & 1)) {
           const double2* sh_base = chunk + bi * CHUNK + (tr * CG - GRP * CG) * CF + ul;
-          if constexpr (VIE_P2_SIGNSPLIT)
-            had_all_ns<KIND, BASIS, S, TH, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF);
-          else
-            had_all<KIND, BASIS, S, TH, 0, true, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF,
-                                                          ~0ull, m1flag, m2flag, mir);
+          had_all_ns<KIND, BASIS, S, TH, GRP, CG>(std::make_integer_sequence<int, NB>{}, yh, xh, sh_base, CF);
         }
         // every Hadamard read of buffer bi has returned (its FMAs were issued), so the
         // warp can sign off without a fence; the last warp out refills the buffer
@@ -337,8 +318,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
       });
       if (valid) {
 #pragma unroll
-        for (int t = 0; t < TH; ++t)
-          pl[t * NP * LS] = VIE_P2_SIGNSPLIT ? flip_sign(yh[t], pattern_sign(SG.pi[t], sbits)) : yh[t];
+        for (int t = 0; t < TH; ++t) pl[t * NP * LS] = flip_sign(yh[t], pattern_sign(SG.pi[t], sbits));
       }
     }
   }
@@ -370,22 +350,14 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     const double2 w1 = __ldg(a.twm3 + min(mp, R1 - 1));
     // branch br: inputs * conj(w_m3^{mp (2k + br)}), then the radix-R0 adjoint
     auto branch = [&](const double2* X, int br, double2(&v)[R0]) {
-      if constexpr (VIE_P2_TWLDG) {
-        const int mpc = min(mp, R1 - 1);
-        v[0] = br ? cmulc(X[off + blk_pos<R0, R1>(0, mpc)], w1) : X[off + blk_pos<R0, R1>(0, mpc)];
+      const int mpc = min(mp, R1 - 1);
+      double2 w = br ? w1 : wstep;
+      v[0] = br ? cmulc(X[off + blk_pos<R0, R1>(0, mpc)], w) : X[off + blk_pos<R0, R1>(0, mpc)];
+      if (br) w = cmul(w, wstep);
 #pragma unroll
-        for (int k = 1; k < R0; ++k)
-          v[k] = cmulc(X[off + blk_pos<R0, R1>(k, mpc)], __ldg(a.twm3 + mpc * (2 * k + br)));
-      } else {
-        const int mpc = min(mp, R1 - 1);
-        double2 w = br ? w1 : wstep;
-        v[0] = br ? cmulc(X[off + blk_pos<R0, R1>(0, mpc)], w) : X[off + blk_pos<R0, R1>(0, mpc)];
-        if (br) w = cmul(w, wstep);
-#pragma unroll
-        for (int k = 1; k < R0; ++k) {
-          v[k] = cmulc(X[off + blk_pos<R0, R1>(k, mpc)], w);
-          if (k + 1 < R0) w = cmul(w, wstep);
-        }
+      for (int k = 1; k < R0; ++k) {
+        v[k] = cmulc(X[off + blk_pos<R0, R1>(k, mpc)], w);
+        if (k + 1 < R0) w = cmul(w, wstep);
       }
       DFTs<R0, true, 1, 0>::run(v);
     };
