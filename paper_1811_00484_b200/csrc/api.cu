@@ -61,6 +61,13 @@ T* dev_alloc(size_t count) {
 void dev_free(void* p) {
   if (p) cudaFree(p);
 }
+// Copy ordered on `st` and complete on return.  A plain cudaMemcpy runs on the legacy
+// stream, which does not order with the non-blocking streams the kernels use, and a
+// pageable host-to-device cudaMemcpy may return before the data has reached the device.
+void copy_sync(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  VIE_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+  VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+}
 
 struct PlanHolder {
   FftPlan plan{};
@@ -265,9 +272,9 @@ const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = fals
   h->tw = dev_alloc<double2>(static_cast<size_t>(n));
   h->slot = dev_alloc<int>(static_cast<size_t>(n));
   h->st = dev_alloc<vie::StageDesc>(sd.size());
-  VIE_CUDA_CHECK(cudaMemcpy(h->tw, tw.data(), sizeof(double2) * n, cudaMemcpyHostToDevice));
-  VIE_CUDA_CHECK(cudaMemcpy(h->slot, slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
-  VIE_CUDA_CHECK(cudaMemcpy(h->st, sd.data(), sizeof(vie::StageDesc) * sd.size(), cudaMemcpyHostToDevice));
+  copy_sync(h->tw, tw.data(), sizeof(double2) * n, ctx->stream);
+  copy_sync(h->slot, slot.data(), sizeof(int) * n, ctx->stream);
+  copy_sync(h->st, sd.data(), sizeof(vie::StageDesc) * sd.size(), ctx->stream);
   P.tw = h->tw;
   P.slot = h->slot;
   P.st = h->st;
@@ -584,7 +591,7 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
     const size_t ncore = static_cast<size_t>(ranks[0] * ranks[1] * ranks[2]);
     check_cplx_finite_host(core_host, ncore, "vie_tucker_from_factors: core");
     t->core = dev_alloc<double2>(ncore);
-    VIE_CUDA_CHECK(cudaMemcpy(t->core, core_host, ncore * sizeof(double2), cudaMemcpyHostToDevice));
+    copy_sync(t->core, core_host, ncore * sizeof(double2), ctx->stream);
     const double* uh[3] = {u1_host, u2_host, u3_host};
     for (int q = 0; q < 3; ++q) {
       const int64_t n = dims[q], r = ranks[q];
@@ -603,7 +610,7 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
         }
         double2* du = dev_alloc<double2>(static_cast<size_t>(n * r));
         try {
-          VIE_CUDA_CHECK(cudaMemcpy(du, uh[q], sizeof(double2) * n * r, cudaMemcpyHostToDevice));
+          copy_sync(du, uh[q], sizeof(double2) * n * r, ctx->stream);
           const FftPlan& P = get_plan(ctx, static_cast<int>(2 * n));
           vie::launch_factor_transform(du, static_cast<int>(n), static_cast<int>(r), sign[q], P.tw, t->uo[q],
                                        ctx->stream);
@@ -629,7 +636,7 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
         std::vector<cd> oct(static_cast<size_t>((n + 1) * r));
         for (int64_t c = 0; c < r; ++c)
           for (int64_t p = 0; p <= n; ++p) oct[static_cast<size_t>(p + (n + 1) * c)] = u[p + m * c];
-        VIE_CUDA_CHECK(cudaMemcpy(t->uo[q], oct.data(), sizeof(double2) * oct.size(), cudaMemcpyHostToDevice));
+        copy_sync(t->uo[q], oct.data(), sizeof(double2) * oct.size(), ctx->stream);
       }
     }
     *out = t.release();
@@ -732,18 +739,13 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       const vie_tucker_s* t = byc[c];
       if (!t) continue;
       const CompDev& d = op->comps_host[c];
-      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_core, t->core, sizeof(double2) * d.r1 * d.r2 * d.r3,
-                                cudaMemcpyDeviceToDevice));
-      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u1, t->uo[0], sizeof(double2) * (g.n1 + 1) * d.r1,
-                                cudaMemcpyDeviceToDevice));
-      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u2, t->uo[1], sizeof(double2) * (g.n2 + 1) * d.r2,
-                                cudaMemcpyDeviceToDevice));
-      VIE_CUDA_CHECK(cudaMemcpy(op->forms + d.off_u3, t->uo[2], sizeof(double2) * (g.n3 + 1) * d.r3,
-                                cudaMemcpyDeviceToDevice));
+      copy_sync(op->forms + d.off_core, t->core, sizeof(double2) * d.r1 * d.r2 * d.r3, ctx->stream);
+      copy_sync(op->forms + d.off_u1, t->uo[0], sizeof(double2) * (g.n1 + 1) * d.r1, ctx->stream);
+      copy_sync(op->forms + d.off_u2, t->uo[1], sizeof(double2) * (g.n2 + 1) * d.r2, ctx->stream);
+      copy_sync(op->forms + d.off_u3, t->uo[2], sizeof(double2) * (g.n3 + 1) * d.r3, ctx->stream);
     }
     op->comps_dev = dev_alloc<CompDev>(cs.size());
-    VIE_CUDA_CHECK(cudaMemcpy(op->comps_dev, op->comps_host.data(), sizeof(CompDev) * cs.size(),
-                              cudaMemcpyHostToDevice));
+    copy_sync(op->comps_dev, op->comps_host.data(), sizeof(CompDev) * cs.size(), ctx->stream);
     const int64_t nv = static_cast<int64_t>(g.n1) * g.n2 * g.n3;
     const int64_t noct = static_cast<int64_t>(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
     op->Z = dev_alloc<double2>(static_cast<size_t>(std::max<int64_t>(zoff, 1)));
@@ -752,6 +754,15 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->B = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
     op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
     op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 2 * nv + 2 * g.S * g.n3 * g.bps);
+    if (const int poison = env_int("VIE_DEBUG_POISON", 0)) {  // debug: NaN-fill workspaces (reads of unwritten data)
+      const int64_t nb = g.S * g.n3 * g.bps;
+      if (poison & 1) VIE_CUDA_CHECK(cudaMemsetAsync(op->Shat, 0xFF, sizeof(double2) * noct * g.NC));
+      if (poison & 2) VIE_CUDA_CHECK(cudaMemsetAsync(op->Z, 0xFF, sizeof(double2) * std::max<int64_t>(zoff, 1)));
+      if (poison & 4) VIE_CUDA_CHECK(cudaMemsetAsync(op->A, 0xFF, sizeof(double2) * g.S * 2 * nv));
+      if (poison & 8) VIE_CUDA_CHECK(cudaMemsetAsync(op->B, 0xFF, sizeof(double2) * nb));
+      if (poison & 16) VIE_CUDA_CHECK(cudaMemsetAsync(op->Bo, 0xFF, sizeof(double2) * nb));
+      VIE_CUDA_CHECK(cudaDeviceSynchronize());
+    }
     op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
@@ -1010,7 +1021,7 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     if (!op->red_partials) {
       op->red_partials = dev_alloc<double2>(vie::kRedBlocks);
       op->red_counter = dev_alloc<unsigned int>(1);
-      VIE_CUDA_CHECK(cudaMemset(op->red_counter, 0, sizeof(unsigned int)));
+      VIE_CUDA_CHECK(cudaMemsetAsync(op->red_counter, 0, sizeof(unsigned int)));
     }
     if (inner + 2 > 256) throw Invalid("gmres: inner > 254 not supported");
     vie::RedBuf rb{op->red_partials, op->red_counter};
@@ -1196,7 +1207,7 @@ int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host
     cudaStream_t st = ctx->stream;
     DevPool dev;
     double2* dt = dev.alloc<double2>(static_cast<size_t>(nv));
-    VIE_CUDA_CHECK(cudaMemcpy(dt, t_host, sizeof(double2) * nv, cudaMemcpyHostToDevice));
+    copy_sync(dt, t_host, sizeof(double2) * nv, st);
     // per mode: Gram on the device, Hermitian Jacobi eigendecomposition on the host
     // (sigma_k = sqrt(lambda_k): the left singular pairs of the unfolding), rank
     // by truncation_rank (decomp.hpp:72-103), U_q = leading eigenvectors.

@@ -79,6 +79,7 @@ def test_matvec_matches_oracle(vie, dft, orc, kind, basis, dims, rank):
 PENCIL2_CASES = [
     (N, PWL, (3, 4, 32), 3), (K, PWL, (4, 3, 100), 3), (N, PWC, (5, 3, 64), 4), (K, PWC, (6, 2, 32), 3),
     (N, PWC, (1, 2, 32), 2), (N, PWL, (7, 5, 64), 3), (N, PWC, (9, 4, 100), 3), (K, PWL, (2, 6, 64), 2),
+    (N, PWL, (4, 3, 100), 3),  # the headline kernel k_pencil2<N, PWL, 10, 20>
 ]
 
 
@@ -298,3 +299,50 @@ def test_linearity_at_head_2mm_size(vie, dft, orc):
     rhs = vie.apply_operator(op, x) + lam * vie.apply_operator(op, z)
     torch.cuda.synchronize()
     assert float((lhs - rhs).norm() / rhs.norm()) < 1e-12
+
+
+def _embedded_value(core, ranks, us, par, d):
+    """T~_c(d) of the circulant embedding (operator.hpp:40-74 / np_circulant_embed):
+    t[|d|] per axis, times the axis parity for negative offsets; d: (P, 3) offsets."""
+    g = np.asarray(core).reshape(tuple(ranks), order="F")
+    rows = [us[q][np.abs(d[:, q]), :] * np.where(d[:, q] < 0, float(par[q]), 1.0)[:, None] for q in range(3)]
+    return np.einsum("abg,pa,pb,pg->p", g, rows[0], rows[1], rows[2], optimize=True)
+
+
+@pytest.mark.parametrize("s0,cell", [(5, (17, 203, 99)), (0, (199, 239, 199)), (11, (0, 0, 0))])
+def test_headline_size_delta_columns(vie, dft, orc, s0, cell):
+    # BASELINE configs[1] shape (1 mm head grid 200x240x200, PWL N, 60 components, r = 25):
+    # a unit current in cell r0 of current s0 returns column (s0, r0) of the operator,
+    # y_t(r) = sum over blocks (t, s0, c, ds) of ds*sigma_c*T~_c(r - r0) (operator.hpp:303-364),
+    # checked at 4096 sampled output cells of every target against the Tucker forms directly.
+    import torch
+
+    dims = (200, 240, 200)
+    rank = 25
+    spatial, par = spatial_tucker_forms(N, PWL, dims, rank, 7)
+    comps, _, _ = vie.component_table(N, PWL)
+    forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in range(len(comps))]
+    op = vie.build_operator_spectra(N, PWL, dims, comps, forms, dft)
+    n1, n2, n3 = dims
+    nv = n1 * n2 * n3
+    x = torch.zeros(12 * nv, dtype=torch.complex128, device="cuda")
+    x[s0 * nv + cell[0] + n1 * (cell[1] + n2 * cell[2])] = 1.0
+    y = vie.apply_operator(op, x)
+    rng = np.random.default_rng(s0)
+    pts = np.stack([rng.integers(0, n, 4096) for n in dims], axis=1)
+    pts[:3] = [[0, 0, 0], [n1 - 1, n2 - 1, n3 - 1], list(cell)]
+    flat_idx = pts[:, 0] + n1 * (pts[:, 1] + n2 * pts[:, 2])
+    idx = torch.from_numpy(np.concatenate([t * nv + flat_idx for t in range(12)])).cuda()
+    got = y[idx].cpu().numpy().reshape(12, -1)
+    _, opar, blocks = orc.component_table(N, PWL)
+    d = pts - np.asarray(cell)[None, :]
+    want = np.zeros((12, len(pts)), np.complex128)
+    cache = {}
+    for t, s, c, ds in blocks:
+        if s != s0:
+            continue
+        if c not in cache:
+            cache[c] = _embedded_value(spatial[c][0], (rank,) * 3, spatial[c][1], opar[c], d)
+        want[t] += ds * float(np.prod(opar[c])) * cache[c]
+    assert np.linalg.norm(want) > 0
+    assert rel(want, got) <= MATVEC_TOL, (s0, cell, rel(want, got))
