@@ -309,34 +309,39 @@ def _embedded_value(core, ranks, us, par, d):
     return np.einsum("abg,pa,pb,pg->p", g, rows[0], rows[1], rows[2], optimize=True)
 
 
-@pytest.mark.parametrize("s0,cell", [(5, (17, 203, 99)), (0, (199, 239, 199)), (11, (0, 0, 0))])
-def test_headline_size_delta_columns(vie, dft, orc, s0, cell):
-    # BASELINE configs[1] shape (1 mm head grid 200x240x200, PWL N, 60 components, r = 25):
-    # a unit current in cell r0 of current s0 returns column (s0, r0) of the operator,
-    # y_t(r) = sum over blocks (t, s0, c, ds) of ds*sigma_c*T~_c(r - r0) (operator.hpp:303-364),
-    # checked at 4096 sampled output cells of every target against the Tucker forms directly.
+@pytest.mark.parametrize("kind,basis,s0,cell", [
+    (N, PWL, 5, (17, 203, 99)), (N, PWL, 0, (199, 239, 199)), (N, PWL, 11, (0, 0, 0)),
+    (K, PWL, 7, (120, 3, 150)), (N, PWC, 1, (5, 120, 198)), (K, PWC, 2, (199, 0, 77)),
+])
+def test_headline_size_delta_columns(vie, dft, orc, kind, basis, s0, cell):
+    # BASELINE configs[1] shape (1 mm head grid 200x240x200, rank 25; the north star is
+    # PWL N with 60 components): a unit current in cell r0 of current s0 returns column
+    # (s0, r0) of the operator, y_t(r) = sum over blocks (t, s0, c, ds) of ds*sigma_c*T~_c(r - r0)
+    # (operator.hpp:303-364), checked at 4096 sampled output cells of every target against
+    # the Tucker forms evaluated directly.
     import torch
 
     dims = (200, 240, 200)
     rank = 25
-    spatial, par = spatial_tucker_forms(N, PWL, dims, rank, 7)
-    comps, _, _ = vie.component_table(N, PWL)
+    S = 12 if basis == PWL else 3
+    spatial, par = spatial_tucker_forms(kind, basis, dims, rank, 7)
+    comps, _, _ = vie.component_table(kind, basis)
     forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in range(len(comps))]
-    op = vie.build_operator_spectra(N, PWL, dims, comps, forms, dft)
+    op = vie.build_operator_spectra(kind, basis, dims, comps, forms, dft)
     n1, n2, n3 = dims
     nv = n1 * n2 * n3
-    x = torch.zeros(12 * nv, dtype=torch.complex128, device="cuda")
+    x = torch.zeros(S * nv, dtype=torch.complex128, device="cuda")
     x[s0 * nv + cell[0] + n1 * (cell[1] + n2 * cell[2])] = 1.0
     y = vie.apply_operator(op, x)
     rng = np.random.default_rng(s0)
     pts = np.stack([rng.integers(0, n, 4096) for n in dims], axis=1)
     pts[:3] = [[0, 0, 0], [n1 - 1, n2 - 1, n3 - 1], list(cell)]
     flat_idx = pts[:, 0] + n1 * (pts[:, 1] + n2 * pts[:, 2])
-    idx = torch.from_numpy(np.concatenate([t * nv + flat_idx for t in range(12)])).cuda()
-    got = y[idx].cpu().numpy().reshape(12, -1)
-    _, opar, blocks = orc.component_table(N, PWL)
+    idx = torch.from_numpy(np.concatenate([t * nv + flat_idx for t in range(S)])).cuda()
+    got = y[idx].cpu().numpy().reshape(S, -1)
+    _, opar, blocks = orc.component_table(kind, basis)
     d = pts - np.asarray(cell)[None, :]
-    want = np.zeros((12, len(pts)), np.complex128)
+    want = np.zeros((S, len(pts)), np.complex128)
     cache = {}
     for t, s, c, ds in blocks:
         if s != s0:
@@ -345,4 +350,4 @@ def test_headline_size_delta_columns(vie, dft, orc, s0, cell):
             cache[c] = _embedded_value(spatial[c][0], (rank,) * 3, spatial[c][1], opar[c], d)
         want[t] += ds * float(np.prod(opar[c])) * cache[c]
     assert np.linalg.norm(want) > 0
-    assert rel(want, got) <= MATVEC_TOL, (s0, cell, rel(want, got))
+    assert rel(want, got) <= MATVEC_TOL, (kind, basis, s0, cell, rel(want, got))
