@@ -112,6 +112,43 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
                     double* final_rel_res, double* history_host, int history_cap, int* history_len,
                     int* converged);
 
+/* ---- scene pipeline around the solve (solve_scene, solver.hpp:148-285) ----
+ * PWC fields (3 component blocks of n_vox, grid.hpp:107-136).  The scene is the
+ * reference's VoxelGrid (grid.hpp:24-46) + DielectricMap frequency (grid.hpp:52-75)
+ * + PlaneWave (grid.hpp:78-100); polarization / direction are normalised here and
+ * VIE_EINVAL is returned when they are not orthogonal (|p.d| > 1e-12, grid.hpp:86-87)
+ * or when a resolution is not > 0 / a dim < 1 (grid.hpp:33-36).  ctx may be NULL:
+ * the caller's current device and `stream` (NULL = legacy default stream).      */
+typedef struct {
+  int64_t dims[3];
+  double resolution[3]; /* meters */
+  double origin[3];     /* minimum corner */
+  double frequency;     /* Hz */
+  double polarization[3];
+  double direction[3];
+  double amplitude; /* V/m */
+} vie_scene;
+
+/* build_rhs (solver.hpp:148-179): rhs_q = c_e chi_e e_inc,q at the voxel centre
+ * (quad_points_per_axis = 1) or the Gauss-integrated voxel average (> 1;
+ * quadrature.hpp:23-52); voxels with chi_e = 0 get 0.  eps_r: n_vox complex
+ * (device); rhs: 3 n_vox complex (device).                                       */
+int vie_build_rhs(vie_ctx ctx, const vie_scene* scene, const double* eps_r, int quad_points_per_axis,
+                  double* rhs, void* stream);
+
+/* recover_fields (solver.hpp:211-249): e = j / (c_e chi_e) where chi_e != 0, else
+ * e_inc(centre); when op_k != NULL (a VIE_KIND_K PWC operator on the same grid),
+ * h = h_inc + (K j) / V through vie_matvec, else h is untouched (may be NULL).    */
+int vie_recover_fields(vie_ctx ctx, const vie_scene* scene, const double* eps_r, const double* j,
+                       vie_op op_k, double* e, double* h, void* stream);
+
+/* postprocess (solver.hpp:258-284): p_abs = sigma_e |e|^2 / 2 (real, n_vox),
+ * *total_absorbed_power_host = V sum p_abs (deterministic order-fixed sum);
+ * when h != NULL, b1_plus = mu0 |h_x + i h_y| (real, n_vox).                    */
+int vie_postprocess(vie_ctx ctx, const vie_scene* scene, const double* eps_r, const double* e,
+                    const double* h, double* p_abs, double* b1_plus, double* total_absorbed_power_host,
+                    void* stream);
+
 /* Timing helpers for the bench: number of kernels the last vie_matvec
  * launched, and per-stage device times (ms) of the last vie_matvec when
  * profiling was enabled with vie_op_set_profiling(op, 1).                   */

@@ -291,3 +291,49 @@ def hosvd(t, dims, tol, rule=1):
     _check(lib().orc_hosvd(_ptr(t), _i64(dims), C.c_double(tol), int(rule), ranks, _ptr(core), _ptr(us[0]),
                            _ptr(us[1]), _ptr(us[2])))
     return core, [us[q].reshape((dims[q], r[q]), order="F") for q in range(3)]
+
+
+# ---- solve_scene stages (solver.hpp:148-285) ---------------------------------
+def _scene_args(scene):
+    """scene: dict(dims, resolution, origin, frequency, polarization, direction, amplitude)."""
+    geo = (C.c_double * 6)(*[float(v) for v in list(scene["resolution"]) + list(scene.get("origin", (0, 0, 0)))])
+    pw = (C.c_double * 7)(*[float(v) for v in list(scene.get("polarization", (1, 0, 0)))
+                            + list(scene.get("direction", (0, 0, 1))) + [scene.get("amplitude", 1.0)]])
+    return _i64(scene["dims"]), geo, C.c_double(float(scene["frequency"])), pw
+
+
+def build_rhs(scene, eps_r, quad: int = 1) -> np.ndarray:
+    """build_rhs (solver.hpp:148-179): 3 n_vox complex."""
+    d, geo, f, pw = _scene_args(scene)
+    e = _c(eps_r).reshape(-1)
+    out = np.empty(3 * e.size, np.complex128)
+    _check(lib().orc_build_rhs(d, geo, f, pw, _ptr(e), C.c_int(int(quad)), _ptr(out)))
+    return out
+
+
+def recover_fields(scene, eps_r, j, kj=None):
+    """recover_fields (solver.hpp:211-249) with K j precomputed (kj) or None: (e, h)."""
+    d, geo, f, pw = _scene_args(scene)
+    e_r = _c(eps_r).reshape(-1)
+    jj = _c(j).reshape(-1)
+    e = np.empty_like(jj)
+    h = np.empty_like(jj) if kj is not None else None
+    kk = _c(kj).reshape(-1) if kj is not None else None
+    _check(lib().orc_recover_fields(d, geo, f, pw, _ptr(e_r), _ptr(jj), _ptr(kk) if kk is not None else None,
+                                    _ptr(e), _ptr(h) if h is not None else None))
+    return e, h
+
+
+def postprocess(scene, eps_r, e, h=None):
+    """postprocess (solver.hpp:258-284): (p_abs, total_absorbed_power, b1_plus or None)."""
+    d, geo, f, _ = _scene_args(scene)
+    e_r = _c(eps_r).reshape(-1)
+    ee = _c(e).reshape(-1)
+    p = np.empty(e_r.size, np.float64)
+    b1 = np.empty(e_r.size, np.float64) if h is not None else None
+    hh = _c(h).reshape(-1) if h is not None else None
+    tot = C.c_double()
+    _check(lib().orc_postprocess(d, geo, f, _ptr(e_r), _ptr(ee), _ptr(hh) if hh is not None else None,
+                                 p.ctypes.data_as(_dp), b1.ctypes.data_as(_dp) if b1 is not None else None,
+                                 C.byref(tot)))
+    return p, tot.value, b1

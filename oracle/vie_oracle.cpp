@@ -1089,3 +1089,178 @@ int orc_hosvd(const double* t, const int64_t dims[3], double tol, int rule, int6
 }
 
 }  // extern "C"
+
+// ---- solve_scene stages (solver.hpp:148-285; grid.hpp:14-100; quadrature.hpp:23-52)
+namespace {
+
+constexpr double kEps0 = 8.8541878128e-12, kMu0 = 1.25663706212e-6, kC0 = 299792458.0;
+constexpr double kPi = 3.141592653589793238462643383279502884;
+
+struct Scene {  // VoxelGrid + DielectricMap frequency + PlaneWave
+  I64 n[3];
+  double res[3], org[3], freq;
+  double pol[3], dir[3], amp;
+  double omega() const { return 2.0 * kPi * freq; }
+  double k0() const { return omega() / kC0; }
+  cd ce() const { return cd(0.0, omega() * kEps0); }
+  I64 nv() const { return n[0] * n[1] * n[2]; }
+  void center(I64 i, I64 j, I64 k, double r[3]) const {
+    r[0] = org[0] + (static_cast<double>(i) + 0.5) * res[0];
+    r[1] = org[1] + (static_cast<double>(j) + 0.5) * res[1];
+    r[2] = org[2] + (static_cast<double>(k) + 0.5) * res[2];
+  }
+  cd phase(const double r[3]) const {
+    return std::exp(cd(0.0, -k0() * (dir[0] * r[0] + dir[1] * r[1] + dir[2] * r[2])));
+  }
+};
+
+Scene make_scene(const int64_t dims[3], const double geo[6], double f, const double* pw) {
+  Scene s{};
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] < 1) throw std::invalid_argument("VoxelGrid: dims must be >= 1");
+    if (!(geo[a] > 0.0)) throw std::invalid_argument("VoxelGrid: resolution must be > 0");
+    s.n[a] = dims[a];
+    s.res[a] = geo[a];
+    s.org[a] = geo[3 + a];
+  }
+  s.freq = f;
+  if (pw) {
+    const double pn = std::sqrt(pw[0] * pw[0] + pw[1] * pw[1] + pw[2] * pw[2]);
+    const double dn = std::sqrt(pw[3] * pw[3] + pw[4] * pw[4] + pw[5] * pw[5]);
+    for (int a = 0; a < 3; ++a) {
+      s.pol[a] = pw[a] / pn;
+      s.dir[a] = pw[3 + a] / dn;
+    }
+    if (std::abs(s.pol[0] * s.dir[0] + s.pol[1] * s.dir[1] + s.pol[2] * s.dir[2]) > 1e-12)
+      throw std::invalid_argument("PlaneWave: polarization must be orthogonal to direction");
+    s.amp = pw[6];
+  }
+  return s;
+}
+
+void gauss01(int p, std::vector<double>& nodes, std::vector<double>& weights) {
+  if (p < 1) throw std::invalid_argument("gauss_rule: need at least one point");
+  nodes.assign(p, 0.0);
+  weights.assign(p, 0.0);
+  for (int i = 0; i < (p + 1) / 2; ++i) {
+    double x = std::cos(kPi * (i + 0.75) / (p + 0.5)), deriv = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int k = 0; k < p; ++k) {
+        const double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * k + 1.0) * x * p2 - k * p3) / (k + 1.0);
+      }
+      deriv = p * (x * p1 - p2) / (x * x - 1.0);
+      const double dx = p1 / deriv;
+      x -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    const double w = 1.0 / ((1.0 - x * x) * deriv * deriv);
+    nodes[i] = 0.5 * (1.0 - x);
+    weights[i] = w;
+    nodes[p - 1 - i] = 0.5 * (1.0 + x);
+    weights[p - 1 - i] = w;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int orc_build_rhs(const int64_t dims[3], const double geo[6], double frequency, const double pw[7],
+                  const double* eps_r, int quad, double* rhs) {
+  return guard([&] {
+    if (quad < 1) throw std::invalid_argument("build_rhs: bad quadrature order");
+    const Scene s = make_scene(dims, geo, frequency, pw);
+    const cd* eps = reinterpret_cast<const cd*>(eps_r);
+    cd* out = reinterpret_cast<cd*>(rhs);
+    const I64 nv = s.nv();
+    std::vector<double> qn, qw;
+    if (quad > 1) gauss01(quad, qn, qw);
+    for (I64 q = 0; q < 3 * nv; ++q) out[q] = cd(0.0);  // CurrentField is zero-initialised
+    for (I64 k = 0; k < s.n[2]; ++k)
+      for (I64 j = 0; j < s.n[1]; ++j)
+        for (I64 i = 0; i < s.n[0]; ++i) {
+          const I64 v = i + s.n[0] * (j + s.n[1] * k);
+          const cd chi = eps[v] - 1.0;
+          if (chi == cd(0.0)) continue;
+          double c[3];
+          s.center(i, j, k, c);
+          cd ph(0.0);
+          if (quad == 1) {
+            ph = s.phase(c);
+          } else {
+            for (int a = 0; a < quad; ++a)
+              for (int b = 0; b < quad; ++b)
+                for (int d = 0; d < quad; ++d) {
+                  const double r[3] = {c[0] + s.res[0] * (qn[a] - 0.5), c[1] + s.res[1] * (qn[b] - 0.5),
+                                       c[2] + s.res[2] * (qn[d] - 0.5)};
+                  ph += qw[a] * qw[b] * qw[d] * s.phase(r);
+                }
+          }
+          for (int q = 0; q < 3; ++q) out[q * nv + v] = s.ce() * chi * (s.pol[q] * (s.amp * ph));
+        }
+  });
+}
+
+int orc_recover_fields(const int64_t dims[3], const double geo[6], double frequency, const double pw[7],
+                       const double* eps_r, const double* j, const double* kj, double* e, double* h) {
+  return guard([&] {
+    const Scene s = make_scene(dims, geo, frequency, pw);
+    const cd* eps = reinterpret_cast<const cd*>(eps_r);
+    const cd* jj = reinterpret_cast<const cd*>(j);
+    cd* eo = reinterpret_cast<cd*>(e);
+    const I64 nv = s.nv();
+    const double inv_v = 1.0 / (s.res[0] * s.res[1] * s.res[2]);
+    const double hd[3] = {s.dir[1] * s.pol[2] - s.dir[2] * s.pol[1], s.dir[2] * s.pol[0] - s.dir[0] * s.pol[2],
+                          s.dir[0] * s.pol[1] - s.dir[1] * s.pol[0]};
+    const double eta0 = std::sqrt(kMu0 / kEps0);
+    for (I64 k = 0; k < s.n[2]; ++k)
+      for (I64 y = 0; y < s.n[1]; ++y)
+        for (I64 i = 0; i < s.n[0]; ++i) {
+          const I64 v = i + s.n[0] * (y + s.n[1] * k);
+          double c[3];
+          s.center(i, y, k, c);
+          const cd chi = eps[v] - 1.0;
+          if (chi == cd(0.0)) {
+            const cd ph = s.phase(c);
+            for (int q = 0; q < 3; ++q) eo[q * nv + v] = s.pol[q] * (s.amp * ph);
+          } else {
+            const cd inv = 1.0 / (s.ce() * chi);
+            for (int q = 0; q < 3; ++q) eo[q * nv + v] = inv * jj[q * nv + v];
+          }
+          if (kj) {
+            const cd ph = s.phase(c);
+            const cd* kk = reinterpret_cast<const cd*>(kj);
+            cd* ho = reinterpret_cast<cd*>(h);
+            for (int q = 0; q < 3; ++q) ho[q * nv + v] = hd[q] * (s.amp / eta0 * ph) + inv_v * kk[q * nv + v];
+          }
+        }
+  });
+}
+
+int orc_postprocess(const int64_t dims[3], const double geo[6], double frequency, const double* eps_r,
+                    const double* e, const double* h, double* p_abs, double* b1, double* total) {
+  return guard([&] {
+    const Scene s = make_scene(dims, geo, frequency, nullptr);
+    const cd* eps = reinterpret_cast<const cd*>(eps_r);
+    const cd* ee = reinterpret_cast<const cd*>(e);
+    const I64 nv = s.nv();
+    double tot = 0.0;
+    for (I64 v = 0; v < nv; ++v) {
+      double e2 = 0.0;
+      for (int q = 0; q < 3; ++q) e2 += std::norm(ee[q * nv + v]);
+      const double p = 0.5 * (-eps[v].imag() * kEps0 * s.omega()) * e2;
+      p_abs[v] = p;
+      tot += p;
+    }
+    if (total) *total = tot * (s.res[0] * s.res[1] * s.res[2]);
+    if (h) {
+      const cd* hh = reinterpret_cast<const cd*>(h);
+      for (I64 v = 0; v < nv; ++v) b1[v] = kMu0 * std::abs(hh[v] + cd(0.0, 1.0) * hh[nv + v]);
+    }
+  });
+}
+
+}  // extern "C"

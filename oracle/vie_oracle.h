@@ -107,6 +107,17 @@ int orc_truncated_svd_values(const double* m, int64_t rows, int64_t cols, double
 int orc_hosvd(const double* t, const int64_t dims[3], double tol, int rule, int64_t ranks[3],
               double* core, double* u1, double* u2, double* u3);
 
+/* solve_scene stages (solver.hpp:148-285), PWC fields (3 blocks of n_vox).
+ * geo = {res0, res1, res2, org0, org1, org2}; pw = {pol0..2, dir0..2, amplitude}
+ * (normalised here, grid.hpp:84-88).  kj may be NULL (no K operator, h untouched);
+ * h may be NULL in postprocess (no b1).                                          */
+int orc_build_rhs(const int64_t dims[3], const double geo[6], double frequency, const double pw[7],
+                  const double* eps_r, int quad, double* rhs);
+int orc_recover_fields(const int64_t dims[3], const double geo[6], double frequency, const double pw[7],
+                       const double* eps_r, const double* j, const double* kj, double* e, double* h);
+int orc_postprocess(const int64_t dims[3], const double geo[6], double frequency, const double* eps_r,
+                    const double* e, const double* h, double* p_abs, double* b1, double* total);
+
 #ifdef __cplusplus
 }
 #endif

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libvie_b200.so")
 SOURCES = ["api.cu", "kernels_fft.cu", "kernels_pencil.cu", "kernels_decomp.cu", "kernels_blas.cu",
-           "kernels_hosvd.cu", "kernels_fft2.cu", "kernels_pencil2.cu"]
+           "kernels_hosvd.cu", "kernels_fft2.cu", "kernels_pencil2.cu", "kernels_scene.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "kernels.cuh", "twiddles_gen.cuh", "hadamard.cuh", "tma.cuh"]
 
 NVCC_FLAGS = [

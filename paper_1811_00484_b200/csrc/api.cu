@@ -1272,3 +1272,136 @@ int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host
 }
 
 }  // extern "C"
+
+// ---- scene stages (solve_scene, solver.hpp:148-285) ----
+namespace {
+
+// VoxelGrid / DielectricMap / PlaneWave (grid.hpp:24-100) -> device descriptor;
+// throws Invalid where the reference constructors throw.
+vie::SceneDev make_scene(const vie_scene* sc, int quad) {
+  if (!sc) throw Invalid("scene: null argument");
+  vie::SceneDev d{};
+  for (int a = 0; a < 3; ++a) {
+    if (sc->dims[a] < 1) throw Invalid("VoxelGrid: dims must be >= 1");
+    if (!(sc->resolution[a] > 0.0)) throw Invalid("VoxelGrid: resolution must be > 0");
+    d.n[a] = sc->dims[a];
+    d.res[a] = sc->resolution[a];
+    d.org[a] = sc->origin[a];
+  }
+  const double pn = std::sqrt(sc->polarization[0] * sc->polarization[0] + sc->polarization[1] * sc->polarization[1] +
+                              sc->polarization[2] * sc->polarization[2]);
+  const double dn = std::sqrt(sc->direction[0] * sc->direction[0] + sc->direction[1] * sc->direction[1] +
+                              sc->direction[2] * sc->direction[2]);
+  if (!(pn > 0.0) || !(dn > 0.0)) throw Invalid("PlaneWave: zero polarization or direction");
+  for (int a = 0; a < 3; ++a) {
+    d.pol[a] = sc->polarization[a] / pn;
+    d.dir[a] = sc->direction[a] / dn;
+  }
+  if (std::abs(d.pol[0] * d.dir[0] + d.pol[1] * d.dir[1] + d.pol[2] * d.dir[2]) > 1e-12)
+    throw Invalid("PlaneWave: polarization must be orthogonal to direction");
+  const double pi = 3.141592653589793238462643383279502884;
+  const double c0 = 299792458.0;
+  d.omega = 2.0 * pi * sc->frequency;                        // grid.hpp:62
+  d.k0 = d.omega / c0;                                       // grid.hpp:63
+  d.ce = make_double2(0.0, d.omega * vie::kEpsilon0);        // grid.hpp:64
+  d.amp = sc->amplitude;
+  d.hdir[0] = d.dir[1] * d.pol[2] - d.dir[2] * d.pol[1];     // direction.cross(polarization)
+  d.hdir[1] = d.dir[2] * d.pol[0] - d.dir[0] * d.pol[2];
+  d.hdir[2] = d.dir[0] * d.pol[1] - d.dir[1] * d.pol[0];
+  d.hamp = sc->amplitude / std::sqrt(vie::kMu0 / vie::kEpsilon0);  // amplitude / eta0
+  if (quad < 1) throw Invalid("build_rhs: bad quadrature order");
+  if (quad > vie::kMaxQuad) throw Invalid("build_rhs: at most 8 quadrature points per axis");
+  d.quad = quad;
+  // Gauss-Legendre on [0, 1]: Newton on the Legendre roots (quadrature.hpp:23-52)
+  const int m = (quad + 1) / 2;
+  for (int i = 0; i < m; ++i) {
+    double x = std::cos(pi * (i + 0.75) / (quad + 0.5));
+    double deriv = 0.0;
+    for (int iter = 0; iter < 100; ++iter) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int k = 0; k < quad; ++k) {
+        const double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * k + 1.0) * x * p2 - k * p3) / (k + 1.0);
+      }
+      deriv = quad * (x * p1 - p2) / (x * x - 1.0);
+      const double dx = p1 / deriv;
+      x -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    const double w = 1.0 / ((1.0 - x * x) * deriv * deriv);
+    d.qn[i] = 0.5 * (1.0 - x);
+    d.qw[i] = w;
+    d.qn[quad - 1 - i] = 0.5 * (1.0 + x);
+    d.qw[quad - 1 - i] = w;
+  }
+  return d;
+}
+
+// ctx may be NULL for the scene stages: the caller's current device, and the
+// given stream (NULL = the legacy default stream).
+cudaStream_t ctx_stream(vie_ctx ctx, void* stream) {
+  if (ctx) VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+  return stream ? static_cast<cudaStream_t>(stream) : (ctx ? ctx->stream : cudaStreamLegacy);
+}
+
+}  // namespace
+
+extern "C" {
+
+int vie_build_rhs(vie_ctx ctx, const vie_scene* scene, const double* eps_r, int quad_points_per_axis, double* rhs,
+                  void* stream) {
+  return guard([&] {
+    if (!eps_r || !rhs) throw Invalid("build_rhs: null argument");
+    const vie::SceneDev sc = make_scene(scene, quad_points_per_axis);
+    vie::launch_build_rhs(sc, reinterpret_cast<const double2*>(eps_r), reinterpret_cast<double2*>(rhs),
+                          ctx_stream(ctx, stream));
+  });
+}
+
+int vie_recover_fields(vie_ctx ctx, const vie_scene* scene, const double* eps_r, const double* j, vie_op op_k,
+                       double* e, double* h, void* stream) {
+  return guard([&] {
+    if (!eps_r || !j || !e) throw Invalid("recover_fields: null argument");
+    const vie::SceneDev sc = make_scene(scene, 1);
+    if (op_k) {
+      if (!h) throw Invalid("recover_fields: h buffer needed with the K operator");
+      if (op_k->kind != VIE_KIND_K) throw Invalid("recover_fields: op_k must be a K operator");
+      if (op_k->g.S != 3) throw Invalid("recover_fields: PWC fields only (grid.hpp:114-115)");
+      if (op_k->g.n1 != sc.n[0] || op_k->g.n2 != sc.n[1] || op_k->g.n3 != sc.n[2])
+        throw Invalid("apply_operator: dim mismatch");
+      if (h == j || h == e) throw Invalid("recover_fields: h must not alias j or e");
+    }
+    cudaStream_t st = ctx_stream(ctx ? ctx : (op_k ? op_k->ctx : nullptr), stream);
+    const double2* eps = reinterpret_cast<const double2*>(eps_r);
+    const double2* jd = reinterpret_cast<const double2*>(j);
+    vie::launch_recover_e(sc, eps, jd, reinterpret_cast<double2*>(e), st);
+    if (op_k) {
+      double2* hd = reinterpret_cast<double2*>(h);
+      run_matvec(op_k, jd, hd, st, nullptr, 0.0, 0);  // K j (solver.hpp:234)
+      vie::launch_add_hinc(sc, 1.0 / (sc.res[0] * sc.res[1] * sc.res[2]), hd, st);
+    }
+  });
+}
+
+int vie_postprocess(vie_ctx ctx, const vie_scene* scene, const double* eps_r, const double* e, const double* h,
+                    double* p_abs, double* b1_plus, double* total_absorbed_power_host, void* stream) {
+  return guard([&] {
+    if (!eps_r || !e || !p_abs) throw Invalid("postprocess: null argument");
+    if (h && !b1_plus) throw Invalid("postprocess: b1_plus buffer needed with h");
+    const vie::SceneDev sc = make_scene(scene, 1);
+    cudaStream_t st = ctx_stream(ctx, stream);
+    double* buf = nullptr;
+    VIE_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (vie::kRedBlocks + 1), st));
+    vie::launch_postprocess(sc, reinterpret_cast<const double2*>(eps_r), reinterpret_cast<const double2*>(e),
+                            reinterpret_cast<const double2*>(h), p_abs, h ? b1_plus : nullptr, buf + 1, buf,
+                            sc.res[0] * sc.res[1] * sc.res[2], st);
+    double total = 0.0;
+    VIE_CUDA_CHECK(cudaMemcpyAsync(&total, buf, sizeof(double), cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaFreeAsync(buf, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (total_absorbed_power_host) *total_absorbed_power_host = total;
+  });
+}
+
+}  // extern "C"

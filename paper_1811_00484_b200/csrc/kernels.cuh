@@ -126,4 +126,27 @@ void launch_scale_inv(const double2* x, double2* y, const double2* s, double div
 void launch_basis_update(double2* x, const double2* V, int64_t ldv, const double2* coef, int j, int64_t n,
                          cudaStream_t st);
 
+// ---- scene stages around the solve (kernels_scene.cu; solver.hpp:148-285)
+constexpr double kEpsilon0 = 8.8541878128e-12;  // grid.hpp:15
+constexpr double kMu0 = 1.25663706212e-6;       // grid.hpp:16
+constexpr int kMaxQuad = 8;
+struct SceneDev {
+  int64_t n[3];
+  double res[3], org[3];
+  double k0, omega;
+  double2 ce;             // c_e = i omega eps0 (grid.hpp:64)
+  double pol[3], dir[3];  // normalised (grid.hpp:84-86)
+  double amp;
+  double hdir[3];         // dir x pol (grid.hpp:97)
+  double hamp;            // amp / eta0
+  int quad;               // build_rhs quadrature points per axis
+  double qn[kMaxQuad], qw[kMaxQuad];  // Gauss rule on [0, 1] (quadrature.hpp:23-52)
+};
+void launch_build_rhs(const SceneDev& sc, const double2* eps, double2* rhs, cudaStream_t st);
+void launch_recover_e(const SceneDev& sc, const double2* eps, const double2* j, double2* e, cudaStream_t st);
+void launch_add_hinc(const SceneDev& sc, double inv_v, double2* h, cudaStream_t st);
+// p_abs, b1 (h != nullptr), total[0] = scale * sum p_abs; partials: kRedBlocks doubles
+void launch_postprocess(const SceneDev& sc, const double2* eps, const double2* e, const double2* h, double* p_abs,
+                        double* b1, double* partials, double* total, double scale, cudaStream_t st);
+
 }  // namespace vie

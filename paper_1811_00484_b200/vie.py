@@ -363,3 +363,122 @@ def gmres(op: EmbeddedSpectrum, eps_r, inv_v: float, rhs, cfg: GmresConfig = Gmr
                                  C.byref(it), C.byref(fr), hist.ctypes.data_as(_dp), int(history_cap),
                                  C.byref(hl), C.byref(cv)))
     return GmresResult(x, hist[: min(hl.value, history_cap)].tolist(), fr.value, it.value, bool(cv.value))
+
+
+# ----------------------------------------------------------------------------- scene stages
+@dataclass
+class VoxelGrid:  # grid.hpp:24-46
+    dims: tuple
+    resolution: tuple = (1.0, 1.0, 1.0)
+    origin: tuple = (0.0, 0.0, 0.0)
+
+    def voxel_volume(self) -> float:
+        return float(self.resolution[0] * self.resolution[1] * self.resolution[2])
+
+
+@dataclass
+class DielectricMap:  # grid.hpp:52-75; eps_r: CUDA complex128 tensor of n_vox (flat = i + n1 (j + n2 k))
+    grid: VoxelGrid
+    eps_r: object
+    frequency: float
+
+
+@dataclass
+class PlaneWave:  # grid.hpp:78-100 (normalised and checked by the library)
+    polarization: tuple = (1.0, 0.0, 0.0)
+    direction: tuple = (0.0, 0.0, 1.0)
+    amplitude: float = 1.0
+
+
+class _Scene(C.Structure):  # vie_scene (include/vie_b200.h)
+    _fields_ = [("dims", C.c_int64 * 3), ("resolution", C.c_double * 3), ("origin", C.c_double * 3),
+                ("frequency", C.c_double), ("polarization", C.c_double * 3), ("direction", C.c_double * 3),
+                ("amplitude", C.c_double)]
+
+
+def _scene(m: DielectricMap, inc: PlaneWave | None) -> _Scene:
+    inc = inc or PlaneWave()
+    return _Scene((C.c_int64 * 3)(*[int(v) for v in m.grid.dims]),
+                  (C.c_double * 3)(*[float(v) for v in m.grid.resolution]),
+                  (C.c_double * 3)(*[float(v) for v in m.grid.origin]), float(m.frequency),
+                  (C.c_double * 3)(*[float(v) for v in inc.polarization]),
+                  (C.c_double * 3)(*[float(v) for v in inc.direction]), float(inc.amplitude))
+
+
+def _eps_dev(m: DielectricMap):
+    torch = _torch()
+    nv = int(np.prod(m.grid.dims))
+    e = m.eps_r
+    if not (isinstance(e, torch.Tensor) and e.is_cuda and e.numel() == nv):
+        raise ValueError("DielectricMap: eps_r must be a CUDA tensor of n_vox values")
+    return e.to(torch.complex128).contiguous()
+
+
+def _field_dev(x, nv: int, what: str):
+    torch = _torch()
+    if not (isinstance(x, torch.Tensor) and x.is_cuda and x.dtype == torch.complex128 and x.numel() == 3 * nv):
+        raise ValueError(f"{what}: expected a CUDA complex128 PWC field of 3 n_vox values")
+    return x.contiguous()
+
+
+def build_rhs(m: DielectricMap, inc: PlaneWave, quad_points_per_axis: int = 1, stream=None):
+    """build_rhs (solver.hpp:148-179) on the device: 3 n_vox complex (PWC)."""
+    torch = _torch()
+    eps = _eps_dev(m)
+    sc = _scene(m, inc)
+    out = torch.empty(3 * eps.numel(), dtype=torch.complex128, device=eps.device)
+    with torch.cuda.device(eps.device):
+        _check(lib().vie_build_rhs(None, C.byref(sc), C.c_void_p(eps.data_ptr()), C.c_int(int(quad_points_per_axis)),
+                                   C.c_void_p(out.data_ptr()), C.c_void_p(_stream_handle(stream, eps.device))))
+    return out
+
+
+@dataclass
+class Fields:  # solver.hpp:202-206
+    e: object
+    h: object = None
+    has_h: bool = False
+
+
+def recover_fields(j, m: DielectricMap, inc: PlaneWave, op_k: "EmbeddedSpectrum | None" = None, stream=None) -> Fields:
+    """recover_fields (solver.hpp:211-249): e from j (incident field where chi_e = 0);
+    h = h_inc + K j / V through the device K matvec when op_k is given."""
+    torch = _torch()
+    eps = _eps_dev(m)
+    j = _field_dev(j, eps.numel(), "recover_fields")
+    sc = _scene(m, inc)
+    e = torch.empty_like(j)
+    h = torch.empty_like(j) if op_k is not None else None
+    with torch.cuda.device(eps.device):
+        _check(lib().vie_recover_fields(None, C.byref(sc), C.c_void_p(eps.data_ptr()), C.c_void_p(j.data_ptr()),
+                                        C.c_void_p(op_k.handle if op_k is not None else None), C.c_void_p(e.data_ptr()),
+                                        C.c_void_p(h.data_ptr() if h is not None else None),
+                                        C.c_void_p(_stream_handle(stream, eps.device))))
+    return Fields(e, h, h is not None)
+
+
+@dataclass
+class PostProcess:  # solver.hpp:251-256
+    p_abs: object
+    total_absorbed_power: float
+    b1_plus: object = None
+    has_b1: bool = False
+
+
+def postprocess(fields: Fields, m: DielectricMap, stream=None) -> PostProcess:
+    """postprocess (solver.hpp:258-284): p_abs = sigma |e|^2 / 2, total power, |b1+|."""
+    torch = _torch()
+    eps = _eps_dev(m)
+    nv = eps.numel()
+    e = _field_dev(fields.e, nv, "postprocess")
+    h = _field_dev(fields.h, nv, "postprocess") if fields.has_h else None
+    sc = _scene(m, None)
+    p = torch.empty(nv, dtype=torch.float64, device=eps.device)
+    b1 = torch.empty(nv, dtype=torch.float64, device=eps.device) if h is not None else None
+    tot = C.c_double()
+    with torch.cuda.device(eps.device):
+        _check(lib().vie_postprocess(None, C.byref(sc), C.c_void_p(eps.data_ptr()), C.c_void_p(e.data_ptr()),
+                                     C.c_void_p(h.data_ptr() if h is not None else None), C.c_void_p(p.data_ptr()),
+                                     C.c_void_p(b1.data_ptr() if b1 is not None else None), C.byref(tot),
+                                     C.c_void_p(_stream_handle(stream, eps.device))))
+    return PostProcess(p, tot.value, b1, b1 is not None)
