@@ -451,7 +451,7 @@ def recover_fields(j, m: DielectricMap, inc: PlaneWave, op_k: "EmbeddedSpectrum 
     h = torch.empty_like(j) if op_k is not None else None
     with torch.cuda.device(eps.device):
         _check(lib().vie_recover_fields(None, C.byref(sc), C.c_void_p(eps.data_ptr()), C.c_void_p(j.data_ptr()),
-                                        C.c_void_p(op_k.handle if op_k is not None else None), C.c_void_p(e.data_ptr()),
+                                        (op_k.handle if op_k is not None else None), C.c_void_p(e.data_ptr()),
                                         C.c_void_p(h.data_ptr() if h is not None else None),
                                         C.c_void_p(_stream_handle(stream, eps.device))))
     return Fields(e, h, h is not None)
