@@ -6,10 +6,11 @@ in include/vie_b200.h); ``vie`` mirrors the reference operator API over it.
 from .vie import (KIND_K, KIND_N, PWC, PWL, DftService, EmbeddedSpectrum, GmresConfig, GmresResult, TuckerForm,
                   VieError, apply_operator, apply_operator_batch, apply_system, build_operator_spectra, component_table, gmres, lib,
                   ncur, tucker_compress, RULE_ENERGY, RULE_SIGMA_MAX, DielectricMap, Fields, PlaneWave,
-                  PostProcess, VoxelGrid, build_rhs, postprocess, recover_fields)
+                  PostProcess, VoxelGrid, build_rhs, postprocess, recover_fields,
+                  SolveReport, solve_scene)
 
 __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "GmresConfig", "GmresResult",
            "TuckerForm", "VieError", "apply_operator", "apply_operator_batch", "apply_system", "build_operator_spectra",
            "component_table", "gmres", "lib", "ncur", "tucker_compress", "RULE_ENERGY", "RULE_SIGMA_MAX",
            "DielectricMap", "Fields", "PlaneWave", "PostProcess", "VoxelGrid", "build_rhs", "postprocess",
-           "recover_fields"]
+           "recover_fields", "SolveReport", "solve_scene"]

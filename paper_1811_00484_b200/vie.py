@@ -482,3 +482,38 @@ def postprocess(fields: Fields, m: DielectricMap, stream=None) -> PostProcess:
                                      C.c_void_p(b1.data_ptr() if b1 is not None else None), C.byref(tot),
                                      C.c_void_p(_stream_handle(stream, eps.device))))
     return PostProcess(p, tot.value, b1, b1 is not None)
+
+
+@dataclass
+class SolveReport:  # solver.hpp:286-295
+    j: object
+    residual_history: list
+    final_relative_residual: float
+    iterations: int
+    converged: bool
+    wall_time_s: float
+    fields: Fields
+    post: PostProcess
+
+
+def solve_scene(m: DielectricMap, inc: PlaneWave, op_n: EmbeddedSpectrum, op_k: "EmbeddedSpectrum | None" = None,
+                cfg: GmresConfig = GmresConfig()) -> SolveReport:
+    """solve_scene (solver.hpp:300-326) on the device: build_rhs, restarted GMRES on the
+    JVIE system (M_eps - M_chi N / V), recover_fields, postprocess.  PWC operators."""
+    import time
+
+    torch = _torch()
+    if op_n.kind != KIND_N or op_n.basis != PWC:
+        raise ValueError("solve_scene: op_n must be the PWC N operator")
+    if tuple(op_n.grid_dims) != tuple(int(d) for d in m.grid.dims):
+        raise ValueError("apply_operator: dim mismatch")
+    eps = _eps_dev(m)
+    torch.cuda.synchronize(eps.device)
+    t0 = time.perf_counter()
+    rhs = build_rhs(m, inc)
+    g = gmres(op_n, eps, 1.0 / m.grid.voxel_volume(), rhs, cfg)
+    f = recover_fields(g.solution, m, inc, op_k)
+    post = postprocess(f, m)
+    torch.cuda.synchronize(eps.device)
+    return SolveReport(g.solution, g.residual_history, g.final_relative_residual, g.iterations, g.converged,
+                       time.perf_counter() - t0, f, post)

@@ -99,3 +99,41 @@ def test_scene_errors_match_reference(vie):
         vie.build_rhs(dmap(vie, sc, eps), vie.PlaneWave((1, 0, 1), (0, 0, 1)))
     with pytest.raises(ValueError, match="quadrature"):
         vie.build_rhs(dmap(vie, sc, eps), vie.PlaneWave(), 0)
+
+
+def test_solve_scene_matches_oracle_pipeline(vie, orc):
+    """solve_scene (solver.hpp:300-326) end to end on the device against the oracle's
+    build_rhs -> gmres(apply_system) -> recover_fields(K) -> postprocess.  Synthetic N/K
+    forms scaled to a well-posed perturbation of M_eps (unit voxels, 1/V = 1)."""
+    N = 0
+    dims = (6, 5, 4)
+    nv = int(np.prod(dims))
+    sc = scene(dims, 2.98e8, res=1.0, pol=(0, 1, 0), d=(1, 0, 0), amp=2.0)
+    rng = np.random.default_rng(21)
+    eps = 1 + rng.uniform(1, 5, nv) - 1j * rng.uniform(0, 1, nv)
+    eps[:: 5] = 1.0  # vacuum voxels keep the incident field
+    dft = vie.DftService(0)
+    ops, oforms = {}, {}
+    for kind, seed in ((N, 31), (K, 32)):
+        spatial, par = spatial_tucker_forms(kind, PWC, dims, 3, seed)
+        spatial = [(core * 1e-4, us) for core, us in spatial]
+        comps, _, _ = vie.component_table(kind, PWC)
+        forms = [vie.TuckerForm(dft, dims, spatial[c][0], spatial[c][1], par[c]) for c in range(len(comps))]
+        ops[kind] = vie.build_operator_spectra(kind, PWC, dims, comps, forms, dft)
+        oforms[kind] = fourier_forms(spatial, par)
+    rep = vie.solve_scene(dmap(vie, sc, eps), pw(vie, sc), ops[N], ops[K], vie.GmresConfig(1e-10, 10, 20))
+
+    rhs = orc.build_rhs(sc, eps)
+    g = orc.gmres_system_tucker(PWC, dims, oforms[N], eps, 1.0, rhs, tol=1e-10, inner=10, outer=20)
+    kj = orc.apply_operator_tucker(K, PWC, dims, oforms[K], g.solution)
+    e, h = orc.recover_fields(sc, eps, g.solution, kj)
+    p, tot, b1 = orc.postprocess(sc, eps, e, h)
+    assert g.converged and rep.converged
+    assert abs(g.iterations - rep.iterations) <= 1
+    assert abs(g.final_relative_residual - rep.final_relative_residual) <= 1e-8
+    assert rel(rep.j.cpu().numpy(), g.solution) < 1e-8
+    assert rel(rep.fields.e.cpu().numpy(), e) < 1e-8
+    assert rel(rep.fields.h.cpu().numpy(), h) < 1e-8
+    assert rel(rep.post.p_abs.cpu().numpy(), p) < 1e-8
+    assert rel(rep.post.b1_plus.cpu().numpy(), b1) < 1e-8
+    assert abs(rep.post.total_absorbed_power - tot) < 1e-8 * abs(tot)
