@@ -411,6 +411,126 @@ inline GmresResult gmres_system(const std::vector<cplx>& eps_r, double inv_v, co
   return res;
 }
 
+// ------------------------------------------------------------------ solve_scene stages
+struct VoxelGrid {  // grid.hpp:24-46
+  std::array<Index, 3> dims{1, 1, 1};
+  std::array<double, 3> resolution{1.0, 1.0, 1.0};
+  std::array<double, 3> origin{0.0, 0.0, 0.0};
+  Index num_voxels() const { return dims[0] * dims[1] * dims[2]; }
+  double voxel_volume() const { return resolution[0] * resolution[1] * resolution[2]; }
+};
+
+struct DielectricMap {  // grid.hpp:52-75: eps_r per voxel, flat = i + n1 (j + n2 k)
+  VoxelGrid grid;
+  std::vector<cplx> eps_r;
+  double frequency = 0.0;
+  DielectricMap() = default;
+  DielectricMap(const VoxelGrid& g, double f)
+      : grid(g), eps_r(static_cast<size_t>(g.num_voxels()), cplx(1.0)), frequency(f) {}
+  cplx& eps(Index i, Index j, Index k) { return eps_r[static_cast<size_t>(i + grid.dims[0] * (j + grid.dims[1] * k))]; }
+  void set_voxel(Index i, Index j, Index k, double eps_prime, double sigma) {  // grid.hpp:72-74
+    eps(i, j, k) = cplx(eps_prime, -sigma / (8.8541878128e-12 * 2.0 * 3.141592653589793238462643383279502884 * frequency));
+  }
+};
+
+struct PlaneWave {  // grid.hpp:78-100 (normalised and checked by the library)
+  std::array<double, 3> polarization{1.0, 0.0, 0.0};
+  std::array<double, 3> direction{0.0, 0.0, 1.0};
+  double amplitude = 1.0;
+};
+
+inline vie_scene make_scene(const DielectricMap& m, const PlaneWave& inc) {
+  vie_scene s{};
+  for (int a = 0; a < 3; ++a) {
+    s.dims[a] = m.grid.dims[a];
+    s.resolution[a] = m.grid.resolution[a];
+    s.origin[a] = m.grid.origin[a];
+    s.polarization[a] = inc.polarization[a];
+    s.direction[a] = inc.direction[a];
+  }
+  s.frequency = m.frequency;
+  s.amplitude = inc.amplitude;
+  return s;
+}
+
+inline CurrentField field_from_device(const DeviceBuffer& b, const std::array<Index, 3>& d) {
+  std::vector<cplx> v(static_cast<size_t>(3 * d[0] * d[1] * d[2]));
+  cuda_check(cudaDeviceSynchronize());
+  b.download(v.data(), v.size() * sizeof(cplx));
+  return CurrentField::from_vector(v, d);
+}
+
+// build_rhs (solver.hpp:148-179)
+inline CurrentField build_rhs(const DielectricMap& m, const PlaneWave& inc, int quad_points_per_axis = 1) {
+  const vie_scene sc = make_scene(m, inc);
+  const size_t nv = m.eps_r.size();
+  DeviceBuffer de(nv * sizeof(cplx)), dr(3 * nv * sizeof(cplx));
+  de.upload(m.eps_r.data(), nv * sizeof(cplx));
+  check(vie_build_rhs(nullptr, &sc, de.get(), quad_points_per_axis, dr.get(), nullptr));
+  return field_from_device(dr, m.grid.dims);
+}
+
+struct Fields {  // solver.hpp:202-206
+  CurrentField e;
+  CurrentField h;
+  bool has_h = false;
+};
+
+// recover_fields (solver.hpp:211-249); op_k: the K operator or nullptr
+inline Fields recover_fields(const CurrentField& j, const DielectricMap& m, const PlaneWave& inc,
+                             const EmbeddedSpectrum* op_k) {
+  if (j.dims() != m.grid.dims || j.comp.size() != 3) throw std::invalid_argument("recover_fields: dim mismatch");
+  const vie_scene sc = make_scene(m, inc);
+  const size_t nv = m.eps_r.size();
+  const std::vector<cplx> jv = j.to_vector();
+  DeviceBuffer de(nv * sizeof(cplx)), dj(3 * nv * sizeof(cplx)), dE(3 * nv * sizeof(cplx));
+  DeviceBuffer dh(op_k ? 3 * nv * sizeof(cplx) : 0);
+  de.upload(m.eps_r.data(), nv * sizeof(cplx));
+  dj.upload(jv.data(), jv.size() * sizeof(cplx));
+  check(vie_recover_fields(nullptr, &sc, de.get(), dj.get(), op_k ? op_k->handle() : nullptr, dE.get(),
+                           op_k ? dh.get() : nullptr, nullptr));
+  Fields f;
+  f.e = field_from_device(dE, m.grid.dims);
+  if (op_k) {
+    f.h = field_from_device(dh, m.grid.dims);
+    f.has_h = true;
+  }
+  return f;
+}
+
+struct PostProcess {  // solver.hpp:251-256 (real per-voxel values)
+  std::vector<double> p_abs;
+  double total_absorbed_power = 0.0;
+  std::vector<double> b1_plus;
+  bool has_b1 = false;
+};
+
+// postprocess (solver.hpp:258-284)
+inline PostProcess postprocess(const Fields& f, const DielectricMap& m) {
+  const vie_scene sc = make_scene(m, PlaneWave{});
+  const size_t nv = m.eps_r.size();
+  const std::vector<cplx> ev = f.e.to_vector();
+  DeviceBuffer de(nv * sizeof(cplx)), dE(3 * nv * sizeof(cplx)), dp(nv * sizeof(double));
+  DeviceBuffer dh(f.has_h ? 3 * nv * sizeof(cplx) : 0), db(f.has_h ? nv * sizeof(double) : 0);
+  de.upload(m.eps_r.data(), nv * sizeof(cplx));
+  dE.upload(ev.data(), ev.size() * sizeof(cplx));
+  if (f.has_h) {
+    const std::vector<cplx> hv = f.h.to_vector();
+    dh.upload(hv.data(), hv.size() * sizeof(cplx));
+  }
+  PostProcess out;
+  check(vie_postprocess(nullptr, &sc, de.get(), dE.get(), f.has_h ? dh.get() : nullptr, dp.get(),
+                        f.has_h ? db.get() : nullptr, &out.total_absorbed_power, nullptr));
+  out.p_abs.resize(nv);
+  dp.download(out.p_abs.data(), nv * sizeof(double));
+  if (f.has_h) {
+    out.b1_plus.resize(nv);
+    db.download(out.b1_plus.data(), nv * sizeof(double));
+    out.has_b1 = true;
+  }
+  return out;
+}
+
 }  // namespace b200
 }  // namespace vie
 

@@ -299,6 +299,75 @@ int main() {
     expect(thrown, "invalid config must throw");
   });
 
+  // solve_scene stages (solver.hpp:148-285) through the wrapper vs the oracle
+  run("SceneStages.MatchOracle", [&] {
+    VoxelGrid g{{5, 4, 6}, {0.004, 0.004, 0.004}, {-0.01, 0.0, 0.02}};
+    DielectricMap m(g, 2.98e8);
+    for (Index k = 1; k < 5; ++k)
+      for (Index j = 1; j < 3; ++j)
+        for (Index i = 1; i < 4; ++i) m.set_voxel(i, j, k, 40.0 + i, 0.5);
+    PlaneWave inc{{0.0, 1.0, -1.0}, {0.0, 1.0, 1.0}, 2.0};
+    const double geo[6] = {0.004, 0.004, 0.004, -0.01, 0.0, 0.02};
+    const double pw[7] = {0.0, 1.0, -1.0, 0.0, 1.0, 1.0, 2.0};
+    const int64_t dims[3] = {5, 4, 6};
+    const size_t nv = m.eps_r.size();
+    auto rel_err = [](const std::vector<cplx>& a, const std::vector<cplx>& b) {
+      double num = 0.0, den = 0.0;
+      for (size_t i = 0; i < a.size(); ++i) {
+        num += std::norm(a[i] - b[i]);
+        den += std::norm(b[i]);
+      }
+      return std::sqrt(num / den);
+    };
+    for (int quad : {1, 3}) {
+      const std::vector<cplx> rhs = build_rhs(m, inc, quad).to_vector();
+      std::vector<cplx> ref(3 * nv);
+      if (orc_build_rhs(dims, geo, 2.98e8, pw, reinterpret_cast<const double*>(m.eps_r.data()), quad,
+                        reinterpret_cast<double*>(ref.data())))
+        throw std::runtime_error(orc_last_error());
+      expect(rel_err(rhs, ref) <= 1e-13, "build_rhs quad " + std::to_string(quad));
+    }
+    CurrentField j(g.dims), h(g.dims);
+    for (int q = 0; q < 3; ++q) {
+      j.comp[q] = Tensor3(5, 4, 6);
+      h.comp[q] = Tensor3(5, 4, 6);
+      if (orc_random_tensor(5, 4, 6, 90 + q, reinterpret_cast<double*>(j.comp[q].data.data())) ||
+          orc_random_tensor(5, 4, 6, 95 + q, reinterpret_cast<double*>(h.comp[q].data.data())))
+        throw std::runtime_error(orc_last_error());
+    }
+    Fields f = recover_fields(j, m, inc, nullptr);
+    expect(!f.has_h, "no K operator, no h");
+    const std::vector<cplx> jv = j.to_vector();
+    std::vector<cplx> eref(3 * nv);
+    if (orc_recover_fields(dims, geo, 2.98e8, pw, reinterpret_cast<const double*>(m.eps_r.data()),
+                           reinterpret_cast<const double*>(jv.data()), nullptr,
+                           reinterpret_cast<double*>(eref.data()), nullptr))
+      throw std::runtime_error(orc_last_error());
+    expect(rel_err(f.e.to_vector(), eref) <= 1e-13, "recover_fields e");
+    f.h = h;
+    f.has_h = true;
+    PostProcess pp = postprocess(f, m);
+    const std::vector<cplx> hv = h.to_vector();
+    std::vector<double> pref(nv), bref(nv);
+    double tref = 0.0;
+    if (orc_postprocess(dims, geo, 2.98e8, reinterpret_cast<const double*>(m.eps_r.data()),
+                        reinterpret_cast<const double*>(eref.data()), reinterpret_cast<const double*>(hv.data()),
+                        pref.data(), bref.data(), &tref))
+      throw std::runtime_error(orc_last_error());
+    for (size_t v = 0; v < nv; ++v) {
+      expect(std::abs(pp.p_abs[v] - pref[v]) <= 1e-12 * std::abs(pref[v]) + 1e-300, "p_abs");
+      expect(std::abs(pp.b1_plus[v] - bref[v]) <= 1e-12 * bref[v], "b1_plus");
+    }
+    expect(std::abs(pp.total_absorbed_power - tref) <= 1e-12 * std::abs(tref), "total power");
+    bool thrown = false;
+    try {
+      build_rhs(m, PlaneWave{{1.0, 0.0, 1.0}, {0.0, 0.0, 1.0}, 1.0});
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    expect(thrown, "non-orthogonal plane wave must throw");
+  });
+
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
 }
