@@ -276,6 +276,40 @@ def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=
     return out
 
 
+def scene_stages_bench(vie, torch, grid, peak, reps=5):
+    """The solve_scene stages around the solve (build_rhs, recover_fields' e pass,
+    postprocess with h; kernels_scene.cu) at the workload grid: one streaming pass
+    each, so each is reported against the HBM roofline with its algorithmic bytes
+    per voxel (eps 16 B, a PWC field 48 B, h_x/h_y 32 B, p_abs / b1 8 B each)."""
+    n1, n2, n3 = grid
+    nv = n1 * n2 * n3
+    eps = torch.ones((n3, n2, n1), dtype=torch.complex128, device="cuda")
+    eps[1:-1, 1:-1, 1:-1] = complex(50.0, -0.7 / (8.8541878128e-12 * 2 * np.pi * 2.98e8))
+    m = vie.DielectricMap(vie.VoxelGrid(grid, (1e-3,) * 3), eps.reshape(-1), 2.98e8)
+    inc = vie.PlaneWave((1, 0, 0), (0, 0, 1), 1.0)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    j = torch.randn(3 * nv, dtype=torch.complex128, device="cuda", generator=g)
+    h = torch.randn(3 * nv, dtype=torch.complex128, device="cuda", generator=g)
+    f = vie.Fields(j, h, True)
+    stages = {"build_rhs": (lambda: vie.build_rhs(m, inc), 16 + 48),
+              "recover_e": (lambda: vie.recover_fields(j, m, inc), 16 + 48 + 48),
+              "postprocess": (lambda: vie.postprocess(f, m), 16 + 48 + 32 + 8 + 8)}
+    out = {"grid": list(grid), "voxels": nv}
+    for name, (fn, bpv) in stages.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = bpv * nv / (ms * 1e-3) / 1e9
+        out[name] = {"ms": ms, "bytes_per_voxel": bpv, "achieved_gbs": gbs, "frac": gbs / peak}
+    return out
+
+
 # ------------------------------------------------------------------ B200 arm
 def run_b200(args):
     import torch
@@ -429,6 +463,9 @@ def run_b200(args):
     solve = None
     if rank == 0 and world == 1 and not args.no_solve:
         solve = gmres_solve_bench(vie, dft, torch, with_cpu=not args.no_cpu_baseline)
+    scene = None
+    if rank == 0 and world == 1 and not args.no_solve:
+        scene = scene_stages_bench(vie, torch, grid, peak)
 
     fl = flops_model(grid, basis, nc, r)
     if rank == 0:
@@ -464,6 +501,7 @@ def run_b200(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gmres_solve": solve,
+            "scene_stages": scene,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -1391,14 +1391,21 @@ int vie_postprocess(vie_ctx ctx, const vie_scene* scene, const double* eps_r, co
     if (h && !b1_plus) throw Invalid("postprocess: b1_plus buffer needed with h");
     const vie::SceneDev sc = make_scene(scene, 1);
     cudaStream_t st = ctx_stream(ctx, stream);
-    double* buf = nullptr;
-    VIE_CUDA_CHECK(cudaMallocAsync(reinterpret_cast<void**>(&buf), sizeof(double) * (vie::kRedBlocks + 1), st));
+    // per-device partials buffer, allocated once (a pool allocation per call costs
+    // milliseconds when the pool trims at the synchronisation below); the call holds
+    // the lock until its result is read, so concurrent calls serialise here
+    static std::mutex buf_mu;
+    static std::map<int, double*> bufs;
+    std::lock_guard<std::mutex> lock(buf_mu);
+    int dev = 0;
+    VIE_CUDA_CHECK(cudaGetDevice(&dev));
+    double*& buf = bufs[dev];
+    if (!buf) VIE_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&buf), sizeof(double) * (vie::kRedBlocks + 1)));
     vie::launch_postprocess(sc, reinterpret_cast<const double2*>(eps_r), reinterpret_cast<const double2*>(e),
                             reinterpret_cast<const double2*>(h), p_abs, h ? b1_plus : nullptr, buf + 1, buf,
                             sc.res[0] * sc.res[1] * sc.res[2], st);
     double total = 0.0;
     VIE_CUDA_CHECK(cudaMemcpyAsync(&total, buf, sizeof(double), cudaMemcpyDeviceToHost, st));
-    VIE_CUDA_CHECK(cudaFreeAsync(buf, st));
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
     if (total_absorbed_power_host) *total_absorbed_power_host = total;
   });
