@@ -66,6 +66,15 @@ int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host
 int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ranks[3],
                             const double* core_host, const double* u1_host, const double* u2_host,
                             const double* u3_host, const int sign[3], int domain, vie_tucker* out);
+/* Tucker+CP form (decomp.hpp:143-148, merged factors W_q = U_q V_q, n_q x rank):
+ * S = sum_l W1(:,l) o W2(:,l) o W3(:,l), held as a Tucker form with the
+ * superdiagonal rank^3 core, so the fused decompress x Hadamard matvec serves the
+ * reference's TuckerCpLoop / decompress_cp strategies (operator.hpp:248-261,
+ * 346-362).  domain as for vie_tucker_from_factors (1 = transform_factors(
+ * TuckerCPForm) output, operator.hpp:92-106).                                   */
+int vie_tucker_from_cp(vie_ctx ctx, const int64_t dims[3], int64_t rank, const double* w1_host,
+                       const double* w2_host, const double* w3_host, const int sign[3], int domain,
+                       vie_tucker* out);
 int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]);
 int vie_tucker_destroy(vie_tucker t);
 

@@ -337,3 +337,12 @@ def postprocess(scene, eps_r, e, h=None):
                                  p.ctypes.data_as(_dp), b1.ctypes.data_as(_dp) if b1 is not None else None,
                                  C.byref(tot)))
     return p, tot.value, b1
+
+
+def decompress_cp(edims, ws) -> np.ndarray:
+    """decompress_cp (operator.hpp:248-261) of merged Fourier factors W_q (2n_q x R)."""
+    ws = [np.asfortranarray(np.asarray(w, np.complex128)) for w in ws]
+    out = np.empty(int(np.prod(edims)), np.complex128)
+    _check(lib().orc_decompress_cp(_i64(edims), C.c_int64(ws[0].shape[1]), ws[0].ctypes.data_as(_dp),
+                                   ws[1].ctypes.data_as(_dp), ws[2].ctypes.data_as(_dp), _ptr(out)))
+    return out

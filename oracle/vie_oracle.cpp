@@ -921,6 +921,32 @@ int orc_decompress_tucker(const int64_t edims[3], const int64_t ranks[3], const 
   });
 }
 
+int orc_decompress_cp(const int64_t edims[3], int64_t rank, const double* w1, const double* w2,
+                      const double* w3, double* dst) {
+  return guard([&] {
+    const I64 m1 = edims[0], m2 = edims[1], m3 = edims[2];
+    const cd* a = reinterpret_cast<const cd*>(w1);
+    const cd* b = reinterpret_cast<const cd*>(w2);
+    const cd* c = reinterpret_cast<const cd*>(w3);
+    cd* out = reinterpret_cast<cd*>(dst);
+    if (rank == 0) {  // operator.hpp:252-255
+      std::fill(out, out + m1 * m2 * m3, cd(0.0));
+      return;
+    }
+    std::vector<cd> w1s(static_cast<size_t>(m1 * rank));
+    for (I64 k = 0; k < m3; ++k) {
+      for (I64 l = 0; l < rank; ++l)  // W1 diag(W3(k, :))
+        for (I64 i = 0; i < m1; ++i) w1s[static_cast<size_t>(i + m1 * l)] = a[i + m1 * l] * c[k + m3 * l];
+      for (I64 j = 0; j < m2; ++j)  // slab = w1s W2^T
+        for (I64 i = 0; i < m1; ++i) {
+          cd s = 0.0;
+          for (I64 l = 0; l < rank; ++l) s += w1s[static_cast<size_t>(i + m1 * l)] * b[j + m2 * l];
+          out[i + m1 * (j + m2 * k)] = s;
+        }
+    }
+  });
+}
+
 int orc_apply_operator_tucker(int kind, int basis, const int64_t grid[3], const int64_t* ranks,
                               const double* const* cores, const double* const* u1s,
                               const double* const* u2s, const double* const* u3s,

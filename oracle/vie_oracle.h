@@ -62,6 +62,11 @@ int orc_component_table(int kind, int basis, int* ncomp, int* comps, int* parity
 int orc_decompress_tucker(const int64_t edims[3], const int64_t ranks[3], const double* core,
                           const double* u1, const double* u2, const double* u3, double* dst);
 
+/* decompress_cp (operator.hpp:248-261): slab_k = W1 diag(W3(k,:)) W2^T, merged
+ * Fourier-domain Tucker+CP factors W_q (2n_q x rank, column-major).          */
+int orc_decompress_cp(const int64_t edims[3], int64_t rank, const double* w1, const double* w2,
+                      const double* w3, double* dst);
+
 /* apply_operator (operator.hpp:273-382), strategy HosvdDecompress.         */
 int orc_apply_operator_tucker(int kind, int basis, const int64_t grid[3], const int64_t* ranks,
                               const double* const* cores, const double* const* u1s,

@@ -643,6 +643,21 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
   });
 }
 
+int vie_tucker_from_cp(vie_ctx ctx, const int64_t dims[3], int64_t rank, const double* w1_host,
+                       const double* w2_host, const double* w3_host, const int sign[3], int domain,
+                       vie_tucker* out) {
+  int rc = guard([&] {
+    if (rank < 1) throw Invalid("TuckerCPForm: rank must be >= 1");
+    if (rank > 64) throw Invalid("TuckerCPForm: rank above the device decompressor's limit (64)");
+  });
+  if (rc != VIE_OK) return rc;
+  std::vector<cd> core(static_cast<size_t>(rank * rank * rank), cd(0.0));
+  for (int64_t l = 0; l < rank; ++l) core[static_cast<size_t>(l + rank * (l + rank * l))] = 1.0;  // superdiagonal
+  const int64_t ranks[3] = {rank, rank, rank};
+  return vie_tucker_from_factors(ctx, dims, ranks, reinterpret_cast<const double*>(core.data()), w1_host, w2_host,
+                                 w3_host, sign, domain, out);
+}
+
 int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]) {
   return guard([&] {
     if (!t || !ranks_out) throw Invalid("vie_tucker_ranks: null argument");

@@ -168,6 +168,25 @@ class TuckerForm:
             pass
 
 
+def tucker_cp_form(dft: DftService, dims, factors: Sequence, sign, domain: int = 0) -> TuckerForm:
+    """TuckerCPForm (decomp.hpp:143-148; merged factors W_q, n_q x R) on the device
+    (vie_tucker_from_cp): served by the fused matvec as the Tucker form with the
+    superdiagonal R^3 core, i.e. the TuckerCpLoop / decompress_cp spectrum
+    (operator.hpp:248-261, 346-362)."""
+    ws = [np.asfortranarray(np.asarray(w, np.complex128)) for w in factors]
+    rank = ws[0].shape[1]
+    if any(w.shape[1] != rank for w in ws):
+        raise ValueError("TuckerCPForm: factor column counts differ")
+    rows = [d if domain == 0 else 2 * d for d in dims]
+    if any(ws[q].shape[0] != rows[q] for q in range(3)):
+        raise ValueError("TuckerCPForm: factor rows do not match dims")
+    h = C.c_void_p()
+    _check(lib().vie_tucker_from_cp(dft.handle, _i64(dims), C.c_int64(rank), ws[0].ctypes.data_as(_dp),
+                                    ws[1].ctypes.data_as(_dp), ws[2].ctypes.data_as(_dp),
+                                    (C.c_int * 3)(*[int(x) for x in sign]), int(domain), C.byref(h)))
+    return TuckerForm._from_handle(dft, h, dims, (rank,) * 3, sign)
+
+
 def tucker_compress(dft: DftService, t, dims, sign, tol: float = 1e-8, rule: int = RULE_ENERGY) -> TuckerForm:
     """hosvd + transform_factors (decomp.hpp:160-176, operator.hpp:76-90) of a spatial
     Toeplitz-defining tensor (flat, reference layout); returns the device form."""
