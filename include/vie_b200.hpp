@@ -82,6 +82,12 @@ struct TuckerForm {
   std::array<Index, 3> ranks{0, 0, 0};
 };
 
+// Spatial-domain Tucker+CP form, merged factors W_q = U_q V_q (decomp.hpp:143-148).
+struct TuckerCPForm {
+  std::array<FactorMatrix, 3> factors;  // n_q x rank
+  Index rank = 0;
+};
+
 struct KernelComponent {  // components.hpp:26-36 (+ PWL polynomial indices)
   OperatorKind op = OperatorKind::N;
   int row_axis = 0;
@@ -255,6 +261,43 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder ord
                                   reinterpret_cast<const double*>(f.factors[0].data.data()),
                                   reinterpret_cast<const double*>(f.factors[1].data.data()),
                                   reinterpret_cast<const double*>(f.factors[2].data.data()), p.sign.data(), 0, &t));
+    hs.push_back(t);
+    comps.insert(comps.end(), {comp.row_axis, comp.col_axis, comp.row_poly, comp.col_poly});
+  }
+  const int64_t g[3] = {grid[0], grid[1], grid[2]};
+  vie_op op = nullptr;
+  check(vie_op_create(dft.handle(), static_cast<int>(kind), static_cast<int>(order), g, static_cast<int>(hs.size()),
+                      comps.data(), hs.data(), &op));
+  return EmbeddedSpectrum(op, kind, order, grid);
+}
+
+// build_operator_spectra from Tucker+CP forms (the reference's tucker_cp
+// representation, operator.hpp:92-106 + 144-177): vie_tucker_from_cp per component.
+inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder order,
+                                               const std::vector<std::pair<KernelComponent, TuckerCPForm>>& forms,
+                                               DftService& dft) {
+  if (forms.empty()) throw std::invalid_argument("build_operator_spectra: no components");
+  const std::array<Index, 3> grid{forms.front().second.factors[0].rows, forms.front().second.factors[1].rows,
+                                  forms.front().second.factors[2].rows};
+  std::vector<vie_tucker> hs;
+  std::vector<int> comps;
+  struct Guard {
+    std::vector<vie_tucker>& h;
+    ~Guard() {
+      for (auto t : h) vie_tucker_destroy(t);
+    }
+  } guard{hs};
+  for (const auto& [comp, f] : forms) {
+    if (comp.op != kind) throw std::invalid_argument("build_operator_spectra: component of another operator");
+    for (int q = 0; q < 3; ++q)
+      if (f.factors[q].rows != grid[q] || f.factors[q].cols != f.rank)
+        throw std::invalid_argument("build_operator_spectra: inconsistent Tucker+CP factor shapes");
+    const Parity p = component_parity(comp, order);
+    const int64_t dims[3] = {grid[0], grid[1], grid[2]};
+    vie_tucker t = nullptr;
+    check(vie_tucker_from_cp(dft.handle(), dims, f.rank, reinterpret_cast<const double*>(f.factors[0].data.data()),
+                             reinterpret_cast<const double*>(f.factors[1].data.data()),
+                             reinterpret_cast<const double*>(f.factors[2].data.data()), p.sign.data(), 0, &t));
     hs.push_back(t);
     comps.insert(comps.end(), {comp.row_axis, comp.col_axis, comp.row_poly, comp.col_poly});
   }

@@ -368,6 +368,50 @@ int main() {
     expect(thrown, "non-orthogonal plane wave must throw");
   });
 
+  // Tucker+CP components through the wrapper: equal to the Tucker path with the
+  // superdiagonal core (decomp.hpp:143-148, operator.hpp:248-261)
+  run("ApplyOperator.TuckerCpEqualsSuperdiagonalTucker", [&] {
+    const std::array<Index, 3> d{4, 5, 3};
+    const Index R = 3;
+    std::vector<std::pair<KernelComponent, TuckerCPForm>> cp;
+    std::vector<std::pair<KernelComponent, TuckerForm>> tk;
+    std::uint64_t seed = 500;
+    for (const auto& c : unique_components(OperatorKind::N, BasisOrder::PWC)) {
+      const Parity p = component_parity(c, BasisOrder::PWC);
+      TuckerCPForm f;
+      f.rank = R;
+      TuckerForm t;
+      t.core = Tensor3(R, R, R);
+      for (Index l = 0; l < R; ++l) t.core(l, l, l) = 1.0;
+      for (int q = 0; q < 3; ++q) {
+        f.factors[q] = random_matrix(d[q], R, ++seed);
+        if (p.sign[q] < 0)
+          for (Index l = 0; l < R; ++l) f.factors[q](0, l) = 0.0;
+        t.factors[q] = f.factors[q];
+      }
+      t.ranks = {R, R, R};
+      cp.emplace_back(c, f);
+      tk.emplace_back(c, t);
+    }
+    EmbeddedSpectrum a = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, cp, dft);
+    EmbeddedSpectrum b = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, tk, dft);
+    CurrentField x(d);
+    for (int q = 0; q < 3; ++q) {
+      x.comp[q] = Tensor3(d[0], d[1], d[2]);
+      if (orc_random_tensor(d[0], d[1], d[2], 600 + q, reinterpret_cast<double*>(x.comp[q].data.data())))
+        throw std::runtime_error(orc_last_error());
+    }
+    ApplyWorkspace ws;
+    const std::vector<cplx> ya = apply_operator(a, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, &ws, dft).to_vector();
+    const std::vector<cplx> yb = apply_operator(b, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, &ws, dft).to_vector();
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < ya.size(); ++i) {
+      num += std::norm(ya[i] - yb[i]);
+      den += std::norm(yb[i]);
+    }
+    expect(std::sqrt(num / den) <= 1e-13, "CP vs superdiagonal Tucker");
+  });
+
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
 }
