@@ -249,15 +249,19 @@ def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=
     rhs = torch.randn(S * nv, dtype=torch.complex128, device="cuda", generator=g)
     cfg = vie.GmresConfig(tol, inner, outer)
     vie.gmres(op, eps, 1.0, rhs, vie.GmresConfig(tol, 2, 1))  # warm-up
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = vie.gmres(op, eps, 1.0, rhs, cfg)
-    torch.cuda.synchronize()
-    t = time.perf_counter() - t0
+    times = []
+    for _ in range(3):  # min of 3 solves: the per-iteration host round trip sees host noise
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = vie.gmres(op, eps, 1.0, rhs, cfg)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = min(times)
     out = {"config": "cube_64: 64^3 PWL N system (BASELINE configs[1]), 60 components rank 25, synthetic",
            "solver": f"restarted GMRES({inner}) to {tol}, device resident (vie_gmres_solve)",
            "iterations": res.iterations, "converged": res.converged,
            "final_relative_residual": res.final_relative_residual, "seconds": t,
+           "seconds_all": times,
            "ms_per_iteration": 1e3 * t / max(res.iterations, 1)}
     if with_cpu:  # the oracle's GMRES on the same system, bounded: 2 iterations, per-iteration time
         from oracle import oracle as orc
