@@ -22,6 +22,7 @@
 #include <cuda_runtime_api.h>
 
 #include <array>
+#include <chrono>
 #include <complex>
 #include <cstdint>
 #include <stdexcept>
@@ -572,6 +573,39 @@ inline PostProcess postprocess(const Fields& f, const DielectricMap& m) {
     out.has_b1 = true;
   }
   return out;
+}
+
+struct SolveReport {  // solver.hpp:286-295
+  CurrentField j;
+  std::vector<double> residual_history;
+  double final_relative_residual = 0.0;
+  int iterations = 0;
+  bool converged = false;
+  double wall_time_s = 0.0;
+  Fields fields;
+  PostProcess post;
+};
+
+// solve_scene (solver.hpp:300-326): build_rhs, restarted GMRES on the JVIE system
+// (M_eps - M_chi N / V) device resident, recover_fields (K operator optional),
+// postprocess.  PWC operators on the map's grid.
+inline SolveReport solve_scene(const DielectricMap& m, const PlaneWave& inc, const EmbeddedSpectrum& op_n,
+                               const EmbeddedSpectrum* op_k, const GmresConfig& cfg = {}) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (op_n.grid_dims != m.grid.dims || op_n.order != BasisOrder::PWC)
+    throw std::invalid_argument("solve_scene: op_n must be the PWC operator of the map's grid");
+  const CurrentField rhs = build_rhs(m, inc);
+  GmresResult g = gmres_system(m.eps_r, 1.0 / m.grid.voxel_volume(), op_n, rhs.to_vector(), cfg);
+  SolveReport rep;
+  rep.j = CurrentField::from_vector(g.solution, m.grid.dims);
+  rep.residual_history = std::move(g.residual_history);
+  rep.final_relative_residual = g.final_relative_residual;
+  rep.iterations = g.iterations;
+  rep.converged = g.converged;
+  rep.fields = recover_fields(rep.j, m, inc, op_k);
+  rep.post = postprocess(rep.fields, m);
+  rep.wall_time_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return rep;
 }
 
 }  // namespace b200

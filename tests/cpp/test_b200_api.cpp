@@ -412,6 +412,54 @@ int main() {
     expect(std::sqrt(num / den) <= 1e-13, "CP vs superdiagonal Tucker");
   });
 
+  // solve_scene (solver.hpp:300-326) through the wrapper vs the oracle pipeline
+  run("SolveScene.MatchesOraclePipeline", [&] {
+    const std::array<Index, 3> d{5, 4, 4};
+    auto famn = make_family(OperatorKind::N, BasisOrder::PWC, d, 3, 131);
+    auto famk = make_family(OperatorKind::K, BasisOrder::PWC, d, 3, 171);
+    for (auto* fam : {&famn, &famk})
+      for (auto& pr : *fam)
+        for (auto& v : pr.second.core.data) v *= 1e-4;
+    EmbeddedSpectrum opn = build_operator_spectra(OperatorKind::N, BasisOrder::PWC, famn, dft);
+    EmbeddedSpectrum opk = build_operator_spectra(OperatorKind::K, BasisOrder::PWC, famk, dft);
+    OracleForms ofn = to_oracle(famn, BasisOrder::PWC), ofk = to_oracle(famk, BasisOrder::PWC);
+    DielectricMap m(VoxelGrid{d, {1.0, 1.0, 1.0}, {0.0, 0.0, 0.0}}, 2.98e8);  // unit voxels: 1/V = 1
+    for (size_t i = 0; i < m.eps_r.size(); ++i)
+      if (i % 4) m.eps_r[i] = cplx(2.0 + 3.0 * static_cast<double>(i % 5) / 5.0, -0.5);
+    PlaneWave inc{{0.0, 1.0, 0.0}, {1.0, 0.0, 0.0}, 2.0};
+    SolveReport rep = solve_scene(m, inc, opn, &opk, GmresConfig{1e-10, 10, 20});
+
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    const double geo[6] = {1.0, 1.0, 1.0, 0.0, 0.0, 0.0};
+    const double pw[7] = {0.0, 1.0, 0.0, 1.0, 0.0, 0.0, 2.0};
+    const size_t nv = m.eps_r.size();
+    const double* eps = reinterpret_cast<const double*>(m.eps_r.data());
+    std::vector<cplx> rhs(3 * nv), x(3 * nv), kj(3 * nv), e(3 * nv), h(3 * nv);
+    std::vector<double> hist(400), p(nv), b1(nv);
+    int it = 0, cv = 0, hl = 0;
+    double fr = 0.0, tot = 0.0;
+    if (orc_build_rhs(g, geo, 2.98e8, pw, eps, 1, reinterpret_cast<double*>(rhs.data())) ||
+        orc_gmres_system_tucker(0, g, ofn.ranks.data(), ofn.pc.data(), ofn.p1.data(), ofn.p2.data(), ofn.p3.data(),
+                                eps, 1.0, reinterpret_cast<const double*>(rhs.data()), nullptr, 1e-10, 10, 20,
+                                reinterpret_cast<double*>(x.data()), &it, &cv, &fr, hist.data(), 400, &hl) ||
+        orc_apply_operator_tucker(1, 0, g, ofk.ranks.data(), ofk.pc.data(), ofk.p1.data(), ofk.p2.data(),
+                                  ofk.p3.data(), reinterpret_cast<const double*>(x.data()),
+                                  reinterpret_cast<double*>(kj.data())) ||
+        orc_recover_fields(g, geo, 2.98e8, pw, eps, reinterpret_cast<const double*>(x.data()),
+                           reinterpret_cast<const double*>(kj.data()), reinterpret_cast<double*>(e.data()),
+                           reinterpret_cast<double*>(h.data())) ||
+        orc_postprocess(g, geo, 2.98e8, eps, reinterpret_cast<const double*>(e.data()),
+                        reinterpret_cast<const double*>(h.data()), p.data(), b1.data(), &tot))
+      throw std::runtime_error(orc_last_error());
+    expect(rep.converged && cv, "not converged");
+    expect(std::abs(rep.iterations - it) <= 1, "iterations");
+    expect(std::abs(rep.final_relative_residual - fr) <= 1e-8, "final residual");
+    expect(rel(x, rep.j.to_vector()) <= 1e-8, "j");
+    expect(rel(e, rep.fields.e.to_vector()) <= 1e-8, "e");
+    expect(rep.fields.has_h && rel(h, rep.fields.h.to_vector()) <= 1e-8, "h");
+    expect(std::abs(rep.post.total_absorbed_power - tot) <= 1e-8 * std::abs(tot), "total power");
+  });
+
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
 }
