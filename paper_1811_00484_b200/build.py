@@ -1,6 +1,11 @@
-"""Builds libvie_b200.so (sm_100a) in-tree with nvcc.  No GPU needed."""
+"""Builds libvie_b200.so (sm_100a) in-tree with nvcc.  No GPU needed.
+
+Each translation unit compiles to its own object in parallel (build/obj/), then
+one nvcc link produces the shared library; only stale objects are rebuilt.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import os
 import subprocess
 import sys
@@ -8,17 +13,23 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
+OBJ = os.path.join(HERE, "build", "obj")
 LIB = os.path.join(HERE, "libvie_b200.so")
 SOURCES = ["api.cu", "kernels_fft.cu", "kernels_pencil.cu", "kernels_decomp.cu", "kernels_blas.cu",
-           "kernels_hosvd.cu", "kernels_fft2.cu", "kernels_pencil2.cu", "kernels_scene.cu"]
+           "kernels_hosvd.cu", "kernels_fft2.cu", "kernels_pencil2.cu", "kernels_scene.cu",
+           "kernels_pencil3.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "kernels.cuh", "twiddles_gen.cuh", "hadamard.cuh", "tma.cuh"]
 
-NVCC_FLAGS = [
-    "-gencode", "arch=compute_100a,code=sm_100a",
-    "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-    "-shared", "-lcudart",
-]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
+# kept for callers that print the flags (one-shot compile of everything)
+NVCC_FLAGS = [*CFLAGS, "-shared", "-lcudart"]
+
+
+def _hdr_mtime() -> float:
+    deps = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "vie_b200.h")]
+    return max(os.path.getmtime(d) for d in deps)
 
 
 def _stale() -> bool:
@@ -29,16 +40,38 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, extra: list[str] | None = None,
+          out: str | None = None, tag: str = "") -> str:
+    """out/tag: a variant library (e.g. -DVIE_PENCIL_PROFILE) with its own object dir."""
+    lib = out or LIB
+    if not force and out is None and not _stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, *(extra or []), "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    objdir = OBJ + tag
+    os.makedirs(objdir, exist_ok=True)
+    hm = _hdr_mtime()
+
+    def compile_one(src: str) -> None:
+        o = os.path.join(objdir, src.replace(".cu", ".o"))
+        s = os.path.join(CSRC, src)
+        if not force and os.path.exists(o) and os.path.getmtime(o) > max(hm, os.path.getmtime(s)) and (not extra or tag):
+            return
+        cmd = [nvcc, *CFLAGS, *(extra or []), "-c", s, "-o", o + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        os.replace(o + ".tmp", o)
+
+    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 4))) as ex:
+        for f in [ex.submit(compile_one, s) for s in SOURCES]:
+            f.result()
+    objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
+    cmd = [nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -124,6 +124,7 @@ struct vie_op_s {
   vie::Pass2 Q1{}, Q2{};           // register-staged two-stage row / column passes
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
   bool pencil2 = false;         // compile-time-shaped two-branch pencil kernel for this n3
+  bool pencil3 = false;         // PWL: whole-mirror-group pencil kernel with the DMMA Hadamard (interior groups)
   int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
   // slab decomposition (vie_op_set_partition): this rank's z-planes [k0, k0 + nk) and
   // axis-1 positions [p1off, p1off + W) (Geom)
@@ -464,7 +465,12 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
     else vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
   }
   mark();
-  if (op->pencil2) {  // compile-time-shaped kernel + the axis-1 edge group on the generic one
+  if (op->pencil3) {  // interior mirror groups on the DMMA kernel; axis-1 edge group, axis-2 edge rows
+    vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st,
+                       1);
+    vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
+    vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+  } else if (op->pencil2) {  // compile-time-shaped kernel + the axis-1 edge group on the generic one
     vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st,
                        1);
     vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
@@ -481,7 +487,7 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
   mark();
   mark2();
   // row, column, (decomp_z + decomp), pencil (+ edge), column, row
-  op->last_launches = 7 + (op->pencil2 ? 1 : 0);
+  op->last_launches = 7 + (op->pencil2 ? 1 : 0) + (op->pencil3 ? 1 : 0);
   if (op->profiling) {
     VIE_CUDA_CHECK(cudaEventSynchronize(op->ev[k - 1]));
     for (int i = 1; i < k; ++i) {
@@ -782,6 +788,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
     op->pencil2 = kPencil2 && vie::pencil2_supported(op->kind, op->basis, g.n3, op->active, g.NC);
+    op->pencil3 = op->pencil2 && vie::pencil3_supported(op->kind, op->basis, g.n3, op->active, g.NC);
     if (kPass2) {  // register-staged passes when the axis has a <= 2-stage wide plan
       std::vector<int> r1, r2;
       const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1);
@@ -910,7 +917,13 @@ int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
     if (g.p1off == 0)
       vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
                          false, g.n1, g.n1 + 1);
-    if (op->pencil2) {
+    if (op->pencil3) {
+      if (g.p1off == 0)
+        vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
+                           st, 1);
+      vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
+      vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+    } else if (op->pencil2) {
       if (g.p1off == 0)
         vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
                            st, 1);
@@ -1195,6 +1208,7 @@ int vie_op_last_stats(vie_op op, int* launches, double* stage_ms) {
 namespace vie {
 void pencil_phase_read(unsigned long long* out8, bool reset);
 void pencil2_phase_read(unsigned long long* out8, bool reset);
+void pencil3_phase_read(unsigned long long* out8, bool reset);
 }
 extern "C" {
 int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
@@ -1202,6 +1216,9 @@ int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
 }
 int vie_debug_pencil2_phases(unsigned long long* out8, int reset) {
   return guard([&] { vie::pencil2_phase_read(out8, reset != 0); });
+}
+int vie_debug_pencil3_phases(unsigned long long* out8, int reset) {
+  return guard([&] { vie::pencil3_phase_read(out8, reset != 0); });
 }
 #endif
 

@@ -59,7 +59,15 @@ void launch_pencil(int kind, int basis, const double2* Bin, double2* Bout, doubl
 // covers with groups = 1.  Returns false (nothing launched) if unsupported.
 bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
 
+// pos2 range [pos2lo, pos2hi) of axis-2 positions (pos2hi < 0: all m2)
 void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+                    const double2* twm3, cudaStream_t st, int pos2lo = 0, int pos2hi = -1);
+// PWL pencil kernel with the Hadamard on the FP64 tensor cores (kernels_pencil3.cu): one
+// 2-CTA cluster per interior mirror group (axis-1 pair group >= 1, axis-2 pair >= 1), all
+// four pencils; the axis-1 edge group (launch_pencil groups = 1) and the axis-2 edge
+// positions 0, 1 (launch_pencil2 with pos2 in [0, 2)) complete the grid.
+bool pencil3_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
+void launch_pencil3(int kind, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
                     const double2* twm3, cudaStream_t st);
 // B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
 void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,

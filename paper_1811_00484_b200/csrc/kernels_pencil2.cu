@@ -92,6 +92,7 @@ struct Pencil2Args {
   int W;       // row length of the slabs (axis-1 positions of this rank)
   int p1off;   // global axis-1 position of slab column 0
   int gfirst;  // first axis-1 group of this launch
+  int pos2lo;  // first axis-2 position of this launch
   FastDiv dnk;
 };
 
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   const int c0 = 2 * P1P * (a.gfirst + (blockIdx.x >> 1));  // first axis-1 position (group 0 is the edge launch)
   const int cl0 = c0 - a.p1off;                              // its slab column
   const int q0 = c0 >> 1;                           // octant row of pair 0
-  const int pos2 = blockIdx.y;  // axis-2 position
+  const int pos2 = a.pos2lo + static_cast<int>(blockIdx.y);  // axis-2 position
   // slab offset of k-plane k: block r = k / nk of the k-planes (one block on one GPU)
   auto koff = [&](int k) -> int64_t {
     const int r = static_cast<int>(a.dnk.div(static_cast<uint32_t>(k)));
@@ -383,26 +384,27 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
   }
 }
 
-#define VIE_PENCIL2_SHAPES(X) X(10, 20) X(10, 10) X(8, 8) X(4, 8)
+#define VIE_PENCIL2_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8)
 
 template <int KIND, int BASIS>
 bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g, const double2* twm3,
-               cudaStream_t st, bool dry) {
+               cudaStream_t st, bool dry, int pos2lo, int pos2hi) {
   auto go = [&](auto fn, size_t smem, int P1P, std::array<int, 3> box) {
     if (dry) return true;
     // axis-1 groups of this rank's positions [p1off, p1off + W); group 0 is the edge launch
     const int glo = std::max(1, g.p1off / (2 * P1P));
     const int ghi = (std::min(g.m1, g.p1off + g.W) + 2 * P1P - 1) / (2 * P1P);
-    if (ghi <= glo) return true;
+    if (pos2hi < 0) pos2hi = g.m2;
+    if (ghi <= glo || pos2hi <= pos2lo) return true;
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3, g.bps, g.bps * g.nk, g.nk, g.W, g.p1off,
-                  glo, {}};
+                  glo, pos2lo, {}};
     a.dnk.init(static_cast<uint32_t>(g.nk));
     CUtensorMap tmap;
     encode_spectrum_map(&tmap, Shat, g, box);
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (ghi - glo), g.m2);
+    cfg.gridDim = dim3(2 * (ghi - glo), pos2hi - pos2lo);
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -435,11 +437,11 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
 }
 
 bool dispatch2(int kind, int basis, int n3, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
-               const double2* twm3, cudaStream_t st, bool dry) {
-  if (kind == 0 && basis == 0) return launch2_t<0, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry);
-  if (kind == 1 && basis == 0) return launch2_t<1, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry);
-  if (kind == 0 && basis == 1) return launch2_t<0, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry);
-  return launch2_t<1, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry);
+               const double2* twm3, cudaStream_t st, bool dry, int pos2lo = 0, int pos2hi = -1) {
+  if (kind == 0 && basis == 0) return launch2_t<0, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry, pos2lo, pos2hi);
+  if (kind == 1 && basis == 0) return launch2_t<1, 0>(n3, Bin, Bout, Shat, g, twm3, st, dry, pos2lo, pos2hi);
+  if (kind == 0 && basis == 1) return launch2_t<0, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry, pos2lo, pos2hi);
+  return launch2_t<1, 1>(n3, Bin, Bout, Shat, g, twm3, st, dry, pos2lo, pos2hi);
 }
 
 }  // namespace
@@ -462,8 +464,8 @@ bool pencil2_supported(int kind, int basis, int n3, uint64_t active_mask, int NC
 }
 
 void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
-                    const double2* twm3, cudaStream_t st) {
-  dispatch2(kind, basis, g.n3, Bin, Bout, Shat, g, twm3, st, false);
+                    const double2* twm3, cudaStream_t st, int pos2lo, int pos2hi) {
+  dispatch2(kind, basis, g.n3, Bin, Bout, Shat, g, twm3, st, false, pos2lo, pos2hi);
 }
 
 }  // namespace vie

@@ -91,6 +91,24 @@ def test_matvec_pencil2_shapes(vie, dft, orc, kind, basis, dims, rank):
     assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims)
 
 
+# PWL interior mirror groups on the DMMA-Hadamard kernel (kernels_pencil3.cu): n3 with a
+# compiled shape (32 = 4x8, 64 = 8x8, 100 = 10x10, 128 = 8x16, 200 = 10x20), both kinds,
+# interior groups in both axes, n2 = 2 (axis-2 edge rows only), n1 = 1 (axis-1 edge only)
+PENCIL3_CASES = [
+    (N, PWL, (5, 6, 32), 3), (K, PWL, (4, 5, 64), 3), (N, PWL, (3, 3, 128), 4), (K, PWL, (3, 4, 200), 3),
+    (N, PWL, (6, 2, 100), 3), (N, PWL, (2, 7, 200), 5), (K, PWL, (1, 4, 64), 2), (N, PWL, (4, 5, 200), 25),
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", PENCIL3_CASES)
+def test_matvec_pencil3_shapes(vie, dft, orc, kind, basis, dims, rank):
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 13 + sum(dims))
+    for trial in range(2):
+        x = random_field(basis, dims, 91 + trial)
+        y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+        assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims)
+
+
 # kernel-path coverage: rank > 28 (FMA decompression fallback), an axis length without a
 # two-stage plan (m = 250 = 2 x 5^3: generic multi-stage passes), and n3 without a compiled
 # pencil shape (generic pencil kernel)
