@@ -49,6 +49,12 @@ const char* vie_version(void);
 int vie_ctx_create(vie_ctx* out, int device);
 int vie_ctx_destroy(vie_ctx ctx);
 int vie_ctx_sync(vie_ctx ctx);
+/* The context's CUDA stream (cudaStream_t as void*), which the calls use when their
+ * `stream` argument is NULL; vie_op_stream: the stream of the operator's context.
+ * Forms and operators keep their context alive: vie_ctx_destroy releases the
+ * caller's reference and the context is freed with its last form / operator.       */
+int vie_ctx_stream(vie_ctx ctx, void** stream);
+int vie_op_stream(vie_op op, void** stream);
 
 /* tucker_compress = hosvd + transform_factors (decomp.hpp:160-176,
  * operator.hpp:76-90): HOSVD of a spatial Toeplitz-defining tensor (host
@@ -98,6 +104,11 @@ int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_by
 /* apply_operator (operator.hpp:273-382), strategy HosvdDecompress semantics:
  * y = A x for device vectors of n_cur * n_vox complex values.                */
 int vie_matvec(vie_op op, const double* x, double* y, void* stream);
+/* apply_operator with ApplyTimings (operator.hpp:189-192): the stages run serialised with
+ * CUDA events between them; fft_ms = the row / column FFT passes (pad, axes 1-2, their
+ * inverses, crop), product_ms = decompression + the fused axis-3 FFT x Hadamard x IFFT
+ * pass.  Device buffers, context stream, returns after completion.                   */
+int vie_matvec_timed(vie_op op, const double* x, double* y, double* fft_ms, double* product_ms);
 /* Same call with HOST buffers (H2D, matvec, D2H) -- the reference-facing call. */
 int vie_matvec_host(vie_op op, const double* x_host, double* y_host);
 /* `count` independent applications with HOST buffers, pipelined: the H2D copy of
@@ -112,14 +123,36 @@ int vie_matvec_host_batch(vie_op op, int64_t count, const double* const* x_host,
 int vie_system_matvec(vie_op op, const double* eps_r, double inv_v, const double* x, double* y,
                       int diag_term, void* stream);
 
+/* A device linear map y = f(x) on vectors of n complex values (the reference's
+ * LinearMap, solver.hpp:26), run on `stream` (the solve's stream).                  */
+typedef void (*vie_linear_map_fn)(void* user, const double* x, double* y, void* stream);
+
+/* Right preconditioner M (solver.hpp:34-36, :74, :131): w = A M v_j, x += M V y.
+ * Either `diag` (device, n complex: M = diag(diag)) or `apply`/`user` (a callback).  */
+typedef struct {
+  const double* diag;
+  vie_linear_map_fn apply;
+  void* user;
+} vie_precond;
+
 /* gmres (solver.hpp:34-142) on apply_system, device resident: restarted
  * GMRES(inner), modified Gram-Schmidt, complex Givens rotations.  x0 may be
- * NULL (zero start).  history_host receives |g_{j+1}|/||b|| per iteration
- * (up to history_cap values; *history_len = total count).                   */
+ * NULL (zero start); precond may be NULL (none).  history_host receives
+ * |g_{j+1}|/||b|| per iteration (up to history_cap values; *history_len = total
+ * count).  The solve runs on the context's stream, ordered after all work queued on
+ * `stream` (NULL: the caller must have completed the producers of eps_r / rhs / x0);
+ * `stream` then waits for the solve.  Returns after the result is on the host.       */
 int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* rhs,
-                    const double* x0, double tol, int inner, int outer, double* x, int* iterations,
-                    double* final_rel_res, double* history_host, int history_cap, int* history_len,
-                    int* converged);
+                    const double* x0, double tol, int inner, int outer, const vie_precond* precond,
+                    double* x, int* iterations, double* final_rel_res, double* history_host,
+                    int history_cap, int* history_len, int* converged, void* stream);
+
+/* The same device GMRES on any linear map of n complex values: gmres(apply, rhs, cfg,
+ * x0, precond) of solver.hpp:34 with the closure as a C callback.                   */
+int vie_gmres(vie_ctx ctx, int64_t n, vie_linear_map_fn apply, void* apply_user, const double* rhs,
+              const double* x0, double tol, int inner, int outer, const vie_precond* precond,
+              double* x, int* iterations, double* final_rel_res, double* history_host,
+              int history_cap, int* history_len, int* converged, void* stream);
 
 /* ---- scene pipeline around the solve (solve_scene, solver.hpp:148-285) ----
  * PWC fields (3 component blocks of n_vox, grid.hpp:107-136).  The scene is the

@@ -21,7 +21,10 @@
 
 #include <cuda_runtime_api.h>
 
+#include <algorithm>
 #include <array>
+#include <cmath>
+#include <functional>
 #include <chrono>
 #include <complex>
 #include <cstdint>
@@ -180,8 +183,17 @@ class DeviceBuffer {
     return *this;
   }
   double* get() const { return static_cast<double*>(p_); }
-  void upload(const void* h, size_t bytes) { cuda_check(cudaMemcpy(p_, h, bytes, cudaMemcpyHostToDevice)); }
-  void download(void* h, size_t bytes) const { cuda_check(cudaMemcpy(h, p_, bytes, cudaMemcpyDeviceToHost)); }
+  // Copies ordered on `st` (the context stream the library's kernels run on) and complete
+  // on return: a plain cudaMemcpy runs on the legacy stream, which does not order with the
+  // context's non-blocking stream, and a pageable H2D copy may return before it lands.
+  void upload(const void* h, size_t bytes, cudaStream_t st) {
+    cuda_check(cudaMemcpyAsync(p_, h, bytes, cudaMemcpyHostToDevice, st));
+    cuda_check(cudaStreamSynchronize(st));
+  }
+  void download(void* h, size_t bytes, cudaStream_t st) const {
+    cuda_check(cudaMemcpyAsync(h, p_, bytes, cudaMemcpyDeviceToHost, st));
+    cuda_check(cudaStreamSynchronize(st));
+  }
 
  private:
   void* p_ = nullptr;
@@ -191,16 +203,27 @@ class DeviceBuffer {
 class DftService {  // fft.hpp DftService: here the CUDA context, stream and plan cache
  public:
   explicit DftService(int device = 0) { check(vie_ctx_create(&ctx_, device)); }
+  // releases the caller's reference; operators built on it keep the context alive
   ~DftService() { vie_ctx_destroy(ctx_); }
   DftService(const DftService&) = delete;
   DftService& operator=(const DftService&) = delete;
   vie_ctx handle() const { return ctx_; }
+  cudaStream_t stream() const {
+    void* s = nullptr;
+    check(vie_ctx_stream(ctx_, &s));
+    return static_cast<cudaStream_t>(s);
+  }
 
  private:
   vie_ctx ctx_ = nullptr;
 };
 
 struct ApplyWorkspace {};  // the device workspace lives in the operator (operator.hpp:181-187)
+
+struct ApplyTimings {  // operator.hpp:189-192
+  double fft_ms = 0.0;      // row / column FFT passes (pad, axes 1-2 and their inverses, crop)
+  double product_ms = 0.0;  // decompression + fused axis-3 FFT x Hadamard x IFFT
+};
 
 class EmbeddedSpectrum {  // operator.hpp:120-129, Tucker representation only
  public:
@@ -217,6 +240,11 @@ class EmbeddedSpectrum {  // operator.hpp:120-129, Tucker representation only
     o.op_ = nullptr;
   }
   vie_op handle() const { return op_; }
+  cudaStream_t stream() const {  // the context stream its kernels run on
+    void* s = nullptr;
+    check(vie_op_stream(op_, &s));
+    return static_cast<cudaStream_t>(s);
+  }
   Index n_cur() const { return order == BasisOrder::PWC ? 3 : 12; }
   Index n_vox() const { return grid_dims[0] * grid_dims[1] * grid_dims[2]; }
 
@@ -353,8 +381,11 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind,
 
 // apply_operator (operator.hpp:273-382).  Host containers in/out; the matvec
 // runs on the device (vie_matvec_host: H2D, matvec, D2H).
+// With `timings` (ApplyTimings, operator.hpp:189-192) the device stages run serialised
+// between CUDA events (vie_matvec_timed) and the split is returned.
 inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentField& x, MatvecStrategy strategy,
-                                   ScratchPolicy policy, ApplyWorkspace* ws, DftService& dft) {
+                                   ScratchPolicy policy, ApplyWorkspace* ws, DftService& dft,
+                                   ApplyTimings* timings = nullptr) {
   (void)ws;
   (void)dft;
   if (x.dims() != op.grid_dims || static_cast<Index>(x.comp.size()) != op.n_cur())
@@ -363,8 +394,76 @@ inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentFiel
     throw std::invalid_argument("apply_operator: decompress strategies need ScratchPolicy::WithBuffer");
   const std::vector<cplx> xv = x.to_vector();
   std::vector<cplx> yv(xv.size());
-  check(vie_matvec_host(op.handle(), reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yv.data())));
+  if (!timings) {
+    check(vie_matvec_host(op.handle(), reinterpret_cast<const double*>(xv.data()),
+                          reinterpret_cast<double*>(yv.data())));
+  } else {
+    const cudaStream_t st = op.stream();
+    const size_t bytes = xv.size() * sizeof(cplx);
+    DeviceBuffer dx(bytes), dy(bytes);
+    dx.upload(xv.data(), bytes, st);
+    check(vie_matvec_timed(op.handle(), dx.get(), dy.get(), &timings->fft_ms, &timings->product_ms));
+    dy.download(yv.data(), bytes, st);
+  }
   return CurrentField::from_vector(yv, op.grid_dims, op.order);
+}
+
+struct MatvecBenchResult {  // operator.hpp:440-450
+  MatvecStrategy strategy = MatvecStrategy::HosvdDecompress;
+  std::array<Index, 3> embedded_dims{0, 0, 0};
+  double median_ms = 0.0;
+  double product_ms = 0.0;      // median over repetitions
+  double product_min_ms = 0.0;  // minimum
+  double fft_ms = 0.0;
+  int repetitions = 0;
+};
+
+// matvec_bench (operator.hpp:451-502): warm-up, then `repetitions` timed device applies
+// (x resident on the device, CUDA events; the stage split from vie_matvec_timed).
+inline MatvecBenchResult matvec_bench(const EmbeddedSpectrum& op, const CurrentField& x, MatvecStrategy strategy,
+                                      int repetitions, DftService& dft) {
+  (void)dft;
+  if (repetitions < 1) throw std::invalid_argument("matvec_bench: repetitions must be >= 1");
+  if (x.dims() != op.grid_dims || static_cast<Index>(x.comp.size()) != op.n_cur())
+    throw std::invalid_argument("apply_operator: dim mismatch");
+  MatvecBenchResult r;
+  r.strategy = strategy;
+  r.embedded_dims = op.embedded_dims;
+  r.repetitions = repetitions;
+  const cudaStream_t st = op.stream();
+  const std::vector<cplx> xv = x.to_vector();
+  const size_t bytes = xv.size() * sizeof(cplx);
+  DeviceBuffer dx(bytes), dy(bytes);
+  dx.upload(xv.data(), bytes, st);
+  check(vie_matvec(op.handle(), dx.get(), dy.get(), nullptr));  // warm-up
+  cudaEvent_t e0, e1;
+  cuda_check(cudaEventCreate(&e0));
+  cuda_check(cudaEventCreate(&e1));
+  std::vector<double> total, prod, fft;
+  for (int rep = 0; rep < repetitions; ++rep) {
+    cuda_check(cudaEventRecord(e0, st));
+    check(vie_matvec(op.handle(), dx.get(), dy.get(), nullptr));
+    cuda_check(cudaEventRecord(e1, st));
+    cuda_check(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cuda_check(cudaEventElapsedTime(&ms, e0, e1));
+    total.push_back(ms);
+    double f = 0.0, p = 0.0;
+    check(vie_matvec_timed(op.handle(), dx.get(), dy.get(), &f, &p));
+    fft.push_back(f);
+    prod.push_back(p);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  auto median = [](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  r.median_ms = median(total);
+  r.product_ms = median(prod);
+  r.product_min_ms = *std::min_element(prod.begin(), prod.end());
+  r.fft_ms = median(fft);
+  return r;
 }
 
 // Many independent applications from host memory (vie_matvec_host_batch): the copies
@@ -398,13 +497,13 @@ inline CurrentField apply_system(const std::vector<cplx>& eps_r, double inv_v, c
     throw std::invalid_argument("apply_system: dim mismatch");
   const std::vector<cplx> xv = x.to_vector();
   const size_t bytes = xv.size() * sizeof(cplx);
+  const cudaStream_t st = op_n.stream();
   DeviceBuffer dx(bytes), dy(bytes), de(eps_r.size() * sizeof(cplx));
-  dx.upload(xv.data(), bytes);
-  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx));
+  dx.upload(xv.data(), bytes, st);
+  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx), st);
   check(vie_system_matvec(op_n.handle(), de.get(), inv_v, dx.get(), dy.get(), 1, nullptr));
   std::vector<cplx> yv(xv.size());
-  cuda_check(cudaDeviceSynchronize());
-  dy.download(yv.data(), bytes);
+  dy.download(yv.data(), bytes, st);
   return CurrentField::from_vector(yv, op_n.grid_dims, op_n.order);
 }
 
@@ -423,31 +522,103 @@ struct GmresResult {  // solver.hpp:18-24
 };
 
 // gmres (solver.hpp:34-142) on the apply_system closure of solve_scene
-// (solver.hpp:309-313), device resident.
+// (solver.hpp:309-313), device resident.  precond_diag: optional diagonal right
+// preconditioner M = diag(precond_diag) (solver.hpp:74, :131).
 inline GmresResult gmres_system(const std::vector<cplx>& eps_r, double inv_v, const EmbeddedSpectrum& op_n,
                                 const std::vector<cplx>& rhs, const GmresConfig& cfg = {},
-                                const std::vector<cplx>* x0 = nullptr) {
+                                const std::vector<cplx>* x0 = nullptr,
+                                const std::vector<cplx>* precond_diag = nullptr) {
   const size_t n = static_cast<size_t>(op_n.n_cur() * op_n.n_vox());
   if (rhs.size() != n || static_cast<Index>(eps_r.size()) != op_n.n_vox())
     throw std::invalid_argument("gmres: size mismatch");
   if (x0 && x0->size() != n) throw std::invalid_argument("gmres: initial guess size mismatch");
+  if (precond_diag && precond_diag->size() != n) throw std::invalid_argument("gmres: preconditioner size mismatch");
   const size_t bytes = n * sizeof(cplx);
+  const cudaStream_t st = op_n.stream();
   DeviceBuffer db(bytes), dx(bytes), de(eps_r.size() * sizeof(cplx));
-  db.upload(rhs.data(), bytes);
-  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx));
-  DeviceBuffer dx0;
+  db.upload(rhs.data(), bytes, st);
+  de.upload(eps_r.data(), eps_r.size() * sizeof(cplx), st);
+  DeviceBuffer dx0, dpc;
   if (x0) {
     dx0 = DeviceBuffer(bytes);
-    dx0.upload(x0->data(), bytes);
+    dx0.upload(x0->data(), bytes, st);
+  }
+  vie_precond pc{nullptr, nullptr, nullptr};
+  if (precond_diag) {
+    dpc = DeviceBuffer(bytes);
+    dpc.upload(precond_diag->data(), bytes, st);
+    pc.diag = dpc.get();
   }
   GmresResult res;
   std::vector<double> hist(static_cast<size_t>(cfg.inner) * static_cast<size_t>(cfg.outer) + 1);
   int it = 0, hl = 0, cv = 0;
   double fr = 0.0;
   check(vie_gmres_solve(op_n.handle(), de.get(), inv_v, db.get(), x0 ? dx0.get() : nullptr, cfg.tolerance, cfg.inner,
-                        cfg.outer, dx.get(), &it, &fr, hist.data(), static_cast<int>(hist.size()), &hl, &cv));
+                        cfg.outer, precond_diag ? &pc : nullptr, dx.get(), &it, &fr, hist.data(),
+                        static_cast<int>(hist.size()), &hl, &cv, nullptr));
   res.solution.resize(n);
-  dx.download(res.solution.data(), bytes);
+  dx.download(res.solution.data(), bytes, st);
+  res.residual_history.assign(hist.begin(), hist.begin() + std::min<long>(hl, static_cast<long>(hist.size())));
+  res.final_relative_residual = fr;
+  res.iterations = it;
+  res.converged = cv != 0;
+  return res;
+}
+
+// gmres(apply, rhs, cfg, x0, precond) with the reference's signature (solver.hpp:26,
+// :34-36): host closures on std::vector, run by the device GMRES (vie_gmres); every
+// application of a closure round-trips its vector through the host.
+using LinearMap = std::function<std::vector<cplx>(const std::vector<cplx>&)>;
+
+namespace detail {
+struct HostMap {
+  const LinearMap* f;
+  size_t n;
+  std::vector<cplx> in;
+  static void call(void* user, const double* x, double* y, void* stream) {
+    auto* h = static_cast<HostMap*>(user);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    h->in.resize(h->n);
+    cuda_check(cudaMemcpyAsync(h->in.data(), x, h->n * sizeof(cplx), cudaMemcpyDeviceToHost, st));
+    cuda_check(cudaStreamSynchronize(st));
+    const std::vector<cplx> out = (*h->f)(h->in);
+    if (out.size() != h->n) throw std::invalid_argument("gmres: linear map changed the vector size");
+    cuda_check(cudaMemcpyAsync(y, out.data(), h->n * sizeof(cplx), cudaMemcpyHostToDevice, st));
+    cuda_check(cudaStreamSynchronize(st));
+  }
+};
+}  // namespace detail
+
+inline GmresResult gmres(const LinearMap& apply, const std::vector<cplx>& rhs, const GmresConfig& cfg = {},
+                         const std::vector<cplx>* x0 = nullptr, const LinearMap& precond = nullptr,
+                         DftService* dft = nullptr) {
+  for (const cplx& v : rhs)
+    if (!std::isfinite(v.real()) || !std::isfinite(v.imag()))
+      throw std::invalid_argument("gmres: non-finite right-hand side");
+  if (cfg.tolerance < 0 || cfg.inner < 1 || cfg.outer < 1) throw std::invalid_argument("gmres: invalid configuration");
+  const size_t n = rhs.size();
+  if (x0 && x0->size() != n) throw std::invalid_argument("gmres: initial guess size mismatch");
+  DftService own(0);
+  DftService& d = dft ? *dft : own;
+  const cudaStream_t st = d.stream();
+  const size_t bytes = n * sizeof(cplx);
+  DeviceBuffer db(bytes), dx(bytes), dx0;
+  db.upload(rhs.data(), bytes, st);
+  if (x0) {
+    dx0 = DeviceBuffer(bytes);
+    dx0.upload(x0->data(), bytes, st);
+  }
+  detail::HostMap ha{&apply, n, {}}, hp{&precond, n, {}};
+  vie_precond pc{nullptr, &detail::HostMap::call, &hp};
+  GmresResult res;
+  std::vector<double> hist(static_cast<size_t>(cfg.inner) * static_cast<size_t>(cfg.outer) + 1);
+  int it = 0, hl = 0, cv = 0;
+  double fr = 0.0;
+  check(vie_gmres(d.handle(), static_cast<int64_t>(n), &detail::HostMap::call, &ha, db.get(), x0 ? dx0.get() : nullptr,
+                  cfg.tolerance, cfg.inner, cfg.outer, precond ? &pc : nullptr, dx.get(), &it, &fr, hist.data(),
+                  static_cast<int>(hist.size()), &hl, &cv, nullptr));
+  res.solution.resize(n);
+  dx.download(res.solution.data(), bytes, st);
   res.residual_history.assign(hist.begin(), hist.begin() + std::min<long>(hl, static_cast<long>(hist.size())));
   res.final_relative_residual = fr;
   res.iterations = it;
@@ -497,10 +668,11 @@ inline vie_scene make_scene(const DielectricMap& m, const PlaneWave& inc) {
   return s;
 }
 
+// The scene-stage calls below pass ctx = NULL and stream = NULL, so the library runs them
+// on the legacy default stream; the copies use the same stream.
 inline CurrentField field_from_device(const DeviceBuffer& b, const std::array<Index, 3>& d) {
   std::vector<cplx> v(static_cast<size_t>(3 * d[0] * d[1] * d[2]));
-  cuda_check(cudaDeviceSynchronize());
-  b.download(v.data(), v.size() * sizeof(cplx));
+  b.download(v.data(), v.size() * sizeof(cplx), cudaStreamLegacy);
   return CurrentField::from_vector(v, d);
 }
 
@@ -509,7 +681,7 @@ inline CurrentField build_rhs(const DielectricMap& m, const PlaneWave& inc, int 
   const vie_scene sc = make_scene(m, inc);
   const size_t nv = m.eps_r.size();
   DeviceBuffer de(nv * sizeof(cplx)), dr(3 * nv * sizeof(cplx));
-  de.upload(m.eps_r.data(), nv * sizeof(cplx));
+  de.upload(m.eps_r.data(), nv * sizeof(cplx), cudaStreamLegacy);
   check(vie_build_rhs(nullptr, &sc, de.get(), quad_points_per_axis, dr.get(), nullptr));
   return field_from_device(dr, m.grid.dims);
 }
@@ -529,10 +701,11 @@ inline Fields recover_fields(const CurrentField& j, const DielectricMap& m, cons
   const std::vector<cplx> jv = j.to_vector();
   DeviceBuffer de(nv * sizeof(cplx)), dj(3 * nv * sizeof(cplx)), dE(3 * nv * sizeof(cplx));
   DeviceBuffer dh(op_k ? 3 * nv * sizeof(cplx) : 0);
-  de.upload(m.eps_r.data(), nv * sizeof(cplx));
-  dj.upload(jv.data(), jv.size() * sizeof(cplx));
+  de.upload(m.eps_r.data(), nv * sizeof(cplx), cudaStreamLegacy);
+  dj.upload(jv.data(), jv.size() * sizeof(cplx), cudaStreamLegacy);
+  // the K matvec runs on the legacy stream too (stream = cudaStreamLegacy, ctx = NULL)
   check(vie_recover_fields(nullptr, &sc, de.get(), dj.get(), op_k ? op_k->handle() : nullptr, dE.get(),
-                           op_k ? dh.get() : nullptr, nullptr));
+                           op_k ? dh.get() : nullptr, cudaStreamLegacy));
   Fields f;
   f.e = field_from_device(dE, m.grid.dims);
   if (op_k) {
@@ -556,20 +729,20 @@ inline PostProcess postprocess(const Fields& f, const DielectricMap& m) {
   const std::vector<cplx> ev = f.e.to_vector();
   DeviceBuffer de(nv * sizeof(cplx)), dE(3 * nv * sizeof(cplx)), dp(nv * sizeof(double));
   DeviceBuffer dh(f.has_h ? 3 * nv * sizeof(cplx) : 0), db(f.has_h ? nv * sizeof(double) : 0);
-  de.upload(m.eps_r.data(), nv * sizeof(cplx));
-  dE.upload(ev.data(), ev.size() * sizeof(cplx));
+  de.upload(m.eps_r.data(), nv * sizeof(cplx), cudaStreamLegacy);
+  dE.upload(ev.data(), ev.size() * sizeof(cplx), cudaStreamLegacy);
   if (f.has_h) {
     const std::vector<cplx> hv = f.h.to_vector();
-    dh.upload(hv.data(), hv.size() * sizeof(cplx));
+    dh.upload(hv.data(), hv.size() * sizeof(cplx), cudaStreamLegacy);
   }
   PostProcess out;
   check(vie_postprocess(nullptr, &sc, de.get(), dE.get(), f.has_h ? dh.get() : nullptr, dp.get(),
                         f.has_h ? db.get() : nullptr, &out.total_absorbed_power, nullptr));
   out.p_abs.resize(nv);
-  dp.download(out.p_abs.data(), nv * sizeof(double));
+  dp.download(out.p_abs.data(), nv * sizeof(double), cudaStreamLegacy);
   if (f.has_h) {
     out.b1_plus.resize(nv);
-    db.download(out.b1_plus.data(), nv * sizeof(double));
+    db.download(out.b1_plus.data(), nv * sizeof(double), cudaStreamLegacy);
     out.has_b1 = true;
   }
   return out;

@@ -7,7 +7,10 @@
 #include <complex>
 #include <cstdlib>
 #include <cstring>
+#include <atomic>
+#include <functional>
 #include <map>
+#include <tuple>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -88,8 +91,24 @@ struct vie_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
-  std::map<int, std::unique_ptr<PlanHolder>> plans;
+  // plan cache keyed by (length, pruned, wide)
+  std::map<std::tuple<int, bool, bool>, std::unique_ptr<PlanHolder>> plans;
+  // references: the caller's (vie_ctx_create) plus one per live Tucker form and operator,
+  // which hold device pointers into the plans and run on the stream
+  std::atomic<int> refs{1};
 };
+
+namespace {
+void ctx_retain(vie_ctx c) { c->refs.fetch_add(1); }
+void ctx_release(vie_ctx c) {
+  if (c->refs.fetch_sub(1) != 1) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->plans.clear();
+  cudaStreamDestroy(c->stream);
+  delete c;
+}
+}  // namespace
 
 struct vie_tucker_s {
   vie_ctx ctx = nullptr;
@@ -101,6 +120,7 @@ struct vie_tucker_s {
   ~vie_tucker_s() {
     dev_free(core);
     for (auto* u : uo) dev_free(u);
+    if (ctx) ctx_release(ctx);
   }
 };
 
@@ -136,13 +156,15 @@ struct vie_op_s {
   double2* hy2 = nullptr;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_h2d[2] = {}, ev_done[2] = {}, ev_d2h[2] = {};
-  // GMRES state
+  // GMRES state (GmresWork, cached for vie_gmres_solve)
   int g_inner = 0;
   double2* V = nullptr;
   double2* tmp = nullptr;
+  double2* zp = nullptr;    // preconditioned vector M v
   double2* scal = nullptr;  // device scalars
   double2* red_partials = nullptr;
   unsigned int* red_counter = nullptr;
+  cudaEvent_t ev_user = nullptr;  // orders the solve after the caller's stream
   // side stream: the x-independent decompression runs concurrently with the
   // forward FFT passes (and with the H2D copy of vie_matvec_host)
   cudaStream_t side = nullptr;
@@ -157,7 +179,7 @@ struct vie_op_s {
                     static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(hx2), static_cast<void*>(hy2),
                     static_cast<void*>(V),
-                    static_cast<void*>(tmp), static_cast<void*>(scal), static_cast<void*>(red_partials),
+                    static_cast<void*>(tmp), static_cast<void*>(zp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
       dev_free(p);
     for (auto& e : ev)
@@ -170,6 +192,8 @@ struct vie_op_s {
     if (side) cudaStreamDestroy(side);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
+    if (ev_user) cudaEventDestroy(ev_user);
+    if (ctx) ctx_release(ctx);
   }
 };
 
@@ -226,7 +250,7 @@ bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::
 // wide = plan for the pencil kernel (radices up to 20, VIE_FFT_RADICES_WIDE)
 const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = false,
                         std::vector<int>* radices = nullptr) {
-  const int key = (pruned ? n : -n) * (wide ? 4096 : 1);
+  const auto key = std::make_tuple(n, pruned, wide);
   std::lock_guard<std::mutex> lk(ctx->mu);
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) {
@@ -532,11 +556,21 @@ int vie_ctx_create(vie_ctx* out, int device) {
 int vie_ctx_destroy(vie_ctx ctx) {
   return guard([&] {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->stream);
-    ctx->plans.clear();
-    cudaStreamDestroy(ctx->stream);
-    delete ctx;
+    ctx_release(ctx);  // freed once the last form / operator of the context is destroyed
+  });
+}
+
+int vie_ctx_stream(vie_ctx ctx, void** stream) {
+  return guard([&] {
+    if (!ctx || !stream) throw Invalid("vie_ctx_stream: null argument");
+    *stream = ctx->stream;
+  });
+}
+
+int vie_op_stream(vie_op op, void** stream) {
+  return guard([&] {
+    if (!op || !stream) throw Invalid("vie_op_stream: null argument");
+    *stream = op->ctx->stream;
   });
 }
 
@@ -588,6 +622,7 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
       if (sign[q] != 1 && sign[q] != -1) throw Invalid("vie_tucker_from_factors: sign must be +-1");
     }
     std::unique_ptr<vie_tucker_s> t(new vie_tucker_s);
+    ctx_retain(ctx);
     t->ctx = ctx;
     for (int q = 0; q < 3; ++q) {
       t->dims[q] = dims[q];
@@ -675,7 +710,7 @@ int vie_tucker_destroy(vie_tucker t) {
   return guard([&] {
     if (t) {
       cudaSetDevice(t->ctx->device);
-      delete t;
+      delete t;  // releases its context reference
     }
   });
 }
@@ -694,6 +729,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     if (grid[0] * grid[1] * grid[2] > (int64_t(1) << 31) / 8)
       throw Invalid("vie_op_create: grid too large for 32-bit spectral indexing");
     std::unique_ptr<vie_op_s> op(new vie_op_s);
+    ctx_retain(ctx);
     op->ctx = ctx;
     op->kind = kind;
     op->basis = basis;
@@ -1024,9 +1060,233 @@ int vie_system_matvec(vie_op op, const double* eps_r, double inv_v, const double
   });
 }
 
+}  // extern "C"
+
+namespace {
+
+// ---------------------------------------------------------------- GMRES core
+// Device-resident restarted GMRES(inner) with modified Gram-Schmidt and complex Givens
+// rotations, exactly the reference's order of operations (solver.hpp:34-142), on any
+// device linear map `apply`, with an optional right preconditioner M (solver.hpp:74,
+// :131: w = A M v_j, x += M V y; residual estimates stay those of the original system).
+// `allreduce`, when set, sums device scalars over the ranks of a distributed solve (the
+// MGS dots and norms) right after each reduction kernel.
+struct GmresWork {
+  double2* V = nullptr;    // (inner + 1) * n basis
+  double2* tmp = nullptr;  // n
+  double2* zp = nullptr;   // n (preconditioned vector), only with a preconditioner
+  double2* scal = nullptr; // 256 device scalars
+  vie::RedBuf rb{};
+};
+struct GmresOut {
+  int iters = 0;
+  bool conv = false;
+  double final_rel = 0.0;
+  std::vector<double> history;
+};
+using DevMap = std::function<void(const double2*, double2*)>;
+using DevReduce = std::function<void(double2*, int)>;
+
+GmresOut gmres_core(cudaStream_t st, int64_t n, const DevMap& apply, const DevMap& precond, const DevReduce& allreduce,
+                    const double2* rhs, const double2* x0, double tol, int inner, int outer, double2* x,
+                    const GmresWork& w) {
+  if (tol < 0 || inner < 1 || outer < 1) throw Invalid("gmres: invalid configuration");
+  if (inner + 2 > 256) throw Invalid("gmres: inner > 254 not supported");
+  double2* V = w.V;
+  double2* tmp = w.tmp;
+  double2* hd = w.scal;  // hd[0..j+1]
+  auto reduce = [&](double2* p, int count) {
+    if (allreduce) allreduce(p, count);
+  };
+  auto fetch = [&](int count, std::vector<double2>& h) {
+    h.resize(static_cast<size_t>(count));
+    VIE_CUDA_CHECK(cudaMemcpyAsync(h.data(), hd, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  };
+  std::vector<double2> hbuf;
+  GmresOut out;
+  // ||b|| (solver.hpp:43) and the non-finite check (:37)
+  vie::launch_nrm2sq(rhs, n, hd, w.rb, st);
+  reduce(hd, 1);
+  fetch(1, hbuf);
+  if (!std::isfinite(hbuf[0].x)) throw Invalid("gmres: non-finite right-hand side");
+  const double bnorm = std::sqrt(hbuf[0].x);
+  if (x0) {
+    if (x0 != x) VIE_CUDA_CHECK(cudaMemcpyAsync(x, x0, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+  }
+  if (bnorm == 0.0) {  // solver.hpp:46-51
+    VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
+    out.conv = true;
+    out.history.push_back(0.0);
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    return out;
+  }
+  const int m = inner;
+  std::vector<cd> hess(static_cast<size_t>((m + 1) * m), cd(0.0));
+  auto H = [&](int i, int j) -> cd& { return hess[static_cast<size_t>(i + (m + 1) * j)]; };
+  std::vector<cd> gv(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m));
+  for (int restart = 0; restart < outer && !out.conv; ++restart) {
+    apply(x, tmp);
+    vie::launch_residual(rhs, tmp, V, n, hd, w.rb, st);  // V_0 = r
+    reduce(hd, 1);
+    fetch(1, hbuf);
+    const double beta = std::sqrt(hbuf[0].x);
+    if (beta / bnorm <= tol) {
+      out.conv = true;
+      break;
+    }
+    vie::launch_scale_inv(V, V, nullptr, beta, n, st);  // basis.col(0) = r / beta
+    std::fill(gv.begin(), gv.end(), cd(0.0));
+    gv[0] = beta;
+    int j = 0;
+    bool breakdown = false;
+    for (; j < m; ++j) {
+      double2* vj = V + static_cast<int64_t>(j) * n;
+      double2* wv = V + static_cast<int64_t>(j + 1) * n;
+      if (precond) {  // w = A (M v_j)
+        precond(vj, w.zp);
+        apply(w.zp, wv);
+      } else {
+        apply(vj, wv);
+      }
+      vie::launch_dot(V, wv, n, hd, w.rb, st);  // h_0j
+      reduce(hd, 1);
+      for (int i = 0; i <= j; ++i) {
+        const double2* vi = V + static_cast<int64_t>(i) * n;
+        const double2* vn = i < j ? V + static_cast<int64_t>(i + 1) * n : nullptr;
+        vie::launch_mgs_step(wv, vi, hd + i, vn, n, hd + i + 1, w.rb, st);
+        reduce(hd + i + 1, 1);
+      }
+      fetch(j + 2, hbuf);
+      for (int i = 0; i <= j; ++i) H(i, j) = cd(hbuf[static_cast<size_t>(i)].x, hbuf[static_cast<size_t>(i)].y);
+      const double wnorm = std::sqrt(hbuf[static_cast<size_t>(j + 1)].x);
+      H(j + 1, j) = wnorm;
+      for (int i = 0; i < j; ++i) {
+        const cd t = cs[static_cast<size_t>(i)] * H(i, j) + sn[static_cast<size_t>(i)] * H(i + 1, j);
+        H(i + 1, j) = -std::conj(sn[static_cast<size_t>(i)]) * H(i, j) + std::conj(cs[static_cast<size_t>(i)]) * H(i + 1, j);
+        H(i, j) = t;
+      }
+      {
+        const cd a = H(j, j), bb = H(j + 1, j);
+        const double denom = std::sqrt(std::norm(a) + std::norm(bb));
+        if (denom == 0.0) {
+          cs[static_cast<size_t>(j)] = 1.0;
+          sn[static_cast<size_t>(j)] = 0.0;
+        } else {
+          cs[static_cast<size_t>(j)] = std::conj(a) / denom;
+          sn[static_cast<size_t>(j)] = std::conj(bb) / denom;
+        }
+        H(j, j) = cs[static_cast<size_t>(j)] * a + sn[static_cast<size_t>(j)] * bb;
+        H(j + 1, j) = 0.0;
+        const cd t = cs[static_cast<size_t>(j)] * gv[static_cast<size_t>(j)];
+        gv[static_cast<size_t>(j + 1)] = -std::conj(sn[static_cast<size_t>(j)]) * gv[static_cast<size_t>(j)];
+        gv[static_cast<size_t>(j)] = t;
+      }
+      ++out.iters;
+      const double rel = std::abs(gv[static_cast<size_t>(j + 1)]) / bnorm;
+      out.history.push_back(rel);
+      if (rel <= tol) {
+        ++j;
+        out.conv = true;
+        break;
+      }
+      if (wnorm < 1e-14 * beta) {
+        ++j;
+        breakdown = true;
+        break;
+      }
+      vie::launch_scale_inv(wv, wv, nullptr, wnorm, n, st);  // basis.col(j+1) = w / wnorm
+    }
+    std::vector<cd> yv(static_cast<size_t>(j), cd(0.0));
+    for (int i = j - 1; i >= 0; --i) {
+      cd sacc = gv[static_cast<size_t>(i)];
+      for (int l = i + 1; l < j; ++l) sacc -= H(i, l) * yv[static_cast<size_t>(l)];
+      yv[static_cast<size_t>(i)] = sacc / H(i, i);
+    }
+    if (j > 0) {
+      std::vector<double2> yd(static_cast<size_t>(j));
+      for (int l = 0; l < j; ++l) yd[static_cast<size_t>(l)] = make_double2(yv[static_cast<size_t>(l)].real(), yv[static_cast<size_t>(l)].imag());
+      VIE_CUDA_CHECK(cudaMemcpyAsync(hd, yd.data(), sizeof(double2) * j, cudaMemcpyHostToDevice, st));
+      if (precond) {  // x += M (V y)  (solver.hpp:130-131)
+        VIE_CUDA_CHECK(cudaMemsetAsync(tmp, 0, sizeof(double2) * n, st));
+        vie::launch_basis_update(tmp, V, n, hd, j, n, st);
+        precond(tmp, w.zp);
+        vie::launch_axpy1(x, w.zp, n, st);
+      } else {
+        vie::launch_basis_update(x, V, n, hd, j, n, st);  // x += V y
+      }
+      VIE_CUDA_CHECK(cudaStreamSynchronize(st));  // the host y staging is reused next cycle
+    }
+    if (breakdown && !out.conv) {
+      apply(x, tmp);
+      vie::launch_residual(rhs, tmp, nullptr, n, hd, w.rb, st);
+      reduce(hd, 1);
+      fetch(1, hbuf);
+      const double rel = std::sqrt(hbuf[0].x) / bnorm;
+      out.conv = rel <= tol;
+      if (out.conv) break;
+    }
+  }
+  apply(x, tmp);
+  vie::launch_residual(rhs, tmp, nullptr, n, hd, w.rb, st);
+  reduce(hd, 1);
+  fetch(1, hbuf);
+  out.final_rel = std::sqrt(hbuf[0].x) / bnorm;
+  VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  return out;
+}
+
+DevMap make_precond(const vie_precond* pc, int64_t n, cudaStream_t st) {
+  if (!pc || (!pc->diag && !pc->apply)) return nullptr;
+  if (pc->diag && pc->apply) throw Invalid("gmres: preconditioner has both a diagonal and a callback");
+  if (pc->diag) {
+    const double2* d = reinterpret_cast<const double2*>(pc->diag);
+    return [d, n, st](const double2* in, double2* out) { vie::launch_cmul_elem(d, in, out, n, st); };
+  }
+  return [pc, st](const double2* in, double2* out) {
+    pc->apply(pc->user, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out), st);
+  };
+}
+
+void report(const GmresOut& g, int* iterations, double* final_rel_res, double* history_host, int history_cap,
+            int* history_len, int* converged) {
+  if (iterations) *iterations = g.iters;
+  if (final_rel_res) *final_rel_res = g.final_rel;
+  if (converged) *converged = g.conv ? 1 : 0;
+  if (history_len) *history_len = static_cast<int>(g.history.size());
+  if (history_host)
+    for (int i = 0; i < history_cap && i < static_cast<int>(g.history.size()); ++i)
+      history_host[i] = g.history[static_cast<size_t>(i)];
+}
+
+// the solve runs on the context stream ordered after `user` (event), and `user` waits for it
+struct StreamJoin {
+  cudaStream_t st, user;
+  cudaEvent_t ev;
+  StreamJoin(cudaStream_t s, cudaStream_t u, cudaEvent_t e) : st(s), user(u), ev(e) {
+    if (user && user != st) {
+      VIE_CUDA_CHECK(cudaEventRecord(ev, user));
+      VIE_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+    }
+  }
+  void done() {
+    if (user && user != st) {
+      VIE_CUDA_CHECK(cudaEventRecord(ev, st));
+      VIE_CUDA_CHECK(cudaStreamWaitEvent(user, ev, 0));
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
 int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* rhs_d, const double* x0_d,
-                    double tol, int inner, int outer, double* x_d, int* iterations, double* final_rel_res,
-                    double* history_host, int history_cap, int* history_len, int* converged) {
+                    double tol, int inner, int outer, const vie_precond* precond, double* x_d, int* iterations,
+                    double* final_rel_res, double* history_host, int history_cap, int* history_len, int* converged,
+                    void* stream) {
   return guard([&] {
     if (!op || !eps_r || !rhs_d || !x_d) throw Invalid("gmres: null argument");
     if (tol < 0 || inner < 1 || outer < 1) throw Invalid("gmres: invalid configuration");
@@ -1035,9 +1295,6 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     cudaStream_t st = op->ctx->stream;
     const Geom& g = op->g;
     const int64_t n = static_cast<int64_t>(g.S) * g.n1 * g.n2 * g.n3;
-    const double2* eps = reinterpret_cast<const double2*>(eps_r);
-    const double2* rhs = reinterpret_cast<const double2*>(rhs_d);
-    double2* x = reinterpret_cast<double2*>(x_d);
     if (op->g_inner < inner) {
       dev_free(op->V);
       op->V = nullptr;
@@ -1045,145 +1302,80 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
       op->g_inner = inner;
     }
     if (!op->tmp) op->tmp = dev_alloc<double2>(static_cast<size_t>(n));
+    if (precond && !op->zp) op->zp = dev_alloc<double2>(static_cast<size_t>(n));
     if (!op->scal) op->scal = dev_alloc<double2>(256);
     if (!op->red_partials) {
       op->red_partials = dev_alloc<double2>(vie::kRedBlocks);
       op->red_counter = dev_alloc<unsigned int>(1);
-      VIE_CUDA_CHECK(cudaMemsetAsync(op->red_counter, 0, sizeof(unsigned int)));
+      VIE_CUDA_CHECK(cudaMemsetAsync(op->red_counter, 0, sizeof(unsigned int), st));
     }
-    if (inner + 2 > 256) throw Invalid("gmres: inner > 254 not supported");
-    vie::RedBuf rb{op->red_partials, op->red_counter};
-    double2* V = op->V;
-    double2* tmp = op->tmp;
-    double2* hd = op->scal;  // hd[0..j+1]
-    auto fetch = [&](int count, std::vector<double2>& h) {
-      h.resize(static_cast<size_t>(count));
-      VIE_CUDA_CHECK(cudaMemcpyAsync(h.data(), hd, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
-      VIE_CUDA_CHECK(cudaStreamSynchronize(st));
-    };
+    if (!op->ev_user) VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_user, cudaEventDisableTiming));
+    StreamJoin sj(st, static_cast<cudaStream_t>(stream), op->ev_user);
+    GmresWork w{op->V, op->tmp, op->zp, op->scal, vie::RedBuf{op->red_partials, op->red_counter}};
+    const double2* eps = reinterpret_cast<const double2*>(eps_r);
     auto sysmv = [&](const double2* in, double2* outv) { run_matvec(op, in, outv, st, eps, inv_v, 1); };
-    std::vector<double2> hbuf;
-    std::vector<double> history;
-    int iters = 0;
-    bool conv = false;
-    // ||b|| (solver.hpp:43) and the non-finite check (:37)
-    vie::launch_nrm2sq(rhs, n, hd, rb, st);
-    fetch(1, hbuf);
-    if (!std::isfinite(hbuf[0].x)) throw Invalid("gmres: non-finite right-hand side");
-    const double bnorm = std::sqrt(hbuf[0].x);
-    if (x0_d) {
-      if (x0_d != x_d) VIE_CUDA_CHECK(cudaMemcpyAsync(x, x0_d, sizeof(double2) * n, cudaMemcpyDeviceToDevice, st));
-    } else {
-      VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
-    }
-    double final_rel = 0.0;
-    if (bnorm == 0.0) {
-      VIE_CUDA_CHECK(cudaMemsetAsync(x, 0, sizeof(double2) * n, st));
-      conv = true;
-      history.push_back(0.0);
-    } else {
-      const int m = inner;
-      std::vector<cd> hess(static_cast<size_t>((m + 1) * m), cd(0.0));
-      auto H = [&](int i, int j) -> cd& { return hess[static_cast<size_t>(i + (m + 1) * j)]; };
-      std::vector<cd> gv(static_cast<size_t>(m + 1)), cs(static_cast<size_t>(m)), sn(static_cast<size_t>(m));
-      for (int restart = 0; restart < outer && !conv; ++restart) {
-        sysmv(x, tmp);
-        vie::launch_residual(rhs, tmp, V, n, hd, rb, st);  // V_0 = r
-        fetch(1, hbuf);
-        const double beta = std::sqrt(hbuf[0].x);
-        if (beta / bnorm <= tol) {
-          conv = true;
-          break;
-        }
-        vie::launch_scale_inv(V, V, nullptr, beta, n, st);  // basis.col(0) = r / beta
-        std::fill(gv.begin(), gv.end(), cd(0.0));
-        gv[0] = beta;
-        int j = 0;
-        bool breakdown = false;
-        for (; j < m; ++j) {
-          double2* vj = V + static_cast<int64_t>(j) * n;
-          double2* w = V + static_cast<int64_t>(j + 1) * n;
-          sysmv(vj, w);
-          vie::launch_dot(V, w, n, hd, rb, st);  // h_0j
-          for (int i = 0; i <= j; ++i) {
-            const double2* vi = V + static_cast<int64_t>(i) * n;
-            const double2* vn = i < j ? V + static_cast<int64_t>(i + 1) * n : nullptr;
-            vie::launch_mgs_step(w, vi, hd + i, vn, n, hd + i + 1, rb, st);
-          }
-          fetch(j + 2, hbuf);
-          for (int i = 0; i <= j; ++i) H(i, j) = cd(hbuf[static_cast<size_t>(i)].x, hbuf[static_cast<size_t>(i)].y);
-          const double wnorm = std::sqrt(hbuf[static_cast<size_t>(j + 1)].x);
-          H(j + 1, j) = wnorm;
-          for (int i = 0; i < j; ++i) {
-            const cd t = cs[static_cast<size_t>(i)] * H(i, j) + sn[static_cast<size_t>(i)] * H(i + 1, j);
-            H(i + 1, j) = -std::conj(sn[static_cast<size_t>(i)]) * H(i, j) + std::conj(cs[static_cast<size_t>(i)]) * H(i + 1, j);
-            H(i, j) = t;
-          }
-          {
-            const cd a = H(j, j), b = H(j + 1, j);
-            const double denom = std::sqrt(std::norm(a) + std::norm(b));
-            if (denom == 0.0) {
-              cs[static_cast<size_t>(j)] = 1.0;
-              sn[static_cast<size_t>(j)] = 0.0;
-            } else {
-              cs[static_cast<size_t>(j)] = std::conj(a) / denom;
-              sn[static_cast<size_t>(j)] = std::conj(b) / denom;
-            }
-            H(j, j) = cs[static_cast<size_t>(j)] * a + sn[static_cast<size_t>(j)] * b;
-            H(j + 1, j) = 0.0;
-            const cd t = cs[static_cast<size_t>(j)] * gv[static_cast<size_t>(j)];
-            gv[static_cast<size_t>(j + 1)] = -std::conj(sn[static_cast<size_t>(j)]) * gv[static_cast<size_t>(j)];
-            gv[static_cast<size_t>(j)] = t;
-          }
-          ++iters;
-          const double rel = std::abs(gv[static_cast<size_t>(j + 1)]) / bnorm;
-          history.push_back(rel);
-          if (rel <= tol) {
-            ++j;
-            conv = true;
-            break;
-          }
-          if (wnorm < 1e-14 * beta) {
-            ++j;
-            breakdown = true;
-            break;
-          }
-          vie::launch_scale_inv(w, w, nullptr, wnorm, n, st);  // basis.col(j+1) = w / wnorm
-        }
-        std::vector<cd> yv(static_cast<size_t>(j), cd(0.0));
-        for (int i = j - 1; i >= 0; --i) {
-          cd s = gv[static_cast<size_t>(i)];
-          for (int l = i + 1; l < j; ++l) s -= H(i, l) * yv[static_cast<size_t>(l)];
-          yv[static_cast<size_t>(i)] = s / H(i, i);
-        }
-        if (j > 0) {
-          std::vector<double2> yd(static_cast<size_t>(j));
-          for (int l = 0; l < j; ++l) yd[static_cast<size_t>(l)] = make_double2(yv[static_cast<size_t>(l)].real(), yv[static_cast<size_t>(l)].imag());
-          VIE_CUDA_CHECK(cudaMemcpyAsync(hd, yd.data(), sizeof(double2) * j, cudaMemcpyHostToDevice, st));
-          vie::launch_basis_update(x, V, n, hd, j, n, st);  // x += V y (solver.hpp:130-131)
-        }
-        if (breakdown && !conv) {
-          sysmv(x, tmp);
-          vie::launch_residual(rhs, tmp, nullptr, n, hd, rb, st);
-          fetch(1, hbuf);
-          const double rel = std::sqrt(hbuf[0].x) / bnorm;
-          conv = rel <= tol;
-          if (conv) break;
-        }
-      }
-      sysmv(x, tmp);
-      vie::launch_residual(rhs, tmp, nullptr, n, hd, rb, st);
-      fetch(1, hbuf);
-      final_rel = std::sqrt(hbuf[0].x) / bnorm;
-    }
+    const GmresOut r = gmres_core(st, n, sysmv, make_precond(precond, n, st), nullptr,
+                                  reinterpret_cast<const double2*>(rhs_d), reinterpret_cast<const double2*>(x0_d), tol,
+                                  inner, outer, reinterpret_cast<double2*>(x_d), w);
+    sj.done();
+    report(r, iterations, final_rel_res, history_host, history_cap, history_len, converged);
+  });
+}
+
+int vie_gmres(vie_ctx ctx, int64_t n, vie_linear_map_fn apply, void* apply_user, const double* rhs_d,
+              const double* x0_d, double tol, int inner, int outer, const vie_precond* precond, double* x_d,
+              int* iterations, double* final_rel_res, double* history_host, int history_cap, int* history_len,
+              int* converged, void* stream) {
+  return guard([&] {
+    if (!ctx || !apply || !rhs_d || !x_d || n < 1) throw Invalid("gmres: null argument");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    DevPool pool;
+    GmresWork w;
+    if (inner >= 1 && inner + 2 <= 256) w.V = pool.alloc<double2>(static_cast<size_t>(n) * (inner + 1));
+    w.tmp = pool.alloc<double2>(static_cast<size_t>(n));
+    if (precond) w.zp = pool.alloc<double2>(static_cast<size_t>(n));
+    w.scal = pool.alloc<double2>(256);
+    w.rb.partials = pool.alloc<double2>(vie::kRedBlocks);
+    w.rb.counter = pool.alloc<unsigned int>(1);
+    VIE_CUDA_CHECK(cudaMemsetAsync(w.rb.counter, 0, sizeof(unsigned int), st));
+    cudaEvent_t ev = nullptr;
+    VIE_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    struct EvGuard {
+      cudaEvent_t e;
+      ~EvGuard() { cudaEventDestroy(e); }
+    } evg{ev};
+    StreamJoin sj(st, static_cast<cudaStream_t>(stream), ev);
+    auto amap = [&](const double2* in, double2* outv) {
+      apply(apply_user, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(outv), st);
+    };
+    const GmresOut r = gmres_core(st, n, amap, make_precond(precond, n, st), nullptr,
+                                  reinterpret_cast<const double2*>(rhs_d), reinterpret_cast<const double2*>(x0_d), tol,
+                                  inner, outer, reinterpret_cast<double2*>(x_d), w);
+    sj.done();
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
-    if (iterations) *iterations = iters;
-    if (final_rel_res) *final_rel_res = final_rel;
-    if (converged) *converged = conv ? 1 : 0;
-    if (history_len) *history_len = static_cast<int>(history.size());
-    if (history_host)
-      for (int i = 0; i < history_cap && i < static_cast<int>(history.size()); ++i)
-        history_host[i] = history[static_cast<size_t>(i)];
+    report(r, iterations, final_rel_res, history_host, history_cap, history_len, converged);
+  });
+}
+
+int vie_matvec_timed(vie_op op, const double* x, double* y, double* fft_ms, double* product_ms) {
+  return guard([&] {
+    if (!op || !x || !y) throw Invalid("apply_operator: null argument");
+    if (x == y) throw Invalid("apply_operator: x and y must not alias");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    const int saved = op->profiling;
+    op->profiling = 1;  // serial stages, one event interval each
+    try {
+      run_matvec(op, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), op->ctx->stream, nullptr,
+                 0.0, 0);
+    } catch (...) {
+      op->profiling = saved;
+      throw;
+    }
+    op->profiling = saved;
+    const double* t = op->stage_ms;  // row, column, decompression, pencil, column^-1, row^-1
+    if (fft_ms) *fft_ms = t[0] + t[1] + t[4] + t[5];
+    if (product_ms) *product_ms = t[2] + t[3];
   });
 }
 

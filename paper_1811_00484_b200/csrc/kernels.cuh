@@ -130,6 +130,10 @@ void launch_residual(const double2* rhs, const double2* ax, double2* r, int64_t 
                      cudaStream_t st);
 // y = x / d with d = s[0].x (device) or `divisor` when s == nullptr
 void launch_scale_inv(const double2* x, double2* y, const double2* s, double divisor, int64_t n, cudaStream_t st);
+// x += z
+void launch_axpy1(double2* x, const double2* z, int64_t n, cudaStream_t st);
+// out = d * in (element-wise complex product: the diagonal right preconditioner)
+void launch_cmul_elem(const double2* d, const double2* in, double2* out, int64_t n, cudaStream_t st);
 // x += sum_l V_l * coef[l]
 void launch_basis_update(double2* x, const double2* V, int64_t ldv, const double2* coef, int j, int64_t n,
                          cudaStream_t st);

@@ -125,7 +125,27 @@ __global__ void k_basis_update(double2* __restrict__ x, const double2* __restric
   }
 }
 
+__global__ void k_axpy1(double2* __restrict__ x, const double2* __restrict__ z, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = cadd(x[i], z[i]);
+}
+
+__global__ void k_cmul_elem(const double2* __restrict__ d, const double2* __restrict__ in, double2* __restrict__ out,
+                            int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = cmul(d[i], in[i]);
+}
+
 }  // namespace
+
+void launch_axpy1(double2* x, const double2* z, int64_t n, cudaStream_t st) {
+  k_axpy1<<<kRedBlocks, kThreads, 0, st>>>(x, z, n);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+void launch_cmul_elem(const double2* d, const double2* in, double2* out, int64_t n, cudaStream_t st) {
+  k_cmul_elem<<<kRedBlocks, kThreads, 0, st>>>(d, in, out, n);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_dot(const double2* a, const double2* b, int64_t n, double2* out, RedBuf rb, cudaStream_t st) {
   k_dot<<<kRedBlocks, kThreads, 0, st>>>(a, b, n, out, rb);

@@ -131,6 +131,7 @@ struct Pencil3Args {
   int nk;      // k-planes per slab block
   int KB;      // k extent of a load box (divides nk)
   int KBS;     // k extent of a store box (divides nk and R1 / 2)
+  int pf;      // L2 prefetch distance in clusters (co-resident clusters; 0 = off)
 };
 
 #ifdef VIE_PENCIL_PROFILE
@@ -150,7 +151,7 @@ __device__ unsigned long long g_p3_phase[8];
 #endif
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
@@ -176,6 +177,18 @@ __device__ __forceinline__ void tma_load5_mc(void* dst, const CUtensorMap* m, in
       "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)), "h"(mask)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch5(const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* m, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
 }
 __device__ __forceinline__ void tma_store5(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3,
                                            int c4) {
@@ -244,6 +257,21 @@ __global__ void __launch_bounds__(512, 1)
       tma_load5_mc(buf + static_cast<size_t>(k) * LINES, &tmIn, 2 * cl0, 0, 2 * j2, k - r * a.nk, r, inbar, 3);
     }
     for (int i = 0; i < NBUF && i < nch; ++i) issue_chunk(i);
+    // L2 prefetch of the cluster that will run on this SM pair next (about pf clusters on in
+    // launch order): its input boxes (this CTA's half) and its spectrum rows of branch b
+    if (a.pf > 0) {
+      const int ng = static_cast<int>(gridDim.x >> 1);
+      const int nxt = static_cast<int>(blockIdx.y) * ng + static_cast<int>(blockIdx.x >> 1) + a.pf;
+      if (nxt < ng * static_cast<int>(gridDim.y)) {
+        const int ni1 = a.gfirst + nxt % ng, nj2 = 1 + nxt / ng;
+        for (int j = b; j < nbox; j += 2) {
+          const int k = j * a.KB;
+          const int r = k / a.nk;
+          tma_prefetch5(&tmIn, 2 * (2 * ni1 - a.p1off), 0, 2 * nj2, k - r * a.nk, r);
+        }
+        for (int q = 0; q < nch; ++q) tma_prefetch3(&tmS, 2 * (b * E + q * U), 0, nj2 * (a.n1 + 1) + ni1);
+      }
+    }
   }
   P3_PHASE(0);
   mbar_wait(inbar, 0);
@@ -506,7 +534,7 @@ bool launch3_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     if (ghi <= glo || g.n2 < 2) return true;
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    Pencil3Args a{twm3, g.n1, g.W, g.p1off, glo, g.nk, kb, kbs};
+    Pencil3Args a{twm3, g.n1, g.W, g.p1off, glo, g.nk, kb, kbs, 0};
     CUtensorMap tmS, tmIn, tmOut;
     encode_spectrum_map(&tmS, Shat, g, {2 * UB, NC, 1});
     encode_slab_map(&tmIn, Bin, g, kb);
@@ -523,6 +551,12 @@ bool launch3_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    static const int pf_env = std::getenv("VIE_P3_PF") ? std::atoi(std::getenv("VIE_P3_PF")) : -1;
+    if (pf_env != 0) {
+      int ncl = 0;
+      VIE_CUDA_CHECK(cudaOccupancyMaxActiveClusters(&ncl, reinterpret_cast<const void*>(fn), &cfg));
+      a.pf = pf_env > 0 ? pf_env : ncl;
+    }
     VIE_CUDA_CHECK(cudaLaunchKernelEx(&cfg, fn, a, tmS, tmIn, tmOut));
     VIE_CUDA_CHECK(cudaGetLastError());
     return true;

@@ -33,6 +33,13 @@ VIE_OK, VIE_EINVAL, VIE_ENOMEM, VIE_ECUDA, VIE_ENCCL = 0, 1, 2, 3, 4
 _dp = C.POINTER(C.c_double)
 _lib = None
 
+# vie_linear_map_fn / vie_precond (include/vie_b200.h)
+_LinearMapFn = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class _Precond(C.Structure):
+    _fields_ = [("diag", C.c_void_p), ("apply", _LinearMapFn), ("user", C.c_void_p)]
+
 
 class VieError(RuntimeError):
     def __init__(self, code: int, msg: str):
@@ -61,8 +68,15 @@ def lib() -> C.CDLL:
         L.vie_slab_inverse.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                        C.c_int, C.c_void_p]
         L.vie_gmres_solve.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_double,
-                                      C.c_int, C.c_int, C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double),
-                                      _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+                                      C.c_int, C.c_int, C.POINTER(_Precond), C.c_void_p, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_double), _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                      C.c_void_p]
+        L.vie_gmres.argtypes = [C.c_void_p, C.c_int64, _LinearMapFn, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                C.c_int, C.c_int, C.POINTER(_Precond), C.c_void_p, C.POINTER(C.c_int),
+                                C.POINTER(C.c_double), _dp, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                C.c_void_p]
+        L.vie_matvec_timed.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -365,23 +379,110 @@ class GmresResult:  # solver.hpp:18-24
     converged: bool
 
 
+class _DevView:
+    """Zero-copy view of n complex128 values at a device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<c16", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _map_callback(fn, n: int, device):
+    """C callback for a Python device map fn(x, y) (torch CUDA tensors), run on the
+    solve's stream."""
+    torch = _torch()
+
+    def cb(user, xp, yp, stream):
+        x = torch.as_tensor(_DevView(xp, n), device=device)
+        y = torch.as_tensor(_DevView(yp, n), device=device)
+        with torch.cuda.stream(torch.cuda.ExternalStream(int(stream or 0), device=device)):
+            fn(x, y)
+
+    return _LinearMapFn(cb)
+
+
+def _precond_struct(precond, n: int, device):
+    """None -> no preconditioner; CUDA tensor of n values -> diagonal M; callable
+    fn(x, y) -> the callback form.  Returns (struct or None, keep-alive)."""
+    torch = _torch()
+    if precond is None:
+        return None, None
+    if isinstance(precond, torch.Tensor):
+        if not (precond.is_cuda and precond.numel() == n):
+            raise ValueError("gmres: diagonal preconditioner must be a CUDA tensor of n values")
+        d = precond.to(torch.complex128).contiguous()
+        return _Precond(d.data_ptr(), _LinearMapFn(), None), d
+    if callable(precond):
+        cb = _map_callback(precond, n, device)
+        return _Precond(None, cb, None), cb
+    raise ValueError("gmres: precond must be None, a CUDA tensor or a callable")
+
+
 def gmres(op: EmbeddedSpectrum, eps_r, inv_v: float, rhs, cfg: GmresConfig = GmresConfig(), x0=None,
-          history_cap: int = 100000) -> GmresResult:
-    """Restarted GMRES on apply_system, device resident (solver.hpp:34-142)."""
+          history_cap: int = 100000, precond=None, stream=None) -> GmresResult:
+    """Restarted GMRES on apply_system, device resident (solver.hpp:34-142); optional
+    right preconditioner (solver.hpp:74, :131): a CUDA tensor (diagonal) or fn(x, y)."""
     torch = _torch()
     rhs = _dev_vec(op, rhs)
     eps_r = eps_r.to(torch.complex128).contiguous()
     x = torch.empty_like(rhs)
     x0p = _dev_vec(op, x0).data_ptr() if x0 is not None else None
+    pc, keep = _precond_struct(precond, rhs.numel(), rhs.device)
     it, hl, cv = C.c_int(), C.c_int(), C.c_int()
     fr = C.c_double()
     hist = np.empty(history_cap, np.float64)
-    torch.cuda.current_stream(rhs.device).synchronize()
     _check(lib().vie_gmres_solve(op.handle, eps_r.data_ptr(), float(inv_v), rhs.data_ptr(), x0p,
-                                 float(cfg.tolerance), int(cfg.inner), int(cfg.outer), x.data_ptr(),
+                                 float(cfg.tolerance), int(cfg.inner), int(cfg.outer),
+                                 C.byref(pc) if pc is not None else None, x.data_ptr(),
                                  C.byref(it), C.byref(fr), hist.ctypes.data_as(_dp), int(history_cap),
-                                 C.byref(hl), C.byref(cv)))
+                                 C.byref(hl), C.byref(cv), _stream_handle(stream, rhs.device)))
+    del keep
     return GmresResult(x, hist[: min(hl.value, history_cap)].tolist(), fr.value, it.value, bool(cv.value))
+
+
+def gmres_map(dft: DftService, apply, rhs, cfg: GmresConfig = GmresConfig(), x0=None, precond=None,
+              history_cap: int = 100000) -> GmresResult:
+    """gmres(apply, rhs, cfg, x0, precond) of solver.hpp:34 for any device linear map
+    apply(x, y) (y = A x, torch CUDA complex128 tensors), on the device GMRES (vie_gmres)."""
+    torch = _torch()
+    if not (isinstance(rhs, torch.Tensor) and rhs.is_cuda and rhs.dtype == torch.complex128):
+        raise ValueError("gmres: rhs must be a CUDA complex128 tensor")
+    rhs = rhs.contiguous()
+    n = rhs.numel()
+    if x0 is not None and x0.numel() != n:
+        raise ValueError("gmres: initial guess size mismatch")
+    x = torch.empty_like(rhs)
+    x0c = x0.to(torch.complex128).contiguous() if x0 is not None else None
+    cb = _map_callback(apply, n, rhs.device)
+    pc, keep = _precond_struct(precond, n, rhs.device)
+    it, hl, cv = C.c_int(), C.c_int(), C.c_int()
+    fr = C.c_double()
+    hist = np.empty(history_cap, np.float64)
+    _check(lib().vie_gmres(dft.handle, n, cb, None, rhs.data_ptr(), x0c.data_ptr() if x0c is not None else None,
+                           float(cfg.tolerance), int(cfg.inner), int(cfg.outer),
+                           C.byref(pc) if pc is not None else None, x.data_ptr(), C.byref(it), C.byref(fr),
+                           hist.ctypes.data_as(_dp), int(history_cap), C.byref(hl), C.byref(cv),
+                           _stream_handle(None, rhs.device)))
+    del keep, cb
+    return GmresResult(x, hist[: min(hl.value, history_cap)].tolist(), fr.value, it.value, bool(cv.value))
+
+
+@dataclass
+class ApplyTimings:  # operator.hpp:189-192
+    fft_ms: float = 0.0
+    product_ms: float = 0.0
+
+
+def apply_operator_timed(op: EmbeddedSpectrum, x, timings: ApplyTimings, out=None):
+    """apply_operator with ApplyTimings (vie_matvec_timed): serialised stages, CUDA events."""
+    torch = _torch()
+    x = _dev_vec(op, x)
+    y = out if out is not None else torch.empty_like(x)
+    torch.cuda.current_stream(x.device).synchronize()
+    f, p = C.c_double(), C.c_double()
+    _check(lib().vie_matvec_timed(op.handle, x.data_ptr(), y.data_ptr(), C.byref(f), C.byref(p)))
+    timings.fft_ms, timings.product_ms = f.value, p.value
+    return y
 
 
 # ----------------------------------------------------------------------------- scene stages

@@ -6,6 +6,7 @@
 #include <complex>
 #include <cstdio>
 #include <functional>
+#include <memory>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -458,6 +459,269 @@ int main() {
     expect(rel(e, rep.fields.e.to_vector()) <= 1e-8, "e");
     expect(rep.fields.has_h && rel(h, rep.fields.h.to_vector()) <= 1e-8, "h");
     expect(std::abs(rep.post.total_absorbed_power - tot) <= 1e-8 * std::abs(tot), "total power");
+  });
+
+  // ---- 64^3 at the BASELINE configs[1] grid (review round 1: the drop-in's copies were
+  // unordered with the context stream; these sizes expose such races)
+  run("ApplySystem.Pwl64.MatchesOracle", [&] {  // test_solver.cpp:153-180 at 64^3 PWL
+    const std::array<Index, 3> d{64, 64, 64};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWL, d, 4, 640);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWL, fam, dft);
+    OracleForms of = to_oracle(fam, BasisOrder::PWL);
+    std::vector<cplx> eps(static_cast<size_t>(op.n_vox()));
+    for (size_t i = 0; i < eps.size(); ++i) eps[i] = cplx(2.0 + 0.1 * static_cast<double>(i % 7), -0.3);
+    CurrentField x = random_field(d, BasisOrder::PWL, 641);
+    CurrentField y = apply_system(eps, 0.37, op, x);
+    const std::vector<cplx> xv = x.to_vector();
+    std::vector<cplx> yref(xv.size());
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_apply_system_tucker(1, g, of.ranks.data(), of.pc.data(), of.p1.data(), of.p2.data(), of.p3.data(),
+                                reinterpret_cast<const double*>(eps.data()), 0.37,
+                                reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yref.data())))
+      throw std::runtime_error(orc_last_error());
+    const double e = rel(yref, y.to_vector());
+    expect(e <= 1e-10, "rel err " + std::to_string(e));
+  });
+
+  run("GmresSystem.Pwl64.HistoryMatchesOracle", [&] {  // solver.hpp:34-142, 6 Arnoldi steps
+    const std::array<Index, 3> d{64, 64, 64};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWL, d, 3, 650);
+    for (auto& pr : fam)
+      for (auto& v : pr.second.core.data) v *= 1e-3;
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWL, fam, dft);
+    OracleForms of = to_oracle(fam, BasisOrder::PWL);
+    std::vector<cplx> eps(static_cast<size_t>(op.n_vox()));
+    for (size_t i = 0; i < eps.size(); ++i) eps[i] = cplx(2.0 + 3.0 * static_cast<double>(i % 5) / 5.0, -0.5);
+    const std::vector<cplx> rhs = random_field(d, BasisOrder::PWL, 651).to_vector();
+    const GmresConfig cfg{1e-14, 6, 1};  // 6 iterations, not converged: compare the whole history
+    GmresResult r = gmres_system(eps, 1.0, op, rhs, cfg);
+    std::vector<cplx> xref(rhs.size());
+    std::vector<double> hist(64);
+    int it = 0, cv = 0, hl = 0;
+    double fr = 0;
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_gmres_system_tucker(1, g, of.ranks.data(), of.pc.data(), of.p1.data(), of.p2.data(), of.p3.data(),
+                                reinterpret_cast<const double*>(eps.data()), 1.0,
+                                reinterpret_cast<const double*>(rhs.data()), nullptr, cfg.tolerance, cfg.inner,
+                                cfg.outer, reinterpret_cast<double*>(xref.data()), &it, &cv, &fr, hist.data(), 64, &hl))
+      throw std::runtime_error(orc_last_error());
+    expect(r.iterations == it && static_cast<int>(r.residual_history.size()) == hl, "iterations");
+    for (int i = 0; i < hl; ++i)
+      expect(std::abs(r.residual_history[i] - hist[i]) <= 1e-10 * hist[i], "history " + std::to_string(i));
+    expect(std::abs(r.final_relative_residual - fr) <= 1e-8 * fr, "final residual");
+    expect(rel(xref, r.solution) <= 1e-10, "iterate");
+  });
+
+  run("RecoverFields.K64.MatchesOracle", [&] {  // solver.hpp:211-249 with the K operator, 64^3 PWC
+    const std::array<Index, 3> d{64, 64, 64};
+    auto famk = make_family(OperatorKind::K, BasisOrder::PWC, d, 4, 660);
+    EmbeddedSpectrum opk = build_operator_spectra(OperatorKind::K, BasisOrder::PWC, famk, dft);
+    OracleForms ofk = to_oracle(famk, BasisOrder::PWC);
+    VoxelGrid vg{d, {0.002, 0.002, 0.002}, {-0.064, -0.064, -0.064}};
+    DielectricMap m(vg, 2.98e8);
+    for (Index k = 8; k < 56; ++k)
+      for (Index j = 8; j < 56; ++j)
+        for (Index i = 8; i < 56; ++i) m.set_voxel(i, j, k, 50.0, 0.6);
+    PlaneWave inc{{1.0, 0.0, 0.0}, {0.0, 0.0, 1.0}, 1.0};
+    const double geo[6] = {0.002, 0.002, 0.002, -0.064, -0.064, -0.064};
+    const double pw[7] = {1.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1.0};
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    CurrentField j = random_field(d, BasisOrder::PWC, 661);
+    Fields f = recover_fields(j, m, inc, &opk);
+    const std::vector<cplx> jv = j.to_vector();
+    const size_t nv = m.eps_r.size();
+    std::vector<cplx> kj(3 * nv), e(3 * nv), h(3 * nv);
+    if (orc_apply_operator_tucker(1, 0, g, ofk.ranks.data(), ofk.pc.data(), ofk.p1.data(), ofk.p2.data(),
+                                  ofk.p3.data(), reinterpret_cast<const double*>(jv.data()),
+                                  reinterpret_cast<double*>(kj.data())) ||
+        orc_recover_fields(g, geo, 2.98e8, pw, reinterpret_cast<const double*>(m.eps_r.data()),
+                           reinterpret_cast<const double*>(jv.data()), reinterpret_cast<const double*>(kj.data()),
+                           reinterpret_cast<double*>(e.data()), reinterpret_cast<double*>(h.data())))
+      throw std::runtime_error(orc_last_error());
+    expect(f.has_h, "h with the K operator");
+    expect(rel(e, f.e.to_vector()) <= 1e-12, "e");
+    expect(rel(h, f.h.to_vector()) <= 1e-10, "h");
+  });
+
+  // ---- gmres(apply, rhs, cfg, x0, precond) known answers, restated from
+  // test_solver.cpp:31-114 and test_scene_io.cpp:107-139 with the same seeded inputs
+  // (test_util.hpp random_matrix == orc_random_matrix), on the device GMRES (vie_gmres)
+  auto rmat = [](Index rows, Index cols, std::uint64_t seed) {
+    std::vector<cplx> m(static_cast<size_t>(rows * cols));
+    if (orc_random_matrix(rows, cols, seed, reinterpret_cast<double*>(m.data())))
+      throw std::runtime_error(orc_last_error());
+    return m;
+  };
+  auto dense = [](const std::vector<cplx>& a, Index n) {  // column-major n x n
+    return [a, n](const std::vector<cplx>& v) {
+      std::vector<cplx> o(static_cast<size_t>(n), cplx(0.0));
+      for (Index j = 0; j < n; ++j)
+        for (Index i = 0; i < n; ++i) o[i] += a[static_cast<size_t>(i + n * j)] * v[j];
+      return o;
+    };
+  };
+  auto diag_map = [](const std::vector<cplx>& d) {
+    return [d](const std::vector<cplx>& v) {
+      std::vector<cplx> o(v.size());
+      for (size_t i = 0; i < v.size(); ++i) o[i] = d[i] * v[i];
+      return o;
+    };
+  };
+  auto norm_rel = [](const std::vector<cplx>& a, const std::vector<cplx>& b) {  // |a - b| / |b|
+    double num = 0.0, den = 0.0;
+    for (size_t i = 0; i < a.size(); ++i) {
+      num += std::norm(a[i] - b[i]);
+      den += std::norm(b[i]);
+    }
+    return std::sqrt(num / den);
+  };
+  run("Gmres.IdentityConvergesInOneIteration", [&] {  // test_solver.cpp:31-38
+    const std::vector<cplx> rhs = rmat(20, 1, 1);
+    GmresResult r = gmres([](const std::vector<cplx>& v) { return v; }, rhs, GmresConfig{}, nullptr, nullptr, &dft);
+    expect(r.converged && r.iterations == 1, "iterations " + std::to_string(r.iterations));
+    expect(norm_rel(r.solution, rhs) < 1e-12, "solution");
+  });
+  run("Gmres.DiagonalSystemMatchesDirectSolve", [&] {  // test_solver.cpp:40-53
+    std::vector<cplx> d(10);
+    for (int i = 0; i < 10; ++i) d[i] = cplx(i + 1.0, 0.5 * i);
+    const std::vector<cplx> rhs = rmat(10, 1, 2);
+    GmresConfig cfg;
+    cfg.tolerance = 1e-12;
+    GmresResult r = gmres(diag_map(d), rhs, cfg, nullptr, nullptr, &dft);
+    std::vector<cplx> ex(10);
+    for (int i = 0; i < 10; ++i) ex[i] = rhs[i] / d[i];
+    expect(r.converged, "converged");
+    expect(norm_rel(r.solution, ex) < 1e-10, "solution");
+  });
+  run("Gmres.RestartsReachTolerance", [&] {  // test_solver.cpp:55-68
+    std::vector<cplx> a0 = rmat(30, 30, 3), a(900, cplx(0.0));
+    for (int i = 0; i < 30; ++i)
+      for (int j = 0; j < 30; ++j) {
+        cplx acc = 0.0;
+        for (int k = 0; k < 30; ++k) acc += a0[i + 30 * k] * std::conj(a0[j + 30 * k]);
+        a[i + 30 * j] = acc / 30.0 + (i == j ? 4.0 : 0.0);
+      }
+    const std::vector<cplx> rhs = rmat(30, 1, 4);
+    GmresConfig cfg{1e-9, 5, 100};
+    GmresResult r = gmres(dense(a, 30), rhs, cfg, nullptr, nullptr, &dft);
+    expect(r.converged, "converged");
+    expect(norm_rel(dense(a, 30)(r.solution), rhs) <= 2e-9, "residual");
+  });
+  run("Gmres.ResidualHistoryMonotoneWithinCycle", [&] {  // test_solver.cpp:70-82
+    std::vector<cplx> a = rmat(25, 25, 5);
+    for (int i = 0; i < 25; ++i) a[i + 25 * i] += 6.0;
+    GmresResult r = gmres(dense(a, 25), rmat(25, 1, 6), GmresConfig{1e-14, 25, 1}, nullptr, nullptr, &dft);
+    for (size_t i = 1; i < r.residual_history.size(); ++i)
+      expect(r.residual_history[i] <= r.residual_history[i - 1] * (1.0 + 1e-12), "monotone");
+  });
+  run("Gmres.ReportedResidualMatchesExternalRecomputation", [&] {  // test_solver.cpp:84-97
+    std::vector<cplx> a = rmat(20, 20, 7);
+    for (int i = 0; i < 20; ++i) a[i + 20 * i] += 5.0;
+    const std::vector<cplx> rhs = rmat(20, 1, 8);
+    GmresResult r = gmres(dense(a, 20), rhs, GmresConfig{1e-8, 50, 200}, nullptr, nullptr, &dft);
+    expect(r.converged, "converged");
+    const double ext = norm_rel(dense(a, 20)(r.solution), rhs);
+    expect(std::abs(ext - r.final_relative_residual) <= 1e-10 * std::max(1.0, ext), "final residual");
+    expect(std::abs(r.residual_history.back() - ext) <= 1e-10, "last Givens estimate");
+  });
+  run("Gmres.NonConvergenceReportedNotThrown", [&] {  // test_solver.cpp:99-114
+    std::vector<cplx> a(1600, cplx(0.0));
+    for (int i = 0; i < 39; ++i) a[(i + 1) + 40 * i] = 1.0;
+    a[0 + 40 * 39] = 1.0;
+    std::vector<cplx> rhs(40, cplx(0.0));
+    rhs[0] = 1.0;
+    GmresResult r = gmres(dense(a, 40), rhs, GmresConfig{1e-12, 3, 2}, nullptr, nullptr, &dft);
+    expect(!r.converged && r.solution.size() == 40, "not converged, full-size iterate");
+    bool thrown = false;
+    try {
+      std::vector<cplx> bad(rhs);
+      bad[3] = cplx(std::nan(""), 0.0);
+      gmres(dense(a, 40), bad, GmresConfig{}, nullptr, nullptr, &dft);
+    } catch (const std::invalid_argument&) {
+      thrown = true;
+    }
+    expect(thrown, "non-finite rhs must throw");
+  });
+  run("GmresHooks.WarmStartSkipsIterations", [&] {  // test_scene_io.cpp:107-121
+    std::vector<cplx> d(8);
+    for (int i = 0; i < 8; ++i) d[i] = cplx(2.0 + i, 0.3);
+    const std::vector<cplx> rhs = rmat(8, 1, 1);
+    GmresConfig cfg;
+    cfg.tolerance = 1e-10;
+    GmresResult cold = gmres(diag_map(d), rhs, cfg, nullptr, nullptr, &dft);
+    expect(cold.converged, "cold");
+    GmresResult warm = gmres(diag_map(d), rhs, cfg, &cold.solution, nullptr, &dft);
+    expect(warm.converged && warm.iterations == 0, "warm start: 0 iterations");
+  });
+  run("GmresHooks.DiagonalRightPreconditionerConvergesImmediately", [&] {  // test_scene_io.cpp:123-139
+    std::vector<cplx> d(12);
+    for (int i = 0; i < 12; ++i) d[i] = cplx(1.0 + 3.0 * i, -0.5 * i);
+    auto pre = [&](const std::vector<cplx>& v) {
+      std::vector<cplx> o(v.size());
+      for (size_t i = 0; i < v.size(); ++i) o[i] = v[i] / d[i];
+      return o;
+    };
+    const std::vector<cplx> rhs = rmat(12, 1, 2);
+    GmresConfig cfg;
+    cfg.tolerance = 1e-12;
+    GmresResult r = gmres(diag_map(d), rhs, cfg, nullptr, pre, &dft);
+    expect(r.converged && r.iterations == 1, "1 iteration, got " + std::to_string(r.iterations));
+    expect(norm_rel(diag_map(d)(r.solution), rhs) < 1e-12, "residual");
+  });
+  run("GmresSystem.DiagonalPreconditionerOnTheJvieSystem", [&] {
+    // zero Tucker forms: N = 0, so apply_system is diag(eps g); M = diag(1 / (eps g)) -> 1 iteration
+    const std::array<Index, 3> d{6, 5, 4};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWL, d, 2, 700);
+    for (auto& pr : fam)
+      for (auto& v : pr.second.core.data) v = 0.0;
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWL, fam, dft);
+    const size_t nv = static_cast<size_t>(op.n_vox());
+    std::vector<cplx> eps(nv), pdiag(12 * nv);
+    for (size_t i = 0; i < nv; ++i) eps[i] = cplx(2.0 + 0.01 * static_cast<double>(i), -0.4);
+    for (size_t s = 0; s < 12; ++s)
+      for (size_t i = 0; i < nv; ++i) pdiag[s * nv + i] = 1.0 / (eps[i] * (s % 4 == 0 ? 1.0 : 1.0 / 12.0));
+    const std::vector<cplx> rhs = random_field(d, BasisOrder::PWL, 701).to_vector();
+    GmresResult plain = gmres_system(eps, 1.0, op, rhs, GmresConfig{1e-12, 50, 4});
+    GmresResult pc = gmres_system(eps, 1.0, op, rhs, GmresConfig{1e-12, 50, 4}, nullptr, &pdiag);
+    expect(pc.converged && pc.iterations == 1, "1 iteration, got " + std::to_string(pc.iterations));
+    expect(plain.converged && plain.iterations > 1, "unpreconditioned needs more");
+    expect(rel(plain.solution, pc.solution) <= 1e-10, "same solution");
+  });
+
+  run("ApplyOperator.TimingsAndMatvecBench", [&] {  // operator.hpp:189-192, 451-502
+    const std::array<Index, 3> d{32, 32, 32};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWL, d, 4, 710);
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, BasisOrder::PWL, fam, dft);
+    CurrentField x = random_field(d, BasisOrder::PWL, 711);
+    ApplyTimings t;
+    const std::vector<cplx> a =
+        apply_operator(op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, nullptr, dft, &t).to_vector();
+    const std::vector<cplx> b =
+        apply_operator(op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, nullptr, dft).to_vector();
+    expect(t.fft_ms > 0.0 && t.product_ms > 0.0, "timings");
+    expect(rel(a, b) == 0.0, "timed == untimed");
+    MatvecBenchResult r = matvec_bench(op, x, MatvecStrategy::HosvdDecompress, 3, dft);
+    expect(r.repetitions == 3 && r.median_ms > 0.0 && r.product_min_ms <= r.product_ms, "bench");
+  });
+
+  run("Lifetime.OperatorOutlivesItsDftService", [&] {  // EmbeddedSpectrum is self-contained (operator.hpp:118-119)
+    const std::array<Index, 3> d{4, 4, 4};
+    auto fam = make_family(OperatorKind::N, BasisOrder::PWC, d, 2, 720);
+    std::unique_ptr<EmbeddedSpectrum> op;
+    {
+      DftService local(0);
+      op.reset(new EmbeddedSpectrum(build_operator_spectra(OperatorKind::N, BasisOrder::PWC, fam, local)));
+    }
+    CurrentField x = random_field(d, BasisOrder::PWC, 721);
+    OracleForms of = to_oracle(fam, BasisOrder::PWC);
+    const std::vector<cplx> xv = x.to_vector();
+    std::vector<cplx> yref(xv.size());
+    const int64_t g[3] = {d[0], d[1], d[2]};
+    if (orc_apply_operator_tucker(0, 0, g, of.ranks.data(), of.pc.data(), of.p1.data(), of.p2.data(), of.p3.data(),
+                                  reinterpret_cast<const double*>(xv.data()), reinterpret_cast<double*>(yref.data())))
+      throw std::runtime_error(orc_last_error());
+    CurrentField y = apply_operator(*op, x, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, nullptr, dft);
+    expect(rel(yref, y.to_vector()) <= 1e-10, "operator after its DftService");
   });
 
   std::printf("%d failure(s)\n", g_fail);

@@ -1,0 +1,138 @@
+"""Parity at the configurations BASELINE.json's north_star names (slow, -m gpu).
+
+* C4 head 1 mm (200 x 240 x 200), PWL N, 60 components rank 25, random x: the full GPU
+  matvec against one full oracle apply_operator_tucker (operator.hpp:273-382) on the
+  same forms and x, rel l2 <= 1e-10.
+* C3 head 2 mm (100 x 120 x 100), PWC and PWL, the same check.
+* C1 32^3 homogeneous cube (eps_r of 298 MHz muscle-like tissue), PWL: one matvec and
+  20 GMRES iterations against the oracle's gmres (solver.hpp:34-142): identical
+  iteration count and history, final residual within 1e-8.
+* C2 64^3 PWL: the full GMRES(50) solve to 1e-6: iterations within +-1, final residual
+  within 1e-8, iterate within 1e-8.
+
+Synthetic forms follow SURVEY 8(d) (spatial CN(0,1) core and factors, parity-zero rows,
+transform_factors on both sides); the system forms are scaled to a well-posed
+perturbation of the PWL Gram term as in bench.py.  Methodology: test_fft_operator.cpp:
+172-190 (compressed vs oracle), solver.hpp:34-142 (GMRES order of operations).
+"""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from tests.helpers import fourier_forms, random_field, spatial_tucker_forms
+
+pytestmark = pytest.mark.gpu
+
+MATVEC_TOL = 1e-10
+N, K, PWC, PWL = 0, 1, 0, 1
+
+
+@pytest.fixture(scope="module")
+def vie():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1811_00484_b200 as v
+
+    orc.set_threads(os.cpu_count() or 1)
+    return v
+
+
+@pytest.fixture(scope="module")
+def dft(vie):
+    return vie.DftService(0)
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(a), 1e-300))
+
+
+def build(vie, dft, kind, basis, grid, spatial, par, scale=1.0):
+    comps, _, _ = vie.component_table(kind, basis)
+    forms = [vie.TuckerForm(dft, grid, spatial[c][0] * scale, spatial[c][1], par[c]) for c in range(len(comps))]
+    return vie.build_operator_spectra(kind, basis, grid, comps, forms, dft)
+
+
+def gpu_apply(vie, op, x):
+    import torch
+
+    y = vie.apply_operator(op, torch.from_numpy(x).cuda())
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("basis,grid", [(PWC, (100, 120, 100)), (PWL, (100, 120, 100)), (PWL, (200, 240, 200))],
+                         ids=["C3-pwc", "C3-pwl", "C4-pwl"])
+def test_headline_configs_random_x(vie, dft, basis, grid):
+    spatial, par = spatial_tucker_forms(N, basis, grid, 25, 1234)
+    op = build(vie, dft, N, basis, grid, spatial, par)
+    x = random_field(basis, grid, 2024)
+    y = gpu_apply(vie, op, x)
+    del op
+    y_ref = orc.apply_operator_tucker(N, basis, grid, fourier_forms(spatial, par), x)
+    err = rel(y_ref, y)
+    print(f"{grid} basis={basis}: rel l2 = {err:.3e}")
+    assert err <= MATVEC_TOL
+
+
+def _system(vie, dft, grid, eps_np, seed):
+    """PWL N system with forms scaled so |(eps - 1) N| ~ 0.2 min |eps g| (bench.py)."""
+    import torch
+
+    spatial, par = spatial_tucker_forms(N, PWL, grid, 25, seed)
+    nv = int(np.prod(grid))
+    x = torch.from_numpy(random_field(PWL, grid, seed + 1)).cuda()
+    op1 = build(vie, dft, N, PWL, grid, spatial, par)
+    rho = float(torch.linalg.vector_norm(vie.apply_operator(op1, x)) / torch.linalg.vector_norm(x))
+    del op1
+    emax = float(np.max(np.abs(eps_np - 1.0)))
+    gmin = float(np.min(np.abs(eps_np))) / 12.0
+    scale = 0.2 * gmin / (max(emax, 1e-300) * max(rho, 1e-300))
+    op = build(vie, dft, N, PWL, grid, spatial, par, scale)
+    scaled = [(core * scale, us) for core, us in spatial]
+    return op, fourier_forms(scaled, par), nv
+
+
+def test_c1_cube_matvec_and_20_gmres_iterations(vie, dft):
+    import torch
+
+    grid = (32, 32, 32)
+    w = 2 * np.pi * 2.98e8
+    eps_c = 65.0 - 1j * 0.6 / (8.8541878128e-12 * w)  # configs/sphere_validate.json:4-7, homogeneous cube
+    nv = int(np.prod(grid))
+    eps_np = np.full(nv, eps_c)
+    op, of, _ = _system(vie, dft, grid, eps_np, 321)
+    x = random_field(PWL, grid, 2024)
+    assert rel(orc.apply_operator_tucker(N, PWL, grid, of, x), gpu_apply(vie, op, x)) <= MATVEC_TOL
+    rhs = random_field(PWL, grid, 77)
+    eps = torch.from_numpy(eps_np).cuda()
+    r = vie.gmres(op, eps, 1.0, torch.from_numpy(rhs).cuda(), vie.GmresConfig(1e-15, 20, 1))
+    ref = orc.gmres_system_tucker(PWL, grid, of, eps_np, 1.0, rhs, tol=1e-15, inner=20, outer=1)
+    assert r.iterations == ref.iterations == 20
+    h, hr = np.array(r.residual_history), np.array(ref.residual_history)
+    assert np.max(np.abs(h - hr) / hr) <= 1e-8
+    assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8 * ref.final_relative_residual
+    assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
+
+
+def test_c2_pwl64_gmres_to_1e6(vie, dft):
+    import torch
+
+    grid = (64, 64, 64)
+    nv = int(np.prod(grid))
+    rng = np.random.default_rng(5)
+    eps_np = 1 + rng.uniform(1, 5, nv) - 1j * rng.uniform(0, 1, nv)
+    op, of, _ = _system(vie, dft, grid, eps_np, 4321)
+    rhs = random_field(PWL, grid, 11)
+    eps = torch.from_numpy(eps_np).cuda()
+    r = vie.gmres(op, eps, 1.0, torch.from_numpy(rhs).cuda(), vie.GmresConfig(1e-6, 50, 200))
+    ref = orc.gmres_system_tucker(PWL, grid, of, eps_np, 1.0, rhs, tol=1e-6, inner=50, outer=200)
+    print(f"C2: gpu {r.iterations} its, res {r.final_relative_residual:.3e}; "
+          f"oracle {ref.iterations} its, res {ref.final_relative_residual:.3e}")
+    assert r.converged and ref.converged
+    assert abs(r.iterations - ref.iterations) <= 1
+    assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8
+    assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
