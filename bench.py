@@ -155,79 +155,147 @@ def measured_peak():
 
 
 # ------------------------------------------------------------------ CPU sample
-def cpu_sample(grid, basis, rank, threads, seed=1234):
-    """Bounded sample of the oracle matvec: one full forward 3D FFT of the
-    embedded grid and one component's decompress + multiply-accumulate, scaled
-    to one matvec (2S FFTs + NC components).  Returns (matvecs/s, info)."""
+def config_dict(args, grid, basis, r, nc, S):
+    """The workload description both arms print (identical dicts)."""
+    return {"workload": f"{args.config}: PWL N-operator apply_operator (vie_matvec), grid {tuple(grid)}, "
+                        f"embedded {tuple(2 * d for d in grid)}, {nc} Tucker components rank {r}, {S} currents",
+            "grid": list(grid), "basis": "PWL" if basis else "PWC", "rank": r, "components": nc,
+            "l2": "inputs 1.8 GB > 126 MB L2 (no flush needed)"}
+
+
+def oracle_staged(grid, basis, rank, seed=1234):
+    """The oracle's apply_operator_tucker (restated HosvdDecompress path, operator.hpp:273-382)
+    as the 2S + NC pieces of ONE matvec on the bench's synthetic forms and a CN(0,1) x."""
     from oracle import oracle as orc
-    from tests.helpers import spatial_tucker_forms, fourier_forms
+    from tests.helpers import fourier_forms, spatial_tucker_forms
+
+    spatial, par = spatial_tucker_forms(0, basis, grid, rank, seed)
+    forms = fourier_forms(spatial, par)
+    S = 3 if basis == 0 else 12
+    nv = int(np.prod(grid))
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(S * nv) + 1j * rng.standard_normal(S * nv)
+    return orc.StagedMatvec(0, basis, grid, forms, x), forms
+
+
+def cpu_sample(grid, basis, rank, threads, seed=1234, reps=3):
+    """Bounded sample (~10-30 s) of the oracle matvec for the b200 arm's cpu_baseline:
+    three real pieces of one staged C4 matvec -- forward3 of current 0, component 0's
+    decompress + mac, inverse3 of target 0 -- timed (median of `reps`) and scaled to the
+    matvec's 2S FFT pieces + NC component pieces.  The reference arm (--impl reference)
+    times every piece of a full matvec instead."""
+    from oracle import oracle as orc
 
     orc.set_threads(threads)
-    n1, n2, n3 = grid
-    ed = (2 * n1, 2 * n2, 2 * n3)
     S = 3 if basis == 0 else 12
-    comps, par, blocks = orc.component_table(0, basis)
-    nc = len(comps)
-    rng = np.random.default_rng(seed)
-    ne = int(np.prod(ed))
-    v = (rng.standard_normal(ne) + 1j * rng.standard_normal(ne)).astype(np.complex128)
-    t0 = time.perf_counter()
-    orc.fft3(v, ed)
-    t_fft = time.perf_counter() - t0
-    spatial, par = spatial_tucker_forms(0, basis, grid, rank, seed)
-    f = fourier_forms(spatial[:1], par[:1])[0]
-    t0 = time.perf_counter()
-    buf = orc.decompress_tucker(ed, f)
-    nblk = int(np.sum(blocks[:, 2] == 0))
-    acc = np.zeros(ne, np.complex128)
-    for _ in range(nblk):  # mac_elementwise per block of the component
-        acc += buf * v
-    t_comp = time.perf_counter() - t0
-    per_mv = 2 * S * t_fft + nc * t_comp
-    info = {"t_fft3_s": round(t_fft, 3), "t_component_s": round(t_comp, 3), "extrapolated_matvec_s": round(per_mv, 2),
-            "sample": f"1 forward 3D FFT of the {ed[0]}x{ed[1]}x{ed[2]} embedded grid + 1 of {nc} components' "
-                      f"decompress+MAC, scaled to {2 * S} FFTs + {nc} components"}
+    mv, _forms = oracle_staged(grid, basis, rank, seed)
+    nc = mv.npieces - 2 * S
+    t_f, t_c, t_i = [], [], []
+    for _ in range(reps):
+        for piece, acc in ((0, t_f), (S, t_c), (S + nc, t_i)):
+            t0 = time.perf_counter()
+            mv.piece(piece)
+            acc.append(time.perf_counter() - t0)
+    mv.close()
+    tf, tc, ti = (float(np.median(v)) for v in (t_f, t_c, t_i))
+    per_mv = S * tf + nc * tc + S * ti
+    info = {"t_forward3_s": round(tf, 3), "t_component_s": round(tc, 3), "t_inverse3_s": round(ti, 3),
+            "scaled_matvec_s": round(per_mv, 2),
+            "sample": f"3 pieces of one staged oracle matvec at {tuple(grid)} (forward3 of current 0, component 0 "
+                      f"decompress+mac, inverse3 of target 0; median of {reps}), scaled to {S}+{S} FFT pieces + {nc} "
+                      f"component pieces; --impl reference times all pieces of a full matvec"}
     return 1.0 / per_mv, info
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The reference's CPU path, timed on ONE full matvec: the oracle's staged
+    apply_operator_tucker (all 2S + NC pieces, all host threads) spread over the K timed
+    steps -- step k runs pieces [k P / K, (k + 1) P / K) of the same matvec (K > P: more
+    matvecs), so the steps sum to complete matvecs and value = matvecs / total time.
+    Warm-up steps run pieces of a throwaway matvec.  Plus a bounded single-thread sample
+    (the reference itself is single-threaded: FFTW_ESTIMATE without threads, Eigen without
+    OpenMP, proj/CMakeLists.txt:28)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    from oracle import oracle as orc
+
     grid, basis, r = CONFIGS[args.config]
+    S = 3 if basis == 0 else 12
     threads = os.cpu_count() or 1
-    vals = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        v, info = cpu_sample(grid, basis, r, threads, seed=1234 + i)
-        if i >= args.warmup:
-            vals.append(v)
-    val = float(np.median(vals))
+    orc.set_threads(threads)
+    t_setup = time.perf_counter()
+    mv, forms = oracle_staged(grid, basis, r)
+    P = mv.npieces
+    nc = P - 2 * S
+    t_setup = time.perf_counter() - t_setup
+    for i in range(min(args.warmup, P)):  # warm-up: pieces of a throwaway matvec
+        mv.piece(i)
+    mv.close()
+    K = max(1, args.steps)
+    n_mv = max(1, -(-K // P))
+    T = n_mv * P
+    step_s = []
+    done = 0
+    for k in range(K):
+        lo, hi = k * T // K, (k + 1) * T // K
+        t0 = time.perf_counter()
+        for i in range(lo, hi):
+            j = i % P
+            if j == 0:
+                if done:
+                    mv.close()
+                mv, forms = oracle_staged(grid, basis, r, seed=1234 + done)
+                done += 1
+            mv.piece(j)
+        step_s.append(time.perf_counter() - t0)
+    mv.close()
+    total = float(sum(step_s))
+    val = n_mv / total
+    # single-thread sample: forward3 of current 0 + component 0 (bounded, ~tens of s)
+    orc.set_threads(1)
+    mv1, _f = oracle_staged(grid, basis, r)
+    t0 = time.perf_counter()
+    mv1.piece(0)
+    t_f1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    mv1.piece(S)
+    t_c1 = time.perf_counter() - t0
+    mv1.close()
+    orc.set_threads(threads)
+    st_val = 1.0 / (2 * S * t_f1 + nc * t_c1)
+    nv = int(np.prod(grid))
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": "matvecs/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / val, "higher_is_better": True,
+        "steps": K, "warmup": args.warmup, "ms_per_step": 1000.0 * total / K, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "c128", "data": "synthetic",
-        "config": {"workload": f"{args.config}: PWL N operator apply, grid {grid}, rank {r}", "grid": grid,
-                   "basis": "PWL" if basis else "PWC", "rank": r},
+        "config": config_dict(args, grid, basis, r, nc, S),
         "cpu_baseline": {"value": val, "unit": "matvecs/s", "cores": threads, "kind": "port",
-                         "sample": info["sample"]},
+                         "sample": f"{n_mv} full oracle matvec(s) at {tuple(grid)} ({P} pieces: {S} forward3, {nc} "
+                                   f"component decompress+mac, {S} inverse3) spread over the {K} timed steps, "
+                                   f"{threads} threads"},
         "e2e": {"value": val, "unit": "matvecs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "detail": info,
+        "detail": {"matvec_s": total / n_mv, "step_s": [round(t, 3) for t in step_s], "pieces_per_matvec": P,
+                   "setup_s": round(t_setup, 2), "x_elems": S * nv,
+                   "single_thread": {"value": st_val, "unit": "matvecs/s", "cores": 1,
+                                     "sample": "forward3 of current 0 + component 0 (decompress+mac), 1 thread, "
+                                               f"scaled to {2 * S} FFT + {nc} component pieces",
+                                     "t_fft3_s": round(t_f1, 2), "t_component_s": round(t_c1, 2)}},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
 # ------------------------------------------------------------------ solve time
-def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=200):
+def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=200, grid=(64, 64, 64), reps=3):
     """Solve time (north star: matvecs/s AND solve time): restarted GMRES(50) to 1e-6 on
-    the PWL system at 64^3 (BASELINE configs[1]), device resident (vie_gmres_solve).
-    Synthetic rank-25 forms are scaled so |(eps - 1) N| ~ 0.2 min|eps g| (a well-posed
-    perturbation of the PWL Gram term); eps = 1 + U(1,5) - i U(0,1)."""
+    the PWL system at 64^3 (BASELINE configs[1]) or the headline grid, device resident
+    (vie_gmres_solve).  Synthetic rank-25 forms are scaled so |(eps - 1) N| ~ 0.2
+    min|eps g| (a well-posed perturbation of the PWL Gram term); eps = 1 + U(1,5) - i U(0,1)."""
     from tests.helpers import spatial_tucker_forms
 
-    grid, basis, r = (64, 64, 64), 1, 25
+    basis, r = 1, 25
     S = vie.ncur(basis)
     nv = int(np.prod(grid))
     comps, _, _ = vie.component_table(0, basis)
@@ -250,14 +318,14 @@ def gmres_solve_bench(vie, dft, torch, with_cpu=True, tol=1e-6, inner=50, outer=
     cfg = vie.GmresConfig(tol, inner, outer)
     vie.gmres(op, eps, 1.0, rhs, vie.GmresConfig(tol, 2, 1))  # warm-up
     times = []
-    for _ in range(3):  # min of 3 solves: the per-iteration host round trip sees host noise
+    for _ in range(reps):  # min of the solves: the per-iteration host round trip sees host noise
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = vie.gmres(op, eps, 1.0, rhs, cfg)
         torch.cuda.synchronize()
         times.append(time.perf_counter() - t0)
     t = min(times)
-    out = {"config": "cube_64: 64^3 PWL N system (BASELINE configs[1]), 60 components rank 25, synthetic",
+    out = {"config": f"{grid} PWL N system, 60 components rank 25, synthetic",
            "solver": f"restarted GMRES({inner}) to {tol}, device resident (vie_gmres_solve)",
            "iterations": res.iterations, "converged": res.converged,
            "final_relative_residual": res.final_relative_residual, "seconds": t,
@@ -464,9 +532,16 @@ def run_b200(args):
         cpu = {"value": v, "unit": "matvecs/s", "cores": threads, "kind": "port", "sample": info["sample"],
                "detail": info}
 
-    solve = None
+    solve = solve_c4 = None
     if rank == 0 and world == 1 and not args.no_solve:
         solve = gmres_solve_bench(vie, dft, torch, with_cpu=not args.no_cpu_baseline)
+        if args.config == "head_1mm":  # the user-visible end-to-end number at the headline grid
+            del op, x, y
+            if e2e is not None:
+                del xh, yh
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
+            solve_c4 = gmres_solve_bench(vie, dft, torch, with_cpu=False, grid=grid, reps=1)
     scene = None
     if rank == 0 and world == 1 and not args.no_solve:
         scene = scene_stages_bench(vie, torch, grid, peak)
@@ -476,15 +551,11 @@ def run_b200(args):
         line = {
             "metric": METRIC, "value": value, "unit": "matvecs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (spatial-domain Tucker forms, CN(0,1), parity rows zeroed; CN(0,1) currents)",
-            "config": {"workload": f"{args.config}: PWL N-operator apply_operator (vie_matvec), grid {grid}, "
-                                   f"embedded {tuple(2 * d for d in grid)}, {nc} Tucker components rank {r}, "
-                                   f"{S} currents", "grid": list(grid), "basis": "PWL" if basis else "PWC",
-                       "rank": r, "components": nc,
-                       "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all)" if slab
-                                       else f"components sharded x{world}") if world > 1 else "1 GPU",
-                       "l2": "inputs 1.8 GB > 126 MB L2 (no flush needed)"},
+            "config": config_dict(args, grid, basis, r, nc, S),
+            "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all)" if slab
+                            else f"components sharded x{world}") if world > 1 else "1 GPU",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "algorithmic_bytes_per_launch": bm[dom]},
@@ -505,6 +576,7 @@ def run_b200(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gmres_solve": solve,
+            "gmres_solve_headline": solve_c4,
             "scene_stages": scene,
         }
         print(json.dumps(line), flush=True)

@@ -46,6 +46,10 @@ def lib():
         L = C.CDLL(_LIB_PATH)
         L.orc_last_error.restype = C.c_char_p
         L.orc_set_threads.argtypes = [C.c_int]
+        L.orc_mv_npieces.argtypes = [C.c_void_p]
+        L.orc_mv_piece.argtypes = [C.c_void_p, C.c_int]
+        L.orc_mv_result.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_mv_destroy.argtypes = [C.c_void_p]
         _lib = L
     return _lib
 
@@ -178,6 +182,39 @@ def apply_operator_tucker(kind, basis, grid, forms, x) -> np.ndarray:
     _check(lib().orc_apply_operator_tucker(int(kind), int(basis), _i64(grid), ranks, cores, u1, u2, u3,
                                            _ptr(x), _ptr(y)))
     return y
+
+
+class StagedMatvec:
+    """apply_operator_tucker as the 2S + NC pieces of one matvec (orc_mv_*): the CPU
+    baseline times every piece of one full matvec, spread over bench steps."""
+
+    def __init__(self, kind, basis, grid, forms, x):
+        self._keep = (forms, _form_arrays(forms))
+        ranks, cores, u1, u2, u3 = self._keep[1]
+        self.x = _c(x).reshape(-1)
+        self.h = C.c_void_p()
+        _check(lib().orc_mv_create(int(kind), int(basis), _i64(grid), ranks, cores, u1, u2, u3, _ptr(self.x),
+                                   C.byref(self.h)))
+        self.npieces = lib().orc_mv_npieces(self.h)
+
+    def piece(self, i: int):
+        _check(lib().orc_mv_piece(self.h, int(i)))
+
+    def result(self) -> np.ndarray:
+        y = np.empty_like(self.x)
+        _check(lib().orc_mv_result(self.h, _ptr(y)))
+        return y
+
+    def close(self):
+        if self.h:
+            lib().orc_mv_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def dense_spectrum(t, dims, sign) -> np.ndarray:

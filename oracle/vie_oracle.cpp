@@ -339,56 +339,103 @@ struct TuckerIn {
   const double* const* u3s;
 };
 
-void apply_operator(int kind, int basis, const I64 grid[3], const TuckerIn* tk,
-                    const double* const* spectra, const cd* x, cd* y) {
+// apply_operator (operator.hpp:273-382) as a staged computation: pieces 0..S-1 pad +
+// forward3 of current s (:290-297), S..S+NC-1 decompress + mac of component c (:303-364),
+// S+NC..2S+NC-1 inverse3 of target t (:367-375).  Running every piece in order is
+// apply_operator; the CPU baseline times the pieces of one full matvec.
+struct StagedMatvec {
+  int kind, basis, S;
+  I64 grid[3], ed[3], nv, ne;
   std::vector<Comp> comps;
   std::vector<Block> blocks;
-  build_table(kind, basis, comps, blocks);
-  for (int a = 0; a < 3; ++a)
-    if (grid[a] < 1) throw invalid("apply_operator: dim mismatch");
-  const int S = ncur(basis);
-  const I64 n1 = grid[0], n2 = grid[1], n3 = grid[2];
-  const I64 ed[3] = {2 * n1, 2 * n2, 2 * n3};
-  const I64 nv = n1 * n2 * n3, ne = ed[0] * ed[1] * ed[2];
-  std::vector<std::vector<cd>> xhat(static_cast<size_t>(S), std::vector<cd>(static_cast<size_t>(ne)));
-  for (int q = 0; q < S; ++q) {
-    cd* p = xhat[static_cast<size_t>(q)].data();
-    for (I64 k = 0; k < n3; ++k)
-      for (I64 j = 0; j < n2; ++j)
-        for (I64 i = 0; i < n1; ++i)
-          p[i + ed[0] * (j + ed[1] * k)] = x[q * nv + i + n1 * (j + n2 * k)];
-    fft3(p, ed[0], ed[1], ed[2], false);
-  }
-  std::vector<std::vector<cd>> yhat(static_cast<size_t>(S), std::vector<cd>(static_cast<size_t>(ne), cd(0.0)));
-  std::vector<cd> buffer(tk ? static_cast<size_t>(ne) : 0);
-  for (int ci = 0; ci < static_cast<int>(comps.size()); ++ci) {
-    const Comp& c = comps[static_cast<size_t>(ci)];
-    const double sigma = c.par[0] * c.par[1] * c.par[2];
-    const cd* s;
-    if (tk) {
-      const I64* rk = tk->ranks + 3 * ci;
-      decompress_tucker(ed, rk, reinterpret_cast<const cd*>(tk->cores[ci]),
-                        reinterpret_cast<const cd*>(tk->u1s[ci]),
-                        reinterpret_cast<const cd*>(tk->u2s[ci]),
-                        reinterpret_cast<const cd*>(tk->u3s[ci]), buffer.data());
-      s = buffer.data();
-    } else {
-      if (!spectra[ci]) throw invalid("apply_operator: dense spectrum absent");
-      s = reinterpret_cast<const cd*>(spectra[ci]);
+  TuckerIn tk{};
+  bool has_tk = false;
+  std::vector<const double*> spectra;
+  std::vector<std::vector<cd>> xhat, yhat;
+  std::vector<cd> buffer, x;
+
+  StagedMatvec(int kind_, int basis_, const I64 g[3], const TuckerIn* t, const double* const* sp, const cd* xin)
+      : kind(kind_), basis(basis_) {
+    build_table(kind, basis, comps, blocks);
+    for (int a = 0; a < 3; ++a)
+      if (g[a] < 1) throw invalid("apply_operator: dim mismatch");
+    S = ncur(basis);
+    for (int a = 0; a < 3; ++a) {
+      grid[a] = g[a];
+      ed[a] = 2 * g[a];
     }
-    for (const Block& b : blocks)
-      if (b.c == ci)
-        mac_elementwise(yhat[static_cast<size_t>(b.t)].data(), s,
-                        xhat[static_cast<size_t>(b.s)].data(), b.dsign * sigma, ne);
+    nv = grid[0] * grid[1] * grid[2];
+    ne = ed[0] * ed[1] * ed[2];
+    if (t) {
+      tk = *t;
+      has_tk = true;
+      buffer.resize(static_cast<size_t>(ne));
+    } else {
+      spectra.assign(sp, sp + comps.size());
+    }
+    x.assign(xin, xin + S * nv);
+    xhat.resize(static_cast<size_t>(S));
+    yhat.assign(static_cast<size_t>(S), std::vector<cd>());
   }
-  for (int q = 0; q < S; ++q) {
-    cd* p = yhat[static_cast<size_t>(q)].data();
-    fft3(p, ed[0], ed[1], ed[2], true);
-    for (I64 k = 0; k < n3; ++k)
-      for (I64 j = 0; j < n2; ++j)
-        for (I64 i = 0; i < n1; ++i)
-          y[q * nv + i + n1 * (j + n2 * k)] = p[i + ed[0] * (j + ed[1] * k)];
+  int npieces() const { return 2 * S + static_cast<int>(comps.size()); }
+  void piece(int i) {
+    const int nc = static_cast<int>(comps.size());
+    if (i < S) {
+      std::vector<cd>& xh = xhat[static_cast<size_t>(i)];
+      xh.assign(static_cast<size_t>(ne), cd(0.0));
+      cd* p = xh.data();
+      for (I64 k = 0; k < grid[2]; ++k)
+        for (I64 j = 0; j < grid[1]; ++j)
+          for (I64 ii = 0; ii < grid[0]; ++ii)
+            p[ii + ed[0] * (j + ed[1] * k)] = x[static_cast<size_t>(i * nv + ii + grid[0] * (j + grid[1] * k))];
+      fft3(p, ed[0], ed[1], ed[2], false);
+      return;
+    }
+    if (i < S + nc) {
+      const int ci = i - S;
+      const Comp& c = comps[static_cast<size_t>(ci)];
+      const double sigma = c.par[0] * c.par[1] * c.par[2];
+      const cd* sp;
+      if (has_tk) {
+        const I64* rk = tk.ranks + 3 * ci;
+        decompress_tucker(ed, rk, reinterpret_cast<const cd*>(tk.cores[ci]), reinterpret_cast<const cd*>(tk.u1s[ci]),
+                          reinterpret_cast<const cd*>(tk.u2s[ci]), reinterpret_cast<const cd*>(tk.u3s[ci]),
+                          buffer.data());
+        sp = buffer.data();
+      } else {
+        if (!spectra[static_cast<size_t>(ci)]) throw invalid("apply_operator: dense spectrum absent");
+        sp = reinterpret_cast<const cd*>(spectra[static_cast<size_t>(ci)]);
+      }
+      for (const Block& bk : blocks)
+        if (bk.c == ci) {
+          std::vector<cd>& yh = yhat[static_cast<size_t>(bk.t)];
+          if (yh.empty()) yh.assign(static_cast<size_t>(ne), cd(0.0));
+          if (xhat[static_cast<size_t>(bk.s)].empty()) throw invalid("apply_operator: piece order");
+          mac_elementwise(yh.data(), sp, xhat[static_cast<size_t>(bk.s)].data(), bk.dsign * sigma, ne);
+        }
+      return;
+    }
+    const int q = i - S - nc;
+    std::vector<cd>& yh = yhat[static_cast<size_t>(q)];
+    if (yh.empty()) yh.assign(static_cast<size_t>(ne), cd(0.0));
+    fft3(yh.data(), ed[0], ed[1], ed[2], true);
   }
+  void result(cd* y) const {
+    for (int q = 0; q < S; ++q) {
+      const cd* p = yhat[static_cast<size_t>(q)].data();
+      for (I64 k = 0; k < grid[2]; ++k)
+        for (I64 j = 0; j < grid[1]; ++j)
+          for (I64 i = 0; i < grid[0]; ++i)
+            y[q * nv + i + grid[0] * (j + grid[1] * k)] = p[i + ed[0] * (j + ed[1] * k)];
+    }
+  }
+};
+
+void apply_operator(int kind, int basis, const I64 grid[3], const TuckerIn* tk,
+                    const double* const* spectra, const cd* x, cd* y) {
+  StagedMatvec mv(kind, basis, grid, tk, spectra, x);
+  for (int i = 0; i < mv.npieces(); ++i) mv.piece(i);
+  mv.result(y);
 }
 
 // apply_system (solver.hpp:183-200), with the PWL Gram weights g_l.
@@ -957,6 +1004,28 @@ int orc_apply_operator_tucker(int kind, int basis, const int64_t grid[3], const 
                    reinterpret_cast<cd*>(y));
   });
 }
+
+int orc_mv_create(int kind, int basis, const int64_t grid[3], const int64_t* ranks, const double* const* cores,
+                  const double* const* u1s, const double* const* u2s, const double* const* u3s, const double* x,
+                  void** handle) {
+  return guard([&] {
+    if (!handle) throw invalid("orc_mv_create: null handle");
+    TuckerIn tk{ranks, cores, u1s, u2s, u3s};
+    *handle = new StagedMatvec(kind, basis, grid, &tk, nullptr, reinterpret_cast<const cd*>(x));
+  });
+}
+int orc_mv_npieces(void* handle) { return handle ? static_cast<StagedMatvec*>(handle)->npieces() : -1; }
+int orc_mv_piece(void* handle, int i) {
+  return guard([&] {
+    auto* mv = static_cast<StagedMatvec*>(handle);
+    if (!mv || i < 0 || i >= mv->npieces()) throw invalid("orc_mv_piece: bad piece");
+    mv->piece(i);
+  });
+}
+int orc_mv_result(void* handle, double* y) {
+  return guard([&] { static_cast<StagedMatvec*>(handle)->result(reinterpret_cast<cd*>(y)); });
+}
+void orc_mv_destroy(void* handle) { delete static_cast<StagedMatvec*>(handle); }
 
 int orc_apply_operator_dense(int kind, int basis, const int64_t grid[3],
                              const double* const* spectra, const double* x, double* y) {

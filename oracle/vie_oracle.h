@@ -73,6 +73,18 @@ int orc_apply_operator_tucker(int kind, int basis, const int64_t grid[3], const 
                               const double* const* u2s, const double* const* u3s,
                               const double* x, double* y);
 /* apply_operator strategy Dense: spectra = ncomp embedded-size spectra.    */
+/* apply_operator_tucker as staged pieces of ONE matvec (the CPU baseline times them):
+ * create (copies x; forms must stay alive), npieces = 2S + NC, piece(i) in order
+ * (0..S-1 forward3 of current i, then components, then inverse3 of each target),
+ * result(y), destroy.  Running all pieces == orc_apply_operator_tucker.             */
+int orc_mv_create(int kind, int basis, const int64_t grid[3], const int64_t* ranks, const double* const* cores,
+                  const double* const* u1s, const double* const* u2s, const double* const* u3s, const double* x,
+                  void** handle);
+int orc_mv_npieces(void* handle);
+int orc_mv_piece(void* handle, int i);
+int orc_mv_result(void* handle, double* y);
+void orc_mv_destroy(void* handle);
+
 int orc_apply_operator_dense(int kind, int basis, const int64_t grid[3],
                              const double* const* spectra, const double* x, double* y);
 /* build the Dense spectrum of one spatial component (operator.hpp:158-162) */
