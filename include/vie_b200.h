@@ -64,6 +64,42 @@ int vie_op_stream(vie_op op, void** stream);
 int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3],
                         double tol, int rule, vie_tucker* out, int64_t ranks_out[3]);
 
+/* The same with a DEVICE tensor (e.g. straight from vie_assemble), ordered after
+ * `stream` (NULL: the context stream); returns after the form is built.          */
+int vie_tucker_compress_device(vie_ctx ctx, const int64_t dims[3], const double* t_dev, const int sign[3],
+                               double tol, int rule, vie_tucker* out, int64_t ranks_out[3], void* stream);
+
+/* ---- Green's-tensor assembly (assembly.hpp:159-246, kernels.hpp, quadrature.hpp) ----
+ * QuadratureSpec (assembly.hpp:24-36); NULL = the defaults {5, 10, 1, 12, 6}.          */
+typedef struct {
+  int far_points_per_axis;
+  int near_points_per_axis;
+  int near_radius; /* Chebyshev voxel distance using the near rule */
+  int surface_points_per_axis; /* self term: static nabla-nabla dyad (face pairs) */
+  int volume_points_per_axis;  /* self term: dynamic remainder (Duffy boxes) */
+} vie_quadrature;
+#define VIE_KIND_G 2 /* OperatorKind::ScalarG (components.hpp:14) */
+
+/* assemble_defining_tensor (assembly.hpp:159-233) on the device: the PWC Galerkin
+ * Toeplitz-defining tensor of component (kind, row_axis, col_axis) of the grid with
+ * voxel edges resolution[3] (m) at wavenumber k0 (1/m), written to t (device,
+ * n1 n2 n3 complex, reference layout, SI units).  basis must be VIE_BASIS_PWC
+ * (VIE_EINVAL otherwise, as the reference throws); zero quadrature budgets are
+ * VIE_EINVAL.  Runs on `stream` (NULL: the context stream); returns when done.   */
+int vie_assemble(vie_ctx ctx, const int64_t dims[3], const double resolution[3], double k0, int kind,
+                 int row_axis, int col_axis, int basis, const vie_quadrature* quad, double* t, void* stream);
+/* detail::correlation_entry (assembly.hpp:49-79) on the device, one entry: kernel op
+ * (0 N, 1 K, 2 scalar g, 3 the N self remainder of kernels.hpp:113-119) at wavenumber k,
+ * displacement d and voxel delta in x-edge units, `points` per axis, Duffy at d when
+ * duffy != 0; out_host = complex result.  (A test hook for the quadrature parity.)   */
+int vie_correlation_entry(vie_ctx ctx, int op, double k, int q, int qp, const double d[3], const double delta[3],
+                          int points, int duffy, double* out_host);
+/* self_static_term (assembly.hpp:127-150): diagonal of the static nabla-nabla dyad of a
+ * delta[0] x delta[1] x delta[2] voxel (off-diagonals vanish), the Gram term (volume),
+ * the surface-rule refinement change and converged = change < 1e-7.               */
+int vie_self_static_term(vie_ctx ctx, const double delta[3], const vie_quadrature* quad, double dyad_diag[3],
+                         double* gram, double* error_indicator, int* converged);
+
 /* Tucker form from given factors (the synthetic-input path, no SVD).
  * domain 0: spatial factors U_q (n_q x r_q, host) -> transform_factors on device
  * domain 1: Fourier factors (2n_q x r_q, host) as returned by transform_factors

@@ -383,3 +383,56 @@ def decompress_cp(edims, ws) -> np.ndarray:
     _check(lib().orc_decompress_cp(_i64(edims), C.c_int64(ws[0].shape[1]), ws[0].ctypes.data_as(_dp),
                                    ws[1].ctypes.data_as(_dp), ws[2].ctypes.data_as(_dp), _ptr(out)))
     return out
+
+
+# ---- Green's-tensor assembly (assembly.hpp, kernels.hpp, quadrature.hpp) ---------
+OP_N, OP_K, OP_G, OP_NREM = 0, 1, 2, 3
+
+
+def _quad5(quad):
+    if quad is None:
+        return None
+    return (C.c_int * 5)(*[int(v) for v in quad])
+
+
+def assemble(dims, res, k0, op, q, qp, quad=None) -> np.ndarray:
+    """assemble_defining_tensor (assembly.hpp:159-233), PWC; flat reference layout."""
+    out = np.empty(int(np.prod(dims)), np.complex128)
+    _check(lib().orc_assemble(_i64(dims), (C.c_double * 3)(*[float(r) for r in res]), C.c_double(k0), int(op),
+                              int(q), int(qp), _quad5(quad), _ptr(out)))
+    return out
+
+
+def self_static_term(delta, quad=None):
+    """self_static_term (assembly.hpp:127-150): (dyad diagonal, gram, error, converged)."""
+    dg = (C.c_double * 3)()
+    gram, err, conv = C.c_double(), C.c_double(), C.c_int()
+    _check(lib().orc_self_static_term((C.c_double * 3)(*delta), _quad5(quad), dg, C.byref(gram), C.byref(err),
+                                      C.byref(conv)))
+    return np.array(dg[:]), gram.value, err.value, bool(conv.value)
+
+
+def correlation_entry(op, k, q, qp, d, delta, points, duffy=False) -> complex:
+    out = (C.c_double * 2)()
+    _check(lib().orc_correlation_entry(int(op), C.c_double(k), int(q), int(qp), (C.c_double * 3)(*d),
+                                       (C.c_double * 3)(*delta), int(points), int(bool(duffy)), out))
+    return complex(out[0], out[1])
+
+
+def kernel_eval(op, k, q, qp, r) -> complex:
+    out = (C.c_double * 2)()
+    _check(lib().orc_kernel_eval(int(op), C.c_double(k), int(q), int(qp), (C.c_double * 3)(*r), out))
+    return complex(out[0], out[1])
+
+
+def radial(R, k, dynamic=False):
+    out = (C.c_double * 6)()
+    _check(lib().orc_radial(C.c_double(R), C.c_double(k), int(bool(dynamic)), out))
+    return tuple(complex(out[2 * i], out[2 * i + 1]) for i in range(3))
+
+
+def brute_pair_integral(op, k, q, qp, d, delta, p) -> complex:
+    out = (C.c_double * 2)()
+    _check(lib().orc_brute_pair_integral(int(op), C.c_double(k), int(q), int(qp), (C.c_double * 3)(*d),
+                                         (C.c_double * 3)(*delta), int(p), out))
+    return complex(out[0], out[1])

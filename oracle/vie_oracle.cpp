@@ -1359,3 +1359,471 @@ int orc_postprocess(const int64_t dims[3], const double geo[6], double frequency
 }
 
 }  // extern "C"
+
+// ============================================================================
+// Green's-tensor assembly (assembly.hpp, kernels.hpp, quadrature.hpp): PWC Galerkin
+// Toeplitz-defining tensors of the N, K and scalar-g kernels on a uniform grid.
+// ============================================================================
+namespace {
+
+struct V3 {
+  double v[3];
+  double operator[](int i) const { return v[i]; }
+  double& operator[](int i) { return v[i]; }
+  double norm() const { return std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
+};
+V3 sub(const V3& a, const V3& b) { return V3{{a[0] - b[0], a[1] - b[1], a[2] - b[2]}}; }
+
+constexpr double kPiA = 3.14159265358979323846264338327950288;
+constexpr double kInv4pi = 1.0 / (4.0 * kPiA);
+
+// kernels.hpp:28-60: entire helpers of x = -i k R by series for |x| <= 1
+cd phi0(cd x) {
+  if (std::abs(x) > 1.0) return std::exp(x) - 1.0;
+  cd term = x, sum = x;
+  for (int n = 2; n < 26; ++n) {
+    term *= x / static_cast<double>(n);
+    sum += term;
+  }
+  return sum;
+}
+cd psi1(cd x) {
+  if (std::abs(x) > 1.0) return (x - 1.0) * std::exp(x) + 1.0;
+  cd xn = x, sum = 0.0;
+  for (int n = 2; n < 28; ++n) {
+    xn *= x / static_cast<double>(n);
+    sum += xn * static_cast<double>(n - 1);
+  }
+  return sum;
+}
+cd psi2(cd x) {
+  if (std::abs(x) > 1.0) return std::exp(x) * (x * x - 2.0 * x + 2.0) - 2.0;
+  cd sum = 0.0;
+  cd xm = x * x / 2.0;
+  for (int m = 3; m < 30; ++m) {
+    xm *= x / static_cast<double>(m);
+    sum += xm * static_cast<double>((m - 1) * (m - 2));
+  }
+  return sum;
+}
+
+struct Radial {
+  cd g, gp, gpp;
+};
+// kernels.hpp:67-76
+Radial radial(double R, double k) {
+  const cd e = std::exp(cd(0.0, -k * R));
+  const cd ikr(0.0, k * R);
+  Radial r;
+  r.g = e * kInv4pi / R;
+  r.gp = -(1.0 + ikr) * e * kInv4pi / (R * R);
+  r.gpp = (2.0 + 2.0 * ikr - k * k * R * R) * e * kInv4pi / (R * R * R);
+  return r;
+}
+// kernels.hpp:84-91
+Radial radial_dynamic(double R, double k) {
+  const cd x(0.0, -k * R);
+  Radial r;
+  r.g = phi0(x) * kInv4pi / R;
+  r.gp = psi1(x) * kInv4pi / (R * R);
+  r.gpp = psi2(x) * kInv4pi / (R * R * R);
+  return r;
+}
+// kernels.hpp:95-99
+cd hessian_entry(const Radial& h, const V3& rhat, double R, int q, int qp) {
+  const cd iso = h.gp / R;
+  const cd aniso = h.gpp - iso;
+  return aniso * rhat[q] * rhat[qp] + (q == qp ? iso : cd(0.0));
+}
+V3 unit(const V3& r, double R) { return V3{{r[0] / R, r[1] / R, r[2] / R}}; }
+// kernels.hpp:103-108
+cd n_kernel(const V3& rv, double k, int q, int qp) {
+  const double R = rv.norm();
+  const Radial h = radial(R, k);
+  return hessian_entry(h, unit(rv, R), R, q, qp) + (q == qp ? k * k * h.g : cd(0.0));
+}
+// kernels.hpp:113-119
+cd n_kernel_self_remainder(const V3& rv, double k, int q, int qp) {
+  const double R = rv.norm();
+  const Radial hd = radial_dynamic(R, k);
+  const cd g_full = hd.g + kInv4pi / R;
+  return hessian_entry(hd, unit(rv, R), R, q, qp) + (q == qp ? k * k * g_full : cd(0.0));
+}
+int levi_civita(int a, int b, int c) {
+  if (a == b || b == c || a == c) return 0;
+  return ((b - a + 3) % 3 == 1) ? 1 : -1;
+}
+// kernels.hpp:128-134
+cd k_kernel(const V3& rv, double k, int q, int qp) {
+  if (q == qp) return 0.0;
+  const int a = 3 - q - qp;
+  const double R = rv.norm();
+  const Radial h = radial(R, k);
+  return static_cast<double>(levi_civita(q, a, qp)) * h.gp * rv[a] / R;
+}
+
+// quadrature.hpp:21-58 (Newton on the Legendre roots, mapped to [0, 1])
+struct GaussRuleO {
+  std::vector<double> nodes, weights;
+};
+const GaussRuleO& gauss_rule_o(int p) {
+  static std::mutex mu;
+  static std::map<int, GaussRuleO> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(p);
+  if (it != cache.end()) return it->second;
+  if (p < 1) throw invalid("gauss_rule: need at least one point");
+  GaussRuleO r;
+  r.nodes.resize(static_cast<size_t>(p));
+  r.weights.resize(static_cast<size_t>(p));
+  const int m = (p + 1) / 2;
+  for (int i = 0; i < m; ++i) {
+    double x = std::cos(kPiA * (i + 0.75) / (p + 0.5));
+    double deriv = 0.0;
+    for (int iter = 0; iter < 100; ++iter) {
+      double p1 = 1.0, p2 = 0.0;
+      for (int k = 0; k < p; ++k) {
+        const double p3 = p2;
+        p2 = p1;
+        p1 = ((2.0 * k + 1.0) * x * p2 - k * p3) / (k + 1.0);
+      }
+      deriv = p * (x * p1 - p2) / (x * x - 1.0);
+      const double dx = p1 / deriv;
+      x -= dx;
+      if (std::abs(dx) < 1e-15) break;
+    }
+    const double w = 1.0 / ((1.0 - x * x) * deriv * deriv);
+    r.nodes[static_cast<size_t>(i)] = 0.5 * (1.0 - x);
+    r.weights[static_cast<size_t>(i)] = w;
+    r.nodes[static_cast<size_t>(p - 1 - i)] = 0.5 * (1.0 + x);
+    r.weights[static_cast<size_t>(p - 1 - i)] = w;
+  }
+  return cache.emplace(p, std::move(r)).first->second;
+}
+
+struct Box3O {
+  double lo[3], hi[3];
+};
+using KFn = std::function<cd(const V3&)>;
+// quadrature.hpp:71-86
+cd integrate_box(const KFn& f, const Box3O& box, int p) {
+  const GaussRuleO& g = gauss_rule_o(p);
+  const double lx = box.hi[0] - box.lo[0], ly = box.hi[1] - box.lo[1], lz = box.hi[2] - box.lo[2];
+  cd sum = 0.0;
+  for (int a = 0; a < p; ++a)
+    for (int b = 0; b < p; ++b)
+      for (int c = 0; c < p; ++c) {
+        V3 u{{box.lo[0] + lx * g.nodes[a], box.lo[1] + ly * g.nodes[b], box.lo[2] + lz * g.nodes[c]}};
+        sum += g.weights[a] * g.weights[b] * g.weights[c] * f(u);
+      }
+  return sum * (lx * ly * lz);
+}
+// quadrature.hpp:92-118
+cd integrate_box_duffy(const KFn& f, const Box3O& box, const int corner[3], int p) {
+  const GaussRuleO& g = gauss_rule_o(p);
+  double base[3], span[3];
+  for (int a = 0; a < 3; ++a) {
+    base[a] = corner[a] ? box.hi[a] : box.lo[a];
+    span[a] = (corner[a] ? box.lo[a] : box.hi[a]) - base[a];
+  }
+  const double jac = std::abs(span[0] * span[1] * span[2]);
+  cd sum = 0.0;
+  for (int radial_ax = 0; radial_ax < 3; ++radial_ax) {
+    const int s1 = (radial_ax + 1) % 3, s2 = (radial_ax + 2) % 3;
+    for (int a = 0; a < p; ++a) {
+      const double t = g.nodes[a];
+      for (int b = 0; b < p; ++b)
+        for (int c = 0; c < p; ++c) {
+          double v[3];
+          v[radial_ax] = t;
+          v[s1] = t * g.nodes[b];
+          v[s2] = t * g.nodes[c];
+          V3 u{{base[0] + span[0] * v[0], base[1] + span[1] * v[1], base[2] + span[2] * v[2]}};
+          sum += g.weights[a] * g.weights[b] * g.weights[c] * (t * t) * f(u);
+        }
+    }
+  }
+  return sum * jac;
+}
+using RFn = std::function<cd(double, double)>;
+// quadrature.hpp:126-136
+cd integrate_rect(const RFn& f, const double lo[2], const double hi[2], int p) {
+  const GaussRuleO& g = gauss_rule_o(p);
+  const double lx = hi[0] - lo[0], ly = hi[1] - lo[1];
+  cd sum = 0.0;
+  for (int a = 0; a < p; ++a)
+    for (int b = 0; b < p; ++b)
+      sum += g.weights[a] * g.weights[b] * f(lo[0] + lx * g.nodes[a], lo[1] + ly * g.nodes[b]);
+  return sum * (lx * ly);
+}
+// quadrature.hpp:139-166
+cd integrate_rect_duffy(const RFn& f, const double lo[2], const double hi[2], const int corner[2], int p) {
+  const GaussRuleO& g = gauss_rule_o(p);
+  double base[2], span[2];
+  for (int a = 0; a < 2; ++a) {
+    base[a] = corner[a] ? hi[a] : lo[a];
+    span[a] = (corner[a] ? lo[a] : hi[a]) - base[a];
+  }
+  const double jac = std::abs(span[0] * span[1]);
+  cd sum = 0.0;
+  for (int radial_ax = 0; radial_ax < 2; ++radial_ax) {
+    const int other = 1 - radial_ax;
+    for (int a = 0; a < p; ++a) {
+      const double t = g.nodes[a];
+      for (int b = 0; b < p; ++b) {
+        double v[2];
+        v[radial_ax] = t;
+        v[other] = t * g.nodes[b];
+        sum += g.weights[a] * g.weights[b] * t * f(base[0] + span[0] * v[0], base[1] + span[1] * v[1]);
+      }
+    }
+  }
+  return sum * jac;
+}
+
+// assembly.hpp:49-79: Galerkin voxel-pair integral as a tent-weighted 3D correlation
+cd correlation_entry(const KFn& kernel, const V3& d, const double delta[3], int points, bool duffy_at_d) {
+  std::vector<double> cuts[3];
+  for (int a = 0; a < 3; ++a) {
+    cuts[a] = {-delta[a], 0.0, delta[a]};
+    if (duffy_at_d && d[a] > -delta[a] && d[a] < delta[a] && d[a] != 0.0) {
+      cuts[a].push_back(d[a]);
+      std::sort(cuts[a].begin(), cuts[a].end());
+    }
+  }
+  KFn weighted = [&](const V3& u) {
+    const double w = (delta[0] - std::abs(u[0])) * (delta[1] - std::abs(u[1])) * (delta[2] - std::abs(u[2]));
+    return kernel(sub(u, d)) * w;
+  };
+  cd sum = 0.0;
+  for (size_t ia = 0; ia + 1 < cuts[0].size(); ++ia)
+    for (size_t ib = 0; ib + 1 < cuts[1].size(); ++ib)
+      for (size_t ic = 0; ic + 1 < cuts[2].size(); ++ic) {
+        Box3O box{{cuts[0][ia], cuts[1][ib], cuts[2][ic]}, {cuts[0][ia + 1], cuts[1][ib + 1], cuts[2][ic + 1]}};
+        bool corner = duffy_at_d;
+        int which[3] = {0, 0, 0};
+        for (int a = 0; a < 3; ++a) {
+          const double lo = box.lo[a], hi = box.hi[a];
+          if (d[a] == lo) which[a] = 0;
+          else if (d[a] == hi) which[a] = 1;
+          else corner = false;
+        }
+        sum += corner ? integrate_box_duffy(weighted, box, which, points) : integrate_box(weighted, box, points);
+      }
+  return sum;
+}
+
+// assembly.hpp:84-104
+double face_pair_static(double dt1, double dt2, double h, int points) {
+  RFn f = [&](double u, double v) {
+    const double w = (dt1 - std::abs(u)) * (dt2 - std::abs(v));
+    return cd(w * kInv4pi / std::sqrt(h * h + u * u + v * v));
+  };
+  cd sum = 0.0;
+  for (int su = 0; su < 2; ++su)
+    for (int sv = 0; sv < 2; ++sv) {
+      const double lo[2] = {su ? 0.0 : -dt1, sv ? 0.0 : -dt2};
+      const double hi[2] = {su ? dt1 : 0.0, sv ? dt2 : 0.0};
+      if (h == 0.0) {
+        const int corner[2] = {su ? 0 : 1, sv ? 0 : 1};
+        sum += integrate_rect_duffy(f, lo, hi, corner, points);
+      } else {
+        sum += integrate_rect(f, lo, hi, points);
+      }
+    }
+  return sum.real();
+}
+
+struct QuadSpec {
+  int far = 5, near = 10, near_radius = 1, surface = 12, volume = 6;
+  void validate() const {
+    if (far < 1 || near < 1 || surface < 1 || volume < 1)
+      throw invalid("QuadratureSpec: quadrature budget of zero");
+    if (near_radius < 1) throw invalid("QuadratureSpec: near_radius must be >= 1");
+  }
+};
+
+// assembly.hpp:127-150 (diagonal of the static nabla-nabla dyad; off-diagonals are 0)
+void self_static_term(const double delta[3], const QuadSpec& quad, double dyad[3], double* gram, double* err,
+                      bool* converged) {
+  quad.validate();
+  *gram = delta[0] * delta[1] * delta[2];
+  auto diagonal = [&](int q, int points) {
+    const int t1 = (q + 1) % 3, t2 = (q + 2) % 3;
+    const double same = face_pair_static(delta[t1], delta[t2], 0.0, points);
+    const double opp = face_pair_static(delta[t1], delta[t2], delta[q], points);
+    return 2.0 * (opp - same);
+  };
+  double max_change = 0.0;
+  for (int q = 0; q < 3; ++q) {
+    const double v = diagonal(q, quad.surface);
+    const double v_refined = diagonal(q, quad.surface + 4);
+    dyad[q] = v_refined;
+    max_change = std::max(max_change, std::abs(v_refined - v) / *gram);
+  }
+  *err = max_change;
+  *converged = max_change < 1e-7;
+}
+
+// assembly.hpp:159-233 (op 0 = N, 1 = K, 2 = scalar g), PWC only
+void assemble_defining_tensor(const I64 dims[3], const double res[3], double k0, int op, int q, int qp,
+                              const QuadSpec& quad, cd* t) {
+  quad.validate();
+  for (int a = 0; a < 3; ++a)
+    if (dims[a] < 1 || !(res[a] > 0.0)) throw invalid("assemble_defining_tensor: bad grid");
+  if (op < 0 || op > 2 || q < 0 || q > 2 || qp < 0 || qp > 2) throw invalid("assemble_defining_tensor: bad component");
+  const double scale = res[0];
+  const double delta[3] = {1.0, res[1] / scale, res[2] / scale};
+  const double k = k0 * scale;
+  // parity (components.hpp:46-65): N(q,q') odd along q and q' (q != q'), K odd along the third axis
+  int par[3] = {1, 1, 1};
+  if (op == 0 && q != qp) par[q] = par[qp] = -1;
+  if (op == 1 && q != qp) par[3 - q - qp] = -1;
+  KFn kernel;
+  double si_power = 3.0;
+  if (op == 0) {
+    kernel = [=](const V3& r) { return n_kernel(r, k, q, qp); };
+  } else if (op == 1) {
+    kernel = [=](const V3& r) { return k_kernel(r, k, q, qp); };
+    si_power = 4.0;
+  } else {
+    kernel = [=](const V3& r) { return radial(r.norm(), k).g; };
+    si_power = 5.0;
+  }
+  const double si_scale = std::pow(scale, si_power);
+  cd self_entry = 0.0;
+  const V3 zero{{0.0, 0.0, 0.0}};
+  if (op == 0) {
+    double dyad[3], gram, err;
+    bool conv;
+    self_static_term(delta, quad, dyad, &gram, &err, &conv);
+    KFn rem = [=](const V3& r) { return n_kernel_self_remainder(r, k, q, qp); };
+    self_entry = correlation_entry(rem, zero, delta, quad.volume, true);
+    self_entry += (q == qp ? gram + dyad[q] : 0.0);
+  } else if (op == 2) {
+    self_entry = correlation_entry(kernel, zero, delta, quad.volume, true);
+  }
+  const I64 n1 = dims[0], n2 = dims[1], n3 = dims[2];
+  parallel_for(n3, [&](I64 kk, int) {
+    for (I64 jj = 0; jj < n2; ++jj)
+      for (I64 ii = 0; ii < n1; ++ii) {
+        cd& out = t[ii + n1 * (jj + n2 * kk)];
+        if ((par[0] < 0 && ii == 0) || (par[1] < 0 && jj == 0) || (par[2] < 0 && kk == 0)) {
+          out = 0.0;
+          continue;
+        }
+        const I64 cheb = std::max({ii, jj, kk});
+        if (cheb == 0) {
+          out = self_entry * si_scale;
+          continue;
+        }
+        const V3 d{{static_cast<double>(ii) * delta[0], static_cast<double>(jj) * delta[1],
+                    static_cast<double>(kk) * delta[2]}};
+        const bool near = cheb <= quad.near_radius;
+        out = correlation_entry(kernel, d, delta, near ? quad.near : quad.far, near) * si_scale;
+      }
+  });
+}
+
+QuadSpec quad_from(const int* q5) {
+  QuadSpec q;
+  if (q5) {
+    q.far = q5[0];
+    q.near = q5[1];
+    q.near_radius = q5[2];
+    q.surface = q5[3];
+    q.volume = q5[4];
+  }
+  return q;
+}
+
+KFn kernel_of(int op, double k, int q, int qp) {
+  if (op == 0) return [=](const V3& r) { return n_kernel(r, k, q, qp); };
+  if (op == 1) return [=](const V3& r) { return k_kernel(r, k, q, qp); };
+  if (op == 3) return [=](const V3& r) { return n_kernel_self_remainder(r, k, q, qp); };
+  return [=](const V3& r) { return radial(r.norm(), k).g; };
+}
+
+}  // namespace
+
+extern "C" {
+
+int orc_assemble(const int64_t dims[3], const double res[3], double k0, int op, int q, int qp, const int* quad5,
+                 double* out) {
+  return guard([&] {
+    const I64 d[3] = {dims[0], dims[1], dims[2]};
+    assemble_defining_tensor(d, res, k0, op, q, qp, quad_from(quad5), reinterpret_cast<cd*>(out));
+  });
+}
+
+int orc_self_static_term(const double delta[3], const int* quad5, double dyad_diag[3], double* gram, double* err,
+                         int* converged) {
+  return guard([&] {
+    bool c = false;
+    self_static_term(delta, quad_from(quad5), dyad_diag, gram, err, &c);
+    if (converged) *converged = c ? 1 : 0;
+  });
+}
+
+int orc_correlation_entry(int op, double k, int q, int qp, const double d[3], const double delta[3], int points,
+                          int duffy, double* out) {
+  return guard([&] {
+    const cd v = correlation_entry(kernel_of(op, k, q, qp), V3{{d[0], d[1], d[2]}}, delta, points, duffy != 0);
+    out[0] = v.real();
+    out[1] = v.imag();
+  });
+}
+
+int orc_kernel_eval(int op, double k, int q, int qp, const double r[3], double* out) {
+  return guard([&] {
+    const V3 rv{{r[0], r[1], r[2]}};
+    if (rv.norm() <= 0.0) throw std::domain_error("green_g: singular point |R| = 0");
+    const cd v = kernel_of(op, k, q, qp)(rv);
+    out[0] = v.real();
+    out[1] = v.imag();
+  });
+}
+
+int orc_radial(double R, double k, int dynamic, double* out6) {
+  return guard([&] {
+    const Radial h = dynamic ? radial_dynamic(R, k) : radial(R, k);
+    const cd v[3] = {h.g, h.gp, h.gpp};
+    for (int i = 0; i < 3; ++i) {
+      out6[2 * i] = v[i].real();
+      out6[2 * i + 1] = v[i].imag();
+    }
+  });
+}
+
+// test_assembly.cpp:14-37: brute-force 6D Gauss over (test voxel) x (source voxel)
+int orc_brute_pair_integral(int op, double k, int q, int qp, const double d[3], const double del[3], int p,
+                            double* out) {
+  return guard([&] {
+    const GaussRuleO& g = gauss_rule_o(p);
+    const KFn kern = kernel_of(op, k, q, qp);
+    std::vector<cd> part(static_cast<size_t>(p));
+    parallel_for(p, [&](I64 a, int) {
+      cd sum = 0.0;
+      for (int b = 0; b < p; ++b)
+        for (int c = 0; c < p; ++c)
+          for (int e = 0; e < p; ++e)
+            for (int f = 0; f < p; ++f)
+              for (int h = 0; h < p; ++h) {
+                const V3 rt{{del[0] * (g.nodes[a] - 0.5), del[1] * (g.nodes[b] - 0.5), del[2] * (g.nodes[c] - 0.5)}};
+                const V3 rs{{d[0] + del[0] * (g.nodes[e] - 0.5), d[1] + del[1] * (g.nodes[f] - 0.5),
+                             d[2] + del[2] * (g.nodes[h] - 0.5)}};
+                sum += g.weights[a] * g.weights[b] * g.weights[c] * g.weights[e] * g.weights[f] * g.weights[h] *
+                       kern(sub(rt, rs));
+              }
+      part[static_cast<size_t>(a)] = sum;
+    });
+    cd sum = 0.0;
+    for (const cd& v : part) sum += v;
+    const double v = del[0] * del[1] * del[2];
+    sum *= v * v;
+    out[0] = sum.real();
+    out[1] = sum.imag();
+  });
+}
+
+}  // extern "C"

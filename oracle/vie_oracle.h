@@ -135,6 +135,25 @@ int orc_recover_fields(const int64_t dims[3], const double geo[6], double freque
 int orc_postprocess(const int64_t dims[3], const double geo[6], double frequency, const double* eps_r,
                     const double* e, const double* h, double* p_abs, double* b1, double* total);
 
+/* ---- Green's-tensor assembly (assembly.hpp:159-233, kernels.hpp, quadrature.hpp) ----
+ * op: 0 = N, 1 = K, 2 = scalar g (ScalarG), 3 = the N self remainder kernel (kernels.hpp:113);
+ * quad5 = {far, near, near_radius, surface, volume} points (QuadratureSpec; NULL = defaults
+ * 5, 10, 1, 12, 6).  out: n1 n2 n3 complex, SI units (entries scale as res^3 / ^4 / ^5).  */
+int orc_assemble(const int64_t dims[3], const double res[3], double k0, int op, int q, int qp,
+                 const int* quad5, double* out);
+/* self_static_term (assembly.hpp:127-150): diagonal of the static nabla-nabla dyad      */
+int orc_self_static_term(const double delta[3], const int* quad5, double dyad_diag[3], double* gram,
+                         double* err, int* converged);
+/* detail::correlation_entry (assembly.hpp:49-79) of kernel op at displacement d (voxel units) */
+int orc_correlation_entry(int op, double k, int q, int qp, const double d[3], const double delta[3],
+                          int points, int duffy, double* out);
+int orc_kernel_eval(int op, double k, int q, int qp, const double r[3], double* out);
+/* kernels::radial / radial_dynamic: (g, g', g'') interleaved complex                     */
+int orc_radial(double R, double k, int dynamic, double* out6);
+/* test_assembly.cpp:14-37 brute-force 6D pair integral                                   */
+int orc_brute_pair_integral(int op, double k, int q, int qp, const double d[3], const double del[3],
+                            int p, double* out);
+
 #ifdef __cplusplus
 }
 #endif

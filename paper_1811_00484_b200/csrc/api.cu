@@ -649,18 +649,20 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
           if (row0 > 1e-24 * nrm)
             throw Invalid("vie_tucker_from_factors: odd-parity factor has a nonzero row 0");
         }
-        double2* du = dev_alloc<double2>(static_cast<size_t>(n * r));
-        try {
-          copy_sync(du, uh[q], sizeof(double2) * n * r, ctx->stream);
-          const FftPlan& P = get_plan(ctx, static_cast<int>(2 * n));
-          vie::launch_factor_transform(du, static_cast<int>(n), static_cast<int>(r), sign[q], P.tw, t->uo[q],
-                                       ctx->stream);
-          VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
-        } catch (...) {
-          dev_free(du);
-          throw;
+        // direct DFT of the embedded columns (any length: only the w_2n twiddles are needed)
+        DevPool tmp;
+        double2* du = tmp.alloc<double2>(static_cast<size_t>(n * r));
+        double2* tw = tmp.alloc<double2>(static_cast<size_t>(2 * n));
+        std::vector<double2> twh(static_cast<size_t>(2 * n));
+        for (int64_t e = 0; e < 2 * n; ++e) {
+          const long double a = -3.14159265358979323846264338327950288L * e / n;
+          twh[static_cast<size_t>(e)] = make_double2(static_cast<double>(cosl(a)), static_cast<double>(sinl(a)));
         }
-        dev_free(du);
+        copy_sync(du, uh[q], sizeof(double2) * n * r, ctx->stream);
+        copy_sync(tw, twh.data(), sizeof(double2) * twh.size(), ctx->stream);
+        vie::launch_factor_transform(du, static_cast<int>(n), static_cast<int>(r), sign[q], tw, t->uo[q],
+                                     ctx->stream);
+        VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
       } else {
         const int64_t m = 2 * n;
         check_cplx_finite_host(uh[q], static_cast<size_t>(m * r), "vie_tucker_from_factors: factor");
@@ -1414,84 +1416,244 @@ int vie_debug_pencil3_phases(unsigned long long* out8, int reset) {
 }
 #endif
 
+}  // extern "C"
+
+namespace {
+// hosvd + transform_factors of a DEVICE spatial tensor dt (decomp.hpp:160-176,
+// operator.hpp:76-90): per mode, the Gram of the unfolding on the device and its
+// Hermitian Jacobi eigendecomposition on the host give a first basis U0; the unfolding
+// is then projected, B = U0^H M (device mode product), and the eigendecomposition of
+// B B^H (rows of B carry the singular values, so its entries are accurate relative to
+// sigma_i sigma_j, not sigma_max^2) refines U = U0 V and sigma_k = sqrt(lambda_k): the
+// squared-condition loss of the one-pass Gram method is removed and small singular
+// values resolve down to ~eps sigma_max, as the reference's QR + JacobiSVD
+// (decomp.hpp:40-70).  Ranks by truncation_rank (decomp.hpp:72-103).
+void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, const int sign[3], double tol,
+                         int rule, vie_tucker* out, int64_t ranks_out[3], int passes) {
+  for (int q = 0; q < 3; ++q) {
+    if (dims[q] < 1) throw Invalid("hosvd: degenerate tensor dimensions");
+    if (sign[q] != 1 && sign[q] != -1) throw Invalid("tucker_compress: sign must be +-1");
+  }
+  if (!(tol >= 0.0)) throw Invalid("truncated_svd: tol must be >= 0");
+  if (rule != VIE_RULE_SIGMA_MAX && rule != VIE_RULE_ENERGY) throw Invalid("tucker_compress: bad rule");
+  if (dims[0] > 4096 || dims[1] > 4096 || dims[2] > 4096) throw Invalid("tucker_compress: dims too large");
+  cudaStream_t st = ctx->stream;
+  DevPool dev;
+  std::vector<cd> U[3];
+  int64_t rk[3];
+  for (int q = 0; q < 3; ++q) {
+    const int n = static_cast<int>(dims[q]);
+    double2* dG = dev.alloc<double2>(static_cast<size_t>(n) * n);
+    auto gram_eig = [&](const double2* t, std::vector<double>& lam, std::vector<cd>& V) {
+      vie::launch_gram(t, dims, q + 1, dG, st);
+      std::vector<cd> G(static_cast<size_t>(n) * n);
+      VIE_CUDA_CHECK(cudaMemcpyAsync(G.data(), dG, sizeof(double2) * G.size(), cudaMemcpyDeviceToHost, st));
+      VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+      herm_eig_jacobi(G, n, lam, V);
+    };
+    std::vector<double> lam;
+    std::vector<cd> V0;
+    gram_eig(dt, lam, V0);
+    std::vector<cd> Ufull = V0;  // n x n
+    for (int pass = 1; pass < passes; ++pass) {
+      // B = Ufull^H x_q t, then the eigendecomposition of B B^H (rotation V), Ufull <- Ufull V
+      double2* dU = dev.alloc<double2>(static_cast<size_t>(n) * n);
+      VIE_CUDA_CHECK(cudaMemcpyAsync(dU, Ufull.data(), sizeof(double2) * Ufull.size(), cudaMemcpyHostToDevice, st));
+      double2* dB = dev.alloc<double2>(static_cast<size_t>(dims[0] * dims[1] * dims[2]));
+      vie::launch_mode_product_h(dt, dims, q + 1, dU, n, dB, st);
+      std::vector<cd> Vr;
+      gram_eig(dB, lam, Vr);
+      std::vector<cd> Un(static_cast<size_t>(n) * n, cd(0.0));
+      for (int c = 0; c < n; ++c)
+        for (int k = 0; k < n; ++k) {
+          const cd v = Vr[static_cast<size_t>(k) + static_cast<size_t>(n) * c];
+          if (v == cd(0.0)) continue;
+          for (int i = 0; i < n; ++i)
+            Un[static_cast<size_t>(i) + static_cast<size_t>(n) * c] += Ufull[static_cast<size_t>(i) + static_cast<size_t>(n) * k] * v;
+        }
+      Ufull.swap(Un);
+    }
+    std::vector<double> sig(static_cast<size_t>(n));
+    for (int k = 0; k < n; ++k) sig[static_cast<size_t>(k)] = std::sqrt(std::max(lam[static_cast<size_t>(k)], 0.0));
+    int64_t r = truncation_rank_host(sig, tol, rule);
+    const bool zero = r == 0;
+    if (zero) r = 1;  // rank-0 form == zero spectrum; keep one (zeroed) column
+    rk[q] = r;
+    U[q].assign(static_cast<size_t>(n * r), cd(0.0));
+    for (int64_t c = 0; c < r; ++c)
+      for (int i = 0; i < n; ++i)
+        U[q][static_cast<size_t>(i + n * c)] = zero ? cd(0.0) : Ufull[static_cast<size_t>(i + n * c)];
+    if (sign[q] < 0) {  // odd axis: the offset-0 row is zero (components.hpp:46-50)
+      double nrm = 0.0, row0 = 0.0;
+      for (int64_t c = 0; c < r; ++c) {
+        row0 += std::norm(U[q][static_cast<size_t>(n * c)]);
+        for (int i = 0; i < n; ++i) nrm += std::norm(U[q][static_cast<size_t>(i + n * c)]);
+      }
+      if (row0 > 1e-20 * std::max(nrm, 1e-300))
+        throw Invalid("tucker_compress: odd-parity component has a nonzero offset-0 plane");
+      for (int64_t c = 0; c < r; ++c) U[q][static_cast<size_t>(n * c)] = 0.0;
+    }
+  }
+  // core = t x1 U1^H x2 U2^H x3 U3^H (decomp.hpp:171-174), on the device
+  int64_t d[3] = {dims[0], dims[1], dims[2]};
+  const double2* cur = dt;
+  for (int q = 0; q < 3; ++q) {
+    double2* dU = dev.alloc<double2>(U[q].size());
+    VIE_CUDA_CHECK(cudaMemcpyAsync(dU, U[q].data(), sizeof(double2) * U[q].size(), cudaMemcpyHostToDevice, st));
+    int64_t od[3] = {d[0], d[1], d[2]};
+    od[q] = rk[q];
+    double2* nxt = dev.alloc<double2>(static_cast<size_t>(od[0] * od[1] * od[2]));
+    vie::launch_mode_product_h(cur, d, q + 1, dU, static_cast<int>(rk[q]), nxt, st);
+    cur = nxt;
+    d[0] = od[0];
+    d[1] = od[1];
+    d[2] = od[2];
+  }
+  std::vector<cd> core(static_cast<size_t>(rk[0] * rk[1] * rk[2]));
+  VIE_CUDA_CHECK(cudaMemcpyAsync(core.data(), cur, sizeof(double2) * core.size(), cudaMemcpyDeviceToHost, st));
+  VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  const int rc = vie_tucker_from_factors(ctx, dims, rk, reinterpret_cast<const double*>(core.data()),
+                                         reinterpret_cast<const double*>(U[0].data()),
+                                         reinterpret_cast<const double*>(U[1].data()),
+                                         reinterpret_cast<const double*>(U[2].data()), sign, 0, out);
+  if (rc != VIE_OK) throw Invalid(g_err);
+  if (ranks_out)
+    for (int q = 0; q < 3; ++q) ranks_out[q] = rk[q];
+}
+
+int hosvd_passes() { return env_int("VIE_HOSVD_PASSES", 2); }
+}  // namespace
+
+extern "C" {
+
 int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host, const int sign[3], double tol,
                         int rule, vie_tucker* out, int64_t ranks_out[3]) {
   return guard([&] {
     if (!ctx || !dims || !t_host || !sign || !out) throw Invalid("tucker_compress: null argument");
-    for (int q = 0; q < 3; ++q) {
+    for (int q = 0; q < 3; ++q)
       if (dims[q] < 1) throw Invalid("hosvd: degenerate tensor dimensions");
-      if (sign[q] != 1 && sign[q] != -1) throw Invalid("tucker_compress: sign must be +-1");
-    }
-    if (!(tol >= 0.0)) throw Invalid("truncated_svd: tol must be >= 0");
-    if (rule != VIE_RULE_SIGMA_MAX && rule != VIE_RULE_ENERGY) throw Invalid("tucker_compress: bad rule");
-    if (dims[0] > 4096 || dims[1] > 4096 || dims[2] > 4096) throw Invalid("tucker_compress: dims too large");
     VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
     const int64_t nv = dims[0] * dims[1] * dims[2];
     check_cplx_finite_host(t_host, static_cast<size_t>(nv), "tucker_compress: tensor");
-    cudaStream_t st = ctx->stream;
     DevPool dev;
     double2* dt = dev.alloc<double2>(static_cast<size_t>(nv));
-    copy_sync(dt, t_host, sizeof(double2) * nv, st);
-    // per mode: Gram on the device, Hermitian Jacobi eigendecomposition on the host
-    // (sigma_k = sqrt(lambda_k): the left singular pairs of the unfolding), rank
-    // by truncation_rank (decomp.hpp:72-103), U_q = leading eigenvectors.
-    std::vector<cd> U[3];
-    int64_t rk[3];
-    for (int q = 0; q < 3; ++q) {
-      const int n = static_cast<int>(dims[q]);
-      double2* dG = dev.alloc<double2>(static_cast<size_t>(n) * n);
-      vie::launch_gram(dt, dims, q + 1, dG, st);
-      std::vector<cd> G(static_cast<size_t>(n) * n);
-      VIE_CUDA_CHECK(cudaMemcpyAsync(G.data(), dG, sizeof(double2) * G.size(), cudaMemcpyDeviceToHost, st));
-      VIE_CUDA_CHECK(cudaStreamSynchronize(st));
-      std::vector<double> lam;
-      std::vector<cd> V;
-      herm_eig_jacobi(G, n, lam, V);
-      std::vector<double> sig(static_cast<size_t>(n));
-      for (int k = 0; k < n; ++k) sig[static_cast<size_t>(k)] = std::sqrt(std::max(lam[static_cast<size_t>(k)], 0.0));
-      int64_t r = truncation_rank_host(sig, tol, rule);
-      const bool zero = r == 0;
-      if (zero) r = 1;  // rank-0 form == zero spectrum; keep one (zeroed) column
-      rk[q] = r;
-      U[q].assign(static_cast<size_t>(n * r), cd(0.0));
-      for (int64_t c = 0; c < r; ++c)
-        for (int i = 0; i < n; ++i) U[q][static_cast<size_t>(i + n * c)] = zero ? cd(0.0) : V[static_cast<size_t>(i + n * c)];
-      if (sign[q] < 0) {  // odd axis: the offset-0 row is zero (components.hpp:46-50)
-        double nrm = 0.0, row0 = 0.0;
-        for (int64_t c = 0; c < r; ++c) {
-          row0 += std::norm(U[q][static_cast<size_t>(n * c)]);
-          for (int i = 0; i < n; ++i) nrm += std::norm(U[q][static_cast<size_t>(i + n * c)]);
-        }
-        if (row0 > 1e-20 * std::max(nrm, 1e-300))
-          throw Invalid("tucker_compress: odd-parity component has a nonzero offset-0 plane");
-        for (int64_t c = 0; c < r; ++c) U[q][static_cast<size_t>(n * c)] = 0.0;
-      }
+    copy_sync(dt, t_host, sizeof(double2) * nv, ctx->stream);
+    tucker_compress_dev(ctx, dims, dt, sign, tol, rule, out, ranks_out, hosvd_passes());
+  });
+}
+
+int vie_tucker_compress_device(vie_ctx ctx, const int64_t dims[3], const double* t_dev, const int sign[3],
+                               double tol, int rule, vie_tucker* out, int64_t ranks_out[3], void* stream) {
+  return guard([&] {
+    if (!ctx || !dims || !t_dev || !sign || !out) throw Invalid("tucker_compress: null argument");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaEvent_t ev = nullptr;
+    VIE_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    StreamJoin sj(ctx->stream, static_cast<cudaStream_t>(stream), ev);
+    try {
+      tucker_compress_dev(ctx, dims, reinterpret_cast<const double2*>(t_dev), sign, tol, rule, out, ranks_out,
+                          hosvd_passes());
+    } catch (...) {
+      cudaEventDestroy(ev);
+      throw;
     }
-    // core = t x1 U1^H x2 U2^H x3 U3^H (decomp.hpp:171-174), on the device
-    int64_t d[3] = {dims[0], dims[1], dims[2]};
-    const double2* cur = dt;
-    for (int q = 0; q < 3; ++q) {
-      double2* dU = dev.alloc<double2>(U[q].size());
-      VIE_CUDA_CHECK(cudaMemcpyAsync(dU, U[q].data(), sizeof(double2) * U[q].size(), cudaMemcpyHostToDevice, st));
-      int64_t od[3] = {d[0], d[1], d[2]};
-      od[q] = rk[q];
-      double2* nxt = dev.alloc<double2>(static_cast<size_t>(od[0] * od[1] * od[2]));
-      vie::launch_mode_product_h(cur, d, q + 1, dU, static_cast<int>(rk[q]), nxt, st);
-      cur = nxt;
-      d[0] = od[0];
-      d[1] = od[1];
-      d[2] = od[2];
-    }
-    std::vector<cd> core(static_cast<size_t>(rk[0] * rk[1] * rk[2]));
-    VIE_CUDA_CHECK(cudaMemcpyAsync(core.data(), cur, sizeof(double2) * core.size(), cudaMemcpyDeviceToHost, st));
+    sj.done();
+    VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    cudaEventDestroy(ev);
+  });
+}
+
+// ---- Green's-tensor assembly (assembly.hpp:159-246) ----
+namespace {
+vie::AssemblyDesc asm_desc(const int64_t dims[3], const double res[3], double k0, int kind, int q, int qp,
+                           const vie_quadrature* quad) {
+  vie::AssemblyDesc ad{};
+  for (int a = 0; a < 3; ++a) {
+    if (dims[a] < 1) throw Invalid("VoxelGrid: dims must be >= 1");
+    if (!(res[a] > 0.0)) throw Invalid("VoxelGrid: resolution must be > 0");
+    ad.dims[a] = dims[a];
+    ad.res[a] = res[a];
+  }
+  if (kind < 0 || kind > 2) throw Invalid("assemble_defining_tensor: kind must be N, K or scalar g");
+  if (q < 0 || q > 2 || qp < 0 || qp > 2) throw Invalid("assemble_defining_tensor: axes must be 0..2");
+  if (!std::isfinite(k0) || k0 < 0.0) throw Invalid("assemble_defining_tensor: k0 must be finite and >= 0");
+  ad.k0 = k0;
+  ad.op = kind;
+  ad.q = q;
+  ad.qp = qp;
+  const vie_quadrature dflt = {5, 10, 1, 12, 6};  // QuadratureSpec defaults (assembly.hpp:24-29)
+  const vie_quadrature& qs = quad ? *quad : dflt;
+  if (qs.far_points_per_axis < 1 || qs.near_points_per_axis < 1 || qs.surface_points_per_axis < 1 ||
+      qs.volume_points_per_axis < 1)
+    throw Invalid("QuadratureSpec: quadrature budget of zero");
+  if (qs.near_radius < 1) throw Invalid("QuadratureSpec: near_radius must be >= 1");
+  ad.far = qs.far_points_per_axis;
+  ad.near = qs.near_points_per_axis;
+  ad.near_radius = qs.near_radius;
+  ad.surface = qs.surface_points_per_axis;
+  ad.volume = qs.volume_points_per_axis;
+  return ad;
+}
+}  // namespace
+
+int vie_assemble(vie_ctx ctx, const int64_t dims[3], const double resolution[3], double k0, int kind, int row_axis,
+                 int col_axis, int basis, const vie_quadrature* quad, double* t, void* stream) {
+  return guard([&] {
+    if (!ctx || !dims || !resolution || !t) throw Invalid("assemble_defining_tensor: null argument");
+    if (basis != VIE_BASIS_PWC)
+      throw Invalid(
+          "assemble_defining_tensor: PWL Galerkin assembly (60 N / 30 K unique entries) is not supported; use PWC");
+    const vie::AssemblyDesc ad = asm_desc(dims, resolution, k0, kind, row_axis, col_axis, quad);
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->stream;
+    DevPool dev;
+    double2* self = dev.alloc<double2>(1);
+    double* rules = dev.alloc<double>(2 * vie::kAsmRuleElems + 4);
+    vie::launch_assemble(ad, reinterpret_cast<double2*>(t), self, rules, st, nullptr, nullptr);
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));  // scratch is freed on return
+  });
+}
+
+int vie_correlation_entry(vie_ctx ctx, int op, double k, int q, int qp, const double d[3], const double delta[3],
+                          int points, int duffy, double* out_host) {
+  return guard([&] {
+    if (!ctx || !d || !delta || !out_host) throw Invalid("correlation_entry: null argument");
+    if (op < 0 || op > 3 || points < 1 || points > 31) throw Invalid("correlation_entry: bad kernel or budget");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    DevPool dev;
+    double* rules = dev.alloc<double>(2 * vie::kAsmRuleElems + 4);
+    double2* o = dev.alloc<double2>(1);
+    vie::launch_correlation_entry(op, k, q, qp, d, delta, points, duffy, rules, o, st);
+    VIE_CUDA_CHECK(cudaMemcpyAsync(out_host, o, sizeof(double2), cudaMemcpyDeviceToHost, st));
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
-    const int rc = vie_tucker_from_factors(ctx, dims, rk, reinterpret_cast<const double*>(core.data()),
-                                           reinterpret_cast<const double*>(U[0].data()),
-                                           reinterpret_cast<const double*>(U[1].data()),
-                                           reinterpret_cast<const double*>(U[2].data()), sign, 0, out);
-    if (rc != VIE_OK) throw Invalid(g_err);
-    if (ranks_out)
-      for (int q = 0; q < 3; ++q) ranks_out[q] = rk[q];
+  });
+}
+
+int vie_self_static_term(vie_ctx ctx, const double delta[3], const vie_quadrature* quad, double dyad_diag[3],
+                         double* gram, double* error_indicator, int* converged) {
+  return guard([&] {
+    if (!ctx || !delta) throw Invalid("self_static_term: null argument");
+    const int64_t one[3] = {1, 1, 1};
+    vie::AssemblyDesc ad = asm_desc(one, delta, 0.0, 0, 0, 0, quad);
+    for (int a = 0; a < 3; ++a) ad.res[a] = delta[a];
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    DevPool dev;
+    double* rules = dev.alloc<double>(2 * vie::kAsmRuleElems + 4);
+    double* out = dev.alloc<double>(4);
+    // the kernel works in x-edge units: rescale the dyad back (it scales as the volume)
+    vie::launch_assemble(ad, nullptr, nullptr, rules, st, out, out + 3);
+    double h[4];
+    VIE_CUDA_CHECK(cudaMemcpyAsync(h, out, sizeof(h), cudaMemcpyDeviceToHost, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    const double s3 = delta[0] * delta[0] * delta[0];
+    if (dyad_diag)
+      for (int a = 0; a < 3; ++a) dyad_diag[a] = h[a] * s3;
+    const double g = delta[0] * delta[1] * delta[2];
+    if (gram) *gram = g;
+    if (error_indicator) *error_indicator = h[3];
+    if (converged) *converged = h[3] < 1e-7 ? 1 : 0;
   });
 }
 

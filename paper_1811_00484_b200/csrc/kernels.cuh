@@ -112,6 +112,27 @@ void launch_gram(const double2* t, const int64_t dims[3], int mode, double2* G, 
 void launch_mode_product_h(const double2* in, const int64_t dims[3], int mode, const double2* U, int r,
                            double2* out, cudaStream_t st);
 
+// ---- Green's-tensor assembly (kernels_assembly.cu; assembly.hpp:159-233)
+struct AssemblyDesc {
+  int64_t dims[3];
+  double res[3];  // voxel edges (m)
+  double k0;      // wavenumber (1/m)
+  int op;         // 0 N, 1 K, 2 scalar g
+  int q, qp;      // row / column axis
+  int far, near, near_radius, surface, volume;  // QuadratureSpec (assembly.hpp:24-36)
+};
+constexpr int kAsmRuleElems = 160;  // Gauss tables: at most 5 point counts <= 31
+// t (device, n1 n2 n3 complex) = the defining tensor; t == nullptr: only the static self
+// term (dyad_out[3] diagonal, err_out the refinement change), both device pointers or null.
+// self_scratch: 1 complex, rules_scratch: 2 kAsmRuleElems + 4 doubles (device).
+void launch_assemble(const AssemblyDesc& ad, double2* t, double2* self_scratch, double* rules_scratch,
+                     cudaStream_t st, double* dyad_out, double* err_out);
+
+// detail::correlation_entry (assembly.hpp:49-79) of kernel op (0 N, 1 K, 2 g, 3 N self
+// remainder) at displacement d, voxel delta (x-edge units), one thread (test hook)
+void launch_correlation_entry(int op, double k, int q, int qp, const double d[3], const double delta[3], int points,
+                              int duffy, double* rules_scratch, double2* out, cudaStream_t st);
+
 // ---- BLAS-1 for GMRES (deterministic two-level reductions) ----
 struct RedBuf {
   double2* partials;       // kRedBlocks entries

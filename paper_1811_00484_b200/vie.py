@@ -203,7 +203,19 @@ def tucker_cp_form(dft: DftService, dims, factors: Sequence, sign, domain: int =
 
 def tucker_compress(dft: DftService, t, dims, sign, tol: float = 1e-8, rule: int = RULE_ENERGY) -> TuckerForm:
     """hosvd + transform_factors (decomp.hpp:160-176, operator.hpp:76-90) of a spatial
-    Toeplitz-defining tensor (flat, reference layout); returns the device form."""
+    Toeplitz-defining tensor (flat, reference layout; host array or CUDA tensor, the
+    latter compressed in place on the device); returns the device form."""
+    if hasattr(t, "is_cuda") and t.is_cuda:
+        torch = _torch()
+        tt = t.reshape(-1).to(torch.complex128).contiguous()
+        if tt.numel() != int(np.prod(dims)):
+            raise ValueError("tucker_compress: tensor size does not match dims")
+        h = C.c_void_p()
+        ranks = (C.c_int64 * 3)()
+        _check(lib().vie_tucker_compress_device(dft.handle, _i64(dims), C.c_void_p(tt.data_ptr()),
+                                                (C.c_int * 3)(*[int(x) for x in sign]), C.c_double(tol), int(rule),
+                                                C.byref(h), ranks, C.c_void_p(_stream_handle(None, tt.device))))
+        return TuckerForm._from_handle(dft, h, dims, [ranks[0], ranks[1], ranks[2]], sign)
     t = _cplx(np.asarray(t).reshape(-1, order="F") if np.asarray(t).ndim == 3 else t).reshape(-1)
     if t.size != int(np.prod(dims)):
         raise ValueError("tucker_compress: tensor size does not match dims")
@@ -483,6 +495,63 @@ def apply_operator_timed(op: EmbeddedSpectrum, x, timings: ApplyTimings, out=Non
     _check(lib().vie_matvec_timed(op.handle, x.data_ptr(), y.data_ptr(), C.byref(f), C.byref(p)))
     timings.fft_ms, timings.product_ms = f.value, p.value
     return y
+
+
+# ----------------------------------------------------------------------------- assembly
+KIND_G = 2  # OperatorKind::ScalarG
+
+
+@dataclass
+class QuadratureSpec:  # assembly.hpp:24-36
+    far_points_per_axis: int = 5
+    near_points_per_axis: int = 10
+    near_radius: int = 1
+    surface_points_per_axis: int = 12
+    volume_points_per_axis: int = 6
+
+
+class _Quad(C.Structure):  # vie_quadrature
+    _fields_ = [("far", C.c_int), ("near", C.c_int), ("near_radius", C.c_int), ("surface", C.c_int),
+                ("volume", C.c_int)]
+
+
+def _quad(q: "QuadratureSpec | None"):
+    q = q or QuadratureSpec()
+    return _Quad(q.far_points_per_axis, q.near_points_per_axis, q.near_radius, q.surface_points_per_axis,
+                 q.volume_points_per_axis)
+
+
+def assemble_defining_tensor(dft: DftService, grid: "VoxelGrid", k0: float, kind: int, row_axis: int, col_axis: int,
+                             quad: "QuadratureSpec | None" = None, basis: int = PWC):
+    """assemble_defining_tensor (assembly.hpp:159-233) on the device: the PWC Galerkin
+    Toeplitz-defining tensor of one component; CUDA complex128 tensor (flat, reference layout)."""
+    torch = _torch()
+    nv = int(np.prod(grid.dims))
+    t = torch.empty(nv, dtype=torch.complex128, device=f"cuda:{dft.device}")
+    qs = _quad(quad)
+    _check(lib().vie_assemble(dft.handle, _i64(grid.dims), (C.c_double * 3)(*[float(r) for r in grid.resolution]),
+                              C.c_double(k0), int(kind), int(row_axis), int(col_axis), int(basis), C.byref(qs),
+                              C.c_void_p(t.data_ptr()), C.c_void_p(_stream_handle(None, t.device))))
+    return t
+
+
+def assemble_operator(dft: DftService, grid: "VoxelGrid", k0: float, kind: int,
+                      quad: "QuadratureSpec | None" = None):
+    """assemble_operator (assembly.hpp:236-244): [(component (q, q', 0, 0), tensor)] over the
+    unique PWC components of kind N or K (components.hpp:71-92), on the device."""
+    comps, _, _ = component_table(kind, PWC)
+    return [(tuple(int(v) for v in c), assemble_defining_tensor(dft, grid, k0, kind, int(c[0]), int(c[1]), quad))
+            for c in comps]
+
+
+def self_static_term(dft: DftService, delta, quad: "QuadratureSpec | None" = None):
+    """self_static_term (assembly.hpp:127-150): (dyad diagonal, gram, error indicator, converged)."""
+    dg = (C.c_double * 3)()
+    gram, err, conv = C.c_double(), C.c_double(), C.c_int()
+    qs = _quad(quad)
+    _check(lib().vie_self_static_term(dft.handle, (C.c_double * 3)(*[float(d) for d in delta]), C.byref(qs), dg,
+                                      C.byref(gram), C.byref(err), C.byref(conv)))
+    return np.array(dg[:]), gram.value, err.value, bool(conv.value)
 
 
 # ----------------------------------------------------------------------------- scene stages
