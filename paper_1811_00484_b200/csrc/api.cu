@@ -386,23 +386,26 @@ int64_t truncation_rank_host(const std::vector<double>& s, double tol, int rule)
 // Cyclic Jacobi eigendecomposition of a Hermitian n x n matrix (col-major):
 // eigenvalues descending in lam, eigenvectors in the columns of V.  Rotation
 // J = [[c, s e^{i phi}], [-s e^{-i phi}, c]] zeroes a_pq = |a_pq| e^{i phi}.
-void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::vector<cd>& V) {
+void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::vector<cd>& V, bool relative = true) {
   auto A = [&](int i, int j) -> cd& { return a[static_cast<size_t>(i) + static_cast<size_t>(n) * j]; };
   std::vector<cd> v(static_cast<size_t>(n) * n, cd(0.0));
   for (int i = 0; i < n; ++i) v[static_cast<size_t>(i) * (n + 1)] = 1.0;
   double fro = 0.0;
   for (const cd& x : a) fro += std::norm(x);
   fro = std::sqrt(fro);
-  for (int sweep = 0; sweep < 60 && fro > 0.0; ++sweep) {
-    double off = 0.0;
-    for (int q = 1; q < n; ++q)
-      for (int p = 0; p < q; ++p) off += std::norm(A(p, q));
-    if (std::sqrt(2.0 * off) <= 1e-15 * fro) break;
+  // relative (Demmel-Veselic) threshold: rotate while |a_pq| > eps sqrt(a_pp a_qq), so the
+  // small eigenvalues of a graded Gram (rows of B = U0^H M carry the singular values) keep
+  // their relative accuracy instead of being flushed at eps * ||A||
+  for (int sweep = 0; sweep < 80 && fro > 0.0; ++sweep) {
+    bool rotated = false;
     for (int p = 0; p < n - 1; ++p)
       for (int q = p + 1; q < n; ++q) {
         const cd apq = A(p, q);
         const double mag = std::abs(apq);
-        if (mag <= 1e-300 || mag <= 1e-18 * fro) continue;
+        if (mag <= 1e-300 || mag <= (relative ? 1e-16 * std::sqrt(std::abs(A(p, p).real() * A(q, q).real()))
+                                              : 1e-16 * fro))
+          continue;
+        rotated = true;
         const double tau = (A(q, q).real() - A(p, p).real()) / (2.0 * mag);
         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (std::abs(tau) + std::sqrt(1.0 + tau * tau));
         const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
@@ -428,6 +431,7 @@ void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::v
           vkq = x * jpq + y * c;
         }
       }
+    if (!rotated) break;
   }
   std::vector<int> order(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) order[static_cast<size_t>(i)] = i;
@@ -790,8 +794,8 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       d.off_z = zoff;
       zoff += static_cast<int64_t>(g.n2 + 1) * d.r1 * d.r3;
     }
-    if (vie::decomp_smem(g.n3, op->rmax) > vie::kMaxSmem && vie::decomp_mma_smem(g.n1, g.n3, op->rmax) > vie::kMaxSmem)
-      throw Invalid("vie_op_create: Tucker rank too large for the decompression tile (rank * (n3 + 1) too big)");
+    if (static_cast<size_t>(op->rmax) * 32 * sizeof(double2) > vie::kMaxSmem)
+      throw Invalid("vie_op_create: Tucker rank above the device limit (443)");
     if (vie::pencil_smem(g.n3, g.S, g.NC) > vie::kMaxSmem) throw Invalid("vie_op_create: grid edge n3 too large");
     op->forms = dev_alloc<double2>(static_cast<size_t>(off));
     for (size_t c = 0; c < cs.size(); ++c) {
@@ -1444,16 +1448,16 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
   for (int q = 0; q < 3; ++q) {
     const int n = static_cast<int>(dims[q]);
     double2* dG = dev.alloc<double2>(static_cast<size_t>(n) * n);
-    auto gram_eig = [&](const double2* t, std::vector<double>& lam, std::vector<cd>& V) {
+    auto gram_eig = [&](const double2* t, std::vector<double>& lam, std::vector<cd>& V, bool relative) {
       vie::launch_gram(t, dims, q + 1, dG, st);
       std::vector<cd> G(static_cast<size_t>(n) * n);
       VIE_CUDA_CHECK(cudaMemcpyAsync(G.data(), dG, sizeof(double2) * G.size(), cudaMemcpyDeviceToHost, st));
       VIE_CUDA_CHECK(cudaStreamSynchronize(st));
-      herm_eig_jacobi(G, n, lam, V);
+      herm_eig_jacobi(G, n, lam, V, relative);
     };
     std::vector<double> lam;
     std::vector<cd> V0;
-    gram_eig(dt, lam, V0);
+    gram_eig(dt, lam, V0, passes <= 1);  // first pass: absolute threshold (a basis to refine)
     std::vector<cd> Ufull = V0;  // n x n
     for (int pass = 1; pass < passes; ++pass) {
       // B = Ufull^H x_q t, then the eigendecomposition of B B^H (rotation V), Ufull <- Ufull V
@@ -1462,7 +1466,7 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
       double2* dB = dev.alloc<double2>(static_cast<size_t>(dims[0] * dims[1] * dims[2]));
       vie::launch_mode_product_h(dt, dims, q + 1, dU, n, dB, st);
       std::vector<cd> Vr;
-      gram_eig(dB, lam, Vr);
+      gram_eig(dB, lam, Vr, true);
       std::vector<cd> Un(static_cast<size_t>(n) * n, cd(0.0));
       for (int c = 0; c < n; ++c)
         for (int k = 0; k < n; ++k) {

@@ -25,25 +25,23 @@ __device__ __forceinline__ void cp_async_wait_all_d() {
   asm volatile("cp.async.wait_group 0;\n" ::);
 }
 
-// CTA per (component, g): stage one core slice G[:,:,g] in smem.
+// CTA per (component, g): Z_c[p2][a][g] for one core slice G[:,:,g] (read through the
+// cache: consecutive threads take consecutive a, so the slice reads coalesce).
 __global__ void __launch_bounds__(kThreads) k_decomp_z(const double2* __restrict__ forms,
                                                        const CompDev* __restrict__ comps, double2* __restrict__ Z,
                                                        int n2) {
-  extern __shared__ double2 gs[];
   const CompDev cd = comps[blockIdx.x];
   const int g = blockIdx.y;
   if (!cd.active || g >= cd.r3) return;
   const int r1 = cd.r1, r2 = cd.r2, r3 = cd.r3;
-  const double2* core = forms + cd.off_core + static_cast<int64_t>(g) * r1 * r2;
-  for (int e = threadIdx.x; e < r1 * r2; e += blockDim.x) gs[e] = core[e];  // gs[a + r1*b]
-  __syncthreads();
+  const double2* core = forms + cd.off_core + static_cast<int64_t>(g) * r1 * r2;  // core[a + r1*b]
   const double2* u2 = forms + cd.off_u2;  // (n2+1) x r2
   const int np = n2 + 1;
   double2* zc = Z + cd.off_z;
   for (int e = threadIdx.x; e < np * r1; e += blockDim.x) {
     const int a = e % r1, p2 = e / r1;
     double2 acc = make_double2(0.0, 0.0);
-    for (int b = 0; b < r2; ++b) cfma(acc, gs[a + r1 * b], __ldg(u2 + p2 + static_cast<int64_t>(np) * b));
+    for (int b = 0; b < r2; ++b) cfma(acc, __ldg(core + a + r1 * b), __ldg(u2 + p2 + static_cast<int64_t>(np) * b));
     zc[(static_cast<int64_t>(p2) * r1 + a) * r3 + g] = acc;
   }
 }
@@ -104,6 +102,76 @@ __global__ void __launch_bounds__(kThreads) k_decomp_s(const double2* __restrict
         for (int j = 0; j < kQ; ++j) {
           const int f = fb + lane + 32 * j;
           uv[j] = f < n3p ? us[g * n3p + f] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < kQ; ++i)
+#pragma unroll
+          for (int j = 0; j < kQ; ++j) cfma(acc[i][j], tv[i], uv[j]);
+      }
+#pragma unroll
+      for (int i = 0; i < kQ; ++i) {
+        const int p1o = p10 + rq * kQ + i;
+        if (rq * kQ + i >= np1) break;
+        double2* dst = Shat + ((static_cast<int64_t>(p2o) * n1p + p1o) * NC + c) * n3p;
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) {
+          const int f = fb + lane + 32 * j;
+          if (f < n3p) dst[(f & 1) ? E + (f >> 1) : (f >> 1)] = acc[i][j];
+        }
+      }
+    }
+  }
+}
+
+// Large-rank fallback (ranks beyond both tiles above, e.g. tight-tolerance HOSVD forms):
+// CTA per (component, p2o); only the T chunk (r3 x kTP1) is staged, Z and U3 are read
+// through the cache (Z_c[p2o] and U3_c are re-read by every chunk: L1/L2 resident).
+__global__ void __launch_bounds__(kThreads) k_decomp_s_big(const double2* __restrict__ forms,
+                                                           const CompDev* __restrict__ comps,
+                                                           const double2* __restrict__ Z, double2* __restrict__ Shat,
+                                                           Geom geo, int NC, int p2lo, int p1lo, int p1hi) {
+  extern __shared__ double2 sm[];
+  const int c = blockIdx.x;
+  const CompDev cd = comps[c];
+  if (!cd.active) return;
+  const int p2o = p2lo + blockIdx.y;
+  const int r1 = cd.r1, r3 = cd.r3;
+  const int n1p = geo.n1 + 1, n3p = geo.n3 + 1;
+  double2* ts = sm;  // r3 x kTP1: ts[g*kTP1 + i]
+  const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;  // [a][g]
+  const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major
+  const double2* u1 = forms + cd.off_u1;  // n1p x r1
+  const int E = geo.n3 / 2 + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  for (int p10 = p1lo; p10 < p1hi; p10 += kTP1) {
+    const int np1 = min(kTP1, p1hi - p10);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kTP1 * r3; e += blockDim.x) {
+      const int i = e % kTP1, g = e / kTP1;
+      double2 acc = make_double2(0.0, 0.0);
+      if (i < np1)
+        for (int a = 0; a < r1; ++a)
+          cfma(acc, __ldg(u1 + (p10 + i) + static_cast<int64_t>(n1p) * a), __ldg(zsrc + static_cast<int64_t>(a) * r3 + g));
+      ts[g * kTP1 + i] = acc;
+    }
+    __syncthreads();
+    const int nfb = (n3p + 127) / 128;
+    const int wtiles = (kTP1 / kQ) * nfb;
+    for (int t = warp; t < wtiles; t += nwarp) {
+      const int fb = (t % nfb) * 128, rq = t / nfb;
+      double2 acc[kQ][kQ];
+#pragma unroll
+      for (int i = 0; i < kQ; ++i)
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) acc[i][j] = make_double2(0.0, 0.0);
+      for (int g = 0; g < r3; ++g) {
+        double2 tv[kQ], uv[kQ];
+#pragma unroll
+        for (int i = 0; i < kQ; ++i) tv[i] = ts[g * kTP1 + rq * kQ + i];
+#pragma unroll
+        for (int j = 0; j < kQ; ++j) {
+          const int f = fb + lane + 32 * j;
+          uv[j] = f < n3p ? __ldg(u3 + f + static_cast<int64_t>(n3p) * g) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int i = 0; i < kQ; ++i)
@@ -352,11 +420,8 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
   if (p2hi < 0) p2hi = g.n2 + 1;
   if (p1hi < 0) p1hi = g.n1 + 1;
   if (p2hi <= p2lo || p1hi <= p1lo) return;
-  const size_t smz = sizeof(double2) * static_cast<size_t>(rmax) * rmax;
-  VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_z),
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smz)));
   if (with_z) {
-    k_decomp_z<<<dim3(g.NC, rmax), kThreads, smz, st>>>(forms, comps_dev, Z, g.n2);
+    k_decomp_z<<<dim3(g.NC, rmax), kThreads, 0, st>>>(forms, comps_dev, Z, g.n2);
     VIE_CUDA_CHECK(cudaGetLastError());
   }
   const size_t sms = decomp_mma_smem(g.n1, g.n3, rmax);
@@ -365,11 +430,17 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
     k_decomp_s_mma<<<dim3(g.NC, (p2hi - p2lo + kMmaPP - 1) / kMmaPP), kMmaThreads, sms, st>>>(
         forms, comps_dev, Z, Shat, g, g.NC, p2lo, p2hi, p1lo, p1hi);
-  } else {
+  } else if (decomp_smem(g.n3, rmax) <= kMaxSmem) {
     const size_t smf = decomp_smem(g.n3, rmax);
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smf)));
     k_decomp_s<<<dim3(g.NC, p2hi - p2lo), kThreads, smf, st>>>(forms, comps_dev, Z, Shat, g, g.NC, p2lo, p1lo, p1hi);
+  } else {
+    const size_t smb = sizeof(double2) * static_cast<size_t>(rmax) * kTP1;
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s_big),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smb)));
+    k_decomp_s_big<<<dim3(g.NC, p2hi - p2lo), kThreads, smb, st>>>(forms, comps_dev, Z, Shat, g, g.NC, p2lo, p1lo,
+                                                                     p1hi);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }

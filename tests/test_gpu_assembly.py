@@ -149,3 +149,22 @@ def test_device_hosvd_ranks_match_oracle_at_tight_tolerances(env, tol):
         ranks_ref = [u.shape[1] for u in O.hosvd(t, dims, tol)[1]]
         f = vie.tucker_compress(dft, t, dims, (1, 1, 1), tol)
         assert tuple(f.ranks) == tuple(int(r) for r in ranks_ref), (dims, tol, f.ranks, ranks_ref)
+
+
+@pytest.mark.parametrize("comp", [(0, 0, 0), (0, 0, 1), (0, 1, 2)])
+def test_device_hosvd_ranks_on_assembled_tensors(env, comp):
+    # the C5 path: an assembled component compressed on the device at tol 1e-4 .. 1e-10 has
+    # the ranks of the oracle's QR + Jacobi SVD HOSVD (decomp.hpp:40-176)
+    vie, torch, dft = env
+    dims, res = (24, 20, 22), (0.005, 0.005, 0.005)
+    k0 = 2 * math.pi * 2.98e8 / C0
+    op, q, qp = comp
+    t_dev = vie.assemble_defining_tensor(dft, vie.VoxelGrid(dims, res), k0, op, q, qp)
+    t = O.assemble(dims, res, k0, op, q, qp)
+    par = [1, 1, 1]
+    if q != qp:
+        par[q] = par[qp] = -1
+    for tol in (1e-4, 1e-6, 1e-8, 1e-10):
+        ranks_ref = [u.shape[1] for u in O.hosvd(t, dims, tol)[1]]
+        f = vie.tucker_compress(dft, t_dev, dims, par, tol)
+        assert tuple(f.ranks) == tuple(ranks_ref), (comp, tol, f.ranks, ranks_ref)

@@ -114,6 +114,7 @@ def test_matvec_pencil3_shapes(vie, dft, orc, kind, basis, dims, rank):
 # pencil shape (generic pencil kernel)
 PATH_CASES = [
     (N, PWC, (6, 5, 7), 30),     # rank 30: k_decomp_s (FMA) instead of the DMMA kernel
+    (N, PWC, (5, 4, 60), 100),   # rank 100 x n3 60: beyond the FMA tile, k_decomp_s_big
     (N, PWC, (125, 4, 3), 2),    # m1 = 250: generic row passes (three-stage plan)
     (N, PWL, (4, 125, 3), 2),    # m2 = 250: generic column passes
     (K, PWL, (3, 4, 9), 3),      # n3 = 9: no compiled pencil shape, generic pencil kernel
