@@ -137,7 +137,22 @@ int vie_op_destroy(vie_op op);
 /* sizes: n_cur (= current components S), n_vox (= N_v), bytes of workspace   */
 int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_bytes);
 
-/* apply_operator (operator.hpp:273-382), strategy HosvdDecompress semantics:
+/* MatvecStrategy of every later apply on this operator (operator.hpp:17-31; the strategy
+ * argument of apply_operator, operator.hpp:273-276, and of the solve closure):
+ *   VIE_STRATEGY_HOSVD_DECOMPRESS: all components' octant spectra are decompressed into one
+ *     HBM buffer, then read by the fused axis-3 FFT x Hadamard pass (default);
+ *   VIE_STRATEGY_HOSVD_LOOP: the reference's buffer-free HosvdLoop -- one persistent kernel
+ *     decompresses 64-row spectrum tiles into an L2-resident ring and consumes them in the same
+ *     launch; only the edge rows (p2o in {0, n2}, p1o in {0, n1}) are stored.  PWL operators
+ *     with ranks <= 28 and a compiled axis-3 shape; VIE_EINVAL otherwise or when partitioned.
+ * Spectrum storage of a strategy is allocated on its first use (vie_op_info reports it).
+ * The TuckerCp strategies map to these two (CP forms are held as Tucker forms).          */
+#define VIE_STRATEGY_HOSVD_DECOMPRESS 1
+#define VIE_STRATEGY_HOSVD_LOOP 2
+int vie_op_set_strategy(vie_op op, int strategy);
+int vie_op_get_strategy(vie_op op, int* strategy);
+
+/* apply_operator (operator.hpp:273-382) with the operator's strategy (vie_op_set_strategy):
  * y = A x for device vectors of n_cur * n_vox complex values.                */
 int vie_matvec(vie_op op, const double* x, double* y, void* stream);
 /* apply_operator with ApplyTimings (operator.hpp:189-192): the stages run serialised with

@@ -43,7 +43,10 @@ using Index = std::int64_t;
 
 enum class OperatorKind { N = VIE_KIND_N, K = VIE_KIND_K };
 enum class BasisOrder { PWC = VIE_BASIS_PWC, PWL = VIE_BASIS_PWL };
-enum class MatvecStrategy { HosvdDecompress, HosvdLoop };
+// operator.hpp:17 (Dense is the reference's uncompressed test path; not served here).
+// *Decompress: all octant spectra in one HBM buffer; *Loop: the buffer-free fused kernel
+// (vie_op_set_strategy).  CP forms are held as Tucker forms, so TuckerCp* select the same paths.
+enum class MatvecStrategy { HosvdDecompress, HosvdLoop, TuckerCpDecompress, TuckerCpLoop };
 enum class ScratchPolicy { WithBuffer, NoBuffer };
 
 inline void check(int rc) {
@@ -379,6 +382,11 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind,
   return EmbeddedSpectrum(op, kind, opts.order, grid);
 }
 
+inline bool is_loop(MatvecStrategy s) { return s == MatvecStrategy::HosvdLoop || s == MatvecStrategy::TuckerCpLoop; }
+inline void set_strategy(const EmbeddedSpectrum& op, MatvecStrategy s) {
+  check(vie_op_set_strategy(op.handle(), is_loop(s) ? VIE_STRATEGY_HOSVD_LOOP : VIE_STRATEGY_HOSVD_DECOMPRESS));
+}
+
 // apply_operator (operator.hpp:273-382).  Host containers in/out; the matvec
 // runs on the device (vie_matvec_host: H2D, matvec, D2H).
 // With `timings` (ApplyTimings, operator.hpp:189-192) the device stages run serialised
@@ -390,8 +398,9 @@ inline CurrentField apply_operator(const EmbeddedSpectrum& op, const CurrentFiel
   (void)dft;
   if (x.dims() != op.grid_dims || static_cast<Index>(x.comp.size()) != op.n_cur())
     throw std::invalid_argument("apply_operator: dim mismatch");
-  if (strategy == MatvecStrategy::HosvdDecompress && policy == ScratchPolicy::NoBuffer)
+  if (!is_loop(strategy) && policy == ScratchPolicy::NoBuffer)
     throw std::invalid_argument("apply_operator: decompress strategies need ScratchPolicy::WithBuffer");
+  set_strategy(op, strategy);
   const std::vector<cplx> xv = x.to_vector();
   std::vector<cplx> yv(xv.size());
   if (!timings) {

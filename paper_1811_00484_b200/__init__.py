@@ -8,7 +8,8 @@ from .vie import (KIND_K, KIND_N, PWC, PWL, DftService, EmbeddedSpectrum, GmresC
                   ncur, tucker_compress, RULE_ENERGY, RULE_SIGMA_MAX, DielectricMap, Fields, PlaneWave,
                   PostProcess, VoxelGrid, build_rhs, postprocess, recover_fields,
                   SolveReport, solve_scene, tucker_cp_form, gmres_map, ApplyTimings, apply_operator_timed,
-                  KIND_G, QuadratureSpec, assemble_defining_tensor, assemble_operator, self_static_term)
+                  KIND_G, QuadratureSpec, assemble_defining_tensor, assemble_operator, self_static_term,
+                  set_strategy, get_strategy)
 
 __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "GmresConfig", "GmresResult",
            "TuckerForm", "VieError", "apply_operator", "apply_operator_batch", "apply_system", "build_operator_spectra",
@@ -16,4 +17,4 @@ __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "
            "DielectricMap", "Fields", "PlaneWave", "PostProcess", "VoxelGrid", "build_rhs", "postprocess",
            "recover_fields", "SolveReport", "solve_scene", "tucker_cp_form", "gmres_map", "ApplyTimings",
            "apply_operator_timed", "KIND_G", "QuadratureSpec", "assemble_defining_tensor", "assemble_operator",
-           "self_static_term"]
+           "self_static_term", "set_strategy", "get_strategy"]

@@ -134,6 +134,7 @@ struct vie_op_s {
   CompDev* comps_dev = nullptr;
   double2* forms = nullptr;
   double2* Z = nullptr;
+  double2* u3img = nullptr;  // U3 shared-memory images of the tile decomposition (decomp_tile.cuh)
   double2* Shat = nullptr;
   double2* A = nullptr;
   double2* B = nullptr;
@@ -145,6 +146,17 @@ struct vie_op_s {
   bool q1 = false, q2 = false;  // (false: generic multi-stage passes P1 / P2)
   bool pencil2 = false;         // compile-time-shaped two-branch pencil kernel for this n3
   bool pencil3 = false;         // PWL: whole-mirror-group pencil kernel with the DMMA Hadamard (interior groups)
+  bool pencil4 = false;         // PWL: half-mirror-group DMMA pencil kernel, 2 CTAs per SM (replaces pencil3)
+  // fused decompression x pencil (kernels_fused.cu): no whole-spectrum buffer; the interior rows
+  // go through an L2-resident tile ring, the edge rows through the compact edge buffer Sedge
+  bool fused = false;     // current strategy is hosvd_loop (fused kernel)
+  bool fused_ok = false;  // the fused kernel supports this operator
+  vie::FusedPlan fp{};
+  int64_t ws_fixed = 0;   // workspace bytes without the spectrum storage
+  double2* ring = nullptr;
+  double2* Sedge = nullptr;
+  int4* fitems = nullptr;
+  unsigned* fcounters = nullptr;
   int fork_after = 0;           // decompression fork point: 0 before the row pass, 1 after it, 2 after the column pass
   // slab decomposition (vie_op_set_partition): this rank's z-planes [k0, k0 + nk) and
   // axis-1 positions [p1off, p1off + W) (Geom)
@@ -175,10 +187,11 @@ struct vie_op_s {
   double stage_ms[8] = {0};
   cudaEvent_t ev[8] = {};
   ~vie_op_s() {
-    for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z),
+    for (void* p : {static_cast<void*>(comps_dev), static_cast<void*>(forms), static_cast<void*>(Z), static_cast<void*>(u3img),
                     static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(hx2), static_cast<void*>(hy2),
-                    static_cast<void*>(V),
+                    static_cast<void*>(V), static_cast<void*>(ring), static_cast<void*>(Sedge), static_cast<void*>(fitems),
+                    static_cast<void*>(fcounters),
                     static_cast<void*>(tmp), static_cast<void*>(zp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
       dev_free(p);
@@ -448,16 +461,69 @@ void herm_eig_jacobi(std::vector<cd>& a, int n, std::vector<double>& lam, std::v
 
 // ---------------------------------------------------------------- matvec
 // Launch the decompression on the side stream after all work queued on `st`.
+// Spectrum storage of the current strategy, allocated on first use (and reported by
+// vie_op_info): hosvd_decompress -> Shat, all octant spectra; hosvd_loop -> the fused
+// kernel's tile ring, work queue and the compact edge rows.
+void ensure_spectra(vie_op op) {
+  const Geom& g = op->g;
+  const int64_t rs = static_cast<int64_t>(g.NC) * (g.n3 + 1);
+  if (op->fused && !op->ring) {
+    std::vector<int4> items;
+    vie::fused_plan_items(op->fp, g, items);
+    op->ring = dev_alloc<double2>(static_cast<size_t>(op->fp.RING) * op->fp.BM * rs);
+    op->Sedge = dev_alloc<double2>(static_cast<size_t>(vie::shat_rows(g.n1, g.n2, 1) * rs));
+    op->fitems = dev_alloc<int4>(items.size());
+    copy_sync(op->fitems, items.data(), sizeof(int4) * items.size(), op->ctx->stream);
+    op->fcounters = dev_alloc<unsigned>(1 + 3 * static_cast<size_t>(op->fp.ntiles));
+    op->fp.forms = op->forms;
+    op->fp.u3img = op->u3img;
+    op->fp.comps = op->comps_dev;
+    op->fp.Z = op->Z;
+    op->fp.ring = op->ring;
+    op->fp.items = op->fitems;
+    op->fp.counters = op->fcounters;
+    op->fp.rmax = op->rmax;
+  }
+  if (!op->fused && !op->Shat) op->Shat = dev_alloc<double2>(static_cast<size_t>(vie::shat_rows(g.n1, g.n2, 0) * rs));
+  int64_t spec = 0;
+  if (op->Shat) spec += vie::shat_rows(g.n1, g.n2, 0) * rs;
+  if (op->ring)
+    spec += static_cast<int64_t>(op->fp.RING) * op->fp.BM * rs + vie::shat_rows(g.n1, g.n2, 1) * rs;
+  op->ws_bytes = op->ws_fixed + static_cast<int64_t>(sizeof(double2)) * spec;
+}
+
+// Geometry of the edge pencil launches of the fused path (compact edge spectrum rows)
+Geom edge_geom(const vie_op_s* op) {
+  Geom ge = op->g;
+  ge.ecompact = op->fused ? 1 : 0;
+  return ge;
+}
+
+// The x-independent decompression stage: the whole octant spectrum (materialised path) or, on
+// the fused path, Z = core x2 U2 and the edge rows only (the interior rows are decompressed
+// inside the fused kernel).
+void decomp_stage(vie_op op, cudaStream_t st) {
+  ensure_spectra(op);  // (vie_matvec_host forks this stage before run_matvec)
+  if (op->fused) {
+    vie::launch_decomp_z(op->forms, op->comps_dev, op->Z, op->g, op->rmax, st);
+    vie::launch_decomp_edges(op->fp, op->Sedge, edge_geom(op), st);
+  } else {
+    vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, op->g, op->rmax, st, 0, -1,
+                       true, 0, -1, op->u3img);
+  }
+}
+
 void fork_decomp(vie_op op, cudaStream_t st) {
   VIE_CUDA_CHECK(cudaEventRecord(op->ev_fork, st));
   VIE_CUDA_CHECK(cudaStreamWaitEvent(op->side, op->ev_fork, 0));
-  vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, op->g, op->rmax, op->side);
+  decomp_stage(op, op->side);
   VIE_CUDA_CHECK(cudaEventRecord(op->ev_join, op->side));
 }
 
 void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const double2* eps, double inv_v,
                 int diag, bool decomp_forked = false) {
   if (op->nranks > 1) throw Invalid("apply_operator: operator is partitioned (use the vie_slab_* stages)");
+  ensure_spectra(op);
   const Geom& g = op->g;
   const double ne = 8.0 * g.n1 * static_cast<double>(g.n2) * g.n3;
   if (op->profiling) {  // serial launches so every stage gets its own event interval
@@ -490,14 +556,21 @@ void run_matvec(vie_op op, const double2* x, double2* y, cudaStream_t st, const 
     mark2();
   } else {
     if (decomp_forked) VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
-    else vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st);
+    else decomp_stage(op, st);
   }
   mark();
-  if (op->pencil3) {  // interior mirror groups on the DMMA kernel; axis-1 edge group, axis-2 edge rows
+  if (op->fused) {  // edge rows from the compact edge buffer, the interior in the fused kernel
+    const Geom ge = edge_geom(op);
+    vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Sedge, ge, op->PH, op->P3.tw, op->active, st,
+                       1);
+    vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Sedge, ge, op->P3.tw, st, 0, 2);
+    vie::launch_fused(op->kind, op->fp, op->B, op->Bo, g, op->P3.tw, st);
+  } else if (op->pencil3) {  // interior mirror groups on the DMMA kernel; axis-1 edge group, axis-2 edge rows
     vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st,
                        1);
     vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
-    vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+    if (op->pencil4) vie::launch_pencil4(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+    else vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
   } else if (op->pencil2) {  // compile-time-shaped kernel + the axis-1 edge group on the generic one
     vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, op->Bo1, op->Shat, g, op->PH, op->P3.tw, op->active, st,
                        1);
@@ -772,7 +845,7 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       byc[static_cast<size_t>(found)] = t;
     }
     // pack forms: core, U1o, U2o, U3o per active component; Z offsets
-    int64_t off = 0, zoff = 0;
+    int64_t off = 0, zoff = 0, u3ioff = 0;
     for (size_t c = 0; c < cs.size(); ++c) {
       const vie_tucker_s* t = byc[c];
       CompDev& d = op->comps_host[c];
@@ -793,6 +866,8 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       off += static_cast<int64_t>(g.n3 + 1) * d.r3;
       d.off_z = zoff;
       zoff += static_cast<int64_t>(g.n2 + 1) * d.r1 * d.r3;
+      d.off_u3i = u3ioff;
+      u3ioff += vie::u3_image_elems(g.n3, d.r3);
     }
     if (static_cast<size_t>(op->rmax) * 32 * sizeof(double2) > vie::kMaxSmem)
       throw Invalid("vie_op_create: Tucker rank above the device limit (443)");
@@ -807,19 +882,34 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       copy_sync(op->forms + d.off_u2, t->uo[1], sizeof(double2) * (g.n2 + 1) * d.r2, ctx->stream);
       copy_sync(op->forms + d.off_u3, t->uo[2], sizeof(double2) * (g.n3 + 1) * d.r3, ctx->stream);
     }
+    op->u3img = dev_alloc<double2>(static_cast<size_t>(std::max<int64_t>(u3ioff, 1)));
+    vie::launch_u3_image(op->forms, op->comps_host.data(), g.NC, g.n3, op->u3img, ctx->stream);
     op->comps_dev = dev_alloc<CompDev>(cs.size());
     copy_sync(op->comps_dev, op->comps_host.data(), sizeof(CompDev) * cs.size(), ctx->stream);
     const int64_t nv = static_cast<int64_t>(g.n1) * g.n2 * g.n3;
-    const int64_t noct = static_cast<int64_t>(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
     op->Z = dev_alloc<double2>(static_cast<size_t>(std::max<int64_t>(zoff, 1)));
-    op->Shat = dev_alloc<double2>(static_cast<size_t>(noct * g.NC));
+    op->pencil2 = kPencil2 && vie::pencil2_supported(op->kind, op->basis, g.n3, op->active, g.NC);
+    op->pencil3 = op->pencil2 && vie::pencil3_supported(op->kind, op->basis, g.n3, op->active, g.NC);
+    op->pencil4 = op->pencil3 && vie::pencil4_supported(op->kind, op->basis, g.n3, op->active, g.NC);
+    op->fused_ok = op->pencil4 && vie::fused_supported(op->kind, op->basis, g, op->active, op->rmax);
+    // spectrum storage follows the strategy (vie_op_set_strategy) and is allocated on first use:
+    // hosvd_decompress -> the whole octant spectrum Shat; hosvd_loop -> tile ring + edge rows
+    {
+      const char* s = std::getenv("VIE_STRATEGY");
+      op->fused = op->fused_ok && s && std::string(s) == "loop";
+    }
     op->A = dev_alloc<double2>(static_cast<size_t>(g.S * 2 * nv));
     op->B = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
     op->Bo = dev_alloc<double2>(static_cast<size_t>(g.S * g.n3 * g.bps));
-    op->ws_bytes = static_cast<int64_t>(sizeof(double2)) * (zoff + noct * g.NC + g.S * 2 * nv + 2 * g.S * g.n3 * g.bps);
+    op->ws_fixed = static_cast<int64_t>(sizeof(double2)) * (zoff + g.S * 2 * nv + 2 * g.S * g.n3 * g.bps);
+    op->ws_bytes = op->ws_fixed;  // + the strategy's spectrum storage, allocated on first use
     if (const int poison = env_int("VIE_DEBUG_POISON", 0)) {  // debug: NaN-fill workspaces (reads of unwritten data)
       const int64_t nb = g.S * g.n3 * g.bps;
-      if (poison & 1) VIE_CUDA_CHECK(cudaMemsetAsync(op->Shat, 0xFF, sizeof(double2) * noct * g.NC));
+      const int64_t noct = static_cast<int64_t>(g.n1 + 1) * (g.n2 + 1) * (g.n3 + 1);
+      if ((poison & 1) && op->Shat) VIE_CUDA_CHECK(cudaMemsetAsync(op->Shat, 0xFF, sizeof(double2) * noct * g.NC));
+      if ((poison & 1) && op->ring)
+        VIE_CUDA_CHECK(cudaMemsetAsync(op->ring, 0xFF,
+                                       sizeof(double2) * op->fp.RING * op->fp.BM * g.NC * (g.n3 + 1)));
       if (poison & 2) VIE_CUDA_CHECK(cudaMemsetAsync(op->Z, 0xFF, sizeof(double2) * std::max<int64_t>(zoff, 1)));
       if (poison & 4) VIE_CUDA_CHECK(cudaMemsetAsync(op->A, 0xFF, sizeof(double2) * g.S * 2 * nv));
       if (poison & 8) VIE_CUDA_CHECK(cudaMemsetAsync(op->B, 0xFF, sizeof(double2) * nb));
@@ -829,8 +919,6 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
     op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
     op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
-    op->pencil2 = kPencil2 && vie::pencil2_supported(op->kind, op->basis, g.n3, op->active, g.NC);
-    op->pencil3 = op->pencil2 && vie::pencil3_supported(op->kind, op->basis, g.n3, op->active, g.NC);
     if (kPass2) {  // register-staged passes when the axis has a <= 2-stage wide plan
       std::vector<int> r1, r2;
       const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1);
@@ -856,6 +944,30 @@ int vie_op_destroy(vie_op op) {
     cudaSetDevice(op->ctx->device);
     cudaStreamSynchronize(op->ctx->stream);
     delete op;
+  });
+}
+
+int vie_op_set_strategy(vie_op op, int strategy) {
+  return guard([&] {
+    if (!op) throw Invalid("set_strategy: null operator");
+    if (strategy != VIE_STRATEGY_HOSVD_DECOMPRESS && strategy != VIE_STRATEGY_HOSVD_LOOP)
+      throw Invalid("set_strategy: unknown strategy");
+    const bool loop = strategy == VIE_STRATEGY_HOSVD_LOOP;
+    if (loop && (!op->fused_ok || op->nranks > 1))
+      throw Invalid("apply_operator: hosvd_loop (fused decompress x pencil kernel) needs a PWL operator with "
+                    "ranks <= 28, a compiled axis-3 shape and no slab partition");
+    if (loop == op->fused) return;
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
+    op->fused = loop;
+    ensure_spectra(op);
+  });
+}
+
+int vie_op_get_strategy(vie_op op, int* strategy) {
+  return guard([&] {
+    if (!op || !strategy) throw Invalid("get_strategy: null argument");
+    *strategy = op->fused ? VIE_STRATEGY_HOSVD_LOOP : VIE_STRATEGY_HOSVD_DECOMPRESS;
   });
 }
 
@@ -893,6 +1005,7 @@ int vie_op_set_partition(vie_op op, int nranks, int rank) {
       throw Invalid("set_partition: axis lengths need two-stage plans for the slab passes");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     VIE_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
+    if (nranks > 1 && op->fused) op->fused = false;  // the slab stages use the materialised rows
     op->nranks = nranks;
     op->rank = rank;
     g.nk = g.n3 / nranks;
@@ -945,6 +1058,7 @@ int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
     if (!op || !recv || !out) throw Invalid("slab_pencil: null argument");
     if (recv == out) throw Invalid("slab_pencil: recv and out must not alias");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    ensure_spectra(op);
     cudaStream_t st = pick_stream(op, stream);
     const Geom& g = op->g;
     const Geom gc = slab_geom_cols(op);
@@ -955,16 +1069,17 @@ int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
     // positions 0, 1 -> rows 0 and n1
     const int lo = g.p1off / 2, hi = (g.p1off + g.W) / 2;
     vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
-                       true, lo, hi);
+                       true, lo, hi, op->u3img);
     if (g.p1off == 0)
       vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
-                         false, g.n1, g.n1 + 1);
+                         false, g.n1, g.n1 + 1, op->u3img);
     if (op->pencil3) {
       if (g.p1off == 0)
         vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
                            st, 1);
       vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
-      vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+      if (op->pencil4) vie::launch_pencil4(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+      else vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
     } else if (op->pencil2) {
       if (g.p1off == 0)
         vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
@@ -1407,6 +1522,7 @@ namespace vie {
 void pencil_phase_read(unsigned long long* out8, bool reset);
 void pencil2_phase_read(unsigned long long* out8, bool reset);
 void pencil3_phase_read(unsigned long long* out8, bool reset);
+void pencil4_phase_read(unsigned long long* out8, bool reset);
 }
 extern "C" {
 int vie_debug_pencil_phases(unsigned long long* out8, int reset) {
@@ -1417,6 +1533,9 @@ int vie_debug_pencil2_phases(unsigned long long* out8, int reset) {
 }
 int vie_debug_pencil3_phases(unsigned long long* out8, int reset) {
   return guard([&] { vie::pencil3_phase_read(out8, reset != 0); });
+}
+int vie_debug_pencil4_phases(unsigned long long* out8, int reset) {
+  return guard([&] { vie::pencil4_phase_read(out8, reset != 0); });
 }
 #endif
 

@@ -1,5 +1,7 @@
 // kernels.cuh -- host-side launch interface of the matvec kernels.
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace vie {
@@ -14,6 +16,7 @@ struct CompDev {
   int64_t off_u2;    // (n2+1) x r2
   int64_t off_u3;    // (n3+1) x r3
   int64_t off_z;     // Z[p2o][a][g]  (n2+1) x r1 x r3
+  int64_t off_u3i;   // U3 shared-memory image of the tile decomposition: [b][NP3][Kp] (decomp_tile.cuh)
 };
 
 struct Geom {
@@ -31,7 +34,23 @@ struct Geom {
   int W;           // axis-1 positions per rank (row length of the exchanged / spectral slabs)
   int p1off;       // first global axis-1 position of this rank's W
   int64_t bps;     // plane stride of B, Bo = m2 * W
+  // Octant-spectrum row layout read by the edge pencil kernels: 0 = the full (n2+1) x (n1+1)
+  // rows; 1 = the compact EDGE buffer of the fused path (only rows p2o in {0, n2} and p1o in
+  // {0, n1} exist, shat_row)
+  int ecompact;
 };
+
+// Row of octant row (p2o, p1o) in the spectrum buffer (Geom::ecompact)
+__host__ __device__ __forceinline__ int64_t shat_row(int p2o, int p1o, int n1, int n2, int compact) {
+  if (!compact) return static_cast<int64_t>(p2o) * (n1 + 1) + p1o;
+  if (p2o == 0) return p1o;
+  if (p2o == n2) return n1 + 1 + p1o;
+  return 2 * (n1 + 1) + 2 * (p2o - 1) + (p1o == 0 ? 0 : 1);  // p1o in {0, n1}
+}
+__host__ __device__ __forceinline__ int64_t shat_rows(int n1, int n2, int compact) {
+  return compact ? 2 * static_cast<int64_t>(n1 + 1) + 2 * static_cast<int64_t>(n2 - 1)
+                 : static_cast<int64_t>(n1 + 1) * (n2 + 1);
+}
 
 // Tuning constants.
 constexpr int kRowsPerCta = 8;     // row FFT kernels
@@ -44,6 +63,9 @@ size_t row_smem(int m);
 size_t col_smem(int m);
 size_t pencil_smem(int n3, int S, int NC);  // (size_t)-1 if it does not fit
 size_t decomp_smem(int n3, int rmax);
+// U3 images of the tile decomposition (decomp_tile.cuh), one per active component
+int64_t u3_image_elems(int n3, int r3);
+void launch_u3_image(const double2* forms, const CompDev* comps_host, int NC, int n3, double2* img, cudaStream_t st);
 size_t decomp_mma_smem(int n1, int n3, int rmax);
 
 void launch_row_fwd(const double2* x, double2* A, const Geom& g, const FftPlan& P1, cudaStream_t st);
@@ -69,6 +91,33 @@ void launch_pencil2(int kind, int basis, const double2* Bin, double2* Bout, cons
 bool pencil3_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
 void launch_pencil3(int kind, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
                     const double2* twm3, cudaStream_t st);
+// Same interior mirror groups, half a group (one axis-2 position) per 2-CTA cluster and two
+// clusters per SM pair (kernels_pencil4.cu); preferred over pencil3 where supported.
+bool pencil4_supported(int kind, int basis, int n3, uint64_t active_mask, int NC);
+void launch_pencil4(int kind, const double2* Bin, double2* Bout, const double2* Shat, const Geom& g,
+                    const double2* twm3, cudaStream_t st);
+// Fused decompression x pencil (kernels_fused.cu): the interior octant rows are decompressed
+// tile by tile into an L2-resident ring and consumed by the pencil items of one persistent kernel.
+struct FusedPlan {
+  const double2* forms = nullptr;
+  const double2* u3img = nullptr;
+  const CompDev* comps = nullptr;
+  const double2* Z = nullptr;
+  double2* ring = nullptr;       // [RING * BM][NC][n3 + 1]
+  const int4* items = nullptr;   // work queue (fused_plan_items)
+  int nitems = 0;
+  unsigned* counters = nullptr;  // queue head, done[ntiles][2], consumed[ntiles]
+  int ntiles = 0, CG = 4, NG = 0, RING = 0, BM = 0, NB = 0, rmax = 0;
+};
+bool fused_supported(int kind, int basis, const Geom& g, uint64_t active_mask, int rmax);
+void fused_plan_items(FusedPlan& fp, const Geom& g, std::vector<int4>& items);
+void launch_fused(int kind, const FusedPlan& fp, const double2* Bin, double2* Bout, const Geom& g,
+                  const double2* twm3, cudaStream_t st);
+// edge rows (p2o in {0, n2}, p1o in {0, n1}) into the compact edge buffer (Geom::ecompact = 1)
+void launch_decomp_edges(const FusedPlan& fp, double2* Sedge, const Geom& g, cudaStream_t st);
+// Z = core x2 U2 only (the fused path's decompression prologue)
+void launch_decomp_z(const double2* forms, const CompDev* comps_dev, double2* Z, const Geom& g, int rmax,
+                     cudaStream_t st);
 // B1 (optional): second slab added to B on load (the pencil kernel's odd branch)
 void launch_col_inv(const double2* B, const double2* B1, double2* A, const Geom& g, const FftPlan& P2,
                     cudaStream_t st);
@@ -98,7 +147,7 @@ void launch_row_inv(const double2* A, double2* y, const Geom& g, const FftPlan& 
 // with_z: also Z = core x2 U2
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
                    double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo = 0, int p2hi = -1,
-                   bool with_z = true, int p1lo = 0, int p1hi = -1);
+                   bool with_z = true, int p1lo = 0, int p1hi = -1, const double2* u3img = nullptr);
 
 // transform_factors on device: spatial factor (n x r, col-major) -> octant rows
 // (n+1) x r of the DFT of the parity embedding (operator.hpp:64-90).

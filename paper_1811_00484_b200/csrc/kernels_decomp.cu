@@ -10,6 +10,9 @@
 // Output layout Shat[p2o][p1o][c][bidx(f3o)], axis 3 branch-major (even
 // octant frequencies 0,2,.. first, then odd 1,3,..) to match the pencil
 // kernel's even/odd half-length branches.
+#include <cstdlib>
+
+#include "decomp_tile.cuh"
 #include "kernels.cuh"
 
 namespace vie {
@@ -377,6 +380,34 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_decomp_s_mma(const double2* 
   }
 }
 
+// Image of U3_c for the tile GEMM: img[b][i][k] = U3_c(2 i + b, k) for i < nb3(b), k < r3, else 0
+// (NP3 x Kp per parity, the exact shared-memory layout of the B operand).
+__global__ void k_u3_image(const double2* __restrict__ u3, int n3, int r3, double2* __restrict__ img) {
+  const int Kp = dtile::kpad(r3), NP3 = (dtile::nb3(n3, 0) + 15) / 16 * 16, n3p = n3 + 1;
+  const int total = 2 * NP3 * Kp;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int b = e / (NP3 * Kp), r = e - b * NP3 * Kp, i = r / Kp, k = r - i * Kp;
+    img[e] = (i < dtile::nb3(n3, b) && k < r3) ? u3[(2 * i + b) + static_cast<int64_t>(n3p) * k] : make_double2(0.0, 0.0);
+  }
+}
+
+// Tile decomposition as its own launch (the tile code of the fused kernel, decomp_tile.cuh):
+// CTA = (64-row p1o block, parity b) x p2o row, 256 threads, two CTAs per SM.
+__global__ void __launch_bounds__(256, 2) k_decomp_tile(const double2* __restrict__ forms,
+                                                        const double2* __restrict__ u3img,
+                                                        const CompDev* __restrict__ comps,
+                                                        const double2* __restrict__ Z, double2* __restrict__ Shat,
+                                                        Geom geo, int NC, int p2lo, int p1lo, int p1hi) {
+  extern __shared__ double2 sm[];
+  const int b = static_cast<int>(blockIdx.x & 1);
+  const int lo = p1lo + static_cast<int>(blockIdx.x >> 1) * dtile::kBM;
+  const int hi = min(p1hi, lo + dtile::kBM);
+  const int p2o = p2lo + static_cast<int>(blockIdx.y);
+  const int64_t rs = static_cast<int64_t>(NC) * (geo.n3 + 1);
+  double2* out = Shat + (static_cast<int64_t>(p2o) * (geo.n1 + 1) + lo) * rs;
+  dtile::run<256>(forms, u3img, comps, Z, 0, NC, geo.n1, geo.n3, p2o, lo, hi, b, out, rs, sm);
+}
+
 // Factor transform: out[p + (n+1) c] = sum_m e_c[m] w_{2n}^{p m}, p <= n,
 // with e_c the parity embedding of column c (embed_column).
 __global__ void k_factor_transform(const double2* __restrict__ u, int n, int r, int sign,
@@ -413,9 +444,28 @@ size_t decomp_smem(int n3, int rmax) {
                             static_cast<size_t>(rmax) * kTP1);
 }
 
+void launch_decomp_z(const double2* forms, const CompDev* comps_dev, double2* Z, const Geom& g, int rmax,
+                     cudaStream_t st) {
+  k_decomp_z<<<dim3(g.NC, rmax), kThreads, 0, st>>>(forms, comps_dev, Z, g.n2);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+
+int64_t u3_image_elems(int n3, int r3) {
+  return 2 * static_cast<int64_t>((dtile::nb3(n3, 0) + 15) / 16 * 16) * dtile::kpad(r3);
+}
+
+void launch_u3_image(const double2* forms, const CompDev* comps_host, int NC, int n3, double2* img, cudaStream_t st) {
+  for (int c = 0; c < NC; ++c) {
+    const CompDev& cd = comps_host[c];
+    if (!cd.active) continue;
+    k_u3_image<<<64, 256, 0, st>>>(forms + cd.off_u3, n3, cd.r3, img + cd.off_u3i);
+    VIE_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
 void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev* comps_host, double2* Z,
                    double2* Shat, const Geom& g, int rmax, cudaStream_t st, int p2lo, int p2hi, bool with_z, int p1lo,
-                   int p1hi) {
+                   int p1hi, const double2* u3img) {
   (void)comps_host;
   if (p2hi < 0) p2hi = g.n2 + 1;
   if (p1hi < 0) p1hi = g.n1 + 1;
@@ -425,7 +475,15 @@ void launch_decomp(const double2* forms, const CompDev* comps_dev, const CompDev
     VIE_CUDA_CHECK(cudaGetLastError());
   }
   const size_t sms = decomp_mma_smem(g.n1, g.n3, rmax);
-  if (sms <= kMaxSmem) {
+  static const bool tile = std::getenv("VIE_DECOMP_TILE") && std::atoi(std::getenv("VIE_DECOMP_TILE")) != 0;
+  const size_t smt = dtile::smem_bytes(g.n3, rmax);
+  if (tile && u3img && smt <= kMaxSmem) {
+    VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_tile),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smt)));
+    const int nblk = (p1hi - p1lo + dtile::kBM - 1) / dtile::kBM;
+    k_decomp_tile<<<dim3(2 * nblk, p2hi - p2lo), 256, smt, st>>>(forms, u3img, comps_dev, Z, Shat, g, g.NC, p2lo,
+                                                                   p1lo, p1hi);
+  } else if (sms <= kMaxSmem) {
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_decomp_s_mma),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(sms)));
     k_decomp_s_mma<<<dim3(g.NC, (p2hi - p2lo + kMmaPP - 1) / kMmaPP), kMmaThreads, sms, st>>>(

@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
         const int c = grp * CG + (rc - tr * CG);
         const int p1o = q0 + tr;
         if (c < NC && p1o <= n1 && u0 + ul < nbo)
-          cp_async16(dst + e, a.Shat + ((static_cast<int64_t>(p2o_tile) * (n1 + 1) + p1o) * NC + c) * n3p +
+          cp_async16(dst + e, a.Shat + (shat_row(p2o_tile, p1o, n1, g.n2, g.ecompact) * NC + c) * n3p +
                                   b * E + u0 + ul);
       }
       cp_async_commit();
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_pencil(PencilArgs a) {
             sh_base = shb + (q & 1) * chunk_elems + (tr * CG - GRP * CG) * CF + ul;
             cstride = CF;
           } else {  // boundary pencils (frequencies 0 / n of a pair) outside the tile
-            sh_base = a.Shat + ((static_cast<int64_t>(p2o) * (n1 + 1) + p1o) * NC) * n3p + b * E + u;
+            sh_base = a.Shat + (shat_row(p2o, p1o, n1, g.n2, g.ecompact) * NC) * n3p + b * E + u;
             cstride = n3p;
           }
           if (half == 0) {

@@ -94,6 +94,7 @@ struct Pencil2Args {
   int gfirst;  // first axis-1 group of this launch
   int pos2lo;  // first axis-2 position of this launch
   FastDiv dnk;
+  int ecompact;  // Geom::ecompact (spectrum rows of the edge buffer)
 };
 
 #ifdef VIE_PENCIL_PROFILE
@@ -181,7 +182,8 @@ __global__ void __launch_bounds__(256, 2) k_pencil2(Pencil2Args a, const __grid_
     const int r = q / NG, grp = q - r * NG;
     uint64_t* bar = full + q % NBUF;
     mbar_expect_tx(bar, static_cast<uint32_t>(CHUNK * sizeof(double2)));
-    tma_chunk(chunk + (q % NBUF) * CHUNK, &tmap, 2 * (b * E + r * CF), grp * CG, p2o * (n1 + 1) + q0, bar);
+    tma_chunk(chunk + (q % NBUF) * CHUNK, &tmap, 2 * (b * E + r * CF), grp * CG,
+              static_cast<int>(shat_row(p2o, q0, n1, a.n2, a.ecompact)), bar);
   };
   // ---- forward stage 0 (radix R0) for BOTH branches of this CTA's half of the lines:
   // the pencils are read from global once per cluster, branch b' of the stage-0
@@ -399,7 +401,7 @@ bool launch2_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     VIE_CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(fn),
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     Pencil2Args a{Bin, Bout, Shat, twm3, g.n1, g.n2, g.m1, g.m2, g.m3, g.bps, g.bps * g.nk, g.nk, g.W, g.p1off,
-                  glo, pos2lo, {}};
+                  glo, pos2lo, {}, g.ecompact};
     a.dnk.init(static_cast<uint32_t>(g.nk));
     CUtensorMap tmap;
     encode_spectrum_map(&tmap, Shat, g, box);

@@ -150,55 +150,6 @@ __device__ unsigned long long g_p3_phase[8];
   } while (0)
 #endif
 
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-__device__ __forceinline__ double2 lds2(uint32_t a) {
-  double2 r;
-  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(r.x), "=d"(r.y) : "r"(a));
-  return r;
-}
-__device__ __forceinline__ double2 ldc2(uint32_t a) {  // partner CTA (shared::cluster window)
-  double2 r;
-  asm volatile("ld.shared::cluster.v2.f64 {%0, %1}, [%2];\n" : "=d"(r.x), "=d"(r.y) : "r"(a));
-  return r;
-}
-__device__ __forceinline__ void sts2(uint32_t a, double2 v) {
-  asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(a), "d"(v.x), "d"(v.y) : "memory");
-}
-// 5-D TMA load of a slab box, multicast to the CTAs in `mask` (same smem offset, each
-// CTA's mbarrier at the same offset receives the bytes landing in it)
-__device__ __forceinline__ void tma_load5_mc(void* dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
-                                             uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
-      "[%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-__device__ __forceinline__ void tma_prefetch5(const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4) {
-  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-               : "memory");
-}
-__device__ __forceinline__ void tma_prefetch3(const CUtensorMap* m, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];\n" ::"l"(
-                   reinterpret_cast<uint64_t>(m)),
-               "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void tma_store5(const CUtensorMap* m, const void* src, int c0, int c1, int c2, int c3,
-                                           int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];\n" ::"l"(
-          reinterpret_cast<uint64_t>(m)),
-      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
-      : "memory");
-}
-
 template <int KIND, int R0, int R1>
 __global__ void __launch_bounds__(512, 1)
     k_pencil3(Pencil3Args a, const __grid_constant__ CUtensorMap tmS, const __grid_constant__ CUtensorMap tmIn,
@@ -483,35 +434,6 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-// Slab B / Bo as a 5-D tensor of doubles: [R blocks][nk k][m2 p2][S s][2 W (p1, re/im)]
-// (innermost first: 2 W, S, m2, nk, R), box [4][12][2][kb][1] = one k-run of a mirror group.
-void encode_slab_map(CUtensorMap* map, const double2* base, const Geom& g, int kb) {
-  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-  static Encode encode = [] {
-    void* fn = nullptr;
-    cudaDriverEntryPointQueryResult q{};
-    VIE_CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess)
-      throw CudaError(cudaErrorNotSupported, "cuTensorMapEncodeTiled entry point", __FILE__, __LINE__);
-    return reinterpret_cast<Encode>(fn);
-  }();
-  const cuuint64_t R = static_cast<cuuint64_t>(g.n3 / g.nk);
-  const cuuint64_t dims[5] = {2 * static_cast<cuuint64_t>(g.W), static_cast<cuuint64_t>(g.S),
-                              static_cast<cuuint64_t>(g.m2), static_cast<cuuint64_t>(g.nk), R};
-  const cuuint64_t e16 = sizeof(double2);
-  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(g.bps) * g.nk * e16, static_cast<cuuint64_t>(g.W) * e16,
-                                 static_cast<cuuint64_t>(g.bps) * e16,
-                                 static_cast<cuuint64_t>(g.bps) * g.nk * g.S * e16};
-  const cuuint32_t boxd[5] = {4, 12, 2, static_cast<cuuint32_t>(kb), 1};
-  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double2*>(base), dims, strides, boxd,
-                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) throw CudaError(cudaErrorInvalidValue, "cuTensorMapEncodeTiled (slab)", __FILE__, __LINE__);
-}
-
 #define VIE_PENCIL3_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8)
 
 // k extent of the load boxes: a divisor of nk, at most 128 (<= 256 per TMA box dim)
@@ -537,8 +459,8 @@ bool launch3_t(int n3, const double2* Bin, double2* Bout, const double2* Shat, c
     Pencil3Args a{twm3, g.n1, g.W, g.p1off, glo, g.nk, kb, kbs, 0};
     CUtensorMap tmS, tmIn, tmOut;
     encode_spectrum_map(&tmS, Shat, g, {2 * UB, NC, 1});
-    encode_slab_map(&tmIn, Bin, g, kb);
-    encode_slab_map(&tmOut, Bout, g, kbs);
+    encode_slab_map(&tmIn, Bin, g, kb, 2);
+    encode_slab_map(&tmOut, Bout, g, kbs, 2);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (ghi - glo), g.n2 - 1);
     cfg.blockDim = dim3(512);

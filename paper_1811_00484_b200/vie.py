@@ -59,6 +59,8 @@ def lib() -> C.CDLL:
         L.vie_system_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p, C.c_void_p, C.c_int,
                                         C.c_void_p]
         L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.vie_op_set_strategy.argtypes = [C.c_void_p, C.c_int]
+        L.vie_op_get_strategy.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
         L.vie_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_matvec_host_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.vie_op_set_partition.argtypes = [C.c_void_p, C.c_int, C.c_int]
@@ -317,17 +319,41 @@ def _dev_vec(op: EmbeddedSpectrum, x):
     return x.contiguous()
 
 
-def apply_operator(op: EmbeddedSpectrum, x, strategy: str = "hosvd_decompress", policy: str = "with_buffer",
+def set_strategy(op: EmbeddedSpectrum, strategy: str) -> None:
+    """Strategy of every later apply on ``op`` (vie_op_set_strategy): 'hosvd_decompress' /
+    'tucker_cp_decompress' or 'hosvd_loop' / 'tucker_cp_loop'."""
+    codes = {"hosvd_decompress": 1, "tucker_cp_decompress": 1, "hosvd_loop": 2, "tucker_cp_loop": 2}
+    if strategy not in codes:
+        raise ValueError(f"set_strategy: unknown strategy {strategy!r}")
+    _check(lib().vie_op_set_strategy(op.handle, codes[strategy]))
+
+
+def get_strategy(op: EmbeddedSpectrum) -> str:
+    v = C.c_int()
+    _check(lib().vie_op_get_strategy(op.handle, C.byref(v)))
+    return "hosvd_loop" if v.value == 2 else "hosvd_decompress"
+
+
+def apply_operator(op: EmbeddedSpectrum, x, strategy: str | None = None, policy: str = "with_buffer",
                    ws=None, dft=None, out=None, stream=None):
     """y = A x (operator.hpp:273).  ``x``: CUDA complex128 tensor (S*N_v) or host numpy array.
 
-    The B200 path is the fused octant HOSVD decompress x Hadamard; the
-    reference's scratch-policy contract is kept: decompress strategies with
-    policy 'no_buffer' raise ValueError (operator.hpp:278-281)."""
-    if strategy not in ("hosvd_decompress", "hosvd_loop"):
+    Strategies (operator.hpp:17-31): 'hosvd_decompress' decompresses every component's octant
+    spectrum into one HBM buffer read by the fused axis-3 FFT x Hadamard pass; 'hosvd_loop' is
+    the buffer-free form -- one persistent kernel decompresses spectrum tiles into an
+    L2-resident ring and consumes them (PWL, ranks <= 28; ValueError otherwise).  The
+    'tucker_cp_*' names select the same two paths (CP forms are held as Tucker forms).  The
+    reference's scratch-policy contract is kept: decompress strategies with policy
+    'no_buffer' raise ValueError (operator.hpp:278-281).  The strategy sticks to the operator
+    (vie_op_set_strategy) for later system matvecs and solves; strategy=None keeps it."""
+    loop = {"hosvd_decompress": False, "tucker_cp_decompress": False, "hosvd_loop": True, "tucker_cp_loop": True}
+    if strategy is None:  # the operator's current strategy (hosvd_decompress unless set)
+        strategy = get_strategy(op)
+    if strategy not in loop:
         raise ValueError(f"apply_operator: strategy {strategy!r} needs a representation this build does not hold")
-    if strategy == "hosvd_decompress" and policy == "no_buffer":
+    if not loop[strategy] and policy == "no_buffer":
         raise ValueError("apply_operator: decompress strategies need ScratchPolicy::WithBuffer")
+    set_strategy(op, strategy)
     if isinstance(x, np.ndarray):
         xa = _cplx(x).reshape(-1)
         if xa.size != op.n_cur * op.n_vox:

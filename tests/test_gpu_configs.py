@@ -64,13 +64,19 @@ def gpu_apply(vie, op, x):
     return y.cpu().numpy()
 
 
-@pytest.mark.parametrize("basis,grid", [(PWC, (100, 120, 100)), (PWL, (100, 120, 100)), (PWL, (200, 240, 200))],
-                         ids=["C3-pwc", "C3-pwl", "C4-pwl"])
-def test_headline_configs_random_x(vie, dft, basis, grid):
+@pytest.mark.parametrize("basis,grid,strategy", [(PWC, (100, 120, 100), "hosvd_decompress"),
+                                                  (PWL, (100, 120, 100), "hosvd_decompress"),
+                                                  (PWL, (100, 120, 100), "hosvd_loop"),
+                                                  (PWL, (200, 240, 200), "hosvd_decompress"),
+                                                  (PWL, (200, 240, 200), "hosvd_loop")],
+                         ids=["C3-pwc", "C3-pwl", "C3-pwl-loop", "C4-pwl", "C4-pwl-loop"])
+def test_headline_configs_random_x(vie, dft, basis, grid, strategy):
+    import torch
+
     spatial, par = spatial_tucker_forms(N, basis, grid, 25, 1234)
     op = build(vie, dft, N, basis, grid, spatial, par)
     x = random_field(basis, grid, 2024)
-    y = gpu_apply(vie, op, x)
+    y = vie.apply_operator(op, torch.from_numpy(x).cuda(), strategy=strategy).cpu().numpy()
     del op
     y_ref = orc.apply_operator_tucker(N, basis, grid, fourier_forms(spatial, par), x)
     err = rel(y_ref, y)
@@ -106,16 +112,22 @@ def test_c1_cube_matvec_and_20_gmres_iterations(vie, dft):
     eps_np = np.full(nv, eps_c)
     op, of, _ = _system(vie, dft, grid, eps_np, 321)
     x = random_field(PWL, grid, 2024)
-    assert rel(orc.apply_operator_tucker(N, PWL, grid, of, x), gpu_apply(vie, op, x)) <= MATVEC_TOL
+    y_ref = orc.apply_operator_tucker(N, PWL, grid, of, x)
+    assert rel(y_ref, gpu_apply(vie, op, x)) <= MATVEC_TOL
     rhs = random_field(PWL, grid, 77)
     eps = torch.from_numpy(eps_np).cuda()
-    r = vie.gmres(op, eps, 1.0, torch.from_numpy(rhs).cuda(), vie.GmresConfig(1e-15, 20, 1))
     ref = orc.gmres_system_tucker(PWL, grid, of, eps_np, 1.0, rhs, tol=1e-15, inner=20, outer=1)
-    assert r.iterations == ref.iterations == 20
-    h, hr = np.array(r.residual_history), np.array(ref.residual_history)
-    assert np.max(np.abs(h - hr) / hr) <= 1e-8
-    assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8 * ref.final_relative_residual
-    assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
+    for strategy in ("hosvd_decompress", "hosvd_loop"):  # the strategy sticks to the operator for the solve
+        vie.set_strategy(op, strategy)
+        if strategy == "hosvd_loop":
+            assert rel(y_ref, gpu_apply(vie, op, x)) <= MATVEC_TOL  # strategy=None: keeps hosvd_loop
+            assert vie.get_strategy(op) == "hosvd_loop"
+        r = vie.gmres(op, eps, 1.0, torch.from_numpy(rhs).cuda(), vie.GmresConfig(1e-15, 20, 1))
+        assert r.iterations == ref.iterations == 20
+        h, hr = np.array(r.residual_history), np.array(ref.residual_history)
+        assert np.max(np.abs(h - hr) / hr) <= 1e-8, strategy
+        assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8 * ref.final_relative_residual
+        assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
 
 
 def test_c2_pwl64_gmres_to_1e6(vie, dft):

@@ -109,6 +109,58 @@ def test_matvec_pencil3_shapes(vie, dft, orc, kind, basis, dims, rank):
         assert rel(y_ref, run_gpu(vie, op, x)) <= MATVEC_TOL, (kind, basis, dims)
 
 
+# strategy hosvd_loop: the fused persistent decompress x pencil kernel (kernels_fused.cu) with the
+# spectrum tiles in an L2 ring.  Cases: every compiled axis-3 shape, both kinds, a tail tile
+# (n1 - 1 not a multiple of 64), ring reuse (more tiles than ring slots), rank 25 and ranks that
+# differ per mode.
+LOOP_CASES = [
+    (N, PWL, (5, 6, 32), 3), (K, PWL, (4, 5, 64), 3), (N, PWL, (3, 3, 128), 4), (K, PWL, (3, 4, 200), 3),
+    (N, PWL, (6, 2, 100), 3), (N, PWL, (70, 9, 32), 4), (K, PWL, (135, 3, 64), 2), (N, PWL, (4, 5, 200), 25),
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", LOOP_CASES)
+def test_matvec_hosvd_loop(vie, dft, orc, kind, basis, dims, rank):
+    import torch
+
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 17 + sum(dims))
+    x = random_field(basis, dims, 93)
+    y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+    y_dec = vie.apply_operator(op, to_dev(x), strategy="hosvd_decompress").cpu().numpy()
+    ws_dec = op.workspace_bytes()
+    y_loop = vie.apply_operator(op, to_dev(x), strategy="hosvd_loop").cpu().numpy()
+    torch.cuda.synchronize()
+    assert vie.get_strategy(op) == "hosvd_loop"
+    assert rel(y_ref, y_loop) <= MATVEC_TOL, (kind, dims)
+    assert rel(y_dec, y_loop) <= 1e-12, (kind, dims)
+    assert op.workspace_bytes() > ws_dec  # both strategies' storage now allocated
+    y_again = vie.apply_operator(op, to_dev(x), strategy="tucker_cp_loop").cpu().numpy()
+    assert np.array_equal(y_again, y_loop)  # deterministic (fixed work order per tile)
+
+
+def test_hosvd_loop_fresh_operator_holds_no_spectrum(vie, dft, orc):
+    """A loop-only operator never allocates the whole-spectrum buffer: its workspace is below
+    the decompress strategy's by about the octant spectra (NC (n1+1)(n2+1)(n3+1) x 16 B)."""
+    dims = (40, 60, 32)  # 41 x 61 octant rows vs a 4 x 64-row ring + 200 edge rows
+    op, oforms, _, _ = make_ops(vie, dft, orc, N, PWL, dims, 3, 5)
+    vie.set_strategy(op, "hosvd_loop")
+    x = random_field(PWL, dims, 3)
+    y = vie.apply_operator(op, to_dev(x), strategy="hosvd_loop").cpu().numpy()
+    assert rel(orc.apply_operator_tucker(N, PWL, dims, oforms, x), y) <= MATVEC_TOL
+    op2, _, _, _ = make_ops(vie, dft, orc, N, PWL, dims, 3, 5)
+    vie.apply_operator(op2, to_dev(x), strategy="hosvd_decompress")
+    noct = 60 * 41 * 61 * 33 * 16
+    assert op2.workspace_bytes() - op.workspace_bytes() >= 0.5 * noct
+
+
+def test_hosvd_loop_unsupported_raises(vie, dft, orc):
+    op, _, _, _ = make_ops(vie, dft, orc, N, PWC, (4, 4, 4), 2, 1)
+    with pytest.raises(ValueError):
+        vie.apply_operator(op, to_dev(random_field(PWC, (4, 4, 4), 1)), strategy="hosvd_loop")
+    with pytest.raises(ValueError):
+        vie.apply_operator(op, to_dev(random_field(PWC, (4, 4, 4), 1)), strategy="dense")
+
+
 # kernel-path coverage: rank > 28 (FMA decompression fallback), an axis length without a
 # two-stage plan (m = 250 = 2 x 5^3: generic multi-stage passes), and n3 without a compiled
 # pencil shape (generic pencil kernel)
