@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--slab", action="store_true", help="slab-decomposed path even on 1 GPU (exercise it)")
+    ap.add_argument("--strategy", default="hosvd_decompress", choices=["hosvd_decompress", "hosvd_loop"],
+                    help="MatvecStrategy of the headline (operator.hpp:17); the other one is timed beside it")
     return ap.parse_args()
 
 
@@ -429,6 +431,9 @@ def run_b200(args):
         x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
     y = torch.empty_like(x)
 
+    if not slab:
+        vie.set_strategy(op, args.strategy)
+
     def step():
         if slab:
             sm.apply(x, out=y)
@@ -525,6 +530,42 @@ def run_b200(args):
                "api": "vie_matvec_host_batch (pinned host x_i -> y_i, copies overlapped with neighbouring matvecs)",
                "sync_call_value": 1.0 / t_sync, "sync_call_api": "vie_matvec_host (H2D, matvec, D2H serialised)"}
 
+    # the other MatvecStrategy on the same operator and input (operator.hpp:17-31): hosvd_decompress
+    # keeps every component's octant spectrum in one HBM buffer; hosvd_loop decompresses tiles
+    # into an L2-resident ring inside one persistent kernel (no whole-spectrum buffer)
+    strategies = None
+    if world == 1 and not slab:
+        strategies = {}
+        y_head = y.clone()
+        n1, n2, n3 = grid
+        rs = 16 * nc * (n3 + 1)
+        la = int(os.environ.get("VIE_FUSED_LA", "4"))
+        storage = {"hosvd_decompress": (n1 + 1) * (n2 + 1) * rs,
+                   "hosvd_loop": ((la + 1) * 32 + 2 * (n1 + 1) + 2 * (n2 - 1)) * rs}
+        for strat in ("hosvd_decompress", "hosvd_loop"):
+            entry = {"spectrum_storage_bytes": storage[strat]}
+            try:
+                vie.set_strategy(op, strat)
+            except ValueError as e:
+                entry["unavailable"] = str(e)
+                strategies[strat] = entry
+                continue
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms_s = e0.elapsed_time(e1) / args.steps
+            entry.update({"ms_per_step": ms_s, "value": 1000.0 / ms_s, "unit": "matvecs/s",
+                          "rel_l2_vs_headline": float(torch.linalg.vector_norm(y - y_head)
+                                                      / torch.linalg.vector_norm(y_head))})
+            strategies[strat] = entry
+        vie.set_strategy(op, args.strategy)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -574,6 +615,8 @@ def run_b200(args):
             "gpu_launches": launches * args.steps,
             "clocks": clk.summary(),
             "e2e": e2e,
+            "strategy": args.strategy,
+            "strategies": strategies,
             "cpu_baseline": cpu,
             "gmres_solve": solve,
             "gmres_solve_headline": solve_c4,

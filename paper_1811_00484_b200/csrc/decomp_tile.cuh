@@ -16,7 +16,10 @@
 namespace vie {
 namespace dtile {
 
-constexpr int kBM = 64;   // p1o rows per tile
+#ifndef VIE_TILE_BM
+#define VIE_TILE_BM 32
+#endif
+constexpr int kBM = VIE_TILE_BM;  // p1o rows per tile
 constexpr int kZS = 34;   // Z row stride (== 2 mod 8: conflict-free B fragments over k)
 
 __host__ __device__ __forceinline__ int kpad(int r) {  // padded inner dimension (== 4 mod 8)
@@ -49,25 +52,27 @@ __device__ __forceinline__ void mma_f64(double& d0, double& d1, double a, double
       : "d"(a), "d"(b));
 }
 
-// One tile on a CTA of NT threads (NT / 32 >= 8 warps), components [c0, c1).
+// One tile on a CTA of NT threads (NT / 32 >= 8 warps): components c0, c0 + cstep, .. < c1,
+// axis-3 parities [b0, b1) (T is formed once per component and serves both parities).
 // P2ROWS = false: rows are p1o in [lo, hi) at p2o = fixed (T = U1 rows x Z_c[p2o], DMMA);
 // P2ROWS = true:  rows are p2o in [lo, hi) at p1o = fixed (the axis-1 edge rows p1o = 0, n1:
 //                 T[p2o] = U1_c(p1o, :) Z_c[p2o], FMA).
 // out + (row - lo) * rs is the branch-major spectrum row (c * (n3 + 1) + column) of the row.
+// KEEP_L2: stores with an L2 evict_last policy (the fused kernel's tile ring).
 template <int NT, bool P2ROWS = false, bool KEEP_L2 = false>
 __device__ __forceinline__ void run(const double2* __restrict__ forms, const double2* __restrict__ u3img,
                                     const CompDev* __restrict__ comps, const double2* __restrict__ Z, int c0,
-                                    int c1, int n1, int n3, int fixed, int lo, int hi, int b,
+                                    int c1, int cstep, int n1, int n3, int fixed, int lo, int hi, int b0, int b1,
                                     double2* __restrict__ out, int64_t rs, double2* sm) {
   static_assert(NT / 32 >= 2 * kBM / 16, "one 16 x 16 T tile per warp");
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int n1p = n1 + 1, n3p = n3 + 1;
-  const int NB = nb3(n3, b), E = nb3(n3, 0);
+  const int E = nb3(n3, 0);
   const int NP3 = (E + 15) / 16 * 16;  // both branches use the even branch's padding
   const int p2o = fixed, p1lo = lo, p1hi = hi;
   const uint64_t pol = KEEP_L2 ? l2_evict_last() : 0ull;
-  for (int c = c0; c < c1; ++c) {
+  for (int c = c0; c < c1; c += cstep) {
     const CompDev cd = comps[c];
     if (!cd.active) continue;
     const int r1 = cd.r1, r3 = cd.r3;
@@ -75,10 +80,13 @@ __device__ __forceinline__ void run(const double2* __restrict__ forms, const dou
     double2* us = sm;                                   // [NP3][Kp]  U3 parity-b rows (B operand)
     double2* zs = us + static_cast<int64_t>(NP3) * Kp;  // [KA][kZS]  Z_c[p2o] (B operand of T)
     double2* ts = zs + KA * kZS;                        // [kBM][Kp]  T (A operand)
-    __syncthreads();  // the previous component's GEMMs are done with us / zs / ts
     // U3 parity-b rows, zero padded: a contiguous copy of the operator's image (k_u3_image)
-    const double2* u3 = u3img + cd.off_u3i + static_cast<int64_t>(b) * NP3 * Kp;
-    for (int e = tid; e < NP3 * Kp; e += NT) cp16(us + e, u3 + e);
+    auto stage_u3 = [&](int b) {
+      const double2* u3 = u3img + cd.off_u3i + static_cast<int64_t>(b) * NP3 * Kp;
+      for (int e = tid; e < NP3 * Kp; e += NT) cp16(us + e, u3 + e);
+    };
+    __syncthreads();  // the previous component's GEMMs are done with us / zs / ts
+    stage_u3(b0);
     if constexpr (!P2ROWS) {
       const double2* zsrc = Z + cd.off_z + static_cast<int64_t>(p2o) * r1 * r3;  // [a][g]
       for (int e = tid; e < KA * kZS; e += NT) {
@@ -149,47 +157,55 @@ __device__ __forceinline__ void run(const double2* __restrict__ forms, const dou
       }
     }
     __syncthreads();
-    // S^ = T U3^T: 16 x 16 warp tiles over (kBM / 16) x (NP3 / 16)
-    const int nrt = (min(kBM, p1hi - p1lo) + 15) / 16, nct = NP3 / 16;
-    for (int t = warp; t < nrt * nct; t += NT / 32) {
-      const int rt = t / nct, ct = t - rt * nct;
-      double p1[2][2][2] = {}, p2[2][2][2] = {}, p3[2][2][2] = {};
-      const double2* ta = ts + (rt * 16 + fr) * Kp + fk;
-      const double2* ub = us + (ct * 16 + fr) * Kp + fk;
-      for (int k0 = 0; k0 < Kp; k0 += 4) {
-        const double2 av[2] = {ta[k0], ta[8 * Kp + k0]};
-        const double2 bv[2] = {ub[k0], ub[8 * Kp + k0]};
-        const double as[2] = {av[0].x + av[0].y, av[1].x + av[1].y};
-        const double bs[2] = {bv[0].x + bv[0].y, bv[1].x + bv[1].y};
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) mma_f64(p1[i][j][0], p1[i][j][1], av[i].x, bv[j].x);
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) mma_f64(p2[i][j][0], p2[i][j][1], av[i].y, bv[j].y);
-#pragma unroll
-        for (int i = 0; i < 2; ++i)
-#pragma unroll
-          for (int j = 0; j < 2; ++j) mma_f64(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
+    for (int b = b0; b < b1; ++b) {
+      if (b > b0) {  // restage U3 for the next parity (T stays)
+        __syncthreads();
+        stage_u3(b);
+        cp_wait_all();
+        __syncthreads();
       }
+      const int NB = nb3(n3, b);
+      // S^ = T U3^T: 16 x 16 warp tiles over (kBM / 16) x (NP3 / 16)
+      const int nrt = (min(kBM, p1hi - p1lo) + 15) / 16, nct = NP3 / 16;
+      for (int t = warp; t < nrt * nct; t += NT / 32) {
+        const int rt = t / nct, ct = t - rt * nct;
+        double p1[2][2][2] = {}, p2[2][2][2] = {}, p3[2][2][2] = {};
+        const double2* ta = ts + (rt * 16 + fr) * Kp + fk;
+        const double2* ub = us + (ct * 16 + fr) * Kp + fk;
+        for (int k0 = 0; k0 < Kp; k0 += 4) {
+          const double2 av[2] = {ta[k0], ta[8 * Kp + k0]};
+          const double2 bv[2] = {ub[k0], ub[8 * Kp + k0]};
+          const double as[2] = {av[0].x + av[0].y, av[1].x + av[1].y};
+          const double bs[2] = {bv[0].x + bv[0].y, bv[1].x + bv[1].y};
 #pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const int prow = rt * 16 + i * 8 + fr;
-        if (p1lo + prow >= p1hi) continue;
-        double2* dst = out + prow * rs + static_cast<int64_t>(c) * n3p + (b ? E : 0);
+          for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const int col = ct * 16 + j * 8 + 2 * fk;
+            for (int j = 0; j < 2; ++j) mma_f64(p1[i][j][0], p1[i][j][1], av[i].x, bv[j].x);
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
-            if (col + h < NB)
-            {
-              const double2 v = make_double2(p1[i][j][h] - p2[i][j][h], p3[i][j][h] - p1[i][j][h] - p2[i][j][h]);
-              if (KEEP_L2) st_hint(dst + col + h, v, pol);
-              else dst[col + h] = v;
-            }
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) mma_f64(p2[i][j][0], p2[i][j][1], av[i].y, bv[j].y);
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) mma_f64(p3[i][j][0], p3[i][j][1], as[i], bs[j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int prow = rt * 16 + i * 8 + fr;
+          if (p1lo + prow >= p1hi) continue;
+          double2* dst = out + prow * rs + static_cast<int64_t>(c) * n3p + (b ? E : 0);
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int col = ct * 16 + j * 8 + 2 * fk;
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (col + h < NB) {
+                const double2 v = make_double2(p1[i][j][h] - p2[i][j][h], p3[i][j][h] - p1[i][j][h] - p2[i][j][h]);
+                if (KEEP_L2) st_hint(dst + col + h, v, pol);
+                else dst[col + h] = v;
+              }
+          }
         }
       }
     }

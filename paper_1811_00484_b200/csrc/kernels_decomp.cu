@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256, 2) k_decomp_tile(const double2* __restric
   const int p2o = p2lo + static_cast<int>(blockIdx.y);
   const int64_t rs = static_cast<int64_t>(NC) * (geo.n3 + 1);
   double2* out = Shat + (static_cast<int64_t>(p2o) * (geo.n1 + 1) + lo) * rs;
-  dtile::run<256>(forms, u3img, comps, Z, 0, NC, geo.n1, geo.n3, p2o, lo, hi, b, out, rs, sm);
+  dtile::run<256>(forms, u3img, comps, Z, 0, NC, 1, geo.n1, geo.n3, p2o, lo, hi, b, b + 1, out, rs, sm);
 }
 
 // Factor transform: out[p + (n+1) c] = sum_m e_c[m] w_{2n}^{p m}, p <= n,

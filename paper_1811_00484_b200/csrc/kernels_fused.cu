@@ -4,17 +4,18 @@
 // of the interior rows are never written to HBM as a whole.  This is the B200 form of the
 // reference's buffer-free HosvdLoop strategy (operator.hpp:327-345: decompress one component,
 // use it, drop it), at the granularity that lets the 25-wide factor GEMMs run on the FP64
-// tensor cores: a TILE = 64 octant rows p1o of one axis-2 octant row p2o, all components.
+// tensor cores: a TILE = 32 octant rows p1o (dtile::kBM) of one axis-2 octant row p2o, all components.
 //
 // Work items (a global queue, one atomicAdd per cluster item, both CTAs of a 2-CTA cluster work
 // on the same item):
 //   D(tau, cg): decompress components [cg CG, (cg+1) CG) of tile tau into ring slot tau % RING;
-//               CTA b produces the axis-3 frequencies of parity b (decomp_tile.cuh)
+//               CTA b takes every other component of the group, both axis-3 parities, so T =
+//               U1 Z is formed once per component (decomp_tile.cuh)
 //   P(tau, i1, m2f): one pencil item of kernels_pencil4.cu (pencil4.cuh p4_item) whose spectrum
 //               row is read from the ring
 // Queue order: D(0..LA-1, *), then per tile tau: D(tau + LA, *), P(tau, *).  Dependencies are
 // counters in global memory: a P item of tile tau waits (thread 0, before its first spectrum
-// TMA) until all NG component groups of its parity are done; a D item writing slot
+// TMA) until both CTAs of all NG component groups are done; a D item writing slot
 // tau % RING waits until every pencil CTA of tile tau - RING has consumed it.  Every wait is on
 // items that precede it in the queue, and items are dequeued only by running clusters, so the
 // earliest unfinished item can always proceed (no deadlock whatever the residency).
@@ -46,7 +47,7 @@ struct FusedArgs {
   const int4* items;     // {type (0 = D, 1 = P), tau, cg | i1, m2f}
   int nitems;
   unsigned* next;        // queue head
-  unsigned* done;        // [tiles][2]: finished component groups per parity
+  unsigned* done;        // [tiles]: finished D-item CTAs (2 per component group)
   unsigned* consumed;    // [tiles]: pencil CTAs done with the tile's spectrum
   int NC, n1, n3;
   int CG, NG;            // components per D item, D items per tile
@@ -110,14 +111,15 @@ __global__ void __launch_bounds__(256, 2)
       }
       __syncthreads();
       double2* out = f.ring + static_cast<int64_t>(tau % f.RING) * f.BM * rs;
+      // CTA b: components c0 + b, c0 + b + 2, .. of the group, both axis-3 parities (T once per component)
       const int c0 = it.z * f.CG, c1 = min(f.NC, c0 + f.CG);
-      dtile::run<256, false, true>(f.forms, f.u3img, f.comps, f.Z, c0, c1, f.n1, f.n3, j2, lo, hi, b, out, rs,
-                                    sm.chunk);
+      dtile::run<256, false, true>(f.forms, f.u3img, f.comps, f.Z, c0 + b, c1, 2, f.n1, f.n3, j2, lo, hi, 0, 2, out,
+                                    rs, sm.chunk);
       // each writer orders its generic-proxy stores before the async-proxy (TMA) reads of the
       // consumers; thread 0 then publishes the group (release, cumulative over the barrier)
       asm volatile("fence.proxy.async.global;\n" ::: "memory");
       __syncthreads();
-      if (tid == 0) red_release_add(f.done + 2 * tau + b, 1u);
+      if (tid == 0) red_release_add(f.done + tau, 1u);
     } else {
       // ---- P(tau, i1, m2f): pencil item on ring row (tau % RING) BM + (i1 - lo)
       const int i1 = it.z, m2f = it.w;
@@ -125,7 +127,7 @@ __global__ void __launch_bounds__(256, 2)
       p4::p4_item<KIND, R0, R1, false>(
           f.pa, &tmS, &tmIn, &tmOut, sm, i1, m2f, j2, b, srow, qbase, npen & 1u,
           [&] {
-            spin_until(f.done + 2 * tau + b, static_cast<unsigned>(f.NG));
+            spin_until(f.done + tau, static_cast<unsigned>(2 * f.NG));  // both CTAs of every group
             asm volatile("fence.proxy.async.global;\n" ::: "memory");
           },
           [&] {
@@ -138,8 +140,8 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 // Edge rows of the octant spectrum into the compact edge buffer (shat_row, Geom::ecompact):
-// P2ROWS = false: rows p2o in {0, n2} (y), all p1o in 64-row blocks;
-// P2ROWS = true:  rows p1o in {0, n1} (y), p2o in [1, n2) in 64-row blocks.
+// P2ROWS = false: rows p2o in {0, n2} (y), all p1o in kBM-row blocks;
+// P2ROWS = true:  rows p1o in {0, n1} (y), p2o in [1, n2) in kBM-row blocks.
 // x = 2 * block + parity, z = component group.
 template <bool P2ROWS>
 __global__ void __launch_bounds__(256, 2) k_decomp_edge(const double2* __restrict__ forms,
@@ -154,13 +156,13 @@ __global__ void __launch_bounds__(256, 2) k_decomp_edge(const double2* __restric
   if (!P2ROWS) {
     const int p2o = blockIdx.y ? n2 : 0;
     const int lo = blk * dtile::kBM, hi = min(n1 + 1, lo + dtile::kBM);
-    dtile::run<256, false>(forms, u3img, comps, Z, c0, c1, n1, n3, p2o, lo, hi, b,
+    dtile::run<256, false>(forms, u3img, comps, Z, c0, c1, 1, n1, n3, p2o, lo, hi, b, b + 1,
                            Sedge + shat_row(p2o, lo, n1, n2, 1) * rs, rs, smd);
   } else {
     const int p1o = blockIdx.y ? n1 : 0;
     const int lo = 1 + blk * dtile::kBM, hi = min(n2, lo + dtile::kBM);
     if (lo >= hi) return;
-    dtile::run<256, true>(forms, u3img, comps, Z, c0, c1, n1, n3, p1o, lo, hi, b,
+    dtile::run<256, true>(forms, u3img, comps, Z, c0, c1, 1, n1, n3, p1o, lo, hi, b, b + 1,
                           Sedge + shat_row(lo, p1o, n1, n2, 1) * rs, 2 * rs, smd);
   }
 }
@@ -199,7 +201,7 @@ bool fused_t(const FusedPlan& fp, const double2* Bin, double2* Bout, const Geom&
     f.nitems = fp.nitems;
     f.next = fp.counters;
     f.done = fp.counters + 1;
-    f.consumed = fp.counters + 1 + 2 * fp.ntiles;
+    f.consumed = fp.counters + 1 + 2 * fp.ntiles;  // (done uses the first ntiles of its 2 ntiles)
     f.NC = g.NC;
     f.n1 = g.n1;
     f.n3 = g.n3;
@@ -261,7 +263,7 @@ void fused_plan_items(FusedPlan& fp, const Geom& g, std::vector<int4>& items) {
   fp.ntiles = fp.NB * (g.n2 - 1);
   fp.CG = std::max(1, env_or("VIE_FUSED_CG", 4));
   fp.NG = (g.NC + fp.CG - 1) / fp.CG;
-  const int LA = std::max(1, env_or("VIE_FUSED_LA", 3));
+  const int LA = std::max(1, env_or("VIE_FUSED_LA", 4));
   fp.RING = LA + 1;
   items.clear();
   auto emit_d = [&](int tau) {
