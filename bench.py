@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--slab", action="store_true", help="slab-decomposed path even on 1 GPU (exercise it)")
+    ap.add_argument("--torch-exchange", action="store_true",
+                    help="N > 1: exchange through torch all_to_all_single instead of the library's NCCL calls")
     ap.add_argument("--strategy", default="hosvd_decompress", choices=["hosvd_decompress", "hosvd_loop"],
                     help="MatvecStrategy of the headline (operator.hpp:17); the other one is timed beside it")
     return ap.parse_args()
@@ -423,9 +425,13 @@ def run_b200(args):
     stream = torch.cuda.Stream()  # dedicated stream: events and kernels on the same queue
     torch.cuda.set_stream(stream)
     if slab:
-        from paper_1811_00484_b200.sharding import SlabMatvec
+        from paper_1811_00484_b200.sharding import SlabMatvec, make_comm
 
-        sm = SlabMatvec(op, rank, world)
+        # the library's NCCL exchange (vie_slab_matvec: grouped send/recv, decomposition on a
+        # side stream during the forward exchange); --torch-exchange: the Python stages +
+        # torch all_to_all_single
+        comm = None if args.torch_exchange else make_comm(dft, rank, world)
+        sm = SlabMatvec(op, rank, world, comm=comm)
         x = torch.randn(sm.x_elems, dtype=torch.complex128, device="cuda", generator=g)  # this rank's z-slab
     else:
         x = torch.randn(n, dtype=torch.complex128, device="cuda", generator=g)
@@ -595,7 +601,8 @@ def run_b200(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (spatial-domain Tucker forms, CN(0,1), parity rows zeroed; CN(0,1) currents)",
             "config": config_dict(args, grid, basis, r, nc, S),
-            "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all)" if slab
+            "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all "
+                            f"{'via torch' if args.torch_exchange else 'inside libvie_b200 (vie_slab_matvec)'})" if slab
                             else f"components sharded x{world}") if world > 1 else "1 GPU",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

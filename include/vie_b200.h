@@ -160,6 +160,26 @@ int vie_matvec(vie_op op, const double* x, double* y, void* stream);
  * inverses, crop), product_ms = decompression + the fused axis-3 FFT x Hadamard x IFFT
  * pass.  Device buffers, context stream, returns after completion.                   */
 int vie_matvec_timed(vie_op op, const double* x, double* y, double* fft_ms, double* product_ms);
+/* ---- multi-GPU exchange inside the library (one process per GPU) ----
+ * vie_comm: an NCCL communicator over the ranks of a slab-partitioned operator.  Rank 0
+ * creates the unique id and the caller broadcasts its bytes (MPI, torch.distributed, ...).
+ * vie_op_set_comm attaches it to the operator (same rank / size as vie_op_set_partition);
+ * then vie_slab_matvec runs this rank's whole matvec -- axis-1 FFTs of the z-slab, the
+ * all-to-all (grouped ncclSend / ncclRecv), axis-2 FFTs + pencil stage on the rank's axis-1
+ * positions, the all-to-all back, inverse axis-1 FFTs (+ apply_system epilogue when eps_local
+ * is given) -- with the x-independent decomposition on a side stream concurrent with the
+ * forward FFTs and exchange; and vie_gmres_solve on the partitioned operator solves with
+ * distributed vectors (this rank's z-slabs), every dot and norm summed by ncclAllReduce
+ * (solver.hpp:75-79).  Replaces the caller-driven vie_slab_* + external all-to-all loop. */
+#define VIE_COMM_ID_BYTES 128
+typedef struct vie_comm_s* vie_comm;
+int vie_comm_unique_id(unsigned char id[VIE_COMM_ID_BYTES]);
+int vie_comm_create(vie_ctx ctx, int nranks, int rank, const unsigned char id[VIE_COMM_ID_BYTES], vie_comm* out);
+int vie_comm_destroy(vie_comm comm);
+int vie_op_set_comm(vie_op op, vie_comm comm);
+int vie_slab_matvec(vie_op op, const double* x_local, double* y_local, const double* eps_local, double inv_v,
+                    int diag_term, void* stream);
+
 /* Same call with HOST buffers (H2D, matvec, D2H) -- the reference-facing call. */
 int vie_matvec_host(vie_op op, const double* x_host, double* y_host);
 /* `count` independent applications with HOST buffers, pipelined: the H2D copy of
@@ -192,7 +212,9 @@ typedef struct {
  * |g_{j+1}|/||b|| per iteration (up to history_cap values; *history_len = total
  * count).  The solve runs on the context's stream, ordered after all work queued on
  * `stream` (NULL: the caller must have completed the producers of eps_r / rhs / x0);
- * `stream` then waits for the solve.  Returns after the result is on the host.       */
+ * `stream` then waits for the solve.  Returns after the result is on the host.
+ * On a slab-partitioned operator with a communicator (vie_op_set_comm) every vector is
+ * this rank's z-slab (vie_slab_info x_elems) and all ranks call it together.           */
 int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* rhs,
                     const double* x0, double tol, int inner, int outer, const vie_precond* precond,
                     double* x, int* iterations, double* final_rel_res, double* history_host,

@@ -25,7 +25,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
           "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]
 # kept for callers that print the flags (one-shot compile of everything)
-NVCC_FLAGS = [*CFLAGS, "-shared", "-lcudart"]
+NVCC_FLAGS = [*CFLAGS, "-shared", "-lcudart", "-lnccl"]
 
 
 def _hdr_mtime() -> float:
@@ -67,7 +67,7 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
         for f in [ex.submit(compile_one, s) for s in SOURCES]:
             f.result()
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
-    cmd = [nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart"]
+    cmd = [nvcc, *ARCH, "-shared", "-o", lib + ".tmp", *objs, "-lcudart", "-lnccl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -1,6 +1,7 @@
 // api.cu -- C ABI (include/vie_b200.h): context + FFT plan cache, device
 // Tucker forms, the operator and its matvec pipeline, device-resident GMRES.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -98,6 +99,16 @@ struct vie_ctx_s {
   std::atomic<int> refs{1};
 };
 
+// NCCL communicator over the ranks of a slab-partitioned operator (one process per GPU)
+struct vie_comm_s {
+  ncclComm_t nccl = nullptr;
+  int nranks = 1, rank = 0;
+  int device = 0;
+  ~vie_comm_s() {
+    if (nccl) ncclCommDestroy(nccl);
+  }
+};
+
 namespace {
 void ctx_retain(vie_ctx c) { c->refs.fetch_add(1); }
 void ctx_release(vie_ctx c) {
@@ -161,6 +172,12 @@ struct vie_op_s {
   // slab decomposition (vie_op_set_partition): this rank's z-planes [k0, k0 + nk) and
   // axis-1 positions [p1off, p1off + W) (Geom)
   int nranks = 1, rank = 0;
+  vie_comm comm = nullptr;  // vie_op_set_comm: the in-library exchange and the distributed GMRES
+  double2* xs_send = nullptr;  // vie_slab_matvec exchange buffers (slab_elems each)
+  double2* xs_recv = nullptr;
+  double2* xs_out = nullptr;
+  double2* xs_back = nullptr;
+  cudaEvent_t ev_slab = nullptr;
   // host-buffer staging (vie_matvec_host; the batch call double-buffers with hx2 / hy2)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -191,7 +208,8 @@ struct vie_op_s {
                     static_cast<void*>(Shat), static_cast<void*>(A), static_cast<void*>(B), static_cast<void*>(Bo), static_cast<void*>(Bo1),
                     static_cast<void*>(hx), static_cast<void*>(hy), static_cast<void*>(hx2), static_cast<void*>(hy2),
                     static_cast<void*>(V), static_cast<void*>(ring), static_cast<void*>(Sedge), static_cast<void*>(fitems),
-                    static_cast<void*>(fcounters),
+                    static_cast<void*>(fcounters), static_cast<void*>(xs_send), static_cast<void*>(xs_recv),
+                    static_cast<void*>(xs_out), static_cast<void*>(xs_back),
                     static_cast<void*>(tmp), static_cast<void*>(zp), static_cast<void*>(scal), static_cast<void*>(red_partials),
                     static_cast<void*>(red_counter)})
       dev_free(p);
@@ -206,6 +224,7 @@ struct vie_op_s {
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
     if (ev_user) cudaEventDestroy(ev_user);
+    if (ev_slab) cudaEventDestroy(ev_slab);
     if (ctx) ctx_release(ctx);
   }
 };
@@ -1053,26 +1072,28 @@ int vie_slab_forward(vie_op op, const double* x_local, double* send, void* strea
   });
 }
 
-int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
-  return guard([&] {
-    if (!op || !recv || !out) throw Invalid("slab_pencil: null argument");
-    if (recv == out) throw Invalid("slab_pencil: recv and out must not alias");
-    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
-    ensure_spectra(op);
-    cudaStream_t st = pick_stream(op, stream);
-    const Geom& g = op->g;
-    const Geom gc = slab_geom_cols(op);
-    // axis-2 FFTs of the rank's W columns over all k-planes: recv -> B
-    if (op->q2) vie::launch_col_fwd2(reinterpret_cast<const double2*>(recv), op->B, gc, op->Q2, st);
-    else vie::launch_col_fwd(reinterpret_cast<const double2*>(recv), op->B, gc, op->P2, st);
-    // octant spectra rows of this rank's axis-1 positions: pairs (2j, 2j+1) -> row j,
-    // positions 0, 1 -> rows 0 and n1
-    const int lo = g.p1off / 2, hi = (g.p1off + g.W) / 2;
+namespace {
+// octant spectra rows of this rank's axis-1 positions: pairs (2j, 2j+1) -> row j,
+// positions 0, 1 -> rows 0 and n1 (x-independent)
+void slab_decomp(vie_op op, cudaStream_t st) {
+  const Geom& g = op->g;
+  const int lo = g.p1off / 2, hi = (g.p1off + g.W) / 2;
+  vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
+                     true, lo, hi, op->u3img);
+  if (g.p1off == 0)
     vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
-                       true, lo, hi, op->u3img);
-    if (g.p1off == 0)
-      vie::launch_decomp(op->forms, op->comps_dev, op->comps_host.data(), op->Z, op->Shat, g, op->rmax, st, 0, -1,
-                         false, g.n1, g.n1 + 1, op->u3img);
+                       false, g.n1, g.n1 + 1, op->u3img);
+}
+
+// axis-2 FFTs of the rank's columns, the pencil stage on its octant rows, inverse axis-2 FFTs
+void slab_pencil_stage(vie_op op, const double2* recv, double2* out, cudaStream_t st, bool with_decomp) {
+  const Geom& g = op->g;
+  const Geom gc = slab_geom_cols(op);
+  // axis-2 FFTs of the rank's W columns over all k-planes: recv -> B
+  if (op->q2) vie::launch_col_fwd2(recv, op->B, gc, op->Q2, st);
+  else vie::launch_col_fwd(recv, op->B, gc, op->P2, st);
+  if (with_decomp) slab_decomp(op, st);
+  {
     if (op->pencil3) {
       if (g.p1off == 0)
         vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
@@ -1088,9 +1109,64 @@ int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
     } else {
       vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st);
     }
-    // inverse axis-2 FFTs: Bo -> out (blocked by z-slab rank)
-    if (op->q2) vie::launch_col_inv2(op->Bo, reinterpret_cast<double2*>(out), gc, op->Q2, st);
-    else vie::launch_col_inv(op->Bo, nullptr, reinterpret_cast<double2*>(out), gc, op->P2, st);
+  }
+  // inverse axis-2 FFTs: Bo -> out (blocked by z-slab rank)
+  if (op->q2) vie::launch_col_inv2(op->Bo, out, gc, op->Q2, st);
+  else vie::launch_col_inv(op->Bo, nullptr, out, gc, op->P2, st);
+}
+
+// equal-split all-to-all of the rank-blocked slab (chunk q <-> rank q) as grouped NCCL
+// point-to-point calls on `st` (the exchange step of SURVEY 8(e))
+void slab_exchange(vie_op op, const double2* send, double2* recv, cudaStream_t st) {
+  const Geom& g = op->g;
+  const size_t chunk = static_cast<size_t>(g.S) * g.nk * g.n2 * g.W;  // double2 per peer
+  vie_comm c = op->comm;
+  if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+  for (int q = 0; q < c->nranks; ++q) {
+    const ncclResult_t r1 = ncclSend(send + q * chunk, 2 * chunk, ncclDouble, q, c->nccl, st);
+    const ncclResult_t r2 = ncclRecv(recv + q * chunk, 2 * chunk, ncclDouble, q, c->nccl, st);
+    if (r1 != ncclSuccess || r2 != ncclSuccess) throw std::runtime_error(std::string("NCCL send/recv: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+  }
+  const ncclResult_t r = ncclGroupEnd();
+  if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGroupEnd: ") + ncclGetErrorString(r));
+}
+
+// The whole slab matvec of this rank with the in-library exchange; the x-independent
+// decomposition runs on the side stream while the axis-1 FFTs and the forward exchange run.
+void slab_matvec_run(vie_op op, const double2* x, double2* y, const double2* eps, double inv_v, int diag,
+                     cudaStream_t st) {
+  if (!op->comm) throw Invalid("slab_matvec: no communicator (vie_op_set_comm)");
+  ensure_spectra(op);
+  const Geom& g = op->g;
+  const int64_t se = static_cast<int64_t>(g.S) * g.nk * g.n2 * g.m1;
+  for (double2** p : {&op->xs_send, &op->xs_recv, &op->xs_out, &op->xs_back})
+    if (!*p) *p = dev_alloc<double2>(static_cast<size_t>(se));
+  if (!op->ev_slab) VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_slab, cudaEventDisableTiming));
+  VIE_CUDA_CHECK(cudaEventRecord(op->ev_fork, st));
+  VIE_CUDA_CHECK(cudaStreamWaitEvent(op->side, op->ev_fork, 0));
+  slab_decomp(op, op->side);
+  VIE_CUDA_CHECK(cudaEventRecord(op->ev_join, op->side));
+  const Geom gl = slab_geom_rows(op);
+  if (op->q1) vie::launch_row_fwd2(x, op->xs_send, gl, op->Q1, st);
+  else vie::launch_row_fwd(x, op->xs_send, gl, op->P1, st);
+  slab_exchange(op, op->xs_send, op->xs_recv, st);
+  VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
+  slab_pencil_stage(op, op->xs_recv, op->xs_out, st, false);
+  slab_exchange(op, op->xs_out, op->xs_back, st);
+  const double ne = 8.0 * g.n1 * static_cast<double>(g.n2) * g.n3;  // global N_e
+  if (op->q1) vie::launch_row_inv2(op->xs_back, y, gl, op->Q1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+  else vie::launch_row_inv(op->xs_back, y, gl, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+}
+}  // namespace
+
+int vie_slab_pencil(vie_op op, const double* recv, double* out, void* stream) {
+  return guard([&] {
+    if (!op || !recv || !out) throw Invalid("slab_pencil: null argument");
+    if (recv == out) throw Invalid("slab_pencil: recv and out must not alias");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    ensure_spectra(op);
+    slab_pencil_stage(op, reinterpret_cast<const double2*>(recv), reinterpret_cast<double2*>(out),
+                      pick_stream(op, stream), true);
   });
 }
 
@@ -1112,6 +1188,62 @@ int vie_slab_inverse(vie_op op, const double* back, double* y_local, const doubl
       vie::launch_row_inv2(A, y, gl, op->Q1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
     else
       vie::launch_row_inv(A, y, gl, op->P1, 1.0 / ne, eps, xin, inv_v, op->basis, diag_term ? 1 : 0, st);
+  });
+}
+
+int vie_comm_unique_id(unsigned char id[VIE_COMM_ID_BYTES]) {
+  return guard([&] {
+    if (!id) throw Invalid("comm_unique_id: null argument");
+    static_assert(sizeof(ncclUniqueId) <= VIE_COMM_ID_BYTES, "NCCL unique id size");
+    ncclUniqueId u;
+    const ncclResult_t r = ncclGetUniqueId(&u);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memset(id, 0, VIE_COMM_ID_BYTES);
+    std::memcpy(id, &u, sizeof(u));
+  });
+}
+
+int vie_comm_create(vie_ctx ctx, int nranks, int rank, const unsigned char id[VIE_COMM_ID_BYTES], vie_comm* out) {
+  return guard([&] {
+    if (!ctx || !id || !out) throw Invalid("comm_create: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw Invalid("comm_create: bad rank / size");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    std::unique_ptr<vie_comm_s> c(new vie_comm_s);
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = ctx->device;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    const ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    *out = c.release();
+  });
+}
+
+int vie_comm_destroy(vie_comm comm) {
+  return guard([&] { delete comm; });
+}
+
+int vie_op_set_comm(vie_op op, vie_comm comm) {
+  return guard([&] {
+    if (!op) throw Invalid("set_comm: null operator");
+    if (comm && (comm->nranks != op->nranks || comm->rank != op->rank))
+      throw Invalid("set_comm: communicator rank / size differ from the operator's partition");
+    if (comm && comm->device != op->ctx->device) throw Invalid("set_comm: communicator on another device");
+    op->comm = comm;
+  });
+}
+
+int vie_slab_matvec(vie_op op, const double* x_local, double* y_local, const double* eps_local, double inv_v,
+                    int diag_term, void* stream) {
+  return guard([&] {
+    if (!op || !x_local || !y_local) throw Invalid("slab_matvec: null argument");
+    if (x_local == y_local) throw Invalid("slab_matvec: x and y must not alias");
+    if (eps_local && op->kind != VIE_KIND_N) throw Invalid("apply_system: needs the N operator");
+    VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
+    slab_matvec_run(op, reinterpret_cast<const double2*>(x_local), reinterpret_cast<double2*>(y_local),
+                    reinterpret_cast<const double2*>(eps_local), inv_v, eps_local ? (diag_term ? 1 : 0) : 0,
+                    pick_stream(op, stream));
   });
 }
 
@@ -1412,10 +1544,13 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     if (!op || !eps_r || !rhs_d || !x_d) throw Invalid("gmres: null argument");
     if (tol < 0 || inner < 1 || outer < 1) throw Invalid("gmres: invalid configuration");
     if (op->kind != VIE_KIND_N) throw Invalid("gmres: needs the N operator");
+    if (op->nranks > 1 && !op->comm) throw Invalid("gmres: partitioned operator needs a communicator (vie_op_set_comm)");
     VIE_CUDA_CHECK(cudaSetDevice(op->ctx->device));
     cudaStream_t st = op->ctx->stream;
     const Geom& g = op->g;
-    const int64_t n = static_cast<int64_t>(g.S) * g.n1 * g.n2 * g.n3;
+    // distributed (slab-partitioned, with a communicator): the vectors are this rank's z-slabs
+    const bool dist = op->comm != nullptr;
+    const int64_t n = static_cast<int64_t>(g.S) * g.n1 * g.n2 * (dist ? g.nk : g.n3);
     if (op->g_inner < inner) {
       dev_free(op->V);
       op->V = nullptr;
@@ -1434,8 +1569,19 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     StreamJoin sj(st, static_cast<cudaStream_t>(stream), op->ev_user);
     GmresWork w{op->V, op->tmp, op->zp, op->scal, vie::RedBuf{op->red_partials, op->red_counter}};
     const double2* eps = reinterpret_cast<const double2*>(eps_r);
-    auto sysmv = [&](const double2* in, double2* outv) { run_matvec(op, in, outv, st, eps, inv_v, 1); };
-    const GmresOut r = gmres_core(st, n, sysmv, make_precond(precond, n, st), nullptr,
+    auto sysmv = [&](const double2* in, double2* outv) {
+      if (dist) slab_matvec_run(op, in, outv, eps, inv_v, 1, st);
+      else run_matvec(op, in, outv, st, eps, inv_v, 1);
+    };
+    // every dot / norm of the distributed solve is summed over the ranks (solver.hpp:75-79 on
+    // distributed vectors): one ncclAllReduce of the device scalars, in place, on the solve stream
+    DevReduce allreduce;
+    if (dist)
+      allreduce = [&](double2* p, int count) {
+        const ncclResult_t rr = ncclAllReduce(p, p, 2 * static_cast<size_t>(count), ncclDouble, ncclSum, op->comm->nccl, st);
+        if (rr != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(rr));
+      };
+    const GmresOut r = gmres_core(st, n, sysmv, make_precond(precond, n, st), allreduce,
                                   reinterpret_cast<const double2*>(rhs_d), reinterpret_cast<const double2*>(x0_d), tol,
                                   inner, outer, reinterpret_cast<double2*>(x_d), w);
     sj.done();

@@ -72,28 +72,81 @@ def local_slab(x, S: int, n3: int, nv_plane: int, rank: int, world: int):
     return x.reshape(S, n3, nv_plane)[:, k0:k0 + nk].reshape(-1)
 
 
+def make_comm(dft, rank: int, world: int, group=None):
+    """The library's NCCL communicator (vie.Comm) over the torch.distributed ranks: rank 0
+    creates the unique id, torch.distributed broadcasts it."""
+    import torch.distributed as dist
+
+    from .vie import Comm, comm_unique_id
+
+    import os
+    import sys
+
+    obj = [comm_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0, group=group)
+    # NCCL may print its version banner on stdout at communicator creation; keep stdout for
+    # the caller's output (bench.py prints exactly one JSON line) by sending it to stderr
+    sys.stdout.flush()
+    saved = os.dup(1)
+    try:
+        os.dup2(2, 1)
+        return Comm(dft, world, rank, obj[0])
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
+
+
 class SlabMatvec:
     """apply_operator / apply_system of a slab-partitioned operator on this rank.
 
-    ``exchange(recv, send)`` defaults to torch.distributed.all_to_all_single over
-    ``group``; tests emulate it for several ranks in one process."""
+    With ``comm`` (vie.Comm, make_comm) the whole matvec runs inside the library
+    (vie_slab_matvec: grouped ncclSend/ncclRecv exchanges, decomposition overlapped with the
+    forward exchange) and ``vie.gmres`` on the operator solves with distributed vectors.
+    Without it, the three vie_slab_* stages run here and ``exchange(recv, send)`` moves the
+    slabs: torch.distributed.all_to_all_single over ``group`` by default; tests emulate it
+    for several ranks in one process (the ``stages`` hooks replace the library calls too)."""
 
-    def __init__(self, op, rank: int, world: int, group=None, exchange=None):
+    def __init__(self, op, rank: int, world: int, group=None, exchange=None, comm=None):
+        self.op, self.rank, self.world, self.group = op, rank, world, group
+        self._exchange = exchange
+        self.comm = comm
+        self.x_elems, self.slab_elems, self.k0, self.nk = self._partition()
+        op.local_elems = self.x_elems
+        if comm is not None:
+            self._set_comm(comm)
+        self.send = self.recv = self.out = self.back = None
+        if comm is None or exchange is not None:
+            self.send, self.recv, self.out, self.back = (self._empty(self.slab_elems) for _ in range(4))
+
+    # library hooks (a host-logic test overrides these with stand-ins)
+    def _partition(self):
         import ctypes as C
-
-        import torch
 
         from .vie import _check, lib
 
-        self.op, self.rank, self.world, self.group = op, rank, world, group
         L = lib()
-        _check(L.vie_op_set_partition(op.handle, world, rank))
+        _check(L.vie_op_set_partition(self.op.handle, self.world, self.rank))
         xe, se, k0, nk = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
-        _check(L.vie_slab_info(op.handle, C.byref(xe), C.byref(se), C.byref(k0), C.byref(nk)))
-        self.x_elems, self.slab_elems, self.k0, self.nk = xe.value, se.value, k0.value, nk.value
-        mk = lambda: torch.empty(self.slab_elems, dtype=torch.complex128, device="cuda")
-        self.send, self.recv, self.out, self.back = mk(), mk(), mk(), mk()
-        self._exchange = exchange
+        _check(L.vie_slab_info(self.op.handle, C.byref(xe), C.byref(se), C.byref(k0), C.byref(nk)))
+        return xe.value, se.value, k0.value, nk.value
+
+    def _set_comm(self, comm):
+        from .vie import _check, lib
+
+        _check(lib().vie_op_set_comm(self.op.handle, comm.handle))
+
+    def _empty(self, n):
+        import torch
+
+        return torch.empty(n, dtype=torch.complex128, device="cuda")
+
+    def _slab_matvec(self, x_local, y, eps_local, inv_v, diag):
+        from .vie import _check, _stream_handle, lib
+
+        _check(lib().vie_slab_matvec(self.op.handle, x_local.data_ptr(), y.data_ptr(),
+                                     None if eps_local is None else eps_local.data_ptr(), float(inv_v),
+                                     int(bool(diag)), _stream_handle(None, x_local.device)))
 
     def exchange(self, recv, send):
         if self._exchange is not None:
@@ -129,12 +182,15 @@ class SlabMatvec:
                                       _stream_handle(stream, y_local.device)))
 
     def apply(self, x_local, out=None, eps_local=None, inv_v=0.0, diag=True):
-        """y_local = (A x)_local (or the system matvec with eps_local); x_local: CUDA complex128."""
+        """y_local = (A x)_local (or the system matvec with eps_local); x_local: complex128."""
         import torch
 
-        if x_local.numel() != self.x_elems or x_local.dtype != torch.complex128 or not x_local.is_cuda:
-            raise ValueError("slab apply: x_local must be this rank's CUDA complex128 z-slab")
+        if x_local.numel() != self.x_elems or x_local.dtype != torch.complex128:
+            raise ValueError("slab apply: x_local must be this rank's complex128 z-slab")
         y = out if out is not None else torch.empty_like(x_local)
+        if self.comm is not None and self._exchange is None:
+            self._slab_matvec(x_local, y, eps_local, inv_v, diag)
+            return y
         self.forward(x_local)
         self.exchange(self.recv, self.send)
         self.pencil()

@@ -60,6 +60,12 @@ def lib() -> C.CDLL:
                                         C.c_void_p]
         L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_op_set_strategy.argtypes = [C.c_void_p, C.c_int]
+        L.vie_comm_unique_id.argtypes = [C.c_char_p]
+        L.vie_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
+        L.vie_comm_destroy.argtypes = [C.c_void_p]
+        L.vie_op_set_comm.argtypes = [C.c_void_p, C.c_void_p]
+        L.vie_slab_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
+                                      C.c_void_p]
         L.vie_op_get_strategy.argtypes = [C.c_void_p, C.POINTER(C.c_int)]
         L.vie_matvec_host.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_matvec_host_batch.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
@@ -238,6 +244,7 @@ class EmbeddedSpectrum:
     handle: C.c_void_p
     dft: DftService
     comps: list = field(default_factory=list)
+    local_elems: int | None = None  # slab-partitioned: this rank's z-slab size (sharding.SlabMatvec)
 
     @property
     def embedded_dims(self):
@@ -311,12 +318,42 @@ def _stream_handle(stream, device):
 
 def _dev_vec(op: EmbeddedSpectrum, x):
     torch = _torch()
-    n = op.n_cur * op.n_vox
+    n = op.local_elems if op.local_elems is not None else op.n_cur * op.n_vox
     if not (isinstance(x, torch.Tensor) and x.is_cuda):
         raise TypeError("expected a CUDA torch.complex128 tensor")
     if x.dtype != torch.complex128 or x.numel() != n:
         raise ValueError("apply_operator: dim mismatch")
     return x.contiguous()
+
+
+COMM_ID_BYTES = 128
+
+
+def comm_unique_id() -> bytes:
+    """NCCL unique id for a new communicator (vie_comm_unique_id); rank 0 creates it and the
+    caller broadcasts the bytes."""
+    buf = C.create_string_buffer(COMM_ID_BYTES)
+    _check(lib().vie_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """NCCL communicator of the library (vie_comm_create) over `world` ranks, one per GPU."""
+
+    def __init__(self, dft: DftService, world: int, rank: int, uid: bytes):
+        if len(uid) != COMM_ID_BYTES:
+            raise ValueError("Comm: unique id must be COMM_ID_BYTES bytes")
+        self.world, self.rank, self.dft = world, rank, dft
+        self.handle = C.c_void_p()
+        _check(lib().vie_comm_create(dft.handle, int(world), int(rank), uid, C.byref(self.handle)))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().vie_comm_destroy(self.handle)
+                self.handle = C.c_void_p()
+        except Exception:
+            pass
 
 
 def set_strategy(op: EmbeddedSpectrum, strategy: str) -> None:

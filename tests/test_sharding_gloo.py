@@ -82,56 +82,89 @@ def test_shard_assignment_partitions():
 
 
 # --------------------------------------------------------------------------
-# Slab decomposition host logic (vie_slab_* dataflow) with real gloo all-to-alls:
-# the per-rank stages are numpy stand-ins for the three C-ABI stages using the same
-# rank-blocked exchange layout [rank][s][k in block][axis-2 row in block][axis-1].
+# Slab decomposition host logic with real gloo all-to-alls: the product's SlabMatvec class
+# (sharding.py: buffers, stage order, the two exchanges over torch.distributed) runs with its
+# three library stages replaced by numpy stand-ins that use the same rank-blocked exchange
+# layout [rank][s][k in block][axis-2 row in block][axis-1] as vie_slab_forward / _pencil /
+# _inverse (the GPU emulation test, test_gpu_slab.py, checks the real stages on that layout).
+def _numpy_slab_class():
+    from paper_1811_00484_b200.sharding import SlabMatvec
+
+    class NumpySlab(SlabMatvec):
+        def __init__(self, rank, world, dims, S, spec, blocks):
+            self.dims, self.S, self.spec, self.blocks = dims, S, spec, blocks
+            n1, n2, n3 = dims
+            self.nkv, self.W = n3 // world, 2 * n1 // world
+            import types
+
+            super().__init__(types.SimpleNamespace(), rank, world)
+
+        def _partition(self):
+            n1, n2, n3 = self.dims
+            return (self.S * n1 * n2 * self.nkv, self.S * self.nkv * n2 * 2 * n1, self.rank * self.nkv, self.nkv)
+
+        def _empty(self, n):
+            return torch.empty(n, dtype=torch.complex128)
+
+        def forward(self, x_local, stream=None):  # stand-in for vie_slab_forward
+            n1, n2, n3 = self.dims
+            m1 = 2 * n1
+            xa = np.zeros((self.S, self.nk, n2, m1), complex)
+            xa[..., :n1] = x_local.numpy().reshape(self.S, self.nk, n2, n1)
+            xa = np.fft.fft(xa, axis=3)
+            W = self.W
+            send = np.stack([xa[..., q * W:(q + 1) * W] for q in range(self.world)]).reshape(-1)
+            self.send.copy_(torch.from_numpy(send))
+
+        def pencil(self, stream=None):  # stand-in for vie_slab_pencil
+            n1, n2, n3 = self.dims
+            m1, m2, m3 = 2 * n1, 2 * n2, 2 * n3
+            S, W, nk, world = self.S, self.W, self.nk, self.world
+            blk = self.recv.numpy().reshape(world, S, nk, n2, W)
+            xp = np.zeros((S, m3, m2, W), complex)
+            xp[:, :n3, :n2] = blk.transpose(1, 0, 2, 3, 4).reshape(S, n3, n2, W)
+            xp = np.fft.fft(np.fft.fft(xp, axis=2), axis=1)
+            cols = slice(self.rank * W, (self.rank + 1) * W)
+            yp = np.zeros_like(xp)
+            for t, s_, c, coef in self.blocks:
+                yp[t] += coef * self.spec[c][:, :, cols] * xp[s_]
+            yp = np.fft.ifft(np.fft.ifft(yp, axis=1)[:, :n3], axis=2)[:, :, :n2]
+            out = np.stack([yp[:, r * nk:(r + 1) * nk] for r in range(world)]).reshape(-1)
+            self.out.copy_(torch.from_numpy(out))
+
+        def inverse(self, y_local, eps_local=None, inv_v=0.0, x_local=None, diag=True, stream=None):
+            n1, n2, n3 = self.dims
+            ya = self.back.numpy().reshape(self.world, self.S, self.nk, n2, self.W)
+            ya = ya.transpose(1, 2, 3, 0, 4).reshape(self.S, self.nk, n2, 2 * n1)
+            y_local.copy_(torch.from_numpy(np.ascontiguousarray(np.fft.ifft(ya, axis=3)[..., :n1]).reshape(-1)))
+
+    return NumpySlab
+
+
 def _slab_worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from oracle import oracle as orc
-    from paper_1811_00484_b200.sharding import local_slab, slab_planes
+    from paper_1811_00484_b200.sharding import local_slab
     from tests.helpers import fourier_forms, random_field, spatial_tucker_forms
 
     kind, basis, dims = 0, 0, (12, 4, 6)
     n1, n2, n3 = dims
-    m1, m2, m3 = 2 * n1, 2 * n2, 2 * n3
     S = 3
     spatial, par = spatial_tucker_forms(kind, basis, dims, 2, 4)
     forms = fourier_forms(spatial, par)
     _, _, blocks = orc.component_table(kind, basis)
-    spec = [orc.decompress_tucker((m1, m2, m3), f).reshape(m3, m2, m1) for f in forms]
+    spec = [orc.decompress_tucker((2 * n1, 2 * n2, 2 * n3), f).reshape(2 * n3, 2 * n2, 2 * n1) for f in forms]
     x = random_field(basis, dims, 8)
-    k0, nk = slab_planes(n3, rank, world)
-    W = m1 // world
-    xl = local_slab(x, S, n3, n1 * n2, rank, world).reshape(S, nk, n2, n1)
-    # stage 1: axis-1 FFT of the local z-slab, blocked by the destination rank's W positions
-    xa = np.zeros((S, nk, n2, m1), complex)
-    xa[..., :n1] = xl
-    xa = np.fft.fft(xa, axis=3)
-    send = np.stack([xa[..., qq * W:(qq + 1) * W] for qq in range(world)]).reshape(-1)
-    recv = torch.empty(send.size, dtype=torch.complex128)
-    dist.all_to_all_single(recv, torch.from_numpy(send))
-    # stage 2: this rank's W positions, all k: axis-2 FFT, axis-3 FFT, Hadamard, inverses
-    blk = recv.numpy().reshape(world, S, nk, n2, W)
-    xp = np.zeros((S, m3, m2, W), complex)
-    xp[:, :n3, :n2] = blk.transpose(1, 0, 2, 3, 4).reshape(S, n3, n2, W)
-    xp = np.fft.fft(np.fft.fft(xp, axis=2), axis=1)
-    cols = slice(rank * W, (rank + 1) * W)
-    yp = np.zeros_like(xp)
-    for t, s_, c, coef in blocks:
-        yp[t] += coef * spec[c][:, :, cols] * xp[s_]
-    yp = np.fft.ifft(np.fft.ifft(yp, axis=1)[:, :n3], axis=2)[:, :, :n2]
-    out = np.stack([yp[:, r * nk:(r + 1) * nk] for r in range(world)]).reshape(-1)
-    back = torch.empty(out.size, dtype=torch.complex128)
-    dist.all_to_all_single(back, torch.from_numpy(out))
-    # stage 3: inverse axis-1 FFT of the local z-slab rows, crop
-    ya = back.numpy().reshape(world, S, nk, n2, W).transpose(1, 2, 3, 0, 4).reshape(S, nk, n2, m1)
-    yl = np.fft.ifft(ya, axis=3)[..., :n1]
-    gathered = [torch.empty(yl.size, dtype=torch.complex128) for _ in range(world)]
-    dist.all_gather(gathered, torch.from_numpy(np.ascontiguousarray(yl).reshape(-1)))
+    sm = _numpy_slab_class()(rank, world, dims, S, spec, blocks)
+    assert sm.op.local_elems == sm.x_elems and sm.k0 == rank * (n3 // world)
+    xl = torch.from_numpy(np.ascontiguousarray(local_slab(x, S, n3, n1 * n2, rank, world)))
+    yl = sm.apply(xl)  # the product's apply(): forward -> all_to_all -> pencil -> all_to_all -> inverse
+    gathered = [torch.empty(yl.numel(), dtype=torch.complex128) for _ in range(world)]
+    dist.all_gather(gathered, yl)
     if rank == 0:
-        y = np.concatenate([g.numpy().reshape(S, nk, n1 * n2) for g in gathered], axis=1).reshape(-1)
+        y = np.concatenate([g.numpy().reshape(S, n3 // world, n1 * n2) for g in gathered], axis=1).reshape(-1)
         ref = orc.apply_operator_tucker(kind, basis, dims, forms, x)
         q.put(np.linalg.norm(y - ref) / np.linalg.norm(ref))
     dist.destroy_process_group()
