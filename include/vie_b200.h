@@ -30,6 +30,7 @@ extern "C" {
 #define VIE_ENOMEM 2
 #define VIE_ECUDA 3
 #define VIE_ENCCL 4
+#define VIE_EIO 5 /* file I/O (the reference's std::runtime_error of container.hpp) */
 
 #define VIE_KIND_N 0 /* OperatorKind::N  (components.hpp:14) */
 #define VIE_KIND_K 1 /* OperatorKind::K                      */
@@ -119,6 +120,23 @@ int vie_tucker_from_cp(vie_ctx ctx, const int64_t dims[3], int64_t rank, const d
                        vie_tucker* out);
 int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]);
 int vie_tucker_destroy(vie_tucker t);
+
+/* ---- VIET container (container.hpp:15-159): the reference's binary file of dense tensors
+ * and compressed forms, byte for byte ("VIET", version 1, kind 0 dense / 1 tucker / 2
+ * tucker_cp, rule, tol, dims, ranks, then (re, im) f64 payload: dense n1 n2 n3 axis-1 fastest;
+ * tucker U1, U2, U3 column-major then the core; tucker_cp W1, W2, W3).  I/O errors (cannot
+ * open, bad magic, unsupported version, truncated, unknown kind) return VIE_EIO.
+ * vie_container_info / _read / _write work on host buffers (no device needed).
+ * vie_tucker_save writes a device form created from spatial factors (domain 0, including
+ * vie_tucker_compress* and vie_tucker_from_cp); vie_tucker_load builds the device form
+ * (transform_factors on the device) from a tucker or tucker_cp file; `sign` is the
+ * component's parity (not stored in the file).                                          */
+int vie_container_info(const char* path, int* kind, int* rule, double* tol, int64_t dims[3], int64_t ranks[3]);
+int vie_container_read(const char* path, double* payload, int64_t capacity_complex);
+int vie_container_write(const char* path, int kind, int rule, double tol, const int64_t dims[3],
+                        const int64_t ranks[3], const double* payload);
+int vie_tucker_save(vie_tucker t, const char* path);
+int vie_tucker_load(vie_ctx ctx, const char* path, const int sign[3], vie_tucker* out);
 
 /* Canonical component table of (kind, basis): components.hpp:71-92 for PWC,
  * its PWL generalisation otherwise.  comps: ncomp x 4 ints (q, q', l, l');

@@ -31,6 +31,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "vie_b200.h"
@@ -82,11 +83,15 @@ struct FactorMatrix {  // column-major rows x cols (Eigen::MatrixXcd layout)
   cplx operator()(Index i, Index j) const { return data[static_cast<size_t>(i + rows * j)]; }
 };
 
+enum class TruncationRule { SigmaMax = VIE_RULE_SIGMA_MAX, Energy = VIE_RULE_ENERGY };  // decomp.hpp:23
+
 // Spatial-domain Tucker form as hosvd returns it (decomp.hpp:123-133).
 struct TuckerForm {
   Tensor3 core;                          // r1 x r2 x r3
   std::array<FactorMatrix, 3> factors;   // n_q x r_q
   std::array<Index, 3> ranks{0, 0, 0};
+  TruncationRule rule = TruncationRule::SigmaMax;
+  double tol = 0.0;
 };
 
 // Spatial-domain Tucker+CP form, merged factors W_q = U_q V_q (decomp.hpp:143-148).
@@ -94,6 +99,65 @@ struct TuckerCPForm {
   std::array<FactorMatrix, 3> factors;  // n_q x rank
   Index rank = 0;
 };
+
+// ---- VIET container (container.hpp:15-159), byte-compatible with the reference's files
+using ContainerValue = std::variant<Tensor3, TuckerForm, TuckerCPForm>;
+
+inline void save_container(const std::string& path, const Tensor3& t) {
+  const int64_t d[3] = {t.dims[0], t.dims[1], t.dims[2]}, r[3] = {0, 0, 0};
+  check(vie_container_write(path.c_str(), 0, 0, 0.0, d, r, reinterpret_cast<const double*>(t.data.data())));
+}
+inline void save_container(const std::string& path, const TuckerForm& f, const std::array<Index, 3>& dims) {
+  std::vector<cplx> p;
+  for (const auto& u : f.factors) p.insert(p.end(), u.data.begin(), u.data.end());
+  p.insert(p.end(), f.core.data.begin(), f.core.data.end());
+  const int64_t d[3] = {dims[0], dims[1], dims[2]}, r[3] = {f.ranks[0], f.ranks[1], f.ranks[2]};
+  check(vie_container_write(path.c_str(), 1, static_cast<int>(f.rule), f.tol, d, r,
+                            reinterpret_cast<const double*>(p.data())));
+}
+inline void save_container(const std::string& path, const TuckerCPForm& f, const std::array<Index, 3>& dims) {
+  std::vector<cplx> p;
+  for (const auto& w : f.factors) p.insert(p.end(), w.data.begin(), w.data.end());
+  const int64_t d[3] = {dims[0], dims[1], dims[2]}, r[3] = {f.rank, f.rank, f.rank};
+  check(vie_container_write(path.c_str(), 2, 0, 0.0, d, r, reinterpret_cast<const double*>(p.data())));
+}
+inline ContainerValue load_container(const std::string& path) {
+  int kind = 0, rule = 0;
+  double tol = 0.0;
+  int64_t d[3], r[3];
+  check(vie_container_info(path.c_str(), &kind, &rule, &tol, d, r));
+  int64_t n = kind == 0 ? d[0] * d[1] * d[2] : d[0] * r[0] + d[1] * r[1] + d[2] * r[2];
+  if (kind == 1) n += r[0] * r[1] * r[2];
+  std::vector<cplx> p(static_cast<size_t>(n));
+  check(vie_container_read(path.c_str(), reinterpret_cast<double*>(p.data()), n));
+  if (kind == 0) {
+    Tensor3 t(d[0], d[1], d[2]);
+    t.data = std::move(p);
+    return t;
+  }
+  std::array<FactorMatrix, 3> fm;
+  size_t off = 0;
+  for (int q = 0; q < 3; ++q) {
+    fm[q] = FactorMatrix(d[q], r[q]);
+    std::copy(p.begin() + static_cast<std::ptrdiff_t>(off), p.begin() + static_cast<std::ptrdiff_t>(off + fm[q].data.size()),
+              fm[q].data.begin());
+    off += fm[q].data.size();
+  }
+  if (kind == 2) {
+    TuckerCPForm f;
+    f.factors = std::move(fm);
+    f.rank = r[0];
+    return f;
+  }
+  TuckerForm f;
+  f.factors = std::move(fm);
+  f.ranks = {r[0], r[1], r[2]};
+  f.core = Tensor3(r[0], r[1], r[2]);
+  std::copy(p.begin() + static_cast<std::ptrdiff_t>(off), p.end(), f.core.data.begin());
+  f.rule = rule == 1 ? TruncationRule::Energy : TruncationRule::SigmaMax;
+  f.tol = tol;
+  return f;
+}
 
 struct KernelComponent {  // components.hpp:26-36 (+ PWL polynomial indices)
   OperatorKind op = OperatorKind::N;
@@ -340,7 +404,6 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder ord
   return EmbeddedSpectrum(op, kind, order, grid);
 }
 
-enum class TruncationRule { SigmaMax = VIE_RULE_SIGMA_MAX, Energy = VIE_RULE_ENERGY };
 
 struct SpectrumBuildOptions {  // operator.hpp:131-139 (Tucker representation only)
   double tol = 1e-8;

@@ -8,6 +8,7 @@
 #include <complex>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <atomic>
 #include <functional>
 #include <map>
@@ -34,6 +35,12 @@ thread_local std::string g_err;
 struct Invalid : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
+struct NcclError : std::runtime_error {  // -> VIE_ENCCL
+  using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {  // -> VIE_EIO (the reference's std::runtime_error of container.hpp)
+  using std::runtime_error::runtime_error;
+};
 
 template <class F>
 int guard(F&& f) {
@@ -46,6 +53,12 @@ int guard(F&& f) {
   } catch (const vie::CudaError& e) {
     g_err = e.what();
     return e.code == cudaErrorMemoryAllocation ? VIE_ENOMEM : VIE_ECUDA;
+  } catch (const NcclError& e) {
+    g_err = e.what();
+    return VIE_ENCCL;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return VIE_EIO;
   } catch (const std::bad_alloc& e) {
     g_err = std::string("host allocation failed: ") + e.what();
     return VIE_ENOMEM;
@@ -128,6 +141,13 @@ struct vie_tucker_s {
   int sign[3] = {1, 1, 1};
   double2* core = nullptr;   // r1*r2*r3
   double2* uo[3] = {nullptr, nullptr, nullptr};  // (n_q + 1) x r_q octant rows
+  // the spatial form as given (domain 0), for the VIET container (container.hpp): factors
+  // n_q x r_q column-major and the core; rule / tol of the compression (-1: none); CP rank (> 0:
+  // a Tucker+CP form held with a superdiagonal core, saved as kind tucker_cp)
+  std::vector<double2> hu[3], hcore;
+  int rule = -1;
+  double tol = 0.0;
+  int64_t cp_rank = 0;
   ~vie_tucker_s() {
     dev_free(core);
     for (auto* u : uo) dev_free(u);
@@ -727,6 +747,13 @@ int vie_tucker_from_factors(vie_ctx ctx, const int64_t dims[3], const int64_t ra
     }
     const size_t ncore = static_cast<size_t>(ranks[0] * ranks[1] * ranks[2]);
     check_cplx_finite_host(core_host, ncore, "vie_tucker_from_factors: core");
+    if (domain == 0) {
+      t->hcore.assign(reinterpret_cast<const double2*>(core_host), reinterpret_cast<const double2*>(core_host) + ncore);
+      const double* uq[3] = {u1_host, u2_host, u3_host};
+      for (int q = 0; q < 3; ++q)
+        t->hu[q].assign(reinterpret_cast<const double2*>(uq[q]),
+                        reinterpret_cast<const double2*>(uq[q]) + dims[q] * ranks[q]);
+    }
     t->core = dev_alloc<double2>(ncore);
     copy_sync(t->core, core_host, ncore * sizeof(double2), ctx->stream);
     const double* uh[3] = {u1_host, u2_host, u3_host};
@@ -793,8 +820,10 @@ int vie_tucker_from_cp(vie_ctx ctx, const int64_t dims[3], int64_t rank, const d
   std::vector<cd> core(static_cast<size_t>(rank * rank * rank), cd(0.0));
   for (int64_t l = 0; l < rank; ++l) core[static_cast<size_t>(l + rank * (l + rank * l))] = 1.0;  // superdiagonal
   const int64_t ranks[3] = {rank, rank, rank};
-  return vie_tucker_from_factors(ctx, dims, ranks, reinterpret_cast<const double*>(core.data()), w1_host, w2_host,
-                                 w3_host, sign, domain, out);
+  const int rc2 = vie_tucker_from_factors(ctx, dims, ranks, reinterpret_cast<const double*>(core.data()), w1_host,
+                                          w2_host, w3_host, sign, domain, out);
+  if (rc2 == VIE_OK) (*out)->cp_rank = rank;
+  return rc2;
 }
 
 int vie_tucker_ranks(vie_tucker t, int64_t ranks_out[3]) {
@@ -1121,14 +1150,14 @@ void slab_exchange(vie_op op, const double2* send, double2* recv, cudaStream_t s
   const Geom& g = op->g;
   const size_t chunk = static_cast<size_t>(g.S) * g.nk * g.n2 * g.W;  // double2 per peer
   vie_comm c = op->comm;
-  if (ncclGroupStart() != ncclSuccess) throw std::runtime_error("ncclGroupStart failed");
+  if (ncclGroupStart() != ncclSuccess) throw NcclError("ncclGroupStart failed");
   for (int q = 0; q < c->nranks; ++q) {
     const ncclResult_t r1 = ncclSend(send + q * chunk, 2 * chunk, ncclDouble, q, c->nccl, st);
     const ncclResult_t r2 = ncclRecv(recv + q * chunk, 2 * chunk, ncclDouble, q, c->nccl, st);
-    if (r1 != ncclSuccess || r2 != ncclSuccess) throw std::runtime_error(std::string("NCCL send/recv: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
+    if (r1 != ncclSuccess || r2 != ncclSuccess) throw NcclError(std::string("NCCL send/recv: ") + ncclGetErrorString(r1 != ncclSuccess ? r1 : r2));
   }
   const ncclResult_t r = ncclGroupEnd();
-  if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGroupEnd: ") + ncclGetErrorString(r));
+  if (r != ncclSuccess) throw NcclError(std::string("ncclGroupEnd: ") + ncclGetErrorString(r));
 }
 
 // The whole slab matvec of this rank with the in-library exchange; the x-independent
@@ -1197,7 +1226,7 @@ int vie_comm_unique_id(unsigned char id[VIE_COMM_ID_BYTES]) {
     static_assert(sizeof(ncclUniqueId) <= VIE_COMM_ID_BYTES, "NCCL unique id size");
     ncclUniqueId u;
     const ncclResult_t r = ncclGetUniqueId(&u);
-    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    if (r != ncclSuccess) throw NcclError(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
     std::memset(id, 0, VIE_COMM_ID_BYTES);
     std::memcpy(id, &u, sizeof(u));
   });
@@ -1215,7 +1244,7 @@ int vie_comm_create(vie_ctx ctx, int nranks, int rank, const unsigned char id[VI
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof(u));
     const ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, u, rank);
-    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    if (r != ncclSuccess) throw NcclError(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     *out = c.release();
   });
 }
@@ -1579,7 +1608,7 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     if (dist)
       allreduce = [&](double2* p, int count) {
         const ncclResult_t rr = ncclAllReduce(p, p, 2 * static_cast<size_t>(count), ncclDouble, ncclSum, op->comm->nccl, st);
-        if (rr != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(rr));
+        if (rr != ncclSuccess) throw NcclError(std::string("ncclAllReduce: ") + ncclGetErrorString(rr));
       };
     const GmresOut r = gmres_core(st, n, sysmv, make_precond(precond, n, st), allreduce,
                                   reinterpret_cast<const double2*>(rhs_d), reinterpret_cast<const double2*>(x0_d), tol,
@@ -1786,6 +1815,8 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
                                          reinterpret_cast<const double*>(U[1].data()),
                                          reinterpret_cast<const double*>(U[2].data()), sign, 0, out);
   if (rc != VIE_OK) throw Invalid(g_err);
+  (*out)->rule = rule;
+  (*out)->tol = tol;
   if (ranks_out)
     for (int q = 0; q < 3; ++q) ranks_out[q] = rk[q];
 }
@@ -2063,6 +2094,178 @@ int vie_postprocess(vie_ctx ctx, const vie_scene* scene, const double* eps_r, co
     VIE_CUDA_CHECK(cudaMemcpyAsync(&total, buf, sizeof(double), cudaMemcpyDeviceToHost, st));
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));
     if (total_absorbed_power_host) *total_absorbed_power_host = total;
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- VIET container
+// container.hpp:15-159: "VIET", u32 version 1, u8 kind (0 dense, 1 tucker, 2 tucker_cp),
+// u8 rule (0 sigma_max, 1 energy), u16 0, f64 tol, u64 dims[3], u64 ranks[3], then complex
+// payload as (re, im) f64 pairs -- dense: n1 n2 n3 axis-1 fastest; tucker: U1, U2, U3
+// (column-major) then the core; tucker_cp: W1, W2, W3.  Little-endian host (x86-64).
+namespace {
+constexpr char kVietMagic[4] = {'V', 'I', 'E', 'T'};
+constexpr uint32_t kVietVersion = 1;
+
+struct VietHeader {
+  int kind = 0, rule = 0;
+  double tol = 0.0;
+  int64_t dims[3] = {0, 0, 0}, ranks[3] = {0, 0, 0};
+};
+
+int64_t viet_payload(const VietHeader& h) {  // complex values
+  if (h.kind == 0) return h.dims[0] * h.dims[1] * h.dims[2];
+  int64_t n = 0;
+  for (int q = 0; q < 3; ++q) n += h.dims[q] * h.ranks[q];
+  return h.kind == 1 ? n + h.ranks[0] * h.ranks[1] * h.ranks[2] : n;
+}
+
+template <class T>
+void put(std::ofstream& os, T v) {
+  os.write(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+template <class T>
+T get(std::ifstream& is) {
+  T v;
+  is.read(reinterpret_cast<char*>(&v), sizeof(T));
+  if (!is) throw IoError("container: truncated file");
+  return v;
+}
+
+void viet_write(const char* path, const VietHeader& h, const std::vector<std::pair<const double2*, int64_t>>& blocks) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw IoError(std::string("container: cannot open ") + path + " for writing");
+  os.write(kVietMagic, 4);
+  put<uint32_t>(os, kVietVersion);
+  put<uint8_t>(os, static_cast<uint8_t>(h.kind));
+  put<uint8_t>(os, static_cast<uint8_t>(h.rule));
+  put<uint16_t>(os, 0);
+  put<double>(os, h.tol);
+  for (int q = 0; q < 3; ++q) put<uint64_t>(os, static_cast<uint64_t>(h.dims[q]));
+  for (int q = 0; q < 3; ++q) put<uint64_t>(os, static_cast<uint64_t>(h.ranks[q]));
+  for (const auto& b : blocks) os.write(reinterpret_cast<const char*>(b.first), static_cast<std::streamsize>(16 * b.second));
+  if (!os) throw IoError(std::string("container: write failed: ") + path);
+}
+
+VietHeader viet_header(std::ifstream& is, const char* path) {
+  if (!is) throw IoError(std::string("container: cannot open ") + path);
+  char magic[4];
+  is.read(magic, 4);
+  if (!is) throw IoError("container: truncated file");
+  if (std::memcmp(magic, kVietMagic, 4) != 0) throw IoError(std::string("container: bad magic in ") + path);
+  if (get<uint32_t>(is) != kVietVersion) throw IoError("container: unsupported version");
+  VietHeader h;
+  h.kind = get<uint8_t>(is);
+  h.rule = get<uint8_t>(is);
+  get<uint16_t>(is);
+  h.tol = get<double>(is);
+  for (int q = 0; q < 3; ++q) h.dims[q] = static_cast<int64_t>(get<uint64_t>(is));
+  for (int q = 0; q < 3; ++q) h.ranks[q] = static_cast<int64_t>(get<uint64_t>(is));
+  if (h.kind < 0 || h.kind > 2) throw IoError("container: unknown form kind");
+  return h;
+}
+
+std::vector<double2> viet_payload_read(std::ifstream& is, const VietHeader& h) {
+  std::vector<double2> p(static_cast<size_t>(viet_payload(h)));
+  is.read(reinterpret_cast<char*>(p.data()), static_cast<std::streamsize>(16 * p.size()));
+  if (!is) throw IoError("container: truncated file");
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+int vie_container_info(const char* path, int* kind, int* rule, double* tol, int64_t dims[3], int64_t ranks[3]) {
+  return guard([&] {
+    if (!path) throw Invalid("container: null path");
+    std::ifstream is(path, std::ios::binary);
+    const VietHeader h = viet_header(is, path);
+    if (kind) *kind = h.kind;
+    if (rule) *rule = h.rule;
+    if (tol) *tol = h.tol;
+    for (int q = 0; q < 3; ++q) {
+      if (dims) dims[q] = h.dims[q];
+      if (ranks) ranks[q] = h.ranks[q];
+    }
+  });
+}
+
+int vie_container_read(const char* path, double* payload, int64_t capacity) {
+  return guard([&] {
+    if (!path || !payload) throw Invalid("container: null argument");
+    std::ifstream is(path, std::ios::binary);
+    const VietHeader h = viet_header(is, path);
+    if (viet_payload(h) > capacity) throw Invalid("container: payload larger than the buffer");
+    const std::vector<double2> p = viet_payload_read(is, h);
+    std::memcpy(payload, p.data(), 16 * p.size());
+  });
+}
+
+int vie_container_write(const char* path, int kind, int rule, double tol, const int64_t dims[3],
+                        const int64_t ranks[3], const double* payload) {
+  return guard([&] {
+    if (!path || !dims || !payload || (kind != 0 && !ranks)) throw Invalid("container: null argument");
+    if (kind < 0 || kind > 2 || rule < 0 || rule > 1) throw Invalid("container: bad kind / rule");
+    VietHeader h;
+    h.kind = kind;
+    h.rule = kind == 1 ? rule : 0;
+    h.tol = kind == 1 ? tol : 0.0;
+    for (int q = 0; q < 3; ++q) {
+      h.dims[q] = dims[q];
+      h.ranks[q] = kind == 0 ? 0 : ranks[q];
+    }
+    viet_write(path, h, {{reinterpret_cast<const double2*>(payload), viet_payload(h)}});
+  });
+}
+
+int vie_tucker_save(vie_tucker t, const char* path) {
+  return guard([&] {
+    if (!t || !path) throw Invalid("save_container: null argument");
+    if (t->hcore.empty()) throw Invalid("save_container: the form was given in the Fourier domain (no spatial factors)");
+    VietHeader h;
+    for (int q = 0; q < 3; ++q) h.dims[q] = t->dims[q];
+    std::vector<std::pair<const double2*, int64_t>> blocks;
+    for (int q = 0; q < 3; ++q) blocks.push_back({t->hu[q].data(), static_cast<int64_t>(t->hu[q].size())});
+    if (t->cp_rank > 0) {
+      h.kind = 2;
+      for (int q = 0; q < 3; ++q) h.ranks[q] = t->cp_rank;
+    } else {
+      h.kind = 1;
+      h.rule = t->rule == VIE_RULE_ENERGY ? 1 : 0;
+      h.tol = t->rule < 0 ? 0.0 : t->tol;
+      for (int q = 0; q < 3; ++q) h.ranks[q] = t->ranks[q];
+      blocks.push_back({t->hcore.data(), static_cast<int64_t>(t->hcore.size())});
+    }
+    viet_write(path, h, blocks);
+  });
+}
+
+int vie_tucker_load(vie_ctx ctx, const char* path, const int sign[3], vie_tucker* out) {
+  return guard([&] {
+    if (!ctx || !path || !sign || !out) throw Invalid("load_container: null argument");
+    std::ifstream is(path, std::ios::binary);
+    const VietHeader h = viet_header(is, path);
+    if (h.kind == 0) throw Invalid("load_container: dense tensor, not a compressed form (vie_container_read)");
+    const std::vector<double2> p = viet_payload_read(is, h);
+    const double* base = reinterpret_cast<const double*>(p.data());
+    const double* u[3];
+    int64_t off = 0;
+    for (int q = 0; q < 3; ++q) {
+      u[q] = base + 2 * off;
+      off += h.dims[q] * h.ranks[q];
+    }
+    int rc;
+    if (h.kind == 2) {
+      rc = vie_tucker_from_cp(ctx, h.dims, h.ranks[0], u[0], u[1], u[2], sign, 0, out);
+    } else {
+      rc = vie_tucker_from_factors(ctx, h.dims, h.ranks, base + 2 * off, u[0], u[1], u[2], sign, 0, out);
+      if (rc == VIE_OK) {
+        (*out)->rule = h.rule == 1 ? VIE_RULE_ENERGY : VIE_RULE_SIGMA_MAX;
+        (*out)->tol = h.tol;
+      }
+    }
+    if (rc != VIE_OK) throw Invalid(g_err);
   });
 }
 

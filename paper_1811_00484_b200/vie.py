@@ -60,6 +60,13 @@ def lib() -> C.CDLL:
                                         C.c_void_p]
         L.vie_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.vie_op_set_strategy.argtypes = [C.c_void_p, C.c_int]
+        L.vie_container_info.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_double),
+                                         C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.vie_container_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int64]
+        L.vie_container_write.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_double, C.POINTER(C.c_int64),
+                                          C.POINTER(C.c_int64), C.c_void_p]
+        L.vie_tucker_save.argtypes = [C.c_void_p, C.c_char_p]
+        L.vie_tucker_load.argtypes = [C.c_void_p, C.c_char_p, C.POINTER(C.c_int), C.POINTER(C.c_void_p)]
         L.vie_comm_unique_id.argtypes = [C.c_char_p]
         L.vie_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
         L.vie_comm_destroy.argtypes = [C.c_void_p]
@@ -207,6 +214,89 @@ def tucker_cp_form(dft: DftService, dims, factors: Sequence, sign, domain: int =
                                     ws[1].ctypes.data_as(_dp), ws[2].ctypes.data_as(_dp),
                                     (C.c_int * 3)(*[int(x) for x in sign]), int(domain), C.byref(h)))
     return TuckerForm._from_handle(dft, h, dims, (rank,) * 3, sign)
+
+
+# ----------------------------------------------------------------------------- VIET container
+CONTAINER_DENSE, CONTAINER_TUCKER, CONTAINER_TUCKER_CP = 0, 1, 2
+
+
+def _path(p) -> bytes:
+    import os
+
+    return os.fsencode(p)
+
+
+def container_info(path) -> dict:
+    """Header of a VIET file (container.hpp:15-29): kind, rule, tol, dims, ranks."""
+    k, r, t = C.c_int(), C.c_int(), C.c_double()
+    d, rk = (C.c_int64 * 3)(), (C.c_int64 * 3)()
+    _check(lib().vie_container_info(_path(path), C.byref(k), C.byref(r), C.byref(t), d, rk))
+    return {"kind": k.value, "rule": r.value, "tol": t.value, "dims": tuple(d), "ranks": tuple(rk)}
+
+
+def save_container(path, value, dims=None) -> None:
+    """save_container (container.hpp:95-123).  value: a 3-D complex array (dense Tensor3,
+    axis-1 fastest: pass it in (n1, n2, n3) Fortran order or as a flat reference-layout
+    vector with `dims`), a device TuckerForm built from spatial factors (tucker_compress,
+    TuckerForm(domain=0), tucker_cp_form), or a host tuple ("tucker", core, (U1, U2, U3),
+    rule, tol) / ("tucker_cp", (W1, W2, W3))."""
+    if isinstance(value, TuckerForm):
+        _check(lib().vie_tucker_save(value.handle, _path(path)))
+        return
+    if isinstance(value, tuple) and value and value[0] in ("tucker", "tucker_cp"):
+        if value[0] == "tucker":
+            _, core, us, rule, tol = value
+            us = [np.asfortranarray(np.asarray(u, np.complex128)) for u in us]
+            ranks = [u.shape[1] for u in us]
+            payload = np.concatenate([u.reshape(-1, order="F") for u in us] +
+                                     [_cplx(np.asarray(core).reshape(-1, order="F"))])
+            kind, rr, tt = CONTAINER_TUCKER, int(rule), float(tol)
+        else:
+            ws = [np.asfortranarray(np.asarray(w, np.complex128)) for w in value[1]]
+            ranks = [ws[0].shape[1]] * 3
+            payload = np.concatenate([w.reshape(-1, order="F") for w in ws])
+            kind, rr, tt = CONTAINER_TUCKER_CP, 0, 0.0
+        d = [u.shape[0] for u in (us if kind == CONTAINER_TUCKER else ws)]
+        _check(lib().vie_container_write(_path(path), kind, rr, tt, _i64(d), _i64(ranks),
+                                         np.ascontiguousarray(payload).ctypes.data))
+        return
+    a = np.asarray(value, np.complex128)
+    if a.ndim == 3:
+        d, flat = a.shape, a.reshape(-1, order="F")
+    else:
+        if dims is None:
+            raise ValueError("save_container: dims needed for a flat tensor")
+        d, flat = tuple(dims), a.reshape(-1)
+    flat = np.ascontiguousarray(flat)
+    _check(lib().vie_container_write(_path(path), CONTAINER_DENSE, 0, 0.0, _i64(d), _i64([0, 0, 0]),
+                                     flat.ctypes.data))
+
+
+def load_container(path, dft: DftService | None = None, sign=None):
+    """load_container (container.hpp:125-159).  Dense files give a (n1, n2, n3) complex array
+    (Fortran order, axis-1 fastest).  Compressed forms give a device TuckerForm when `dft`
+    and the component parity `sign` are passed, else the host tuple of save_container."""
+    info = container_info(path)
+    if info["kind"] != CONTAINER_DENSE and dft is not None:
+        if sign is None:
+            raise ValueError("load_container: the component parity `sign` is needed for a device form")
+        h = C.c_void_p()
+        _check(lib().vie_tucker_load(dft.handle, _path(path), (C.c_int * 3)(*[int(x) for x in sign]), C.byref(h)))
+        return TuckerForm._from_handle(dft, h, info["dims"], info["ranks"], sign)
+    d, rk = info["dims"], info["ranks"]
+    n = int(np.prod(d)) if info["kind"] == CONTAINER_DENSE else \
+        sum(d[q] * rk[q] for q in range(3)) + (int(np.prod(rk)) if info["kind"] == CONTAINER_TUCKER else 0)
+    buf = np.empty(n, np.complex128)
+    _check(lib().vie_container_read(_path(path), buf.ctypes.data, n))
+    if info["kind"] == CONTAINER_DENSE:
+        return buf.reshape(d, order="F")
+    mats, off = [], 0
+    for q in range(3):
+        mats.append(buf[off:off + d[q] * rk[q]].reshape(d[q], rk[q], order="F"))
+        off += d[q] * rk[q]
+    if info["kind"] == CONTAINER_TUCKER_CP:
+        return ("tucker_cp", tuple(mats))
+    return ("tucker", buf[off:].reshape(rk, order="F"), tuple(mats), info["rule"], info["tol"])
 
 
 def tucker_compress(dft: DftService, t, dims, sign, tol: float = 1e-8, rule: int = RULE_ENERGY) -> TuckerForm:

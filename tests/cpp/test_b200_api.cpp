@@ -724,6 +724,50 @@ int main() {
     expect(rel(yref, y.to_vector()) <= 1e-10, "operator after its DftService");
   });
 
+  // test_container.cpp:22-66 through the drop-in's save_container / load_container
+  run("Container.RoundTripsAndRejectsGarbage", [&] {
+    const std::string dir = "/tmp/";
+    Tensor3 t(3, 4, 5);
+    if (orc_random_tensor(3, 4, 5, 1, reinterpret_cast<double*>(t.data.data()))) throw std::runtime_error(orc_last_error());
+    save_container(dir + "vie_b200_dense.bin", t);
+    ContainerValue v = load_container(dir + "vie_b200_dense.bin");
+    expect(std::holds_alternative<Tensor3>(v) && std::get<Tensor3>(v).data == t.data, "dense round trip");
+    TuckerForm f;
+    f.ranks = {2, 3, 2};
+    f.core = Tensor3(2, 3, 2);
+    for (int q = 0; q < 3; ++q) f.factors[q] = random_matrix(4 + q, f.ranks[static_cast<size_t>(q)], 700 + q);
+    for (size_t i = 0; i < f.core.data.size(); ++i) f.core.data[i] = cplx(0.5 * i, -0.25 * i);
+    f.rule = TruncationRule::Energy;
+    f.tol = 1e-6;
+    save_container(dir + "vie_b200_tucker.bin", f, {4, 5, 6});
+    v = load_container(dir + "vie_b200_tucker.bin");
+    expect(std::holds_alternative<TuckerForm>(v), "tucker kind");
+    const TuckerForm& g = std::get<TuckerForm>(v);
+    expect(g.ranks == f.ranks && g.rule == f.rule && g.tol == f.tol && g.core.data == f.core.data, "tucker header/core");
+    for (int q = 0; q < 3; ++q) expect(g.factors[q].data == f.factors[q].data, "tucker factors");
+    TuckerCPForm c;
+    c.rank = 3;
+    for (int q = 0; q < 3; ++q) c.factors[q] = random_matrix(5, 3, 800 + q);
+    save_container(dir + "vie_b200_tcp.bin", c, {5, 5, 5});
+    v = load_container(dir + "vie_b200_tcp.bin");
+    expect(std::holds_alternative<TuckerCPForm>(v) && std::get<TuckerCPForm>(v).factors[2].data == c.factors[2].data,
+           "tucker_cp round trip");
+    {
+      std::FILE* fp = std::fopen((dir + "vie_b200_garbage.bin").c_str(), "wb");
+      std::fputs("not a container", fp);
+      std::fclose(fp);
+    }
+    bool threw = false;
+    try {
+      load_container(dir + "vie_b200_garbage.bin");
+    } catch (const std::runtime_error&) {
+      threw = true;
+    }
+    expect(threw, "garbage must throw std::runtime_error");
+    for (const char* n : {"vie_b200_dense.bin", "vie_b200_tucker.bin", "vie_b200_tcp.bin", "vie_b200_garbage.bin"})
+      std::remove((dir + n).c_str());
+  });
+
   std::printf("%d failure(s)\n", g_fail);
   return g_fail;
 }
