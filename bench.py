@@ -288,7 +288,7 @@ def run_reference(args):
                                                f"scaled to {2 * S} FFT + {nc} component pieces",
                                      "t_fft3_s": round(t_f1, 2), "t_component_s": round(t_c1, 2)}},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -630,13 +630,33 @@ def run_b200(args):
             "gmres_solve_headline": solve_c4,
             "scene_stages": scene,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist is not None:
         dist.destroy_process_group()
     return 0
 
 
+_JSON_FD = None
+
+
+def emit(line):
+    """The one JSON line of the run, on the original stdout (every other byte -- NCCL banners,
+    library prints -- goes to stderr, see main())."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
 def main():
+    global _JSON_FD
+    # keep stdout for the JSON line alone: native code (NCCL's version banner, ...) may print on
+    # file descriptor 1, so fd 1 is pointed at stderr for the rest of the run
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     args = parse()
     if args.impl == "reference":
         return run_reference(args)

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(256, 2) k_decomp_edge(const double2* __restric
   }
 }
 
-#define VIE_FUSED_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8)
+#define VIE_FUSED_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8) X(8, 20) X(10, 12) X(8, 12) X(8, 10) X(6, 8)
 
 int env_or(const char* name, int dflt) {
   const char* v = std::getenv(name);

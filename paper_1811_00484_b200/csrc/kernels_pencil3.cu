@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(512, 1)
   }
 }
 
-#define VIE_PENCIL3_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8)
+#define VIE_PENCIL3_SHAPES(X) X(10, 20) X(10, 10) X(8, 16) X(8, 8) X(4, 8) X(8, 20) X(10, 12) X(8, 12) X(8, 10) X(6, 8)
 
 // k extent of the load boxes: a divisor of nk, at most 128 (<= 256 per TMA box dim)
 int load_box_k(int nk) {

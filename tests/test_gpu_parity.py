@@ -97,6 +97,8 @@ def test_matvec_pencil2_shapes(vie, dft, orc, kind, basis, dims, rank):
 PENCIL3_CASES = [
     (N, PWL, (5, 6, 32), 3), (K, PWL, (4, 5, 64), 3), (N, PWL, (3, 3, 128), 4), (K, PWL, (3, 4, 200), 3),
     (N, PWL, (6, 2, 100), 3), (N, PWL, (2, 7, 200), 5), (K, PWL, (1, 4, 64), 2), (N, PWL, (4, 5, 200), 25),
+    (N, PWL, (3, 4, 48), 3), (K, PWL, (3, 3, 80), 2), (N, PWL, (4, 3, 96), 3), (K, PWL, (3, 3, 120), 2),
+    (N, PWL, (3, 3, 160), 3), (N, PWC, (8, 3, 120), 3), (K, PWC, (8, 4, 96), 2),
 ]
 
 
@@ -115,6 +117,8 @@ def test_matvec_pencil3_shapes(vie, dft, orc, kind, basis, dims, rank):
 # differ per mode.
 LOOP_CASES = [
     (N, PWL, (5, 6, 32), 3), (K, PWL, (4, 5, 64), 3), (N, PWL, (3, 3, 128), 4), (K, PWL, (3, 4, 200), 3),
+    (N, PWL, (3, 4, 48), 3), (K, PWL, (3, 3, 80), 2), (N, PWL, (4, 3, 96), 3), (K, PWL, (3, 3, 120), 2),
+    (N, PWL, (3, 3, 160), 3),
     (N, PWL, (6, 2, 100), 3), (N, PWL, (70, 9, 32), 4), (K, PWL, (135, 3, 64), 2), (N, PWL, (4, 5, 200), 25),
 ]
 
