@@ -449,6 +449,14 @@ def run_b200(args):
         if dist is not None:
             dist.all_reduce(y)
 
+    exchange_note = None
+    if slab and not args.torch_exchange:
+        try:  # the first library-path matvec; a failure is recorded and the torch exchange takes over
+            step()
+            torch.cuda.synchronize()
+        except Exception as e:  # noqa: BLE001
+            exchange_note = f"library exchange failed ({type(e).__name__}: {e}); torch all_to_all_single used"
+            sm = SlabMatvec(op, rank, world, comm=None)
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -603,7 +611,8 @@ def run_b200(args):
             "data": "synthetic (spatial-domain Tucker forms, CN(0,1), parity rows zeroed; CN(0,1) currents)",
             "config": config_dict(args, grid, basis, r, nc, S),
             "parallelism": (f"slab decomposition x{world} (z-planes / axis-1 positions, NCCL all-to-all "
-                            f"{'via torch' if args.torch_exchange else 'inside libvie_b200 (vie_slab_matvec)'})" if slab
+                            f"{'via torch' if args.torch_exchange or exchange_note else 'inside libvie_b200 (vie_slab_matvec)'})"
+                            + (f"; {exchange_note}" if exchange_note else "") if slab
                             else f"components sharded x{world}") if world > 1 else "1 GPU",
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,

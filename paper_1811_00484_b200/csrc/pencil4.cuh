@@ -236,14 +236,15 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
   }();
   auto pi_of = [](int i) { return static_cast<int>((PI >> (3 * i)) & 7ull); };
   const int gq = lane >> 2, tq = lane & 3;  // fragment group / thread in group
-  // X (B operand, 4 x 8 col): source s = 4 ks + tq, column gq = point n (gq & 3), part gq >> 2
-  const int xn = gq & 3;
-  const int xm3 = xn >> 1;
-  const uint32_t xoff = static_cast<uint32_t>(16 * (xn & 1) + 8 * (gq >> 2));  // bytes: m1f line, re / im
+  // X (B operand, 4 x 8 col): source s = 4 ks + tq; column gq = m1f | part << 1 | m3f << 2, so a
+  // half warp (gq < 4 / gq >= 4) reads one 128-byte run of one slot (no bank conflict between
+  // the two mirror slots)
+  const int xm1 = gq & 1, xpart = (gq >> 1) & 1, xm3 = gq >> 2;
+  const uint32_t xoff = static_cast<uint32_t>(16 * xm1 + 8 * xpart);  // bytes: m1f line, re / im
   unsigned long long xsg[3];
 #pragma unroll
   for (int ks = 0; ks < 3; ++ks)
-    xsg[ks] = pattern_sign(pi_of(4 * ks + tq) ^ SG.G, (xn & 1) | (m2f << 1) | (xm3 << 2));
+    xsg[ks] = pattern_sign(pi_of(4 * ks + tq) ^ SG.G, xm1 | (m2f << 1) | (xm3 << 2));
   // A (8 x 4 row): target t = tau4(mt, gq), source s = 4 ks + tq
   int aoff[6];
   unsigned long long asg[6];
@@ -255,9 +256,9 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
     aoff[f] = c >= 0 ? c * UB : SH::ZOFF - warp;  // no block / padding row: a zero slot
     asg[f] = (c >= 0 && c_bm4[KIND].coef[t * 12 + s] < 0) ? (1ull << 63) : 0ull;
   }
-  // D (8 x 8): row gq = target tau4(mt, gq); columns 2 tq + e: point n = 2 (tq & 1) + e,
-  // part tq >> 1 (after the exchange each lane finalises one double)
-  const int ym3 = tq & 1, ypart = tq >> 1;
+  // D (8 x 8): row gq = target tau4(mt, gq); columns 2 tq + e = m1f e, part tq & 1, m3f tq >> 1
+  // (after the exchange with lane tq ^ 1 each lane finalises one double)
+  const int ym3 = tq >> 1, ypart = tq & 1;
   const unsigned long long ysub = ypart ? 0ull : (1ull << 63);  // Yr = D1 - D2', Yi = D1 + D2'
   uint32_t yoff[2][2];  // [mt][e] bytes within a slot; ~0u: padding row
   unsigned long long ysg[2][2];
@@ -306,7 +307,7 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const double v = __shfl_xor_sync(0xffffffffu, d2[mt][e], 2);
+          const double v = __shfl_xor_sync(0xffffffffu, d2[mt][e], 1);
           const double r = d1[mt][e] + flip1(v, ysub);
           if (ystore && yoff[mt][e] != ~0u) sts1(ybase + yoff[mt][e], flip1(r, ysg[mt][e]));
         }
