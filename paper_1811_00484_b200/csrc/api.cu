@@ -105,6 +105,8 @@ struct vie_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   std::mutex mu;
+  double* post_partials = nullptr;  // vie_postprocess partial sums (kRedBlocks + 1), allocated once
+  std::mutex post_mu;               // serialises vie_postprocess calls on this context
   // plan cache keyed by (length, pruned, wide)
   std::map<std::tuple<int, bool, bool>, std::unique_ptr<PlanHolder>> plans;
   // references: the caller's (vie_ctx_create) plus one per live Tucker form and operator,
@@ -129,6 +131,7 @@ void ctx_release(vie_ctx c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->stream);
   c->plans.clear();
+  if (c->post_partials) cudaFree(c->post_partials);
   cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -2077,16 +2080,20 @@ int vie_postprocess(vie_ctx ctx, const vie_scene* scene, const double* eps_r, co
     if (h && !b1_plus) throw Invalid("postprocess: b1_plus buffer needed with h");
     const vie::SceneDev sc = make_scene(scene, 1);
     cudaStream_t st = ctx_stream(ctx, stream);
-    // per-device partials buffer, allocated once (a pool allocation per call costs
-    // milliseconds when the pool trims at the synchronisation below); the call holds
-    // the lock until its result is read, so concurrent calls serialise here
-    static std::mutex buf_mu;
-    static std::map<int, double*> bufs;
-    std::lock_guard<std::mutex> lock(buf_mu);
-    int dev = 0;
-    VIE_CUDA_CHECK(cudaGetDevice(&dev));
-    double*& buf = bufs[dev];
-    if (!buf) VIE_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&buf), sizeof(double) * (vie::kRedBlocks + 1)));
+    // partials buffer: owned by the context and allocated once (a pool allocation per call
+    // costs milliseconds when the pool trims at the synchronisation below); calls on one
+    // context serialise on its lock until their result is read.  Without a context: a
+    // per-call allocation, freed on return.
+    std::unique_lock<std::mutex> lock;
+    DevPool own;
+    double* buf = nullptr;
+    if (ctx) {
+      lock = std::unique_lock<std::mutex>(ctx->post_mu);
+      if (!ctx->post_partials) ctx->post_partials = dev_alloc<double>(vie::kRedBlocks + 1);
+      buf = ctx->post_partials;
+    } else {
+      buf = own.alloc<double>(vie::kRedBlocks + 1);
+    }
     vie::launch_postprocess(sc, reinterpret_cast<const double2*>(eps_r), reinterpret_cast<const double2*>(e),
                             reinterpret_cast<const double2*>(h), p_abs, h ? b1_plus : nullptr, buf + 1, buf,
                             sc.res[0] * sc.res[1] * sc.res[2], st);
