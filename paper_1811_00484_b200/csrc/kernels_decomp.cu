@@ -43,9 +43,16 @@ __global__ void __launch_bounds__(kThreads) k_decomp_z(const double2* __restrict
   double2* zc = Z + cd.off_z;
   for (int e = threadIdx.x; e < np * r1; e += blockDim.x) {
     const int a = e % r1, p2 = e / r1;
-    double2 acc = make_double2(0.0, 0.0);
-    for (int b = 0; b < r2; ++b) cfma(acc, __ldg(core + a + r1 * b), __ldg(u2 + p2 + static_cast<int64_t>(np) * b));
-    zc[(static_cast<int64_t>(p2) * r1 + a) * r3 + g] = acc;
+    // four independent partial sums: the loads of four b run ahead of the FMA chain
+    double2 acc[4] = {};
+    int b = 0;
+    for (; b + 4 <= r2; b += 4)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        cfma(acc[i], __ldg(core + a + r1 * (b + i)), __ldg(u2 + p2 + static_cast<int64_t>(np) * (b + i)));
+    for (; b < r2; ++b) cfma(acc[0], __ldg(core + a + r1 * b), __ldg(u2 + p2 + static_cast<int64_t>(np) * b));
+    zc[(static_cast<int64_t>(p2) * r1 + a) * r3 + g] =
+        make_double2((acc[0].x + acc[1].x) + (acc[2].x + acc[3].x), (acc[0].y + acc[1].y) + (acc[2].y + acc[3].y));
   }
 }
 
