@@ -194,6 +194,13 @@ typedef struct vie_comm_s* vie_comm;
 int vie_comm_unique_id(unsigned char id[VIE_COMM_ID_BYTES]);
 int vie_comm_create(vie_ctx ctx, int nranks, int rank, const unsigned char id[VIE_COMM_ID_BYTES], vie_comm* out);
 int vie_comm_destroy(vie_comm comm);
+/* Loopback transport for tests: R ranks of ONE process (one host thread per rank, e.g. all on
+ * one GPU) exchanging by device copies between host barriers; every call that exchanges or
+ * all-reduces must be made by all R threads.                                              */
+typedef struct vie_loopback_s* vie_loopback;
+int vie_loopback_create(int nranks, vie_loopback* out);
+int vie_loopback_destroy(vie_loopback lb);
+int vie_comm_create_loopback(vie_ctx ctx, vie_loopback lb, int rank, vie_comm* out);
 int vie_op_set_comm(vie_op op, vie_comm comm);
 int vie_slab_matvec(vie_op op, const double* x_local, double* y_local, const double* eps_local, double inv_v,
                     int diag_term, void* stream);

@@ -10,6 +10,7 @@
 #include <cstring>
 #include <fstream>
 #include <atomic>
+#include <condition_variable>
 #include <functional>
 #include <map>
 #include <tuple>
@@ -115,8 +116,35 @@ struct vie_ctx_s {
 };
 
 // NCCL communicator over the ranks of a slab-partitioned operator (one process per GPU)
+// Loopback transport (tests): R ranks of one process (one host thread each, any devices),
+// exchanging through device-to-device copies between host barriers -- no kernel ever waits on
+// another rank's kernel.  Same chunk semantics as the NCCL exchange.
+struct vie_loopback_s {
+  int nranks = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t generation = 0;
+  std::vector<void*> ptr;             // per rank: the buffer published for the current step
+  std::vector<std::vector<double>> h;  // per rank: host scalars of an all-reduce
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t gen = generation;
+    if (++arrived == nranks) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
+// NCCL communicator over the ranks of a slab-partitioned operator (one process per GPU), or
+// the loopback transport above
 struct vie_comm_s {
   ncclComm_t nccl = nullptr;
+  vie_loopback_s* lb = nullptr;
   int nranks = 1, rank = 0;
   int device = 0;
   ~vie_comm_s() {
@@ -1153,6 +1181,18 @@ void slab_exchange(vie_op op, const double2* send, double2* recv, cudaStream_t s
   const Geom& g = op->g;
   const size_t chunk = static_cast<size_t>(g.S) * g.nk * g.n2 * g.W;  // double2 per peer
   vie_comm c = op->comm;
+  if (c->lb) {  // loopback: send chunk q -> rank q's recv chunk [rank], between host barriers
+    vie_loopback_s* lb = c->lb;
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));  // send is complete, recv is free
+    lb->ptr[static_cast<size_t>(c->rank)] = recv;
+    lb->barrier();
+    for (int q = 0; q < c->nranks; ++q)
+      VIE_CUDA_CHECK(cudaMemcpyAsync(static_cast<double2*>(lb->ptr[static_cast<size_t>(q)]) + c->rank * chunk,
+                                     send + q * chunk, sizeof(double2) * chunk, cudaMemcpyDefault, st));
+    VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+    lb->barrier();  // every rank's chunks have landed
+    return;
+  }
   if (ncclGroupStart() != ncclSuccess) throw NcclError("ncclGroupStart failed");
   for (int q = 0; q < c->nranks; ++q) {
     const ncclResult_t r1 = ncclSend(send + q * chunk, 2 * chunk, ncclDouble, q, c->nccl, st);
@@ -1254,6 +1294,34 @@ int vie_comm_create(vie_ctx ctx, int nranks, int rank, const unsigned char id[VI
 
 int vie_comm_destroy(vie_comm comm) {
   return guard([&] { delete comm; });
+}
+
+int vie_loopback_create(int nranks, vie_loopback* out) {
+  return guard([&] {
+    if (nranks < 1 || !out) throw Invalid("loopback_create: bad size / null argument");
+    std::unique_ptr<vie_loopback_s> lb(new vie_loopback_s);
+    lb->nranks = nranks;
+    lb->ptr.assign(static_cast<size_t>(nranks), nullptr);
+    lb->h.assign(static_cast<size_t>(nranks), {});
+    *out = lb.release();
+  });
+}
+
+int vie_loopback_destroy(vie_loopback lb) {
+  return guard([&] { delete lb; });
+}
+
+int vie_comm_create_loopback(vie_ctx ctx, vie_loopback lb, int rank, vie_comm* out) {
+  return guard([&] {
+    if (!ctx || !lb || !out) throw Invalid("comm_create_loopback: null argument");
+    if (rank < 0 || rank >= lb->nranks) throw Invalid("comm_create_loopback: bad rank");
+    std::unique_ptr<vie_comm_s> c(new vie_comm_s);
+    c->lb = lb;
+    c->nranks = lb->nranks;
+    c->rank = rank;
+    c->device = ctx->device;
+    *out = c.release();
+  });
 }
 
 int vie_op_set_comm(vie_op op, vie_comm comm) {
@@ -1610,7 +1678,23 @@ int vie_gmres_solve(vie_op op, const double* eps_r, double inv_v, const double* 
     DevReduce allreduce;
     if (dist)
       allreduce = [&](double2* p, int count) {
-        const ncclResult_t rr = ncclAllReduce(p, p, 2 * static_cast<size_t>(count), ncclDouble, ncclSum, op->comm->nccl, st);
+        vie_comm c = op->comm;
+        if (c->lb) {  // loopback: host sum in rank order, the same on every rank
+          vie_loopback_s* lb = c->lb;
+          auto& mine = lb->h[static_cast<size_t>(c->rank)];
+          mine.resize(2 * static_cast<size_t>(count));
+          VIE_CUDA_CHECK(cudaMemcpyAsync(mine.data(), p, sizeof(double2) * count, cudaMemcpyDeviceToHost, st));
+          VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+          lb->barrier();
+          std::vector<double> sum(2 * static_cast<size_t>(count), 0.0);
+          for (int q = 0; q < c->nranks; ++q)
+            for (size_t i = 0; i < sum.size(); ++i) sum[i] += lb->h[static_cast<size_t>(q)][i];
+          lb->barrier();  // every rank has read every contribution
+          VIE_CUDA_CHECK(cudaMemcpyAsync(p, sum.data(), sizeof(double2) * count, cudaMemcpyHostToDevice, st));
+          VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+          return;
+        }
+        const ncclResult_t rr = ncclAllReduce(p, p, 2 * static_cast<size_t>(count), ncclDouble, ncclSum, c->nccl, st);
         if (rr != ncclSuccess) throw NcclError(std::string("ncclAllReduce: ") + ncclGetErrorString(rr));
       };
     const GmresOut r = gmres_core(st, n, sysmv, make_precond(precond, n, st), allreduce,

@@ -70,6 +70,9 @@ def lib() -> C.CDLL:
         L.vie_comm_unique_id.argtypes = [C.c_char_p]
         L.vie_comm_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.POINTER(C.c_void_p)]
         L.vie_comm_destroy.argtypes = [C.c_void_p]
+        L.vie_loopback_create.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+        L.vie_loopback_destroy.argtypes = [C.c_void_p]
+        L.vie_comm_create_loopback.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
         L.vie_op_set_comm.argtypes = [C.c_void_p, C.c_void_p]
         L.vie_slab_matvec.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_int,
                                       C.c_void_p]
@@ -427,14 +430,39 @@ def comm_unique_id() -> bytes:
     return buf.raw
 
 
-class Comm:
-    """NCCL communicator of the library (vie_comm_create) over `world` ranks, one per GPU."""
+class Loopback:
+    """Shared state of a loopback transport (vie_loopback_create): `world` ranks of this process,
+    one host thread each, exchanging by device copies between host barriers (tests)."""
 
-    def __init__(self, dft: DftService, world: int, rank: int, uid: bytes):
-        if len(uid) != COMM_ID_BYTES:
-            raise ValueError("Comm: unique id must be COMM_ID_BYTES bytes")
-        self.world, self.rank, self.dft = world, rank, dft
+    def __init__(self, world: int):
+        self.world = world
         self.handle = C.c_void_p()
+        _check(lib().vie_loopback_create(int(world), C.byref(self.handle)))
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().vie_loopback_destroy(self.handle)
+                self.handle = C.c_void_p()
+        except Exception:
+            pass
+
+
+class Comm:
+    """Communicator of the library over `world` ranks: NCCL (vie_comm_create, one process per
+    GPU) or, with `loopback`, the test transport (vie_comm_create_loopback)."""
+
+    def __init__(self, dft: DftService, world: int, rank: int, uid: bytes | None = None,
+                 loopback: Loopback | None = None):
+        self.world, self.rank, self.dft, self._lb = world, rank, dft, loopback
+        self.handle = C.c_void_p()
+        if loopback is not None:
+            if loopback.world != world:
+                raise ValueError("Comm: loopback size differs from world")
+            _check(lib().vie_comm_create_loopback(dft.handle, loopback.handle, int(rank), C.byref(self.handle)))
+            return
+        if uid is None or len(uid) != COMM_ID_BYTES:
+            raise ValueError("Comm: unique id must be COMM_ID_BYTES bytes")
         _check(lib().vie_comm_create(dft.handle, int(world), int(rank), uid, C.byref(self.handle)))
 
     def __del__(self):

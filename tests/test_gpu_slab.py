@@ -128,3 +128,66 @@ def test_library_exchange_and_distributed_gmres_single_rank(vie, dft, orc):
     assert np.max(np.abs(np.array(r1.residual_history) - np.array(r2.residual_history))
                   / np.array(r1.residual_history)) <= 1e-10
     assert rel(r1.solution.cpu().numpy(), r2.solution.cpu().numpy()) <= 1e-10
+
+
+@pytest.mark.parametrize("world,dims,basis", [(2, (6, 4, 6), PWL), (3, (6, 4, 6), PWL), (4, (4, 4, 8), PWL),
+                                              (2, (8, 6, 10), PWC)])
+def test_library_slab_matvec_and_distributed_gmres_loopback(vie, dft, orc, world, dims, basis):
+    """vie_slab_matvec and the distributed vie_gmres_solve at R > 1: R ranks as R host threads of
+    this process on one GPU, each with its own context, operator and loopback communicator (the
+    library's exchange and all-reduce paths with device copies between host barriers instead of
+    NCCL -- no kernel waits on another rank).  The assembled result equals the single-GPU path."""
+    import threading
+
+    import torch
+
+    from paper_1811_00484_b200.sharding import SlabMatvec, local_slab
+
+    S = 3 if basis == PWC else 12
+    n1, n2, n3 = dims
+    nv = int(np.prod(dims))
+    x = torch.from_numpy(random_field(basis, dims, 61)).cuda()
+    rng = np.random.default_rng(12)
+    eps = torch.from_numpy(2 + rng.random(nv) + 0.3j * rng.random(nv)).cuda()
+    rhs = torch.from_numpy(random_field(basis, dims, 62)).cuda()
+    op1 = make_ops(vie, dft, orc, N, basis, dims, 3, 23, scale=0.05)[0]
+    y_ref = vie.apply_operator(op1, x)
+    ys_ref = vie.apply_system(eps, 0.7, op1, x)
+    cfg = vie.GmresConfig(1e-10, 12, 2)
+    g_ref = vie.gmres(op1, eps, 0.7, rhs, cfg)
+    lb = vie.Loopback(world)
+    dfts = [vie.DftService(0) for _ in range(world)]
+    ops = [make_ops(vie, dfts[r], orc, N, basis, dims, 3, 23, scale=0.05)[0] for r in range(world)]
+    comms = [vie.Comm(dfts[r], world, r, loopback=lb) for r in range(world)]
+    sms = [SlabMatvec(ops[r], r, world, comm=comms[r]) for r in range(world)]
+    xs = [local_slab(x, S, n3, n1 * n2, r, world).contiguous() for r in range(world)]
+    es = [local_slab(eps, 1, n3, n1 * n2, r, world).contiguous() for r in range(world)]
+    bs = [local_slab(rhs, S, n3, n1 * n2, r, world).contiguous() for r in range(world)]
+    out, errs = [None] * world, []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            y = sms[r].apply(xs[r])
+            ys = sms[r].apply(xs[r], eps_local=es[r], inv_v=0.7)
+            g = vie.gmres(ops[r], es[r], 0.7, bs[r], cfg)
+            torch.cuda.synchronize()
+            out[r] = (y, ys, g)
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    nk = n3 // world
+    cat = lambda vs: torch.cat([v.view(S, nk, n1 * n2) for v in vs], dim=1).reshape(-1).cpu().numpy()
+    assert rel(y_ref.cpu().numpy(), cat([o[0] for o in out])) <= 1e-13
+    assert rel(ys_ref.cpu().numpy(), cat([o[1] for o in out])) <= 1e-13
+    for o in out:  # every rank reports the same (global) iteration history
+        assert o[2].iterations == g_ref.iterations and o[2].converged == g_ref.converged
+        assert np.max(np.abs(np.array(o[2].residual_history) - np.array(g_ref.residual_history))
+                      / np.array(g_ref.residual_history)) <= 1e-9
+    assert rel(g_ref.solution.cpu().numpy(), cat([o[2].solution for o in out])) <= 1e-9
