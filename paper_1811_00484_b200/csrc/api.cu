@@ -229,6 +229,8 @@ struct vie_op_s {
   double2* xs_out = nullptr;
   double2* xs_back = nullptr;
   cudaEvent_t ev_slab = nullptr;
+  cudaStream_t s_comm = nullptr;     // vie_slab_matvec: the exchange stream
+  std::vector<cudaEvent_t> ev_grp;   // vie_slab_matvec: per current group, 4 events
   // host-buffer staging (vie_matvec_host; the batch call double-buffers with hx2 / hy2)
   double2* hx = nullptr;
   double2* hy = nullptr;
@@ -276,6 +278,8 @@ struct vie_op_s {
     if (s_d2h) cudaStreamDestroy(s_d2h);
     if (ev_user) cudaEventDestroy(ev_user);
     if (ev_slab) cudaEventDestroy(ev_slab);
+    for (cudaEvent_t e : ev_grp) cudaEventDestroy(e);
+    if (s_comm) cudaStreamDestroy(s_comm);
     if (ctx) ctx_release(ctx);
   }
 };
@@ -1145,42 +1149,50 @@ void slab_decomp(vie_op op, cudaStream_t st) {
                        false, g.n1, g.n1 + 1, op->u3img);
 }
 
+// The rank's pencil kernels on its axis-1 groups (B -> Bo)
+void slab_pencils(vie_op op, cudaStream_t st) {
+  const Geom& g = op->g;
+  if (op->pencil3) {
+    if (g.p1off == 0)
+      vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
+                         st, 1);
+    vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
+    if (op->pencil4) vie::launch_pencil4(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+    else vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+  } else if (op->pencil2) {
+    if (g.p1off == 0)
+      vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
+                         st, 1);
+    vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
+  } else {
+    vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st);
+  }
+}
+
+// axis-2 FFTs of the rank's W columns over all k-planes (recv -> B) / inverse (Bo -> out); gc:
+// the column geometry of the currents moved, pm: their planes in B (current groups)
+void slab_col_fwd(vie_op op, const double2* recv, const Geom& gc, vie::PlaneMap pm, cudaStream_t st) {
+  if (op->q2) vie::launch_col_fwd2(recv, op->B, gc, op->Q2, st, pm);
+  else vie::launch_col_fwd(recv, op->B, gc, op->P2, st);
+}
+void slab_col_inv(vie_op op, double2* out, const Geom& gc, vie::PlaneMap pm, cudaStream_t st) {
+  if (op->q2) vie::launch_col_inv2(op->Bo, out, gc, op->Q2, st, pm);
+  else vie::launch_col_inv(op->Bo, nullptr, out, gc, op->P2, st);
+}
+
 // axis-2 FFTs of the rank's columns, the pencil stage on its octant rows, inverse axis-2 FFTs
 void slab_pencil_stage(vie_op op, const double2* recv, double2* out, cudaStream_t st, bool with_decomp) {
-  const Geom& g = op->g;
   const Geom gc = slab_geom_cols(op);
-  // axis-2 FFTs of the rank's W columns over all k-planes: recv -> B
-  if (op->q2) vie::launch_col_fwd2(recv, op->B, gc, op->Q2, st);
-  else vie::launch_col_fwd(recv, op->B, gc, op->P2, st);
+  slab_col_fwd(op, recv, gc, {}, st);
   if (with_decomp) slab_decomp(op, st);
-  {
-    if (op->pencil3) {
-      if (g.p1off == 0)
-        vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
-                           st, 1);
-      vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st, 0, 2);
-      if (op->pencil4) vie::launch_pencil4(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
-      else vie::launch_pencil3(op->kind, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
-    } else if (op->pencil2) {
-      if (g.p1off == 0)
-        vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active,
-                           st, 1);
-      vie::launch_pencil2(op->kind, op->basis, op->B, op->Bo, op->Shat, g, op->P3.tw, st);
-    } else {
-      vie::launch_pencil(op->kind, op->basis, op->B, op->Bo, nullptr, op->Shat, g, op->PH, op->P3.tw, op->active, st);
-    }
-  }
-  // inverse axis-2 FFTs: Bo -> out (blocked by z-slab rank)
-  if (op->q2) vie::launch_col_inv2(op->Bo, out, gc, op->Q2, st);
-  else vie::launch_col_inv(op->Bo, nullptr, out, gc, op->P2, st);
+  slab_pencils(op, st);
+  slab_col_inv(op, out, gc, {}, st);
 }
 
 // equal-split all-to-all of the rank-blocked slab (chunk q <-> rank q) as grouped NCCL
 // point-to-point calls on `st` (the exchange step of SURVEY 8(e))
-void slab_exchange(vie_op op, const double2* send, double2* recv, cudaStream_t st) {
-  const Geom& g = op->g;
-  const size_t chunk = static_cast<size_t>(g.S) * g.nk * g.n2 * g.W;  // double2 per peer
-  vie_comm c = op->comm;
+void slab_exchange(vie_op op, const double2* send, double2* recv, size_t chunk, cudaStream_t st) {
+  vie_comm c = op->comm;  // chunk: double2 per peer
   if (c->lb) {  // loopback: send chunk q -> rank q's recv chunk [rank], between host barriers
     vie_loopback_s* lb = c->lb;
     VIE_CUDA_CHECK(cudaStreamSynchronize(st));  // send is complete, recv is free
@@ -1203,8 +1215,12 @@ void slab_exchange(vie_op op, const double2* send, double2* recv, cudaStream_t s
   if (r != ncclSuccess) throw NcclError(std::string("ncclGroupEnd: ") + ncclGetErrorString(r));
 }
 
-// The whole slab matvec of this rank with the in-library exchange; the x-independent
-// decomposition runs on the side stream while the axis-1 FFTs and the forward exchange run.
+// The whole slab matvec of this rank with the in-library exchange.  The x-independent
+// decomposition runs on the side stream from the start; the S currents move in G groups (SURVEY
+// 8(e): the all-to-all of one group overlaps the FFTs of the others): on the compute stream the
+// axis-1 FFTs of every group, then per group [wait for its exchange] its axis-2 FFTs; the
+// exchanges run on the comm stream as each group's FFTs finish.  The same on the way back.
+// Exchange buffers are group-major: [g][rank][s in group][k][j][w < W].
 void slab_matvec_run(vie_op op, const double2* x, double2* y, const double2* eps, double inv_v, int diag,
                      cudaStream_t st) {
   if (!op->comm) throw Invalid("slab_matvec: no communicator (vie_op_set_comm)");
@@ -1213,21 +1229,76 @@ void slab_matvec_run(vie_op op, const double2* x, double2* y, const double2* eps
   const int64_t se = static_cast<int64_t>(g.S) * g.nk * g.n2 * g.m1;
   for (double2** p : {&op->xs_send, &op->xs_recv, &op->xs_out, &op->xs_back})
     if (!*p) *p = dev_alloc<double2>(static_cast<size_t>(se));
-  if (!op->ev_slab) VIE_CUDA_CHECK(cudaEventCreateWithFlags(&op->ev_slab, cudaEventDisableTiming));
+  // current groups: PWL 3 x 4 (the apply_system weights repeat every 4 currents), PWC 3 x 1
+  static const int g_env = env_int("VIE_SLAB_GROUPS", 3);
+  const int G = (op->q1 && op->q2 && g_env > 1 && g.S % g_env == 0 && (g.S / g_env) % (g.S == 12 ? 4 : 1) == 0)
+                    ? g_env : 1;
+  const int Sg = g.S / G, R = op->nranks;
+  if (!op->s_comm) VIE_CUDA_CHECK(cudaStreamCreateWithFlags(&op->s_comm, cudaStreamNonBlocking));
+  if (static_cast<int>(op->ev_grp.size()) < 4 * G) {
+    for (cudaEvent_t e : op->ev_grp) cudaEventDestroy(e);
+    op->ev_grp.assign(static_cast<size_t>(4 * G), nullptr);
+    for (cudaEvent_t& e : op->ev_grp) VIE_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaEvent_t* ev_row = op->ev_grp.data();
+  cudaEvent_t* ev_in = ev_row + G;
+  cudaEvent_t* ev_ci = ev_in + G;
+  cudaEvent_t* ev_back = ev_ci + G;
+  cudaStream_t cs = op->s_comm;
   VIE_CUDA_CHECK(cudaEventRecord(op->ev_fork, st));
   VIE_CUDA_CHECK(cudaStreamWaitEvent(op->side, op->ev_fork, 0));
   slab_decomp(op, op->side);
   VIE_CUDA_CHECK(cudaEventRecord(op->ev_join, op->side));
-  const Geom gl = slab_geom_rows(op);
-  if (op->q1) vie::launch_row_fwd2(x, op->xs_send, gl, op->Q1, st);
-  else vie::launch_row_fwd(x, op->xs_send, gl, op->P1, st);
-  slab_exchange(op, op->xs_send, op->xs_recv, st);
+  Geom gl = slab_geom_rows(op);  // one group's rows: S = Sg
+  gl.S = Sg;
+  Geom gc = slab_geom_cols(op);  // one group's column planes
+  gc.S = Sg;
+  const size_t chunk = static_cast<size_t>(Sg) * g.nk * g.n2 * g.W;  // double2 per peer per group
+  const int64_t xg = static_cast<int64_t>(Sg) * g.nk * g.n2 * g.n1;   // x / y elements per group
+  const int64_t blk = static_cast<int64_t>(R) * chunk;                // exchange elements per group
+  auto pmap = [&](int gi) {
+    vie::PlaneMap pm;
+    pm.in_per_r = Sg * g.nk;
+    pm.out_per_r = g.S * g.nk;
+    pm.off = gi * Sg * g.nk;
+    return pm;
+  };
+  for (int gi = 0; gi < G; ++gi) {
+    if (op->q1) vie::launch_row_fwd2(x + gi * xg, op->xs_send + gi * blk, gl, op->Q1, st);
+    else vie::launch_row_fwd(x + gi * xg, op->xs_send + gi * blk, gl, op->P1, st);
+    VIE_CUDA_CHECK(cudaEventRecord(ev_row[gi], st));
+  }
+  for (int gi = 0; gi < G; ++gi) {
+    VIE_CUDA_CHECK(cudaStreamWaitEvent(cs, ev_row[gi], 0));
+    slab_exchange(op, op->xs_send + gi * blk, op->xs_recv + gi * blk, chunk, cs);
+    VIE_CUDA_CHECK(cudaEventRecord(ev_in[gi], cs));
+  }
+  for (int gi = 0; gi < G; ++gi) {
+    VIE_CUDA_CHECK(cudaStreamWaitEvent(st, ev_in[gi], 0));
+    slab_col_fwd(op, op->xs_recv + gi * blk, gc, pmap(gi), st);
+  }
   VIE_CUDA_CHECK(cudaStreamWaitEvent(st, op->ev_join, 0));
-  slab_pencil_stage(op, op->xs_recv, op->xs_out, st, false);
-  slab_exchange(op, op->xs_out, op->xs_back, st);
+  slab_pencils(op, st);
+  for (int gi = 0; gi < G; ++gi) {
+    slab_col_inv(op, op->xs_out + gi * blk, gc, pmap(gi), st);
+    VIE_CUDA_CHECK(cudaEventRecord(ev_ci[gi], st));
+  }
+  for (int gi = 0; gi < G; ++gi) {
+    VIE_CUDA_CHECK(cudaStreamWaitEvent(cs, ev_ci[gi], 0));
+    slab_exchange(op, op->xs_out + gi * blk, op->xs_back + gi * blk, chunk, cs);
+    VIE_CUDA_CHECK(cudaEventRecord(ev_back[gi], cs));
+  }
   const double ne = 8.0 * g.n1 * static_cast<double>(g.n2) * g.n3;  // global N_e
-  if (op->q1) vie::launch_row_inv2(op->xs_back, y, gl, op->Q1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
-  else vie::launch_row_inv(op->xs_back, y, gl, op->P1, 1.0 / ne, eps, x, inv_v, op->basis, diag, st);
+  for (int gi = 0; gi < G; ++gi) {
+    VIE_CUDA_CHECK(cudaStreamWaitEvent(st, ev_back[gi], 0));
+    const double2* xgi = x + gi * xg;
+    if (op->q1)
+      vie::launch_row_inv2(op->xs_back + gi * blk, y + gi * xg, gl, op->Q1, 1.0 / ne, eps, xgi, inv_v, op->basis, diag,
+                           st);
+    else
+      vie::launch_row_inv(op->xs_back + gi * blk, y + gi * xg, gl, op->P1, 1.0 / ne, eps, xgi, inv_v, op->basis, diag,
+                          st);
+  }
 }
 }  // namespace
 

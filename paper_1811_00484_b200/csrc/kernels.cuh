@@ -133,8 +133,17 @@ struct Pass2 {
 };
 bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw, int row_lines);
 void launch_row_fwd2(const double2* x, double2* A, const Geom& g, const Pass2& P, cudaStream_t st);
-void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st);
-void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st);
+// Plane remap of the slab-blocked column passes (current groups of the overlapped multi-GPU
+// exchange): plane p of the group-local side <-> plane (p / in_per_r) out_per_r + off + p % in_per_r
+// of the full spectral slab.  Default: identity.
+struct PlaneMap {
+  int in_per_r = 1 << 30, out_per_r = 1 << 30, off = 0;
+  __host__ __device__ int64_t operator()(int p) const {
+    return static_cast<int64_t>(p / in_per_r) * out_per_r + off + p % in_per_r;
+  }
+};
+void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st, PlaneMap pm = {});
+void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st, PlaneMap pm = {});
 void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P, double scale, const double2* eps,
                      const double2* xin, double inv_v, int basis, int diag, cudaStream_t st);
 

@@ -248,14 +248,14 @@ static_assert((kCW & (kCW - 1)) == 0, "column tile must be a power of two");
 constexpr int kLgCW = kCW == 8 ? 3 : (kCW == 4 ? 2 : (kCW == 16 ? 4 : 0));
 
 __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
-                                                     Pass2 P, int64_t bps) {
+                                                     Pass2 P, int64_t bps, PlaneMap pm) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
   const int wc = min(kCW, m1 - c0);
   const int64_t plane = blockIdx.y;
   const double2* src = A + plane * n * m1 + c0;
-  double2* dst = B + plane * bps + c0;
+  double2* dst = B + pm(static_cast<int>(plane)) * bps + c0;
   if (R1 == 1) {
     const int w = threadIdx.x;
     if (w < wc)
@@ -293,13 +293,13 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
 }
 
 __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
-                                                     Pass2 P, int64_t bps) {
+                                                     Pass2 P, int64_t bps, PlaneMap pm) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
   const int c0 = blockIdx.x * kCW;
   const int wc = min(kCW, m1 - c0);
   const int64_t plane = blockIdx.y;
-  const double2* src = B + plane * bps + c0;
+  const double2* src = B + pm(static_cast<int>(plane)) * bps + c0;
   double2* dst = A + plane * n * m1 + c0;
   if (R1 == 1) {
     const int w = threadIdx.x;
@@ -407,21 +407,21 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
 
 // Column passes over the S * nk planes of a Geom, rows of length W (= m1 on one GPU;
 // the rank's axis-1 positions in the slab-decomposed pencil stage).
-void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st) {
+void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P, cudaStream_t st, PlaneMap pm) {
   const size_t sm = pass2_smem(P, kCW);
   dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
   if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2), sm);
-  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.W, P, g.bps);
+  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.W, P, g.bps, pm);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st) {
+void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P, cudaStream_t st, PlaneMap pm) {
   const size_t sm = pass2_smem(P, kCW);
   dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
   if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2), sm);
-  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.W, P, g.bps);
+  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.W, P, g.bps, pm);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
