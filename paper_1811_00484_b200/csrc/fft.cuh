@@ -67,11 +67,43 @@ __device__ __forceinline__ double2 twc(double2 x) {
   }
 }
 
+constexpr int gcd_c(int a, int b) { return b == 0 ? a : gcd_c(b, a % b); }
+constexpr int inv_mod(int a, int m) {  // a^-1 mod m (a, m coprime)
+  for (int x = 1; x < m; ++x)
+    if ((a * x) % m == 1) return x;
+  return 1;
+}
+
 template <int R, bool INV, int ST, int OFF>
 struct DFTs {
   static constexpr int A = first_factor(R);
   static constexpr int B = R / A;
   __device__ __forceinline__ static void run(double2* v) {
+    if constexpr (gcd_c(A, B) == 1 && B > 1) {
+      // Good-Thomas prime-factor algorithm (A, B coprime): no inner twiddles.  Input index
+      // n = (B n1 + A n2) mod R; output k = k1 (mod A), k2 (mod B).  All index maps are
+      // compile-time register renamings; X[k] lands at the same register as in the
+      // Cooley-Tukey form below (out_idx), so callers see one contract.
+      double2 t[R];
+      sfor<A>([&](auto n1c) {
+        sfor<B>([&](auto n2c) {
+          constexpr int n1 = decltype(n1c)::value, n2 = decltype(n2c)::value;
+          t[n2 * A + n1] = v[OFF + ST * ((B * n1 + A * n2) % R)];
+        });
+      });
+      sfor<B>([&](auto n2c) { DFTs<A, INV, 1, decltype(n2c)::value * A>::run(t); });
+      sfor<A>([&](auto k1c) { DFTs<B, INV, A, out_idx(A, decltype(k1c)::value)>::run(t); });
+      // W^(n k) = W_A^(n1 k) W_B^(n2 k): the A-point stage gives k mod A, the B-point stage
+      // k mod B, so t[out_idx(B, k2) A + out_idx(A, k1)] = X[k] with k = CRT(k1, k2)
+      sfor<A>([&](auto k1c) {
+        sfor<B>([&](auto k2c) {
+          constexpr int k1 = decltype(k1c)::value, k2 = decltype(k2c)::value;
+          constexpr int k = (k1 * B * inv_mod(B % A, A) + k2 * A * inv_mod(A % B, B)) % R;
+          v[OFF + ST * out_idx(R, k)] = t[out_idx(B, k2) * A + out_idx(A, k1)];
+        });
+      });
+      return;
+    }
     sfor<B>([&](auto n2c) {
       constexpr int n2 = decltype(n2c)::value;
       DFTs<A, INV, ST * B, OFF + ST * n2>::run(v);
