@@ -39,6 +39,7 @@ CONFIGS = {
     "cube_32": ((32, 32, 32), 1, 25),         # configs[0]
     "head_1mm_pwc": ((200, 240, 200), 0, 25),
     "cube_128": ((128, 128, 128), 1, 25),     # configs[4] grid (the C5 sweep itself: scripts/sweep_c5.py)
+    "duke_head": ((93, 119, 125), 1, 25),     # the paper's Duke head grid (m = 186 = 6x31, 238 = 14x17, 250)
 }
 METRIC = "compressed-VIE matvecs/s at 1mm head grid; achieved HBM GB/s vs B200 peak"
 

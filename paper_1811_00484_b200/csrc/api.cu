@@ -109,7 +109,7 @@ struct vie_ctx_s {
   double* post_partials = nullptr;  // vie_postprocess partial sums (kRedBlocks + 1), allocated once
   std::mutex post_mu;               // serialises vie_postprocess calls on this context
   // plan cache keyed by (length, pruned, wide)
-  std::map<std::tuple<int, bool, bool>, std::unique_ptr<PlanHolder>> plans;
+  std::map<std::tuple<int, bool, bool, bool>, std::unique_ptr<PlanHolder>> plans;
   // references: the caller's (vie_ctx_create) plus one per live Tucker form and operator,
   // which hold device pointers into the plans and run on the stream
   std::atomic<int> refs{1};
@@ -291,7 +291,15 @@ namespace {
 // at kMaxRadix: larger register DFTs raise register pressure and cut the warps
 // per SM below what the shared-memory passes need to hide latency (ncu r1).
 const int kRadices[] = {24, 20, 16, 15, 12, 10, 8, 7, 6, 5, 4, 3, 2};  // must match VIE_FFT_RADICES(_WIDE)
+// lengths with a prime factor 11..31: the EXT two-stage passes (fft.cuh VIE_FFT_RADICES_EXT)
+const int kExtRadices[] = {34, 31, 29, 26, 24, 23, 22, 20, 19, 17, 16, 15, 14, 13, 12, 11, 10, 8, 7, 6, 5, 4, 3, 2};
 constexpr int kMaxRadix = 10;
+
+bool has_ext_prime(int n) {  // a prime factor > 7 (the EXT radix set covers 11..31)
+  for (int p : {2, 3, 5, 7})
+    while (n % p == 0) n /= p;
+  return n > 1;
+}
 #ifndef VIE_WIDE_PASSES
 #define VIE_WIDE_PASSES 1
 #endif
@@ -313,7 +321,7 @@ int env_int(const char* name, int dflt) {  // tuning overrides (benchmarks only)
 // Fewest stages, then smallest largest radix; first radix even when the
 // transform is pad/crop pruned (half_in / half_out).
 bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::vector<int>& best,
-                 int maxr = kMaxRadix) {
+                 int maxr = kMaxRadix, bool ext = false) {
   if (n == 1) {
     if (best.empty() || cur.size() < best.size() ||
         (cur.size() == best.size() && *std::max_element(cur.begin(), cur.end()) <
@@ -323,21 +331,25 @@ bool factor_plan(int n, bool even_first, int depth, std::vector<int>& cur, std::
   }
   if (depth == 0) return false;
   bool any = false;
-  for (int r : kRadices) {
-    if (r > maxr || n % r) continue;
-    if (r > 10 && r != 12 && r != 15 && r != 16 && r != 20 && r != 24) continue;  // VIE_FFT_RADICES_WIDE
-    if (even_first && cur.empty() && (r & 1)) continue;
+  auto step = [&](int r) {
+    if (r > maxr || n % r) return;
+    if (even_first && cur.empty() && (r & 1)) return;
     cur.push_back(r);
-    any |= factor_plan(n / r, even_first, depth - 1, cur, best, maxr);
+    any |= factor_plan(n / r, even_first, depth - 1, cur, best, maxr, ext);
     cur.pop_back();
-  }
+  };
+  if (ext)
+    for (int r : kExtRadices) step(r);
+  else
+    for (int r : kRadices) step(r);
   return any;
 }
 
 // wide = plan for the pencil kernel (radices up to 20, VIE_FFT_RADICES_WIDE)
+// ext = lengths with a prime factor 11..31, for the EXT two-stage passes only (<= 2 stages)
 const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = false,
-                        std::vector<int>* radices = nullptr) {
-  const auto key = std::make_tuple(n, pruned, wide);
+                        std::vector<int>* radices = nullptr, bool ext = false) {
+  const auto key = std::make_tuple(n, pruned, wide, ext);
   std::lock_guard<std::mutex> lk(ctx->mu);
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) {
@@ -346,10 +358,12 @@ const FftPlan& get_plan(vie_ctx ctx, int n, bool pruned = true, bool wide = fals
   }
   if (n < 1 || (pruned && (n & 1))) throw Invalid("FFT plan: embedded length must be even");
   std::vector<int> rad, cur;
-  for (int depth = 1; depth <= vie::kMaxStages && rad.empty(); ++depth)
-    factor_plan(n, pruned, depth, cur, rad, wide ? 24 : kMaxRadix);
+  for (int depth = 1; depth <= (ext ? 2 : vie::kMaxStages) && rad.empty(); ++depth)
+    factor_plan(n, pruned, depth, cur, rad, ext ? 34 : (wide ? 24 : kMaxRadix), ext);
   if (n > 1 && rad.empty())
-    throw Invalid("FFT plan: length " + std::to_string(n) + " has a prime factor > 7");
+    throw Invalid("FFT plan: length " + std::to_string(n) +
+                  (ext ? " is not R0 x R1 with an even R0 <= 34 and R1 <= 34 of 2,3,5,7,11,..,31-smooth radices"
+                       : " has a prime factor > 7"));
   auto h = std::make_unique<PlanHolder>();
   h->radices = rad;
   if (radices) *radices = rad;
@@ -999,16 +1013,19 @@ int vie_op_create(vie_ctx ctx, int kind, int basis, const int64_t grid[3], int n
       if (poison & 16) VIE_CUDA_CHECK(cudaMemsetAsync(op->Bo, 0xFF, sizeof(double2) * nb));
       VIE_CUDA_CHECK(cudaDeviceSynchronize());
     }
-    op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
-    op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->P3 = get_plan(ctx, g.m3);
-    if (kPass2) {  // register-staged passes when the axis has a <= 2-stage wide plan
+    // axes 1 and 2: register-staged two-stage passes when the axis has a <= 2-stage wide plan
+    // (lengths with a prime factor 11..31 -- the Duke head's 186 and 238 -- only this way)
+    if (kPass2 || has_ext_prime(g.m1) || has_ext_prime(g.m2)) {
       std::vector<int> r1, r2;
-      const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1);
-      const FftPlan& W2 = get_plan(ctx, g.m2, true, true, &r2);
+      const FftPlan& W1 = get_plan(ctx, g.m1, true, true, &r1, has_ext_prime(g.m1));
+      const FftPlan& W2 = get_plan(ctx, g.m2, true, true, &r2, has_ext_prime(g.m2));
       op->q1 = vie::pass2_init(op->Q1, g.m1, r1.data(), static_cast<int>(r1.size()), W1.tw, env_int("VIE_ROW_LINES", 0));
       op->q2 = vie::pass2_init(op->Q2, g.m2, r2.data(), static_cast<int>(r2.size()), W2.tw, 0);
     }
+    // generic multi-stage passes otherwise (7-smooth lengths only)
+    if (!op->q1) op->P1 = get_plan(ctx, g.m1, true, kWidePasses);  // rows: two-stage plans measured faster
+    if (!op->q2) op->P2 = get_plan(ctx, g.m2, true, false);        // columns: radix <= 10 at 3 CTAs/SM measured faster
     op->PH = get_plan(ctx, g.n3, false, true);
     int prio_lo = 0, prio_hi = 0;  // high priority: decompression CTAs are dispatched before FFT-pass CTAs
     VIE_CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));

@@ -32,7 +32,14 @@ namespace vie {
 constexpr int first_factor(int R) {
   return (R % 4 == 0 && R > 4) ? 4 : (R % 2 == 0 ? 2 : (R % 3 == 0 ? 3 : (R % 5 == 0 ? 5 : R)));
 }
-constexpr bool is_base(int R) { return R == 1 || R == 2 || R == 3 || R == 4 || R == 5 || R == 7; }
+// primes 11..31: direct symmetric-pair DFTs (the Duke head's embedded lengths 186 = 6 x 31 and
+// 238 = 14 x 17 need them); only the EXT instantiations of the two-stage passes use them
+constexpr bool is_ext_prime(int R) {
+  return R == 11 || R == 13 || R == 17 || R == 19 || R == 23 || R == 29 || R == 31;
+}
+constexpr bool is_base(int R) {
+  return R == 1 || R == 2 || R == 3 || R == 4 || R == 5 || R == 7 || is_ext_prime(R);
+}
 constexpr int out_idx(int R, int k) {
   return is_base(R) ? k
                     : (R / first_factor(R)) * out_idx(first_factor(R), k % first_factor(R)) +
@@ -79,7 +86,37 @@ struct DFTs {
   static constexpr int A = first_factor(R);
   static constexpr int B = R / A;
   __device__ __forceinline__ static void run(double2* v) {
-    if constexpr (gcd_c(A, B) == 1 && B > 1) {
+    if constexpr (is_ext_prime(R)) {
+      // prime R: pairs a_j = x_j + x_{R-j}, b_j = x_j - x_{R-j} (j <= H); X_0 = x_0 + sum a_j,
+      // X_k, X_{R-k} = x_0 + sum_j cos(2 pi j k / R) a_j -+ i sum_j sin(2 pi j k / R) b_j
+      // (signs swapped for the inverse), ~R^2 real FMAs instead of 2 R^2 complex ones
+      constexpr int H = (R - 1) / 2;
+      double2 a[H], b[H];
+      const double2 x0 = v[OFF];
+      sfor<H>([&](auto jc) {
+        constexpr int j = decltype(jc)::value + 1;
+        a[j - 1] = cadd(v[OFF + ST * j], v[OFF + ST * (R - j)]);
+        b[j - 1] = csub(v[OFF + ST * j], v[OFF + ST * (R - j)]);
+      });
+      double2 s0 = x0;
+      sfor<H>([&](auto jc) { s0 = cadd(s0, a[decltype(jc)::value]); });
+      sfor<H>([&](auto kc) {
+        constexpr int kk = decltype(kc)::value + 1;
+        double2 re = x0, im = make_double2(0.0, 0.0);
+        sfor<H>([&](auto jc) {
+          constexpr int j = decltype(jc)::value + 1;
+          constexpr double c = tw_re(R, (j * kk) % R);
+          constexpr double s = -tw_im(R, (j * kk) % R);  // sin(2 pi j k / R)
+          re = make_double2(fma(c, a[j - 1].x, re.x), fma(c, a[j - 1].y, re.y));
+          im = make_double2(fma(s, b[j - 1].x, im.x), fma(s, b[j - 1].y, im.y));
+        });
+        const double2 t = mul_mi<INV>(im);
+        v[OFF + ST * kk] = cadd(re, t);
+        v[OFF + ST * (R - kk)] = csub(re, t);
+      });
+      v[OFF] = s0;
+      return;
+    } else if constexpr (gcd_c(A, B) == 1 && B > 1) {
       // Good-Thomas prime-factor algorithm (A, B coprime): no inner twiddles.  Input index
       // n = (B n1 + A n2) mod R; output k = k1 (mod A), k2 (mod B).  All index maps are
       // compile-time register renamings; X[k] lands at the same register as in the
@@ -103,7 +140,7 @@ struct DFTs {
         });
       });
       return;
-    }
+    } else {
     sfor<B>([&](auto n2c) {
       constexpr int n2 = decltype(n2c)::value;
       DFTs<A, INV, ST * B, OFF + ST * n2>::run(v);
@@ -117,6 +154,7 @@ struct DFTs {
       constexpr int k1 = decltype(k1c)::value;
       DFTs<B, INV, ST, OFF + ST * B * out_idx(A, k1)>::run(v);
     });
+    }
   }
 };
 
@@ -291,6 +329,9 @@ __device__ __forceinline__ void dit_stage_adj(double2* buf, int nlines, int ls, 
 // owns its SM and has 128 registers per thread.
 #define VIE_FFT_RADICES(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(10)
 #define VIE_FFT_RADICES_WIDE(X) VIE_FFT_RADICES(X) X(12) X(15) X(16) X(20) X(24)
+// radices with a prime factor 11..31 (two-stage row / column passes only, EXT instantiation)
+#define VIE_FFT_RADICES_EXT_EVEN(X) X(14) X(22) X(26) X(34)
+#define VIE_FFT_RADICES_EXT(X) VIE_FFT_RADICES_EXT_EVEN(X) X(11) X(13) X(17) X(19) X(23) X(29) X(31)
 
 template <bool INV, bool WIDE = false>
 __device__ __forceinline__ void run_stage(double2* buf, int nlines, int ls, int n, const StageDesc& sd,

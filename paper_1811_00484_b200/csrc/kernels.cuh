@@ -128,6 +128,7 @@ struct Pass2 {
   int R0, R1;   // radices (R1 == 1: single stage)
   int R1p, ls;  // padded block length (odd) and smem line stride (odd)
   int lines;    // rows per CTA (row passes)
+  int ext;      // a radix has a prime factor 11..31: the EXT instantiation of the passes
   const double2* tw;  // w_m^e
   FastDiv dR0, dR1;
 };

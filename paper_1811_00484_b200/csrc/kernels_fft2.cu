@@ -24,7 +24,11 @@ namespace vie {
 
 namespace {
 
-template <class F>
+// EXT = false: the wide register-DFT set (7-smooth lengths; every production grid).
+// EXT = true: the wide set plus the radices with a prime factor 11..31 (VIE_FFT_RADICES_EXT),
+// a separate instantiation so the large prime DFTs never raise the register count of the
+// 7-smooth passes.
+template <bool EXT, class F>
 __device__ __forceinline__ void radix_dispatch(int R, F&& f) {
   switch (R) {
 #define VIE_CASE(RR)                          \
@@ -32,14 +36,21 @@ __device__ __forceinline__ void radix_dispatch(int R, F&& f) {
     f(std::integral_constant<int, RR>{});     \
     break;
     VIE_FFT_RADICES_WIDE(VIE_CASE)
-#undef VIE_CASE
     default:
-      break;  // host plan selection only produces radices of the wide set
+      if constexpr (EXT) {
+        switch (R) {
+          VIE_FFT_RADICES_EXT(VIE_CASE)
+          default:
+            break;
+        }
+      }
+      break;  // host plan selection only produces radices of the instantiated set
+#undef VIE_CASE
   }
 }
 
-// first (pruned) stage: even radices of the wide set only
-template <class F>
+// first (pruned) stage: even radices only
+template <bool EXT, class F>
 __device__ __forceinline__ void even_dispatch(int R, F&& f) {
   switch (R) {
 #define VIE_CASE(RR)                          \
@@ -47,9 +58,16 @@ __device__ __forceinline__ void even_dispatch(int R, F&& f) {
     f(std::integral_constant<int, RR>{});     \
     break;
     VIE_CASE(2) VIE_CASE(4) VIE_CASE(6) VIE_CASE(8) VIE_CASE(10) VIE_CASE(12) VIE_CASE(16) VIE_CASE(20) VIE_CASE(24)
-#undef VIE_CASE
     default:
+      if constexpr (EXT) {
+        switch (R) {
+          VIE_FFT_RADICES_EXT_EVEN(VIE_CASE)
+          default:
+            break;
+        }
+      }
       break;
+#undef VIE_CASE
   }
 }
 
@@ -135,8 +153,8 @@ __device__ __forceinline__ int64_t arow(int row, int pos, int m, const FastDiv& 
 }
 
 // x: rows of n (voxel order) -> A: rows of m, mirror-paired spectral positions.
-template <bool BLOCKED>
-__global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__ x, double2* __restrict__ A,
+template <bool BLOCKED, bool EXT>
+__global__ void __launch_bounds__(256, EXT ? 1 : 2) k_row_fwd2(const double2* __restrict__ x, double2* __restrict__ A,
                                                      int nrows, Pass2 P, FastDiv dW, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
@@ -145,7 +163,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__
   const double2* src = x + static_cast<int64_t>(row0) * n;
   if (R1 == 1) {  // single stage: no shared memory
     for (int r = threadIdx.x; r < nr; r += blockDim.x)
-      even_dispatch(R0, [&](auto rc) {
+      even_dispatch<EXT>(R0, [&](auto rc) {
         fwd_first<decltype(rc)::value>(
             0, P.tw, [&](int i) { return src[r * n + i]; },
             [&](int k, double2 v) { A[arow<BLOCKED>(row0 + r, pos_of_freq(k, n), m, dW, blk)] = v; });
@@ -157,7 +175,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__
     const int r = static_cast<int>(P.dR1.div(u)), mp = u - r * R1;
     const double2* s = src + r * n + mp;
     double2* b = buf + r * ls + mp;
-    even_dispatch(R0, [&](auto rc) {
+    even_dispatch<EXT>(R0, [&](auto rc) {
       fwd_first<decltype(rc)::value>(
           mp, P.tw, [&](int i) { return s[i * R1]; }, [&](int k, double2 v) { b[k * R1p] = v; });
     });
@@ -166,7 +184,7 @@ __global__ void __launch_bounds__(256, 2) k_row_fwd2(const double2* __restrict__
   for (int u = threadIdx.x; u < nr * R0; u += blockDim.x) {
     const int r = static_cast<int>(P.dR0.div(u)), bk = u - r * R0;
     const double2* b = buf + r * ls + bk * R1p;
-    radix_dispatch(R1, [&](auto rc) {
+    radix_dispatch<EXT>(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, false>(
           [&](int i) { return b[i]; },
           [&](int k, double2 v) { A[arow<BLOCKED>(row0 + r, pos_of_freq(bk + R0 * k, n), m, dW, blk)] = v; });
@@ -200,8 +218,8 @@ struct RowEpi {
   }
 };
 
-template <bool BLOCKED>
-__global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__ A, double2* __restrict__ y,
+template <bool BLOCKED, bool EXT>
+__global__ void __launch_bounds__(256, EXT ? 1 : 2) k_row_inv2(const double2* __restrict__ A, double2* __restrict__ y,
                                                      int nrows, Pass2 P, RowEpi epi, FastDiv dW, int64_t blk) {
   extern __shared__ double2 buf[];
   const int n = P.n, m = P.m, R0 = P.R0, R1 = P.R1;
@@ -210,7 +228,7 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
   double2* dst = y + static_cast<int64_t>(row0) * n;
   if (R1 == 1) {
     for (int r = threadIdx.x; r < nr; r += blockDim.x)
-      even_dispatch(R0, [&](auto rc) {
+      even_dispatch<EXT>(R0, [&](auto rc) {
         inv_last<decltype(rc)::value>(
             0, P.tw, [&](int k) { return A[arow<BLOCKED>(row0 + r, pos_of_freq(k, n), m, dW, blk)]; },
             [&](int i, double2 v) { dst[r * n + i] = epi(v, row0 + r, i, n); });
@@ -221,7 +239,7 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
   for (int u = threadIdx.x; u < nr * R0; u += blockDim.x) {
     const int r = static_cast<int>(P.dR0.div(u)), bk = u - r * R0;
     double2* b = buf + r * ls + bk * R1p;
-    radix_dispatch(R1, [&](auto rc) {
+    radix_dispatch<EXT>(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, true>(
           [&](int k) { return A[arow<BLOCKED>(row0 + r, pos_of_freq(bk + R0 * k, n), m, dW, blk)]; },
           [&](int i, double2 v) { b[i] = v; });
@@ -232,7 +250,7 @@ __global__ void __launch_bounds__(256, 2) k_row_inv2(const double2* __restrict__
     const int r = static_cast<int>(P.dR1.div(u)), mp = u - r * R1;
     const double2* b = buf + r * ls + mp;
     double2* d = dst + r * n + mp;
-    even_dispatch(R0, [&](auto rc) {
+    even_dispatch<EXT>(R0, [&](auto rc) {
       inv_last<decltype(rc)::value>(
           mp, P.tw, [&](int k) { return b[k * R1p]; },
           [&](int i, double2 v) { d[i * R1] = epi(v, row0 + r, mp + i * R1, n); });
@@ -247,7 +265,8 @@ constexpr int kCW = kColsPerCta;
 static_assert((kCW & (kCW - 1)) == 0, "column tile must be a power of two");
 constexpr int kLgCW = kCW == 8 ? 3 : (kCW == 4 ? 2 : (kCW == 16 ? 4 : 0));
 
-__global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
+template <bool EXT>
+__global__ void __launch_bounds__(256, EXT ? 1 : 2) k_col_fwd2(const double2* __restrict__ A, double2* __restrict__ B, int m1,
                                                      Pass2 P, int64_t bps, PlaneMap pm) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
   if (R1 == 1) {
     const int w = threadIdx.x;
     if (w < wc)
-      even_dispatch(R0, [&](auto rc) {
+      even_dispatch<EXT>(R0, [&](auto rc) {
         fwd_first<decltype(rc)::value>(
             0, P.tw, [&](int i) { return src[static_cast<int64_t>(i) * m1 + w]; },
             [&](int k, double2 v) { dst[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w] = v; });
@@ -273,7 +292,7 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
     const double2* s = src + static_cast<int64_t>(mp) * m1 + w;
     double2* b = buf + w * ls + mp;
     const int64_t step = static_cast<int64_t>(R1) * m1;
-    even_dispatch(R0, [&](auto rc) {
+    even_dispatch<EXT>(R0, [&](auto rc) {
       fwd_first<decltype(rc)::value>(
           mp, P.tw, [&](int i) { return s[i * step]; }, [&](int k, double2 v) { b[k * R1p] = v; });
     });
@@ -284,7 +303,7 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
     if (w >= wc) continue;
     const double2* b = buf + w * ls + bk * R1p;
     double2* d = dst + w;
-    radix_dispatch(R1, [&](auto rc) {
+    radix_dispatch<EXT>(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, false>(
           [&](int i) { return b[i]; },
           [&](int k, double2 v) { d[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1] = v; });
@@ -292,7 +311,8 @@ __global__ void __launch_bounds__(256, 2) k_col_fwd2(const double2* __restrict__
   }
 }
 
-__global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
+template <bool EXT>
+__global__ void __launch_bounds__(256, EXT ? 1 : 2) k_col_inv2(const double2* __restrict__ B, double2* __restrict__ A, int m1,
                                                      Pass2 P, int64_t bps, PlaneMap pm) {
   extern __shared__ double2 buf[];
   const int n = P.n, R0 = P.R0, R1 = P.R1;
@@ -304,7 +324,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
   if (R1 == 1) {
     const int w = threadIdx.x;
     if (w < wc)
-      even_dispatch(R0, [&](auto rc) {
+      even_dispatch<EXT>(R0, [&](auto rc) {
         inv_last<decltype(rc)::value>(
             0, P.tw, [&](int k) { return src[static_cast<int64_t>(pos_of_freq(k, n)) * m1 + w]; },
             [&](int i, double2 v) { dst[static_cast<int64_t>(i) * m1 + w] = v; });
@@ -317,7 +337,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     if (w >= wc) continue;
     const double2* s = src + w;
     double2* b = buf + w * ls + bk * R1p;
-    radix_dispatch(R1, [&](auto rc) {
+    radix_dispatch<EXT>(R1, [&](auto rc) {
       plain_stage<decltype(rc)::value, true>(
           [&](int k) { return s[static_cast<int64_t>(pos_of_freq(bk + R0 * k, n)) * m1]; },
           [&](int i, double2 v) { b[i] = v; });
@@ -330,7 +350,7 @@ __global__ void __launch_bounds__(256, 2) k_col_inv2(const double2* __restrict__
     const double2* b = buf + w * ls + mp;
     double2* d = dst + static_cast<int64_t>(mp) * m1 + w;
     const int64_t step = static_cast<int64_t>(R1) * m1;
-    even_dispatch(R0, [&](auto rc) {
+    even_dispatch<EXT>(R0, [&](auto rc) {
       inv_last<decltype(rc)::value>(
           mp, P.tw, [&](int k) { return b[k * R1p]; }, [&](int i, double2 v) { d[i * step] = v; });
     });
@@ -358,6 +378,17 @@ bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw,
   P.R0 = R0;
   P.R1 = R1;
   P.R1p = R1 | 1;
+  auto wide = [](int r) {
+    switch (r) {
+#define VIE_CASE(RR) case RR:
+      VIE_FFT_RADICES_WIDE(VIE_CASE)
+#undef VIE_CASE
+      return true;
+      default:
+        return r == 1;
+    }
+  };
+  P.ext = !(wide(R0) && wide(R1));
   P.ls = (R0 * P.R1p) | 1;
   P.tw = tw;
   P.dR0.init(static_cast<uint32_t>(R0));
@@ -367,6 +398,20 @@ bool pass2_init(Pass2& P, int m, const int* radices, int nst, const double2* tw,
   return true;
 }
 
+template <bool BLOCKED, bool EXT>
+void row_fwd2_t(const double2* x, double2* A, int nrows, const Pass2& P, const FastDiv& dW, int64_t blk, size_t sm,
+                int threads, cudaStream_t st) {
+  if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2<BLOCKED, EXT>), sm);
+  k_row_fwd2<BLOCKED, EXT><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P, dW, blk);
+}
+
+template <bool BLOCKED, bool EXT>
+void row_inv2_t(const double2* A, double2* y, int nrows, const Pass2& P, const RowEpi& epi, const FastDiv& dW,
+                int64_t blk, size_t sm, int threads, cudaStream_t st) {
+  if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2<BLOCKED, EXT>), sm);
+  k_row_inv2<BLOCKED, EXT><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi, dW, blk);
+}
+
 void launch_row_fwd2(const double2* x, double2* A, const Geom& g, const Pass2& P, cudaStream_t st) {
   const int nrows = g.S * g.n2 * g.n3;
   const size_t sm = pass2_smem(P, P.lines);
@@ -374,12 +419,13 @@ void launch_row_fwd2(const double2* x, double2* A, const Geom& g, const Pass2& P
   FastDiv dW;
   dW.init(static_cast<uint32_t>(g.W));
   const int64_t blk = static_cast<int64_t>(nrows) * g.W;
-  if (g.W == g.m1) {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2<false>), sm);
-    k_row_fwd2<false><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P, dW, blk);
+  const bool blocked = g.W != g.m1;
+  if (P.ext) {
+    if (blocked) row_fwd2_t<true, true>(x, A, nrows, P, dW, blk, sm, threads, st);
+    else row_fwd2_t<false, true>(x, A, nrows, P, dW, blk, sm, threads, st);
   } else {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_fwd2<true>), sm);
-    k_row_fwd2<true><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(x, A, nrows, P, dW, blk);
+    if (blocked) row_fwd2_t<true, false>(x, A, nrows, P, dW, blk, sm, threads, st);
+    else row_fwd2_t<false, false>(x, A, nrows, P, dW, blk, sm, threads, st);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
@@ -395,12 +441,13 @@ void launch_row_inv2(const double2* A, double2* y, const Geom& g, const Pass2& P
   FastDiv dW;
   dW.init(static_cast<uint32_t>(g.W));
   const int64_t blk = static_cast<int64_t>(nrows) * g.W;
-  if (g.W == g.m1) {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2<false>), sm);
-    k_row_inv2<false><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi, dW, blk);
+  const bool blocked = g.W != g.m1;
+  if (P.ext) {
+    if (blocked) row_inv2_t<true, true>(A, y, nrows, P, epi, dW, blk, sm, threads, st);
+    else row_inv2_t<false, true>(A, y, nrows, P, epi, dW, blk, sm, threads, st);
   } else {
-    if (sm) set_smem2(reinterpret_cast<const void*>(k_row_inv2<true>), sm);
-    k_row_inv2<true><<<(nrows + P.lines - 1) / P.lines, threads, sm, st>>>(A, y, nrows, P, epi, dW, blk);
+    if (blocked) row_inv2_t<true, false>(A, y, nrows, P, epi, dW, blk, sm, threads, st);
+    else row_inv2_t<false, false>(A, y, nrows, P, epi, dW, blk, sm, threads, st);
   }
   VIE_CUDA_CHECK(cudaGetLastError());
 }
@@ -411,8 +458,9 @@ void launch_col_fwd2(const double2* A, double2* B, const Geom& g, const Pass2& P
   const size_t sm = pass2_smem(P, kCW);
   dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_fwd2), sm);
-  k_col_fwd2<<<grid, threads, sm, st>>>(A, B, g.W, P, g.bps, pm);
+  auto fn = P.ext ? k_col_fwd2<true> : k_col_fwd2<false>;
+  if (sm) set_smem2(reinterpret_cast<const void*>(fn), sm);
+  fn<<<grid, threads, sm, st>>>(A, B, g.W, P, g.bps, pm);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -420,8 +468,9 @@ void launch_col_inv2(const double2* B, double2* A, const Geom& g, const Pass2& P
   const size_t sm = pass2_smem(P, kCW);
   dim3 grid((g.W + kCW - 1) / kCW, g.S * g.nk);
   const int threads = round_threads(P.R1 == 1 ? kCW : kCW * std::max(P.R0, P.R1));
-  if (sm) set_smem2(reinterpret_cast<const void*>(k_col_inv2), sm);
-  k_col_inv2<<<grid, threads, sm, st>>>(B, A, g.W, P, g.bps, pm);
+  auto fn = P.ext ? k_col_inv2<true> : k_col_inv2<false>;
+  if (sm) set_smem2(reinterpret_cast<const void*>(fn), sm);
+  fn<<<grid, threads, sm, st>>>(B, A, g.W, P, g.bps, pm);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

@@ -84,6 +84,23 @@ def test_headline_configs_random_x(vie, dft, basis, grid, strategy):
     assert err <= MATVEC_TOL
 
 
+def test_duke_head_grid_random_x(vie, dft):
+    """The paper's Duke head grid 93 x 119 x 125 (PAPER.md; m = 186 = 6 x 31, 238 = 14 x 17,
+    250): PWL N rank 25, random x, full GPU matvec vs the oracle, rel l2 <= 1e-10."""
+    import torch
+
+    grid = (93, 119, 125)
+    spatial, par = spatial_tucker_forms(N, PWL, grid, 25, 4321)
+    op = build(vie, dft, N, PWL, grid, spatial, par)
+    x = random_field(PWL, grid, 99)
+    y = vie.apply_operator(op, torch.from_numpy(x).cuda()).cpu().numpy()
+    del op
+    y_ref = orc.apply_operator_tucker(N, PWL, grid, fourier_forms(spatial, par), x)
+    err = rel(y_ref, y)
+    print(f"{grid}: rel l2 = {err:.3e}")
+    assert err <= MATVEC_TOL
+
+
 def _system(vie, dft, grid, eps_np, seed):
     """PWL N system with forms scaled so |(eps - 1) N| ~ 0.2 min |eps g| (bench.py)."""
     import torch

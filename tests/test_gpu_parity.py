@@ -76,6 +76,30 @@ def test_matvec_matches_oracle(vie, dft, orc, kind, basis, dims, rank):
 # n3 with a compile-time pencil shape (kernels_pencil2.cu: 32 = 4x8, 64 = 8x8, 100 = 10x10):
 # odd/even axis-1 edges, partial last pair group (PWC packs 4 pairs per CTA), m1 = 2
 # (edge launch only), both kinds and bases.
+# Embedded lengths with a prime factor 11..31 on axes 1 / 2 (the Duke head's 186 = 6 x 31 and
+# 238 = 14 x 17 are the motivation): the EXT two-stage row / column passes (fft.cuh prime
+# DFTs).  Single-stage (22, 26, 34) and two-stage (62 = 2 x 31, 38, 46, 58, 186, 238) plans.
+EXT_CASES = [
+    (N, PWL, (11, 17, 6), 3), (K, PWC, (13, 19, 5), 3), (N, PWC, (31, 7, 8), 4), (N, PWL, (23, 29, 4), 3),
+    (K, PWL, (19, 11, 32), 3), (N, PWL, (93, 13, 6), 4), (N, PWC, (7, 119, 5), 3),
+]
+
+
+@pytest.mark.parametrize("kind,basis,dims,rank", EXT_CASES)
+def test_matvec_ext_prime_lengths(vie, dft, orc, kind, basis, dims, rank):
+    op, oforms, _, _ = make_ops(vie, dft, orc, kind, basis, dims, rank, 5 + sum(dims))
+    x = random_field(basis, dims, 77)
+    y_ref = orc.apply_operator_tucker(kind, basis, dims, oforms, x)
+    y = run_gpu(vie, op, x)
+    assert rel(y_ref, y) <= MATVEC_TOL, (kind, basis, dims)
+
+
+def test_ext_prime_axis3_rejected(vie, dft, orc):
+    """Axis 3 keeps the 7-smooth plans (pencil kernels): m3 = 2 x 17 is refused loudly."""
+    with pytest.raises(ValueError):
+        make_ops(vie, dft, orc, N, PWC, (4, 4, 17), 2, 3)
+
+
 PENCIL2_CASES = [
     (N, PWL, (3, 4, 32), 3), (K, PWL, (4, 3, 100), 3), (N, PWC, (5, 3, 64), 4), (K, PWC, (6, 2, 32), 3),
     (N, PWC, (1, 2, 32), 2), (N, PWL, (7, 5, 64), 3), (N, PWC, (9, 4, 100), 3), (K, PWL, (2, 6, 64), 2),
