@@ -82,6 +82,7 @@ def test_matvec_matches_oracle(vie, dft, orc, kind, basis, dims, rank):
 EXT_CASES = [
     (N, PWL, (11, 17, 6), 3), (K, PWC, (13, 19, 5), 3), (N, PWC, (31, 7, 8), 4), (N, PWL, (23, 29, 4), 3),
     (K, PWL, (19, 11, 32), 3), (N, PWL, (93, 13, 6), 4), (N, PWC, (7, 119, 5), 3),
+    (N, PWL, (5, 3, 125), 3), (K, PWC, (6, 4, 125), 3),  # n3 = 125: odd axis-3 branch (generic pencil, the Duke grid)
 ]
 
 
