@@ -70,6 +70,28 @@ int vie_tucker_compress(vie_ctx ctx, const int64_t dims[3], const double* t_host
 int vie_tucker_compress_device(vie_ctx ctx, const int64_t dims[3], const double* t_dev, const int sign[3],
                                double tol, int rule, vie_tucker* out, int64_t ranks_out[3], void* stream);
 
+/* tucker_cp (decomp.hpp:336-373): hosvd on the device (as vie_tucker_compress_device), CP-ALS
+ * on the r1 x r2 x r3 core (cp_als, decomp.hpp:237-298: SVD-initialised factors, seed 0x5eed,
+ * cp_iters sweeps at most, stop when the error decrease < stall_tol), merged factors
+ * W_q = U_q V_q.  t: n1 n2 n3 complex, a DEVICE buffer when t_on_device (ordered after
+ * `stream`, NULL = the context stream) else a host buffer.  CP rank = cp_rank if >= 0 else
+ * min(r1, r2, r3).  Every output is optional (NULL): out = the device form of
+ * transform_factors(TuckerCPForm) (as vie_tucker_from_cp); rank_out; w1..w3 = the spatial
+ * W_q on the host (n_q x w_cap column-major capacity each, VIE_EINVAL if rank > w_cap);
+ * errs = {hosvd_relative_error, core_cp_relative_error, stats.achieved_relative_error};
+ * trace = the CP error per sweep (up to trace_cap), ntrace = the number of sweeps.       */
+int vie_tucker_cp(vie_ctx ctx, const int64_t dims[3], const double* t, int t_on_device, const int sign[3],
+                  double tol, int rule, int cp_iters, int64_t cp_rank, double stall_tol, vie_tucker* out,
+                  int64_t* rank_out, double* w1, double* w2, double* w3, int64_t w_cap, double errs[3],
+                  double* trace, int trace_cap, int* ntrace, void* stream);
+/* cp_als (decomp.hpp:237-298) of a host tensor (dims[0] x dims[1] x dims[2], the reference
+ * layout) at rank r: factors f_q (dims[q] x r, host, optional), the relative error per sweep
+ * (trace, up to trace_cap; ntrace = sweeps run), flags = {converged, ill_posed_rank}.
+ * Host computation (meant for Tucker cores; no device needed).                          */
+int vie_cp_als(const int64_t dims[3], const double* t_host, int64_t r, int max_iters, double stall_tol,
+               uint64_t seed, double* f1, double* f2, double* f3, double* trace, int trace_cap, int* ntrace,
+               int flags[2]);
+
 /* ---- Green's-tensor assembly (assembly.hpp:159-246, kernels.hpp, quadrature.hpp) ----
  * QuadratureSpec (assembly.hpp:24-36); NULL = the defaults {5, 10, 1, 12, 6}.          */
 typedef struct {

@@ -285,6 +285,95 @@ class DftService {  // fft.hpp DftService: here the CUDA context, stream and pla
   vie_ctx ctx_ = nullptr;
 };
 
+// ---- CP-ALS and Tucker+CP (decomp.hpp:135-148, 184-373)
+struct CPForm {  // decomp.hpp:135-140
+  std::array<FactorMatrix, 3> factors;
+  Index rank = 0;
+};
+struct CpAlsResult {  // decomp.hpp:184-190
+  CPForm form;
+  std::vector<double> rel_error_trace;  // one entry per completed sweep
+  bool converged = false;
+  bool ill_posed_rank = false;
+};
+// cp_als (decomp.hpp:237-298): the library's host CP-ALS (sized for Tucker cores)
+inline CpAlsResult cp_als(const Tensor3& t, Index r, int max_iters = 100, double stall_tol = 1e-12,
+                          std::uint64_t seed = 0x5eed) {
+  CpAlsResult res;
+  res.form.rank = r;
+  const int64_t d[3] = {t.dims[0], t.dims[1], t.dims[2]};
+  for (int q = 0; q < 3; ++q) res.form.factors[static_cast<size_t>(q)] = FactorMatrix(d[q], std::max<Index>(r, 0));
+  std::vector<double> tr(static_cast<size_t>(std::max(max_iters, 1)) + 1);
+  int nt = 0, flags[2] = {0, 0};
+  check(vie_cp_als(d, reinterpret_cast<const double*>(t.data.data()), r, max_iters, stall_tol, seed,
+                   reinterpret_cast<double*>(res.form.factors[0].data.data()),
+                   reinterpret_cast<double*>(res.form.factors[1].data.data()),
+                   reinterpret_cast<double*>(res.form.factors[2].data.data()), tr.data(), static_cast<int>(tr.size()),
+                   &nt, flags));
+  res.rel_error_trace.assign(tr.begin(), tr.begin() + std::min<size_t>(static_cast<size_t>(nt), tr.size()));
+  res.converged = flags[0] != 0;
+  res.ill_posed_rank = flags[1] != 0;
+  return res;
+}
+
+struct CompressionStats {  // decomp.hpp:150-156
+  std::int64_t original_elements = 0;
+  std::int64_t compressed_elements = 0;
+  double compression_factor = 0.0;
+  double achieved_relative_error = 0.0;
+  std::array<Index, 3> ranks{0, 0, 0};
+};
+struct TuckerCpResult {  // decomp.hpp:300-307
+  TuckerCPForm form;
+  CompressionStats stats;
+  double hosvd_relative_error = 0.0;
+  double core_cp_relative_error = 0.0;
+  std::vector<double> cp_error_trace;
+};
+// tucker_cp (decomp.hpp:336-373): HOSVD on the device of `dft`, CP-ALS on the core, merged
+// factors; every residual norm on the device.  `parity_sign` is only checked (odd axes must
+// have a zero offset-0 plane) -- the spatial result does not depend on it.
+inline TuckerCpResult tucker_cp(const Tensor3& t, double tol, int cp_iters, TruncationRule rule, Index cp_rank,
+                                double stall_tol, DftService& dft, const std::array<int, 3>& parity_sign = {1, 1, 1}) {
+  const int64_t d[3] = {t.dims[0], t.dims[1], t.dims[2]};
+  const int64_t cap = cp_rank >= 0 ? cp_rank : std::min({d[0], d[1], d[2]});
+  std::array<std::vector<cplx>, 3> w;
+  for (int q = 0; q < 3; ++q) w[static_cast<size_t>(q)].assign(static_cast<size_t>(std::max<int64_t>(d[q] * cap, 1)), 0.0);
+  std::vector<double> tr(static_cast<size_t>(std::max(cp_iters, 1)) + 1);
+  int64_t rank = 0;
+  double errs[3] = {0, 0, 0};
+  int nt = 0;
+  check(vie_tucker_cp(dft.handle(), d, reinterpret_cast<const double*>(t.data.data()), 0, parity_sign.data(), tol,
+                      static_cast<int>(rule), cp_iters, cp_rank, stall_tol, nullptr, &rank,
+                      reinterpret_cast<double*>(w[0].data()), reinterpret_cast<double*>(w[1].data()),
+                      reinterpret_cast<double*>(w[2].data()), cap, errs, tr.data(), static_cast<int>(tr.size()), &nt,
+                      nullptr));
+  TuckerCpResult res;
+  res.form.rank = rank;
+  for (int q = 0; q < 3; ++q) {
+    FactorMatrix f(d[q], rank);
+    std::copy(w[static_cast<size_t>(q)].begin(), w[static_cast<size_t>(q)].begin() + d[q] * rank, f.data.begin());
+    res.form.factors[static_cast<size_t>(q)] = std::move(f);
+  }
+  res.hosvd_relative_error = errs[0];
+  res.core_cp_relative_error = errs[1];
+  res.cp_error_trace.assign(tr.begin(), tr.begin() + std::min<size_t>(static_cast<size_t>(nt), tr.size()));
+  res.stats.original_elements = d[0] * d[1] * d[2];  // compression_stats(TuckerCPForm) (decomp.hpp:324-334)
+  res.stats.ranks = {rank, rank, rank};
+  res.stats.compressed_elements = rank * (d[0] + d[1] + d[2]);
+  res.stats.compression_factor = static_cast<double>(res.stats.original_elements) /
+                                 static_cast<double>(std::max<std::int64_t>(res.stats.compressed_elements, 1));
+  res.stats.achieved_relative_error = errs[2];
+  return res;
+}
+// the reference signature: a temporary context on device 0
+inline TuckerCpResult tucker_cp(const Tensor3& t, double tol, int cp_iters = 1000,
+                                TruncationRule rule = TruncationRule::Energy, Index cp_rank = -1,
+                                double stall_tol = 0.0) {
+  DftService dft(0);
+  return tucker_cp(t, tol, cp_iters, rule, cp_rank, stall_tol, dft);
+}
+
 struct ApplyWorkspace {};  // the device workspace lives in the operator (operator.hpp:181-187)
 
 struct ApplyTimings {  // operator.hpp:189-192
@@ -405,10 +494,13 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind, BasisOrder ord
 }
 
 
-struct SpectrumBuildOptions {  // operator.hpp:131-139 (Tucker representation only)
+struct SpectrumBuildOptions {  // operator.hpp:131-139 (one compressed representation per component)
   double tol = 1e-8;
   TruncationRule rule = TruncationRule::Energy;
   BasisOrder order = BasisOrder::PWC;
+  bool tucker_cp = false;  // compress with tucker_cp (TuckerCPForm) instead of hosvd (TuckerForm)
+  int cp_iters = 1000;
+  Index cp_rank = -1;      // default min(r1, r2, r3)
 };
 
 // build_operator_spectra (operator.hpp:144-177) from SPATIAL defining tensors,
@@ -433,8 +525,13 @@ inline EmbeddedSpectrum build_operator_spectra(OperatorKind kind,
     const int64_t dims[3] = {grid[0], grid[1], grid[2]};
     int64_t ranks[3] = {0, 0, 0};
     vie_tucker h = nullptr;
-    check(vie_tucker_compress(dft.handle(), dims, reinterpret_cast<const double*>(t.data.data()), p.sign.data(),
-                              opts.tol, static_cast<int>(opts.rule), &h, ranks));
+    if (opts.tucker_cp)  // operator.hpp:165-168: tucker_cp, then transform_factors(TuckerCPForm)
+      check(vie_tucker_cp(dft.handle(), dims, reinterpret_cast<const double*>(t.data.data()), 0, p.sign.data(),
+                          opts.tol, static_cast<int>(opts.rule), opts.cp_iters, opts.cp_rank, 0.0, &h, nullptr,
+                          nullptr, nullptr, nullptr, 0, nullptr, nullptr, 0, nullptr, nullptr));
+    else
+      check(vie_tucker_compress(dft.handle(), dims, reinterpret_cast<const double*>(t.data.data()), p.sign.data(),
+                                opts.tol, static_cast<int>(opts.rule), &h, ranks));
     hs.push_back(h);
     comps.insert(comps.end(), {comp.row_axis, comp.col_axis, comp.row_poly, comp.col_poly});
   }

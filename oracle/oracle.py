@@ -385,6 +385,51 @@ def decompress_cp(edims, ws) -> np.ndarray:
     return out
 
 
+class CpAls:
+    def __init__(self, factors, trace, converged, ill_posed):
+        self.factors, self.trace, self.converged, self.ill_posed = factors, trace, converged, ill_posed
+
+
+def cp_als(t, dims, r, max_iters=100, stall_tol=1e-12, seed=0x5EED) -> CpAls:
+    """cp_als (decomp.hpp:237-298): factors (dims[q], r), per-sweep relative error trace."""
+    t = _c(t).reshape(-1)
+    fs = [np.empty(dims[q] * r, np.complex128) for q in range(3)]
+    cap = max(int(max_iters), 1) + 1
+    tr = np.empty(cap)
+    nt = C.c_int()
+    flags = (C.c_int * 2)()
+    _check(lib().orc_cp_als(_ptr(t), _i64(dims), C.c_int64(r), int(max_iters), C.c_double(stall_tol),
+                            C.c_uint64(seed), _ptr(fs[0]), _ptr(fs[1]), _ptr(fs[2]),
+                            tr.ctypes.data_as(_dp), cap, C.byref(nt), flags))
+    return CpAls([fs[q].reshape((dims[q], r), order="F") for q in range(3)], tr[:nt.value].copy(),
+                 bool(flags[0]), bool(flags[1]))
+
+
+class TuckerCp:
+    def __init__(self, factors, rank, hosvd_err, core_err, achieved, trace):
+        self.factors, self.rank = factors, rank
+        self.hosvd_relative_error, self.core_cp_relative_error = hosvd_err, core_err
+        self.achieved_relative_error, self.trace = achieved, trace
+
+
+def tucker_cp(t, dims, tol, cp_iters=1000, rule=1, cp_rank=-1, stall_tol=0.0) -> TuckerCp:
+    """tucker_cp (decomp.hpp:336-373): merged factors W_q = U_q V_q (dims[q], rank)."""
+    t = _c(t).reshape(-1)
+    rk = C.c_int64()
+    nt = C.c_int()
+    errs = (C.c_double * 3)()
+    args = (_ptr(t), _i64(dims), C.c_double(tol), int(cp_iters), int(rule), C.c_int64(cp_rank), C.c_double(stall_tol))
+    _check(lib().orc_tucker_cp(*args, C.byref(rk), None, None, None, errs, None, 0, C.byref(nt)))
+    r = rk.value
+    ws = [np.empty(dims[q] * r, np.complex128) for q in range(3)]
+    cap = int(cp_iters) + 1
+    tr = np.empty(cap)
+    _check(lib().orc_tucker_cp(*args, C.byref(rk), _ptr(ws[0]), _ptr(ws[1]), _ptr(ws[2]), errs,
+                               tr.ctypes.data_as(_dp), cap, C.byref(nt)))
+    return TuckerCp([ws[q].reshape((dims[q], r), order="F") for q in range(3)], r, errs[0], errs[1], errs[2],
+                    tr[:nt.value].copy())
+
+
 # ---- Green's-tensor assembly (assembly.hpp, kernels.hpp, quadrature.hpp) ---------
 OP_N, OP_K, OP_G, OP_NREM = 0, 1, 2, 3
 

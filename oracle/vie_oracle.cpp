@@ -16,6 +16,7 @@
 #include <complex>
 #include <cstring>
 #include <functional>
+#include <limits>
 #include <map>
 #include <mutex>
 #include <random>
@@ -867,6 +868,144 @@ std::vector<cd> n_mode(const std::vector<cd>& t, I64 d[3], const Mat& u, int mod
   return out;
 }
 
+// ---- CP-ALS (decomp.hpp:184-298) and tucker_cp (decomp.hpp:336-373) ----
+// khatri_rao (tensor.hpp:146-153): column l = a(:, l) (x) b(:, l), b fastest
+Mat khatri_rao(const Mat& a, const Mat& b) {
+  Mat o(a.rows * b.rows, a.cols);
+  for (I64 l = 0; l < a.cols; ++l)
+    for (I64 ia = 0; ia < a.rows; ++ia)
+      for (I64 ib = 0; ib < b.rows; ++ib) o(ia * b.rows + ib, l) = a(ia, l) * b(ib, l);
+  return o;
+}
+
+// cp_reconstruct (tensor.hpp:157-168): mode-1 unfolding = v1 khatri_rao(v3, v2)^T
+std::vector<cd> cp_reconstruct(const Mat& v1, const Mat& v2, const Mat& v3) {
+  std::vector<cd> t(static_cast<size_t>(v1.rows * v2.rows * v3.rows), cd(0.0));
+  if (v1.cols == 0) return t;
+  const Mat kr = khatri_rao(v3, v2);
+  for (I64 p = 0; p < kr.rows; ++p)
+    for (I64 l = 0; l < v1.cols; ++l) {
+      const cd z = kr(p, l);
+      for (I64 i = 0; i < v1.rows; ++i) t[static_cast<size_t>(i + v1.rows * p)] += v1(i, l) * z;
+    }
+  return t;
+}
+
+double fro(const std::vector<cd>& t) {
+  double s = 0.0;
+  for (const cd& x : t) s += std::norm(x);
+  return std::sqrt(s);
+}
+
+// detail::cp_ls_update (decomp.hpp:200-219): v = (a_unf conj(z)) conj(pinv(gram)),
+// gram = (b^H b) .* (c^H c), pinv by a Jacobi SVD with relative cutoff 1e-12
+Mat cp_ls_update(const Mat& a_unf, const Mat& b, const Mat& c) {
+  const Mat z = khatri_rao(c, b);
+  Mat zc = z;
+  for (cd& x : zc.a) x = std::conj(x);
+  const Mat rhs = matmul(a_unf, zc);
+  const Mat gb = matmul(adjoint(b), b), gc = matmul(adjoint(c), c);
+  Mat gram(gb.rows, gb.cols);
+  for (size_t e = 0; e < gram.a.size(); ++e) gram.a[e] = gb.a[e] * gc.a[e];
+  Mat u, v;
+  std::vector<double> s;
+  jacobi_svd(gram, u, s, v);
+  const double cutoff = (s.empty() ? 0.0 : s[0]) * 1e-12;
+  const I64 r = gram.rows;
+  Mat pinv(r, r);  // V diag(sinv) U^H
+  for (size_t j = 0; j < s.size(); ++j) {
+    if (!(s[j] > cutoff)) continue;
+    const double inv = 1.0 / s[j];
+    for (I64 col = 0; col < r; ++col) {
+      const cd uc = std::conj(u(col, static_cast<I64>(j))) * inv;
+      for (I64 row = 0; row < r; ++row) pinv(row, col) += v(row, static_cast<I64>(j)) * uc;
+    }
+  }
+  for (cd& x : pinv.a) x = std::conj(x);
+  return matmul(rhs, pinv);
+}
+
+// detail::cp_normalize_columns (decomp.hpp:221-230)
+void cp_normalize_columns(Mat f[3]) {
+  for (I64 l = 0; l < f[0].cols; ++l) {
+    double n[3];
+    for (int q = 0; q < 3; ++q) {
+      double s = 0.0;
+      for (I64 i = 0; i < f[q].rows; ++i) s += std::norm(f[q](i, l));
+      n[q] = std::sqrt(s);
+    }
+    const double mag = std::cbrt(n[0] * n[1] * n[2]);
+    for (int q = 0; q < 3; ++q)
+      if (n[q] > 0)
+        for (I64 i = 0; i < f[q].rows; ++i) f[q](i, l) *= mag / n[q];
+  }
+}
+
+struct CpAlsOut {
+  Mat f[3];
+  std::vector<double> trace;
+  bool converged = false, ill_posed = false;
+};
+
+// cp_als (decomp.hpp:237-298): SVD-initialised factors (seeded Gaussian columns beyond
+// the unfolding's rank), ALS sweeps over the three modes, column normalisation, relative
+// error per sweep, stop when the decrease falls below stall_tol
+CpAlsOut cp_als(const cd* t, const I64 d[3], I64 r, int max_iters, double stall_tol, uint64_t seed) {
+  if (r < 0) throw invalid("cp_als: rank must be >= 0");
+  if (max_iters < 1) throw invalid("cp_als: max_iters must be >= 1");
+  CpAlsOut res;
+  const std::vector<cd> tv(t, t + d[0] * d[1] * d[2]);
+  const double tnorm = fro(tv);
+  I64 sorted[3] = {d[0], d[1], d[2]};
+  std::sort(sorted, sorted + 3);
+  res.ill_posed = r > sorted[0] * sorted[1];
+  if (r == 0 || tnorm == 0.0) {
+    for (int q = 0; q < 3; ++q) res.f[q] = Mat(d[q], r);
+    res.trace.push_back(tnorm == 0.0 ? 0.0 : 1.0);
+    res.converged = tnorm == 0.0;
+    return res;
+  }
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> gauss(0.0, 1.0);
+  Mat unf[3];
+  for (int q = 0; q < 3; ++q) {
+    unf[q] = unfold(t, d, q + 1);
+    Mat u, v;
+    std::vector<double> s;
+    thin_svd(unf[q], u, s, v);
+    const I64 have = std::min<I64>(u.cols, r);
+    Mat f(d[q], r);
+    for (I64 l = 0; l < have; ++l)
+      for (I64 i = 0; i < d[q]; ++i) f(i, l) = u(i, l);
+    for (I64 l = have; l < r; ++l) {
+      for (I64 i = 0; i < d[q]; ++i) f(i, l) = cd(gauss(rng), gauss(rng));
+      double nn = 0.0;
+      for (I64 i = 0; i < d[q]; ++i) nn += std::norm(f(i, l));
+      nn = std::sqrt(nn);
+      if (nn > 0)
+        for (I64 i = 0; i < d[q]; ++i) f(i, l) /= nn;
+    }
+    res.f[q] = std::move(f);
+  }
+  double prev = std::numeric_limits<double>::infinity();
+  for (int sweep = 0; sweep < max_iters; ++sweep) {
+    res.f[0] = cp_ls_update(unf[0], res.f[1], res.f[2]);
+    res.f[1] = cp_ls_update(unf[1], res.f[0], res.f[2]);
+    res.f[2] = cp_ls_update(unf[2], res.f[0], res.f[1]);
+    cp_normalize_columns(res.f);
+    std::vector<cd> rec = cp_reconstruct(res.f[0], res.f[1], res.f[2]);
+    for (size_t e = 0; e < rec.size(); ++e) rec[e] -= tv[e];
+    const double err = fro(rec) / tnorm;
+    res.trace.push_back(err);
+    if (prev - err < stall_tol) {
+      res.converged = err <= prev + stall_tol;
+      break;
+    }
+    prev = err;
+  }
+  return res;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -1180,6 +1319,71 @@ int orc_hosvd(const double* t, const int64_t dims[3], double tol, int rule, int6
     double* us[3] = {u1, u2, u3};
     for (int q = 0; q < 3; ++q)
       if (us[q]) std::copy(factors[q].a.begin(), factors[q].a.end(), reinterpret_cast<cd*>(us[q]));
+  });
+}
+
+// cp_als (decomp.hpp:237-298).  f_q: dims[q] x r column-major (may be null); trace: up to
+// trace_cap entries; flags[0] = converged, flags[1] = ill_posed_rank.
+int orc_cp_als(const double* t, const int64_t dims[3], int64_t r, int max_iters, double stall_tol, uint64_t seed,
+               double* f1, double* f2, double* f3, double* trace, int trace_cap, int* ntrace, int flags[2]) {
+  return guard([&] {
+    CpAlsOut o = cp_als(reinterpret_cast<const cd*>(t), dims, r, max_iters, stall_tol, seed);
+    double* fs[3] = {f1, f2, f3};
+    for (int q = 0; q < 3; ++q)
+      if (fs[q]) std::copy(o.f[q].a.begin(), o.f[q].a.end(), reinterpret_cast<cd*>(fs[q]));
+    *ntrace = static_cast<int>(o.trace.size());
+    for (int i = 0; i < std::min(trace_cap, *ntrace); ++i) trace[i] = o.trace[static_cast<size_t>(i)];
+    flags[0] = o.converged;
+    flags[1] = o.ill_posed;
+  });
+}
+
+// tucker_cp (decomp.hpp:336-373): hosvd, cp_als on the core (rank min(r_q) unless cp_rank >= 0,
+// default seed), W_q = U_q V_q.  w_q: dims[q] x rank (null: only *rank_out is set).
+// errs = {hosvd_relative_error, core_cp_relative_error, achieved_relative_error}.
+int orc_tucker_cp(const double* t, const int64_t dims[3], double tol, int cp_iters, int rule, int64_t cp_rank,
+                  double stall_tol, int64_t* rank_out, double* w1, double* w2, double* w3, double errs[3],
+                  double* trace, int trace_cap, int* ntrace) {
+  return guard([&] {
+    int64_t rk[3];
+    if (orc_hosvd(t, dims, tol, rule, rk, nullptr, nullptr, nullptr, nullptr) != 0) throw invalid(g_err);
+    std::vector<cd> core(static_cast<size_t>(rk[0] * rk[1] * rk[2]));
+    Mat U[3];
+    for (int q = 0; q < 3; ++q) U[q] = Mat(dims[q], rk[q]);
+    if (orc_hosvd(t, dims, tol, rule, rk, reinterpret_cast<double*>(core.data()),
+                  reinterpret_cast<double*>(U[0].a.data()), reinterpret_cast<double*>(U[1].a.data()),
+                  reinterpret_cast<double*>(U[2].a.data())) != 0)
+      throw invalid(g_err);
+    const I64 r = cp_rank >= 0 ? cp_rank : std::min({rk[0], rk[1], rk[2]});
+    *rank_out = r;
+    if (!w1) return;
+    const cd* tc = reinterpret_cast<const cd*>(t);
+    const std::vector<cd> tv(tc, tc + dims[0] * dims[1] * dims[2]);
+    const double tnorm = fro(tv);
+    {  // ||t - tucker reconstruct|| / ||t||
+      std::vector<cd> rec = core;
+      I64 d[3] = {rk[0], rk[1], rk[2]};
+      for (int q = 0; q < 3; ++q) rec = n_mode(rec, d, U[q], q + 1);
+      for (size_t e = 0; e < rec.size(); ++e) rec[e] -= tv[e];
+      errs[0] = tnorm > 0 ? fro(rec) / tnorm : 0.0;
+    }
+    const I64 cd3[3] = {rk[0], rk[1], rk[2]};
+    CpAlsOut cp = cp_als(core.data(), cd3, r, cp_iters, stall_tol, 0x5eed);
+    errs[1] = cp.trace.empty() ? 0.0 : cp.trace.back();
+    Mat W[3];
+    for (int q = 0; q < 3; ++q) W[q] = matmul(U[q], cp.f[q]);
+    double* ws[3] = {w1, w2, w3};
+    for (int q = 0; q < 3; ++q) std::copy(W[q].a.begin(), W[q].a.end(), reinterpret_cast<cd*>(ws[q]));
+    if (tnorm > 0) {
+      std::vector<cd> rec = cp_reconstruct(W[0], W[1], W[2]);
+      for (size_t e = 0; e < rec.size(); ++e) rec[e] -= tv[e];
+      errs[2] = fro(rec) / tnorm;
+    } else {
+      errs[2] = 0.0;
+    }
+    *ntrace = static_cast<int>(cp.trace.size());
+    if (trace)
+      for (int i = 0; i < std::min(trace_cap, *ntrace); ++i) trace[i] = cp.trace[static_cast<size_t>(i)];
   });
 }
 

@@ -123,6 +123,15 @@ int orc_truncated_svd_values(const double* m, int64_t rows, int64_t cols, double
  * buffers sized core r1*r2*r3, U_q n_q*r_q.                                */
 int orc_hosvd(const double* t, const int64_t dims[3], double tol, int rule, int64_t ranks[3],
               double* core, double* u1, double* u2, double* u3);
+/* cp_als (decomp.hpp:237-298): f_q dims[q] x r (col-major, may be NULL), trace up to
+ * trace_cap sweeps, flags = {converged, ill_posed_rank}. */
+int orc_cp_als(const double* t, const int64_t dims[3], int64_t r, int max_iters, double stall_tol, uint64_t seed,
+               double* f1, double* f2, double* f3, double* trace, int trace_cap, int* ntrace, int flags[2]);
+/* tucker_cp (decomp.hpp:336-373): merged factors W_q (dims[q] x rank; NULL = rank only),
+ * errs = {hosvd_relative_error, core_cp_relative_error, achieved_relative_error}. */
+int orc_tucker_cp(const double* t, const int64_t dims[3], double tol, int cp_iters, int rule, int64_t cp_rank,
+                  double stall_tol, int64_t* rank_out, double* w1, double* w2, double* w3, double errs[3],
+                  double* trace, int trace_cap, int* ntrace);
 
 /* solve_scene stages (solver.hpp:148-285), PWC fields (3 blocks of n_vox).
  * geo = {res0, res1, res2, org0, org1, org2}; pw = {pol0..2, dir0..2, amplitude}

@@ -10,7 +10,7 @@ from .vie import (KIND_K, KIND_N, PWC, PWL, DftService, EmbeddedSpectrum, GmresC
                   SolveReport, solve_scene, tucker_cp_form, gmres_map, ApplyTimings, apply_operator_timed,
                   KIND_G, QuadratureSpec, assemble_defining_tensor, assemble_operator, self_static_term,
                   set_strategy, get_strategy, save_container, load_container, container_info, Comm, Loopback,
-                  comm_unique_id)
+                  comm_unique_id, cp_als, tucker_cp, CpAlsResult, TuckerCpResult)
 
 __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "GmresConfig", "GmresResult",
            "TuckerForm", "VieError", "apply_operator", "apply_operator_batch", "apply_system", "build_operator_spectra",
@@ -19,4 +19,5 @@ __all__ = ["KIND_N", "KIND_K", "PWC", "PWL", "DftService", "EmbeddedSpectrum", "
            "recover_fields", "SolveReport", "solve_scene", "tucker_cp_form", "gmres_map", "ApplyTimings",
            "apply_operator_timed", "KIND_G", "QuadratureSpec", "assemble_defining_tensor", "assemble_operator",
            "self_static_term", "set_strategy", "get_strategy", "save_container", "load_container",
-           "container_info", "Comm", "Loopback", "comm_unique_id"]
+           "container_info", "Comm", "Loopback", "comm_unique_id", "cp_als", "tucker_cp",
+           "CpAlsResult", "TuckerCpResult"]

@@ -17,7 +17,7 @@ OBJ = os.path.join(HERE, "build", "obj")
 LIB = os.path.join(HERE, "libvie_b200.so")
 SOURCES = ["api.cu", "kernels_fft.cu", "kernels_pencil.cu", "kernels_decomp.cu", "kernels_blas.cu",
            "kernels_hosvd.cu", "kernels_fft2.cu", "kernels_pencil2.cu", "kernels_scene.cu",
-           "kernels_pencil3.cu", "kernels_assembly.cu", "kernels_pencil4.cu", "kernels_fused.cu"]
+           "kernels_pencil3.cu", "kernels_assembly.cu", "kernels_pencil4.cu", "kernels_fused.cu", "cp_als.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "kernels.cuh", "twiddles_gen.cuh", "hadamard.cuh", "tma.cuh",
            "decomp_tile.cuh", "pencil4.cuh"]
 

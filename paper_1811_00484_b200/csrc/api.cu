@@ -1901,8 +1901,17 @@ namespace {
 // squared-condition loss of the one-pass Gram method is removed and small singular
 // values resolve down to ~eps sigma_max, as the reference's QR + JacobiSVD
 // (decomp.hpp:40-70).  Ranks by truncation_rank (decomp.hpp:72-103).
-void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, const int sign[3], double tol,
-                         int rule, vie_tucker* out, int64_t ranks_out[3], int passes) {
+struct HosvdResult {
+  std::vector<cd> U[3];  // n_q x r_q spatial factors (host)
+  int64_t rk[3];
+  std::vector<cd> core;       // r1 r2 r3 (host)
+  const double2* core_dev;    // the same on the device (owned by the caller's pool)
+};
+
+void hosvd_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, const int sign[3], double tol, int rule,
+               int passes, DevPool& dev, HosvdResult& h) {
+  std::vector<cd>* U = h.U;
+  int64_t* rk = h.rk;
   for (int q = 0; q < 3; ++q) {
     if (dims[q] < 1) throw Invalid("hosvd: degenerate tensor dimensions");
     if (sign[q] != 1 && sign[q] != -1) throw Invalid("tucker_compress: sign must be +-1");
@@ -1911,9 +1920,6 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
   if (rule != VIE_RULE_SIGMA_MAX && rule != VIE_RULE_ENERGY) throw Invalid("tucker_compress: bad rule");
   if (dims[0] > 4096 || dims[1] > 4096 || dims[2] > 4096) throw Invalid("tucker_compress: dims too large");
   cudaStream_t st = ctx->stream;
-  DevPool dev;
-  std::vector<cd> U[3];
-  int64_t rk[3];
   for (int q = 0; q < 3; ++q) {
     const int n = static_cast<int>(dims[q]);
     double2* dG = dev.alloc<double2>(static_cast<size_t>(n) * n);
@@ -1982,9 +1988,20 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
     d[1] = od[1];
     d[2] = od[2];
   }
-  std::vector<cd> core(static_cast<size_t>(rk[0] * rk[1] * rk[2]));
-  VIE_CUDA_CHECK(cudaMemcpyAsync(core.data(), cur, sizeof(double2) * core.size(), cudaMemcpyDeviceToHost, st));
+  h.core.assign(static_cast<size_t>(rk[0] * rk[1] * rk[2]), cd(0.0));
+  VIE_CUDA_CHECK(cudaMemcpyAsync(h.core.data(), cur, sizeof(double2) * h.core.size(), cudaMemcpyDeviceToHost, st));
   VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  h.core_dev = cur;
+}
+
+void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, const int sign[3], double tol,
+                         int rule, vie_tucker* out, int64_t ranks_out[3], int passes) {
+  DevPool dev;
+  HosvdResult h;
+  hosvd_dev(ctx, dims, dt, sign, tol, rule, passes, dev, h);
+  const int64_t* rk = h.rk;
+  const std::vector<cd>* U = h.U;
+  const std::vector<cd>& core = h.core;
   const int rc = vie_tucker_from_factors(ctx, dims, rk, reinterpret_cast<const double*>(core.data()),
                                          reinterpret_cast<const double*>(U[0].data()),
                                          reinterpret_cast<const double*>(U[1].data()),
@@ -1997,6 +2014,96 @@ void tucker_compress_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, 
 }
 
 int hosvd_passes() { return env_int("VIE_HOSVD_PASSES", 2); }
+
+// tucker_cp (decomp.hpp:336-373) of a DEVICE tensor: the device HOSVD above, cp_als on its core
+// (cp_als.cu), merged factors W_q = U_q V_q; the three relative errors of TuckerCpResult
+// (hosvd, core CP, achieved) from device residual norms.  out (optional): the device form of
+// transform_factors(TuckerCPForm) (vie_tucker_from_cp); w (optional): the spatial W_q on the host.
+void tucker_cp_dev(vie_ctx ctx, const int64_t dims[3], const double2* dt, const int sign[3], double tol, int rule,
+                   int cp_iters, int64_t cp_rank, double stall_tol, vie_tucker* out, int64_t* rank_out,
+                   double* const w[3], int64_t w_cap, double errs[3], double* trace, int trace_cap, int* ntrace) {
+  if (cp_iters < 1) throw Invalid("cp_als: max_iters must be >= 1");
+  DevPool dev;
+  HosvdResult h;
+  hosvd_dev(ctx, dims, dt, sign, tol, rule, hosvd_passes(), dev, h);
+  const int64_t r = cp_rank >= 0 ? cp_rank : std::min({h.rk[0], h.rk[1], h.rk[2]});
+  if (rank_out) *rank_out = r;
+  if (w && r > w_cap) throw Invalid("tucker_cp: factor buffers hold fewer columns than the CP rank");
+  const vie::CpAlsHost cp =
+      vie::cp_als_host(reinterpret_cast<const double2*>(h.core.data()), h.rk, r, cp_iters, stall_tol, 0x5eedull);
+  std::vector<cd> W[3];
+  for (int q = 0; q < 3; ++q) {
+    const int64_t n = dims[q], rq = h.rk[q];
+    W[q].assign(static_cast<size_t>(n * r), cd(0.0));
+    for (int64_t l = 0; l < r; ++l)
+      for (int64_t k = 0; k < rq; ++k) {
+        const double2 v = cp.f[q][static_cast<size_t>(k + rq * l)];
+        const cd vk(v.x, v.y);
+        if (vk == cd(0.0)) continue;
+        for (int64_t i = 0; i < n; ++i)
+          W[q][static_cast<size_t>(i + n * l)] += h.U[q][static_cast<size_t>(i + n * k)] * vk;
+      }
+  }
+  cudaStream_t st = ctx->stream;
+  const int64_t nv = dims[0] * dims[1] * dims[2];
+  double* acc = dev.alloc<double>(3);
+  VIE_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * sizeof(double), st));
+  vie::launch_diff_norm2(dt, nullptr, nv, acc, st);
+  {  // Tucker reconstruction core x1 U1 x2 U2 x3 U3 (mode products with U_q^H as the "U^H" operand)
+    int64_t d[3] = {h.rk[0], h.rk[1], h.rk[2]};
+    const double2* cur = h.core_dev;
+    for (int q = 0; q < 3; ++q) {
+      const int64_t n = dims[q], rq = h.rk[q];
+      std::vector<cd> uh(static_cast<size_t>(rq * n));
+      for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = 0; k < rq; ++k)
+          uh[static_cast<size_t>(k + rq * i)] = std::conj(h.U[q][static_cast<size_t>(i + n * k)]);
+      double2* du = dev.alloc<double2>(uh.size());
+      VIE_CUDA_CHECK(cudaMemcpyAsync(du, uh.data(), sizeof(double2) * uh.size(), cudaMemcpyHostToDevice, st));
+      int64_t od[3] = {d[0], d[1], d[2]};
+      od[q] = n;
+      double2* nxt = dev.alloc<double2>(static_cast<size_t>(od[0] * od[1] * od[2]));
+      vie::launch_mode_product_h(cur, d, q + 1, du, static_cast<int>(n), nxt, st);
+      VIE_CUDA_CHECK(cudaStreamSynchronize(st));  // uh leaves scope
+      cur = nxt;
+      d[0] = od[0];
+      d[1] = od[1];
+      d[2] = od[2];
+    }
+    vie::launch_diff_norm2(dt, cur, nv, acc + 1, st);
+  }
+  double2* dw[3];
+  for (int q = 0; q < 3; ++q) {
+    dw[q] = dev.alloc<double2>(std::max<size_t>(W[q].size(), 1));
+    if (!W[q].empty())
+      VIE_CUDA_CHECK(cudaMemcpyAsync(dw[q], W[q].data(), sizeof(double2) * W[q].size(), cudaMemcpyHostToDevice, st));
+  }
+  vie::launch_cp_residual2(dt, dims, dw[0], dw[1], dw[2], static_cast<int>(r), acc + 2, st);
+  double hacc[3];
+  VIE_CUDA_CHECK(cudaMemcpyAsync(hacc, acc, sizeof(hacc), cudaMemcpyDeviceToHost, st));
+  VIE_CUDA_CHECK(cudaStreamSynchronize(st));
+  const double tn = std::sqrt(hacc[0]);
+  if (errs) {
+    errs[0] = tn > 0 ? std::sqrt(hacc[1]) / tn : 0.0;
+    errs[1] = cp.trace.empty() ? 0.0 : cp.trace.back();
+    errs[2] = tn > 0 ? std::sqrt(hacc[2]) / tn : 0.0;
+  }
+  if (ntrace) *ntrace = static_cast<int>(cp.trace.size());
+  if (trace)
+    for (int i = 0; i < std::min(trace_cap, static_cast<int>(cp.trace.size())); ++i)
+      trace[i] = cp.trace[static_cast<size_t>(i)];
+  if (w)
+    for (int q = 0; q < 3; ++q)
+      if (w[q]) std::copy(W[q].begin(), W[q].end(), reinterpret_cast<cd*>(w[q]));
+  if (out) {
+    const int rc = vie_tucker_from_cp(ctx, dims, r, reinterpret_cast<const double*>(W[0].data()),
+                                      reinterpret_cast<const double*>(W[1].data()),
+                                      reinterpret_cast<const double*>(W[2].data()), sign, 0, out);
+    if (rc != VIE_OK) throw Invalid(g_err);
+    (*out)->rule = rule;
+    (*out)->tol = tol;
+  }
+}
 }  // namespace
 
 extern "C" {
@@ -2035,6 +2142,66 @@ int vie_tucker_compress_device(vie_ctx ctx, const int64_t dims[3], const double*
     sj.done();
     VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
     cudaEventDestroy(ev);
+  });
+}
+
+int vie_tucker_cp(vie_ctx ctx, const int64_t dims[3], const double* t, int t_on_device, const int sign[3],
+                  double tol, int rule, int cp_iters, int64_t cp_rank, double stall_tol, vie_tucker* out,
+                  int64_t* rank_out, double* w1, double* w2, double* w3, int64_t w_cap, double errs[3], double* trace,
+                  int trace_cap, int* ntrace, void* stream) {
+  return guard([&] {
+    if (!ctx || !dims || !t || !sign) throw Invalid("tucker_cp: null argument");
+    for (int q = 0; q < 3; ++q)
+      if (dims[q] < 1) throw Invalid("hosvd: degenerate tensor dimensions");
+    VIE_CUDA_CHECK(cudaSetDevice(ctx->device));
+    double* const w[3] = {w1, w2, w3};
+    const bool want_w = w1 || w2 || w3;
+    if (!t_on_device) {
+      const int64_t nv = dims[0] * dims[1] * dims[2];
+      check_cplx_finite_host(t, static_cast<size_t>(nv), "tucker_cp: tensor");
+      DevPool dev;
+      double2* dt = dev.alloc<double2>(static_cast<size_t>(nv));
+      copy_sync(dt, t, sizeof(double2) * nv, ctx->stream);
+      tucker_cp_dev(ctx, dims, dt, sign, tol, rule, cp_iters, cp_rank, stall_tol, out, rank_out,
+                    want_w ? w : nullptr, w_cap, errs, trace, trace_cap, ntrace);
+      return;
+    }
+    cudaEvent_t ev = nullptr;
+    VIE_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    StreamJoin sj(ctx->stream, static_cast<cudaStream_t>(stream), ev);
+    try {
+      tucker_cp_dev(ctx, dims, reinterpret_cast<const double2*>(t), sign, tol, rule, cp_iters, cp_rank, stall_tol,
+                    out, rank_out, want_w ? w : nullptr, w_cap, errs, trace, trace_cap, ntrace);
+    } catch (...) {
+      cudaEventDestroy(ev);
+      throw;
+    }
+    sj.done();
+    VIE_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    cudaEventDestroy(ev);
+  });
+}
+
+int vie_cp_als(const int64_t dims[3], const double* t_host, int64_t r, int max_iters, double stall_tol,
+               uint64_t seed, double* f1, double* f2, double* f3, double* trace, int trace_cap, int* ntrace,
+               int flags[2]) {
+  return guard([&] {
+    if (!dims || !t_host) throw Invalid("cp_als: null argument");
+    for (int q = 0; q < 3; ++q)
+      if (dims[q] < 0) throw Invalid("cp_als: negative dims");
+    const vie::CpAlsHost o =
+        vie::cp_als_host(reinterpret_cast<const double2*>(t_host), dims, r, max_iters, stall_tol, seed);
+    double* fs[3] = {f1, f2, f3};
+    for (int q = 0; q < 3; ++q)
+      if (fs[q]) std::copy(o.f[q].begin(), o.f[q].end(), reinterpret_cast<double2*>(fs[q]));
+    if (ntrace) *ntrace = static_cast<int>(o.trace.size());
+    if (trace)
+      for (int i = 0; i < std::min(trace_cap, static_cast<int>(o.trace.size())); ++i)
+        trace[i] = o.trace[static_cast<size_t>(i)];
+    if (flags) {
+      flags[0] = o.converged;
+      flags[1] = o.ill_posed;
+    }
   });
 }
 

@@ -170,6 +170,21 @@ void launch_gram(const double2* t, const int64_t dims[3], int mode, double2* G, 
 // out = in x_mode U^H (U: n_mode x r col-major)
 void launch_mode_product_h(const double2* in, const int64_t dims[3], int mode, const double2* U, int r,
                            double2* out, cudaStream_t st);
+// *acc += sum |a - b|^2 (b null: sum |a|^2); acc is a device double the caller zeroes
+void launch_diff_norm2(const double2* a, const double2* b, int64_t n, double* acc, cudaStream_t st);
+// *acc += sum |t - cp(W1, W2, W3)|^2 (W_q: dims[q] x R col-major, device)
+void launch_cp_residual2(const double2* t, const int64_t dims[3], const double2* w1, const double2* w2,
+                         const double2* w3, int R, double* acc, cudaStream_t st);
+
+// ---- cp_als (decomp.hpp:237-298) on a host tensor (the HOSVD core: r1 r2 r3 <= a few
+// 10^4 entries, setup work like the r x r eigenproblems of the HOSVD); cp_als.cu
+struct CpAlsHost {
+  std::vector<double2> f[3];  // d_q x r col-major
+  std::vector<double> trace;  // relative error per sweep
+  bool converged = false, ill_posed = false;
+};
+CpAlsHost cp_als_host(const double2* t, const int64_t d[3], int64_t r, int max_iters, double stall_tol,
+                      uint64_t seed);
 
 // ---- Green's-tensor assembly (kernels_assembly.cu; assembly.hpp:159-233)
 struct AssemblyDesc {

@@ -66,6 +66,58 @@ __global__ void k_mode_product_h(const double2* __restrict__ in, int64_t d1, int
   }
 }
 
+// sum |a - b|^2 (b may be null) into *acc (one double, zeroed by the caller)
+__global__ void k_diff_norm2(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                             double* __restrict__ acc) {
+  double s = 0.0;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double2 v = a[e];
+    if (b) {
+      v.x -= b[e].x;
+      v.y -= b[e].y;
+    }
+    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += ws[w];
+    atomicAdd(acc, t);
+  }
+}
+
+// sum |t - cp(W1, W2, W3)|^2, cp(i,j,k) = sum_l W1(i,l) W2(j,l) W3(k,l) (tensor.hpp:157-168)
+__global__ void k_cp_residual2(const double2* __restrict__ t, int64_t n1, int64_t n2, int64_t n3,
+                               const double2* __restrict__ w1, const double2* __restrict__ w2,
+                               const double2* __restrict__ w3, int R, double* __restrict__ acc) {
+  double s = 0.0;
+  const int64_t n = n1 * n2 * n3;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = e % n1, j = (e / n1) % n2, k = e / (n1 * n2);
+    double2 rec = make_double2(0.0, 0.0);
+    for (int l = 0; l < R; ++l) {
+      const double2 p = cmul(w1[i + n1 * l], w2[j + n2 * l]);
+      rec = cadd(rec, cmul(p, w3[k + n3 * l]));
+    }
+    const double dx = t[e].x - rec.x, dy = t[e].y - rec.y;
+    s = fma(dx, dx, fma(dy, dy, s));
+  }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double ws[8];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tt = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tt += ws[w];
+    atomicAdd(acc, tt);
+  }
+}
+
 }  // namespace
 
 void launch_gram(const double2* t, const int64_t dims[3], int mode, double2* G, cudaStream_t st) {
@@ -80,6 +132,20 @@ void launch_mode_product_h(const double2* in, const int64_t dims[3], int mode, c
   const int64_t total = (mode == 1 ? r : dims[0]) * (mode == 2 ? r : dims[1]) * (mode == 3 ? r : dims[2]);
   const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
   k_mode_product_h<<<std::max(blocks, 1), 256, 0, st>>>(in, dims[0], dims[1], dims[2], mode, U, r, out);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_diff_norm2(const double2* a, const double2* b, int64_t n, double* acc, cudaStream_t st) {
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_diff_norm2<<<std::max(blocks, 1), 256, 0, st>>>(a, b, n, acc);
+  VIE_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_cp_residual2(const double2* t, const int64_t dims[3], const double2* w1, const double2* w2,
+                         const double2* w3, int R, double* acc, cudaStream_t st) {
+  const int64_t n = dims[0] * dims[1] * dims[2];
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 8));
+  k_cp_residual2<<<std::max(blocks, 1), 256, 0, st>>>(t, dims[0], dims[1], dims[2], w1, w2, w3, R, acc);
   VIE_CUDA_CHECK(cudaGetLastError());
 }
 

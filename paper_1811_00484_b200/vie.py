@@ -53,6 +53,10 @@ def lib() -> C.CDLL:
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"libvie_b200.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        try:  # torch first: its (newer) NCCL must own libnccl.so.2 before the library pulls it in
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         L = C.CDLL(LIB_PATH)
         L.vie_last_error.restype = C.c_char_p
         L.vie_version.restype = C.c_char_p
@@ -326,6 +330,83 @@ def tucker_compress(dft: DftService, t, dims, sign, tol: float = 1e-8, rule: int
                                      (C.c_int * 3)(*[int(x) for x in sign]), C.c_double(tol), int(rule),
                                      C.byref(h), ranks))
     return TuckerForm._from_handle(dft, h, dims, [ranks[0], ranks[1], ranks[2]], sign)
+
+
+@dataclass
+class CpAlsResult:
+    """CpAlsResult (decomp.hpp:184-190): factors (dims[q], r), error per sweep, flags."""
+    factors: list
+    rel_error_trace: np.ndarray
+    converged: bool
+    ill_posed_rank: bool
+
+
+def cp_als(t, dims, r: int, max_iters: int = 100, stall_tol: float = 1e-12, seed: int = 0x5EED) -> CpAlsResult:
+    """cp_als (decomp.hpp:237-298) of a host tensor (flat, reference layout): the CP fitting
+    of a Tucker core (r1 r2 r3 entries), run by the library next to the HOSVD's r x r
+    eigenproblems (cp_als.cu)."""
+    t = _cplx(np.asarray(t).reshape(-1, order="F") if np.asarray(t).ndim == 3 else t).reshape(-1)
+    if t.size != int(np.prod(dims)):
+        raise ValueError("cp_als: tensor size does not match dims")
+    if r < 0:
+        raise ValueError("cp_als: rank must be >= 0")
+    fs = [np.zeros(max(int(dims[q]) * int(r), 1), np.complex128) for q in range(3)]
+    cap = max(int(max_iters), 1) + 1
+    tr = np.empty(cap)
+    nt = C.c_int()
+    flags = (C.c_int * 2)()
+    _check(lib().vie_cp_als(_i64(dims), t.ctypes.data_as(_dp), C.c_int64(r), int(max_iters), C.c_double(stall_tol),
+                            C.c_uint64(seed), fs[0].ctypes.data_as(_dp), fs[1].ctypes.data_as(_dp),
+                            fs[2].ctypes.data_as(_dp), tr.ctypes.data_as(_dp), cap, C.byref(nt), flags))
+    facs = [fs[q][:int(dims[q]) * int(r)].reshape((int(dims[q]), int(r)), order="F") for q in range(3)]
+    return CpAlsResult(facs, tr[:nt.value].copy(), bool(flags[0]), bool(flags[1]))
+
+
+@dataclass
+class TuckerCpResult:
+    """TuckerCpResult (decomp.hpp:300-307): `form` is the device form of
+    transform_factors(TuckerCPForm) (operator.hpp:92-106), `factors` the spatial merged
+    factors W_q = U_q V_q."""
+    form: "TuckerForm"
+    factors: list
+    rank: int
+    hosvd_relative_error: float
+    core_cp_relative_error: float
+    achieved_relative_error: float
+    cp_error_trace: np.ndarray
+
+
+def tucker_cp(dft: DftService, t, dims, sign, tol: float, cp_iters: int = 1000, rule: int = RULE_ENERGY,
+              cp_rank: int = -1, stall_tol: float = 0.0) -> TuckerCpResult:
+    """tucker_cp (decomp.hpp:336-373): HOSVD on the device, CP-ALS on the core, merged
+    factors; t is a host array or a CUDA tensor (flat, reference layout)."""
+    on_dev = hasattr(t, "is_cuda") and t.is_cuda
+    if on_dev:
+        tt = t.reshape(-1).to(_torch().complex128).contiguous()
+        ptr, n = C.c_void_p(tt.data_ptr()), tt.numel()
+        stream = C.c_void_p(_stream_handle(None, tt.device))
+    else:
+        tt = _cplx(np.asarray(t).reshape(-1, order="F") if np.asarray(t).ndim == 3 else t).reshape(-1)
+        ptr, n, stream = C.c_void_p(tt.ctypes.data), tt.size, None
+    if n != int(np.prod(dims)):
+        raise ValueError("tucker_cp: tensor size does not match dims")
+    cap = int(cp_rank) if cp_rank >= 0 else int(min(dims))
+    ws = [np.zeros(max(int(dims[q]) * cap, 1), np.complex128) for q in range(3)]
+    h = C.c_void_p()
+    rk = C.c_int64()
+    errs = (C.c_double * 3)()
+    trc = int(cp_iters) + 1
+    tr = np.empty(trc)
+    nt = C.c_int()
+    _check(lib().vie_tucker_cp(dft.handle, _i64(dims), ptr, int(on_dev), (C.c_int * 3)(*[int(x) for x in sign]),
+                               C.c_double(tol), int(rule), int(cp_iters), C.c_int64(cp_rank), C.c_double(stall_tol),
+                               C.byref(h), C.byref(rk), ws[0].ctypes.data_as(_dp), ws[1].ctypes.data_as(_dp),
+                               ws[2].ctypes.data_as(_dp), C.c_int64(cap), errs, tr.ctypes.data_as(_dp), trc,
+                               C.byref(nt), stream))
+    r = rk.value
+    form = TuckerForm._from_handle(dft, h, dims, (r,) * 3, sign)
+    facs = [ws[q][:int(dims[q]) * r].reshape((int(dims[q]), r), order="F") for q in range(3)]
+    return TuckerCpResult(form, facs, r, errs[0], errs[1], errs[2], tr[:nt.value].copy())
 
 
 @dataclass

@@ -413,6 +413,69 @@ int main() {
     expect(std::sqrt(num / den) <= 1e-13, "CP vs superdiagonal Tucker");
   });
 
+  // tucker_cp / cp_als through the wrapper (decomp.hpp:237-373) vs the oracle restatement
+  run("TuckerCp.MatchesOracle", [&] {
+    const int64_t d[3] = {7, 6, 5};
+    Tensor3 t(d[0], d[1], d[2]);
+    if (orc_random_tensor(d[0], d[1], d[2], 77, reinterpret_cast<double*>(t.data.data())))
+      throw std::runtime_error(orc_last_error());
+    const TuckerCpResult a = tucker_cp(t, 0.3, 60, TruncationRule::Energy, -1, 0.0, dft);
+    int64_t rk = 0;
+    double errs[3];
+    int nt = 0;
+    if (orc_tucker_cp(reinterpret_cast<const double*>(t.data.data()), d, 0.3, 60, VIE_RULE_ENERGY, -1, 0.0, &rk,
+                      nullptr, nullptr, nullptr, errs, nullptr, 0, &nt))
+      throw std::runtime_error(orc_last_error());
+    expect(a.form.rank == rk, "tucker_cp rank");
+    std::vector<double> w(static_cast<size_t>(2 * (d[0] + d[1] + d[2]) * rk));
+    std::vector<double> tr(61);
+    if (orc_tucker_cp(reinterpret_cast<const double*>(t.data.data()), d, 0.3, 60, VIE_RULE_ENERGY, -1, 0.0, &rk,
+                      w.data(), w.data() + 2 * d[0] * rk, w.data() + 2 * (d[0] + d[1]) * rk, errs, tr.data(), 61, &nt))
+      throw std::runtime_error(orc_last_error());
+    expect(static_cast<int>(a.cp_error_trace.size()) == nt, "tucker_cp sweeps");
+    for (int i = 0; i < nt; ++i) expect(std::abs(a.cp_error_trace[i] - tr[i]) <= 1e-8, "tucker_cp trace");
+    expect(std::abs(a.hosvd_relative_error - errs[0]) <= 1e-9, "hosvd error");
+    expect(std::abs(a.stats.achieved_relative_error - errs[2]) <= 1e-9, "achieved error");
+    const CpAlsResult c = cp_als(t, 3, 30, 0.0);
+    expect(c.rel_error_trace.size() == 30 && !c.ill_posed_rank, "cp_als sweeps");
+    SpectrumBuildOptions opts;
+    opts.tucker_cp = true;
+    opts.tol = 1e-6;
+    opts.cp_iters = 100;
+    std::vector<std::pair<KernelComponent, Tensor3>> tens;
+    const std::array<Index, 3> g{4, 5, 3};
+    std::uint64_t seed = 900;
+    for (const auto& comp : unique_components(OperatorKind::N, BasisOrder::PWC)) {
+      const Parity p = component_parity(comp, BasisOrder::PWC);
+      Tensor3 x(g[0], g[1], g[2]);
+      FactorMatrix f[3];
+      for (int q = 0; q < 3; ++q) {
+        f[q] = random_matrix(g[q], 2, ++seed);
+        if (p.sign[q] < 0)
+          for (Index l = 0; l < 2; ++l) f[q](0, l) = 0.0;
+      }
+      for (Index k = 0; k < g[2]; ++k)
+        for (Index j = 0; j < g[1]; ++j)
+          for (Index i = 0; i < g[0]; ++i)
+            for (Index l = 0; l < 2; ++l) x(i, j, k) += f[0](i, l) * f[1](j, l) * f[2](k, l);
+      tens.emplace_back(comp, x);
+    }
+    EmbeddedSpectrum op = build_operator_spectra(OperatorKind::N, tens, opts, dft);
+    CurrentField xf(g);
+    for (int q = 0; q < 3; ++q) {
+      xf.comp[q] = Tensor3(g[0], g[1], g[2]);
+      if (orc_random_tensor(g[0], g[1], g[2], 950 + q, reinterpret_cast<double*>(xf.comp[q].data.data())))
+        throw std::runtime_error(orc_last_error());
+    }
+    ApplyWorkspace ws;
+    const std::vector<cplx> y = apply_operator(op, xf, MatvecStrategy::TuckerCpDecompress, ScratchPolicy::WithBuffer, &ws, dft).to_vector();
+    opts.tucker_cp = false;
+    opts.tol = 1e-12;
+    EmbeddedSpectrum opt = build_operator_spectra(OperatorKind::N, tens, opts, dft);
+    const std::vector<cplx> yt = apply_operator(opt, xf, MatvecStrategy::HosvdDecompress, ScratchPolicy::WithBuffer, &ws, dft).to_vector();
+    expect(rel(yt, y) <= 1e-6, "tucker_cp operator vs Tucker operator");
+  });
+
   // solve_scene (solver.hpp:300-326) through the wrapper vs the oracle pipeline
   run("SolveScene.MatchesOraclePipeline", [&] {
     const std::array<Index, 3> d{5, 4, 4};

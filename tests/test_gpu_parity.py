@@ -361,10 +361,10 @@ def test_error_behaviour(vie, dft, orc):
         vie.build_operator_spectra(N, PWC, dims, [comps[0]], [other], dft)
     with pytest.raises(ValueError):  # odd axis with a nonzero offset-0 row
         vie.TuckerForm(dft, dims, np.ones(1), [np.ones((3, 1)), np.ones((3, 1)), np.ones((3, 1))], (-1, -1, 1))
-    with pytest.raises(ValueError):  # embedded length with a prime factor > 7 (2 * 11)
-        f11 = vie.TuckerForm(dft, (11, 3, 3), np.ones(1), [np.ones((11, 1)), np.ones((3, 1)), np.ones((3, 1))],
+    with pytest.raises(ValueError):  # embedded length with a prime factor > 31 (2 * 37; 11..31 are served)
+        f37 = vie.TuckerForm(dft, (37, 3, 3), np.ones(1), [np.ones((37, 1)), np.ones((3, 1)), np.ones((3, 1))],
                              (1, 1, 1))
-        vie.build_operator_spectra(N, PWC, (11, 3, 3), [comps[0]], [f11], dft)
+        vie.build_operator_spectra(N, PWC, (37, 3, 3), [comps[0]], [f37], dft)
     op = vie.build_operator_spectra(N, PWC, dims, comps, forms, dft)
     with pytest.raises(ValueError):
         vie.apply_operator(op, np.zeros(5, complex))
