@@ -28,9 +28,31 @@ CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
 NVCC_FLAGS = [*CFLAGS, "-shared", "-lcudart", "-lnccl"]
 
 
-def _hdr_mtime() -> float:
-    deps = [os.path.join(CSRC, f) for f in HEADERS] + [os.path.join(ROOT, "include", "vie_b200.h")]
-    return max(os.path.getmtime(d) for d in deps)
+def _includes(path: str) -> list[str]:
+    out = []
+    for line in open(path):
+        line = line.strip()
+        if line.startswith("#include \""):
+            out.append(line.split('"')[1])
+    return out
+
+
+def _deps(src: str) -> set[str]:
+    """The in-tree headers a translation unit includes, transitively."""
+    seen: set[str] = set()
+    todo = [os.path.join(CSRC, src)]
+    while todo:
+        for inc in _includes(todo.pop()):
+            p = os.path.normpath(os.path.join(CSRC, inc))
+            if os.path.exists(p) and p not in seen:
+                seen.add(p)
+                todo.append(p)
+    return seen
+
+
+def _hdr_mtime(src: str) -> float:
+    deps = _deps(src)
+    return max([os.path.getmtime(d) for d in deps] or [0.0])
 
 
 def _stale() -> bool:
@@ -50,11 +72,10 @@ def build(force: bool = False, verbose: bool = False, extra: list[str] | None = 
     nvcc = os.environ.get("NVCC", "nvcc")
     objdir = OBJ + tag
     os.makedirs(objdir, exist_ok=True)
-    hm = _hdr_mtime()
-
     def compile_one(src: str) -> None:
         o = os.path.join(objdir, src.replace(".cu", ".o"))
         s = os.path.join(CSRC, src)
+        hm = _hdr_mtime(src)
         if not force and os.path.exists(o) and os.path.getmtime(o) > max(hm, os.path.getmtime(s)) and (not extra or tag):
             return
         cmd = [nvcc, *CFLAGS, *(extra or []), "-c", s, "-o", o + ".tmp"]
