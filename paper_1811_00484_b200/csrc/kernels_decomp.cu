@@ -259,7 +259,13 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_decomp_s_mma(const double2* 
     if (n < n3p && k < r3) cp_async16(us + e, u3 + n + static_cast<int64_t>(n3p) * k);
     else us[e] = make_double2(0.0, 0.0);
   }
-  for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) zs[e] = make_double2(0.0, 0.0);  // pads
+  // zero only the pads: the r1 x r3 block is written by load_z's cp.async, and a generic store
+  // of another thread to the same slot would be unordered with it (a stale zero could land
+  // after the data)
+  for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) {
+    const int a = e / kZS, gcol = e - a * kZS;
+    if (a >= r1 || gcol >= r3) zs[e] = make_double2(0.0, 0.0);
+  }
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
   for (int e = threadIdx.x; e < NPad1 * KA; e += blockDim.x) {
     const int a = e / NPad1, i = e - a * NPad1;  // i fastest: coalesced column reads

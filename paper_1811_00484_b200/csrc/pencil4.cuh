@@ -12,6 +12,9 @@
 #ifndef VIE_P4_NBUF
 #define VIE_P4_NBUF 3
 #endif
+#ifndef VIE_P4_SMTW  // 1: the w_m3 table (2 n3 entries) staged in shared memory per item
+#define VIE_P4_SMTW 1
+#endif
 
 namespace vie {
 namespace p4 {
@@ -35,8 +38,9 @@ struct Shape4 {
   static constexpr int ZOFF = CHUNK;                                   // 8 zero double2 after the TMA box
   static constexpr int CHUNK_STRIDE = ((CHUNK + 8) * 16 + 127) / 128 * 8;  // double2, 128-byte aligned buffers
   static constexpr int BUF_ELEMS = N3 * LINES;
+  static constexpr int TW_ELEMS = VIE_P4_SMTW ? 2 * N3 : 0;  // w_m3^e, e < m3 (after the line buffer)
   static constexpr size_t smem_bytes =
-      128 + sizeof(double2) * (static_cast<size_t>(NBUF) * CHUNK_STRIDE + BUF_ELEMS);
+      128 + sizeof(double2) * (static_cast<size_t>(NBUF) * CHUNK_STRIDE + BUF_ELEMS + TW_ELEMS);
   static_assert(LINES * HR1 <= THREADS && LINES * R0 <= THREADS, "one FFT unit per thread");
   static_assert(R1 % 2 == 0, "the last inverse stage splits its columns between the CTAs");
 };
@@ -182,6 +186,15 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
     spectrum_ready();  // the fused kernel waits here for this item's spectrum tile
     for (int i = 0; i < NBUF && i < nch; ++i) issue_chunk(i);
   }
+#if VIE_P4_SMTW
+  // the stage-0 / inverse-stage-0 twiddles w_m3^e from shared memory instead of L1 (__ldg)
+  const double2* twm3 = buf + SH::BUF_ELEMS;
+  for (int e = tid; e < 2 * N3; e += SH::THREADS) buf[SH::BUF_ELEMS + e] = __ldg(a.twm3 + e);
+  __syncthreads();
+#define P4_TW(e) twm3[e]
+#else
+#define P4_TW(e) __ldg(a.twm3 + (e))
+#endif
   P4_PHASE(0);
   mbar_wait(inbar, inpar);
   P4_PHASE(1);
@@ -206,7 +219,7 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
     int ex = b ? mp : 0;
     sfor<R0>([&](auto kc) {
       constexpr int k = decltype(kc)::value;
-      const double2 y = (k == 0 && b == 0) ? v[out_idx(R0, k)] : cmul(v[out_idx(R0, k)], __ldg(a.twm3 + ex));
+      const double2 y = (k == 0 && b == 0) ? v[out_idx(R0, k)] : cmul(v[out_idx(R0, k)], P4_TW(ex));
       sts2(base + 16u * (k * R1 * LINES), y);
       ex += 2 * mp;
       if (ex >= 2 * N3) ex -= 2 * N3;
@@ -355,12 +368,12 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
     // from the table), then the radix-R0 adjoint
     auto branch = [&](auto LD, int br, double2(&vv)[R0]) {
       int ex = br ? mpc : 0;
-      vv[0] = br ? cmulc(LD(off), __ldg(a.twm3 + ex)) : LD(off);
+      vv[0] = br ? cmulc(LD(off), P4_TW(ex)) : LD(off);
 #pragma unroll
       for (int k = 1; k < R0; ++k) {
         ex += 2 * mpc;
         if (ex >= 2 * N3) ex -= 2 * N3;
-        vv[k] = cmulc(LD(off + 16u * (k * R1 * LINES)), __ldg(a.twm3 + ex));
+        vv[k] = cmulc(LD(off + 16u * (k * R1 * LINES)), P4_TW(ex));
       }
       DFTs<R0, true, 1, 0>::run(vv);
     };
@@ -403,6 +416,7 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
     }
     P4_PHASE(7);
   }
+#undef P4_TW
 }
 
 }  // namespace p4
