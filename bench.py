@@ -606,6 +606,42 @@ def run_b200(args):
                "api": "vie_matvec_host_batch (pinned host x_i -> y_i, copies overlapped with neighbouring matvecs)",
                "sync_call_value": 1.0 / t_sync, "sync_call_api": "vie_matvec_host (H2D, matvec, D2H serialised)"}
 
+    # N > 1 (slab-decomposed): every rank copies its z-slab of x from pinned host memory, runs the
+    # library's slab matvec (vie_slab_matvec: NCCL exchanges inside) and copies its slab of y back;
+    # per-step bytes are the whole job's (all ranks' slabs); time = max over ranks
+    if not args.no_e2e and slab and e2e is None:
+        xh = torch.empty(sm.x_elems, dtype=torch.complex128).pin_memory()
+        yh = torch.empty(sm.x_elems, dtype=torch.complex128).pin_memory()
+        xh.copy_(x.cpu())
+        xd, yd = torch.empty_like(x), torch.empty_like(x)
+
+        def e2e_step():
+            xd.copy_(xh, non_blocking=True)
+            sm.apply(xd, out=yd)
+            yh.copy_(yd, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        ne2e = max(3, args.steps)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ne2e):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_e = e0.elapsed_time(e1) / ne2e
+        if dist is not None:
+            tt = torch.tensor([t_e], device="cuda", dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_e = float(tt.item())
+        tot = 16 * sm.x_elems * world
+        e2e = {"value": 1000.0 / t_e, "unit": "matvecs/s", "h2d_bytes_per_step": tot, "d2h_bytes_per_step": tot,
+               "steps": ne2e, "api": f"per rank: pinned host z-slab -> device, SlabMatvec.apply (vie_slab_matvec), "
+                                     f"device -> pinned host; {world} rank(s), time = max over ranks"}
+
     # the other MatvecStrategy on the same operator and input (operator.hpp:17-31): hosvd_decompress
     # keeps every component's octant spectrum in one HBM buffer; hosvd_loop decompresses tiles
     # into an L2-resident ring inside one persistent kernel (no whole-spectrum buffer)

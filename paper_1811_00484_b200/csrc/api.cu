@@ -1071,6 +1071,23 @@ int vie_op_get_strategy(vie_op op, int* strategy) {
   });
 }
 
+// Debug hook (not part of the drop-in ABI): device pointer and element count of an operator
+// buffer -- 0 Shat (octant spectra), 1 A, 2 B, 3 Bo, 4 Z -- for the determinism probes.
+int vie_debug_op_buffer(vie_op op, int which, void** ptr, int64_t* elems) {
+  return guard([&] {
+    if (!op || !ptr || !elems) throw Invalid("vie_debug_op_buffer: null argument");
+    const Geom& g = op->g;
+    const int64_t nv = static_cast<int64_t>(g.n1) * g.n2 * g.n3;
+    switch (which) {
+      case 0: *ptr = op->Shat; *elems = op->Shat ? static_cast<int64_t>(g.n1 + 1) * (g.n2 + 1) * g.NC * (g.n3 + 1) : 0; break;
+      case 1: *ptr = op->A; *elems = g.S * 2 * nv; break;
+      case 2: *ptr = op->B; *elems = static_cast<int64_t>(g.S) * g.n3 * g.bps; break;
+      case 3: *ptr = op->Bo; *elems = static_cast<int64_t>(g.S) * g.n3 * g.bps; break;
+      default: throw Invalid("vie_debug_op_buffer: unknown buffer");
+    }
+  });
+}
+
 int vie_op_info(vie_op op, int64_t* n_cur, int64_t* n_vox, int64_t* workspace_bytes) {
   return guard([&] {
     if (!op) throw Invalid("vie_op_info: null operator");

@@ -44,7 +44,7 @@ __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_wait_all() {
   asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 0;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 __device__ __forceinline__ void mma_f64(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"

@@ -25,7 +25,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all_d() {
   asm volatile("cp.async.commit_group;\n" ::);
-  asm volatile("cp.async.wait_group 0;\n" ::);
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
 // CTA per (component, g): Z_c[p2][a][g] for one core slice G[:,:,g] (read through the
@@ -254,17 +254,14 @@ __global__ void __launch_bounds__(kMmaThreads, 1) k_decomp_s_mma(const double2* 
   const int NPad1 = (n1p + 15) / 16 * 16;
   double2* u1s = ts + kMmaMC * Kp;                     // [NPad1][KA] A operand of T: all of U1, staged once
   const double2* u3 = forms + cd.off_u3;  // n3p x r3 col-major
+  // Z staging block zeroed (pads included) and the barrier before any cp.async: the r1 x r3 block
+  // is written by load_z's cp.async of OTHER threads, unordered with a generic store otherwise
+  for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) zs[e] = make_double2(0.0, 0.0);
+  __syncthreads();
   for (int e = threadIdx.x; e < NPad * Kp; e += blockDim.x) {
     const int n = e / Kp, k = e - n * Kp;
     if (n < n3p && k < r3) cp_async16(us + e, u3 + n + static_cast<int64_t>(n3p) * k);
     else us[e] = make_double2(0.0, 0.0);
-  }
-  // zero only the pads: the r1 x r3 block is written by load_z's cp.async, and a generic store
-  // of another thread to the same slot would be unordered with it (a stale zero could land
-  // after the data)
-  for (int e = threadIdx.x; e < KA * kZS; e += blockDim.x) {
-    const int a = e / kZS, gcol = e - a * kZS;
-    if (a >= r1 || gcol >= r3) zs[e] = make_double2(0.0, 0.0);
   }
   const double2* u1 = forms + cd.off_u1;  // n1p x r1
   for (int e = threadIdx.x; e < NPad1 * KA; e += blockDim.x) {

@@ -1,8 +1,8 @@
 #!/bin/bash
-# round-2 evidence run (v4): GPU tests, smoke, bench (both arms), launch lists (both strategies),
+# round-2 evidence run (v4, v5, ...: EVID): GPU tests, smoke, bench (both arms), launch lists (both strategies),
 # ncu --set full of each hot kernel summarised ON THE BOX (the .ncu-rep files are deleted so
 # gpurun_out stays under the copy-back limit), config lines, pencil phase profile.
-O=gpurun_out/v4
+O=gpurun_out/${EVID:-v5}
 mkdir -p $O/configs
 cd $GRAFT_REPO_ROOT
 timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -6 > $O/gputests.txt; cat $O/gputests.txt
