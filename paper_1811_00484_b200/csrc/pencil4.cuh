@@ -183,11 +183,11 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
         tma_load5_mc_hint(buf + static_cast<size_t>(k) * LINES, tmIn, 2 * cl0, 0, pos2, k - r * a.nk, r, inbar, 3,
                           l2_evict_first());
     }
-    spectrum_ready();  // the fused kernel waits here for this item's spectrum tile
-    for (int i = 0; i < NBUF && i < nch; ++i) issue_chunk(i);
   }
 #if VIE_P4_SMTW
-  // the stage-0 / inverse-stage-0 twiddles w_m3^e from shared memory instead of L1 (__ldg)
+  // the stage-0 / inverse-stage-0 twiddles w_m3^e from shared memory instead of L1 (__ldg);
+  // filled after the input loads are issued and before (fused kernel) thread 0 waits for the
+  // spectrum tile, so this barrier never waits on that spin
   const double2* twm3 = buf + SH::BUF_ELEMS;
   for (int e = tid; e < 2 * N3; e += SH::THREADS) buf[SH::BUF_ELEMS + e] = __ldg(a.twm3 + e);
   __syncthreads();
@@ -195,6 +195,10 @@ __device__ __forceinline__ void p4_item(const Pencil4Args& a, const CUtensorMap*
 #else
 #define P4_TW(e) __ldg(a.twm3 + (e))
 #endif
+  if (tid == 0) {
+    spectrum_ready();  // the fused kernel waits here for this item's spectrum tile
+    for (int i = 0; i < NBUF && i < nch; ++i) issue_chunk(i);
+  }
   P4_PHASE(0);
   mbar_wait(inbar, inpar);
   P4_PHASE(1);
