@@ -165,3 +165,32 @@ def test_c2_pwl64_gmres_to_1e6(vie, dft):
     assert abs(r.iterations - ref.iterations) <= 1
     assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8
     assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
+
+
+@pytest.mark.skipif(os.environ.get("VIE_SLOW_TESTS") != "1", reason="C3 full oracle GMRES: ~10 min (VIE_SLOW_TESTS=1)")
+def test_c3_pwl_head2mm_gmres_to_1e6(vie, dft):
+    """configs[2] (the 2 mm head grid, 100 x 120 x 100, PWL N system, 60 components rank 25): the
+    full restarted GMRES(50) solve to 1e-6 on the device, under both strategies, against the
+    oracle's gmres (solver.hpp:34-142) on the same forms, eps and rhs: iterations within +-1,
+    final residual within 1e-8, iterate within 1e-8.  Oracle: ~50 full C3 matvecs on the host."""
+    import torch
+
+    grid = (100, 120, 100)
+    nv = int(np.prod(grid))
+    rng = np.random.default_rng(7)
+    eps_np = 1 + rng.uniform(1, 5, nv) - 1j * rng.uniform(0, 1, nv)
+    op, of, _ = _system(vie, dft, grid, eps_np, 2468)
+    rhs = random_field(PWL, grid, 13)
+    eps = torch.from_numpy(eps_np).cuda()
+    gpu = {}
+    for strategy in ("hosvd_decompress", "hosvd_loop"):
+        vie.set_strategy(op, strategy)
+        gpu[strategy] = vie.gmres(op, eps, 1.0, torch.from_numpy(rhs).cuda(), vie.GmresConfig(1e-6, 50, 200))
+    ref = orc.gmres_system_tucker(PWL, grid, of, eps_np, 1.0, rhs, tol=1e-6, inner=50, outer=200)
+    for strategy, r in gpu.items():
+        print(f"C3 {strategy}: gpu {r.iterations} its, res {r.final_relative_residual:.3e}; "
+              f"oracle {ref.iterations} its, res {ref.final_relative_residual:.3e}")
+        assert r.converged and ref.converged
+        assert abs(r.iterations - ref.iterations) <= 1
+        assert abs(r.final_relative_residual - ref.final_relative_residual) <= 1e-8
+        assert rel(ref.solution, r.solution.cpu().numpy()) <= 1e-8
